@@ -1,0 +1,428 @@
+"""GGArray benchmark (BASELINE.json config 2 is the headline; configs 3-5 are
+reported beside it).
+
+A *step* is the config-2 insertion phase on one GPU: reset the array (all
+buckets back to the arena free lists), insert 2^20 int32 over 512 LFVectors
+(from a device-resident batch), then 10 doubling rounds of {grow(2n);
+every LFVector appends a copy of its committed contents; commit} up to 2^30
+elements.  ``value`` = elements inserted / device time of the K timed steps
+(Gelem/s, whole job = sum over ranks / max-over-ranks time).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Under torchrun (N>1) every rank owns its own 512 LFVectors (weak scaling) and
+the only cross-GPU step is the all-gather of the per-GPU committed sizes that
+forms the global directory.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+S, FB, N0, ROUNDS = 512, 32, 1 << 20, 10
+METRIC = "GGArray insert Gelem/s"
+UNIT = "Gelem/s"
+WORKLOAD = "config2: GGArray-512 doubling 2^20->2^30 int32 (grow + duplicate-insert per round)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.path = index, None, f"/tmp/gg_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 7 and parts[0].isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(int(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- device legs
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+class Step:
+    """One config-2 schedule on a persistent array; per-phase CUDA events."""
+
+    def __init__(self, gg, torch, device):
+        self.gg, self.torch = gg, torch
+        self.arr = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+        self.vals = torch.arange(N0, dtype=torch.int32, device=device)
+        self.offsets = np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(N0 // S), N0)
+        self.dup_ms, self.grow_ms, self.dup_elems = [], [], 0
+
+    def run(self, timed_phases: bool):
+        a, torch = self.arr, self.torch
+        a.shrink(0)                                   # reset: buckets -> free lists
+        a.insert_csr(self.vals, self.offsets)         # 2^20 initial elements
+        ev = []
+        for _ in range(ROUNDS):
+            n = a.committed_size
+            if timed_phases:
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record()
+                a.grow(2 * n)
+                e1.record()
+                a.insert_duplicate()
+                e2.record()
+                ev.append((e0, e1, e2, n))
+            else:
+                a.grow(2 * n)
+                a.insert_duplicate()
+        return ev
+
+    def collect(self, ev):
+        for e0, e1, e2, n in ev:
+            self.grow_ms.append(e0.elapsed_time(e1))
+            self.dup_ms.append(e1.elapsed_time(e2))
+            self.dup_elems += n
+
+
+def run_device(args, rank, world, local_rank):
+    import torch
+    import paper_2209_00103_b200 as gg
+    from paper_2209_00103_b200 import _lib
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    peaks, peaks_kind = _peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+
+    step = Step(gg, torch, device)
+    for _ in range(args.warmup):
+        step.run(False)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches0 = _lib.lib.gg_kernel_launches()
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        t0, t1 = _events(torch)
+        torch.cuda.synchronize()
+        t0.record()
+        evs = [step.run(True) for _ in range(args.steps)]
+        t1.record()
+        torch.cuda.synchronize()
+    launches = _lib.lib.gg_kernel_launches() - launches0
+    ms = t0.elapsed_time(t1)
+    for ev in evs:
+        step.collect(ev)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # global directory: all-gather of per-GPU committed sizes (the one exchange)
+        sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([step.arr.committed_size], device=device))
+    inserted_per_step = 1 << 30                        # 2^20 initial + sum of duplicates
+    value = world * inserted_per_step * args.steps / (ms * 1e-3) / 1e9
+
+    a = step.arr
+    assert a.committed_size == 1 << 30
+    mem = a.memory_stats()
+    dup_bytes = 8 * step.dup_elems                     # read 4 + write 4 per element
+    dup_ms = sum(step.dup_ms)
+    achieved = dup_bytes / (dup_ms * 1e-3) / 1e9
+    last_round = [m for i, m in enumerate(step.dup_ms) if i % ROUNDS == ROUNDS - 1]
+    last_gbs = (8 * (1 << 29)) / (np.mean(last_round) * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (np.arange tags, as bench_cli.py)",
+        "config": {"workload": WORKLOAD, "shards_per_gpu": S, "first_bucket_size": FB,
+                   "initial_elements": N0, "rounds": ROUNDS, "final_elements_per_gpu": 1 << 30,
+                   "parallelism": f"lfvector-sharded x{world}",
+                   "l2": "inputs larger than L2 (4 GiB live, 8 GiB capacity per GPU)"},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "k_walk<4,W_DUP> (duplicate insert)",
+                     "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "peak_kind": peaks_kind,
+                     "traffic": None, "algorithmic_bytes_per_elem": 8,
+                     "last_round_2p29_gbs": round(float(last_gbs), 1)},
+        "phases": {"insert_ms_per_step": round(dup_ms / args.steps, 4),
+                   "grow_ms_per_step": round(sum(step.grow_ms) / args.steps, 4),
+                   "insert_only_gelem_s": round(step.dup_elems / (dup_ms * 1e-3) / 1e9, 2)},
+        "footprint": {"needed_bytes": mem["needed_bytes"], "capacity_bytes": mem["capacity_bytes"],
+                      "mapped_bytes": mem["mapped_bytes"],
+                      "capacity_over_needed": round(mem["capacity_over_needed"], 6),
+                      "mapped_over_needed": round(mem["mapped_over_needed"], 6)},
+        "clocks": sampler.summary(),
+    }
+    if not args.quick:
+        out.update(secondary(args, gg, torch, device, step, hbm))
+        out["e2e"] = e2e_leg(args, gg, torch, device, world, dist)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(args)
+    return out
+
+
+def _time(torch, fn, reps=1):
+    e0, e1 = _events(torch)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def secondary(args, gg, torch, device, step, hbm):
+    """Configs 3 (r/w), flatten, and the static / semi-static / memMap baselines."""
+    a = step.arr
+    n = a.committed_size
+    passes = args.rw_passes
+    res = {}
+    # --- config 3: 100 x (+1) sweeps over 2^30 elements
+    rw = {}
+    for mode in ("per_shard", "global"):
+        p = passes if mode == "per_shard" else max(1, passes // 10)
+        a.rw_add(1, passes=1, mode=mode)
+        ms = _time(torch, lambda: a.rw_add(1, passes=p, mode=mode)) / p
+        rw[f"ggarray_{mode}"] = {"ms_per_pass": round(ms, 4), "gbs": round(8 * n / ms / 1e6, 1),
+                                 "frac": round(8 * n / ms / 1e6 / hbm, 4), "passes": p}
+    ms = _time(torch, lambda: a.rw_add(1, passes=passes, mode="fused"))
+    rw["ggarray_fused_100_in_registers"] = {"ms": round(ms, 4)}
+    flat = a.flatten_device()
+    fl_ms = _time(torch, lambda: a.flatten_device(out=flat), reps=5)
+    res["flatten"] = {"ms": round(fl_ms, 4), "gbs": round(8 * n / fl_ms / 1e6, 1),
+                      "frac": round(8 * n / fl_ms / 1e6 / hbm, 4)}
+    from paper_2209_00103_b200 import _lib
+    import ctypes as C
+    one = np.ones(1, np.int32)
+    fl = lambda: _lib.lib.gg_flat_add(C.c_void_p(flat.data_ptr()), n, 4, one.ctypes.data_as(C.c_void_p),
+                                      passes, 0, torch.cuda.current_stream().cuda_stream)
+    ms = _time(torch, fl) / passes
+    rw["flattened_contiguous"] = {"ms_per_pass": round(ms, 4), "gbs": round(8 * n / ms / 1e6, 1),
+                                  "frac": round(8 * n / ms / 1e6 / hbm, 4)}
+    res["rw_config3"] = rw
+    del flat
+    # --- baselines: the last doubling step 2^29 -> 2^30 (paper Table II)
+    half = 1 << 29
+    src = torch.arange(half, dtype=torch.int32, device=device)
+    base = {}
+    st = gg.StaticArray(1 << 30, dtype=np.int32, device=device)
+    st.insert_batch(src)
+    for algo in ("atomic", "warp", "block"):
+        def ins(algo=algo):
+            st._count = half
+            st._d_count.fill_(half)
+            st.insert_batch(src, algo=algo)
+        ins()
+        ms = _time(torch, ins, reps=3)
+        base[f"static_insert_{algo}"] = {"ms": round(ms, 4), "gelem_s": round(half / ms / 1e6, 2)}
+    ms = _time(torch, lambda: st.rw_add(1, passes=passes)) / passes
+    base["static_rw"] = {"ms_per_pass": round(ms, 4), "gbs": round(8 * (1 << 30) / ms / 1e6, 1)}
+    del st
+    torch.cuda.empty_cache()
+    # semi-static doubling: resize (new + D2D copy + free), then insert
+    g_ms, i_ms = [], []
+    for _ in range(3):
+        d = gg.DoublingArray(half, dtype=np.int32, device=device)
+        d.insert_batch(src)
+        torch.cuda.synchronize()
+        g_ms.append(_time(torch, lambda: d.resize(1 << 30)))
+        i_ms.append(_time(torch, lambda: d.insert_batch(src, algo="block")))
+        del d
+    base["doubling"] = {"grow_ms": round(min(g_ms), 4), "insert_ms": round(min(i_ms), 4),
+                        "insert_gelem_s": round(half / min(i_ms) / 1e6, 2)}
+    # memMap (VMM append, no copy)
+    g_ms, i_ms = [], []
+    for _ in range(3):
+        c = gg.ChunkTableArray(dtype=np.int32, device=device)
+        c.resize(half)
+        c.insert_batch(src)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g_ms.append(_time(torch, lambda: c.resize(1 << 30)))
+        i_ms.append(_time(torch, lambda: c.insert_batch(src, algo="block")))
+        del c
+    base["memmap"] = {"grow_ms": round(min(g_ms), 4), "insert_ms": round(min(i_ms), 4),
+                      "insert_gelem_s": round(half / min(i_ms) / 1e6, 2)}
+    # ggarray, same last step
+    last = step.dup_ms[ROUNDS - 1::ROUNDS]
+    lastg = step.grow_ms[ROUNDS - 1::ROUNDS]
+    base["ggarray512"] = {"grow_ms": round(float(np.mean(lastg)), 4),
+                          "insert_ms": round(float(np.mean(last)), 4),
+                          "insert_gelem_s": round(half / float(np.mean(last)) / 1e6, 2)}
+    res["baselines_last_doubling_2p29"] = base
+    del src
+    torch.cuda.empty_cache()
+    return res
+
+
+def e2e_leg(args, gg, torch, device, world, dist):
+    """The same schedule through the public API with HOST input: a fresh pinned
+    host batch is copied H2D inside the timed region every step, and the
+    per-shard sizes are read back D2H at its end."""
+    host = torch.arange(N0, dtype=torch.int32).pin_memory()
+    arr = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+    offs = np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(N0 // S), N0)
+    res = torch.empty(S, dtype=torch.int64).pin_memory()
+
+    def one():
+        arr.shrink(0)
+        arr.insert_csr(host.to(device, non_blocking=True), offs)
+        for _ in range(ROUNDS):
+            arr.grow(2 * arr.committed_size)
+            arr.insert_duplicate()
+        return arr
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    k = max(2, args.steps)
+    t0 = time.perf_counter()
+    for _ in range(k):
+        one()
+        st = arr.device_state()                           # D2H of the step's result
+        assert int(st["prefix"][-1]) == 1 << 30
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([sec], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    d2h = S * 8 * 4 + (S + 1) * 8 + S * arr.max_buckets * 4
+    return {"value": round(world * (1 << 30) * k / sec / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": N0 * 4, "d2h_bytes_per_step": d2h,
+            "api": "GrowableArray.insert_csr(host batch) + grow + insert_duplicate + device_state"}
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_baseline(args):
+    """The oracle port (numpy restatement of growarray) on this host's cores: a
+    bounded sample of the same schedule (2^20 -> 2^(20+R) elements)."""
+    from oracle import ggoracle as O
+    cores = len(os.sched_getaffinity(0))
+    rounds = args.cpu_rounds
+    best = None
+    t_end = time.perf_counter() + 20
+    runs = 0
+    while runs < 1 or (time.perf_counter() < t_end and runs < 3):
+        t0 = time.perf_counter()
+        _, inserted, t_ins, t_grow = O.doubling_schedule_cpu(N0, rounds, S, FB, np.int32, cores)
+        wall = time.perf_counter() - t0
+        v = inserted / wall / 1e9
+        best = v if best is None else max(best, v)
+        runs += 1
+    return {"value": round(best, 5), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle.ggoracle doubling_schedule_cpu: S=512 int32 2^20 -> 2^{20 + rounds} "
+                      f"({rounds} rounds, wall incl. grow), best of {runs}"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    from oracle import ggoracle as O
+    cores = len(os.sched_getaffinity(0))
+    rounds = args.cpu_rounds
+    for _ in range(args.warmup):
+        O.doubling_schedule_cpu(N0, min(rounds, 2), S, FB, np.int32, cores)
+    t0 = time.perf_counter()
+    inserted = 0
+    for _ in range(args.steps):
+        _, ins, _, _ = O.doubling_schedule_cpu(N0, rounds, S, FB, np.int32, cores)
+        inserted += ins
+    sec = time.perf_counter() - t0
+    v = inserted / sec / 1e9
+    return {"metric": METRIC, "value": round(v, 5), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (np.arange tags)", "impl": "reference",
+            "config": {"workload": WORKLOAD, "shards_per_gpu": S, "first_bucket_size": FB,
+                       "cpu_sample_final_elements": 1 << (20 + rounds)},
+            "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"S=512 int32 2^20 -> 2^{20 + rounds} per step (bounded sample)"},
+            "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ggarray", choices=["ggarray", "reference"])
+    ap.add_argument("--rw-passes", type=int, default=100)
+    ap.add_argument("--cpu-rounds", type=int, default=7)
+    ap.add_argument("--quick", action="store_true", help="headline only")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_device(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

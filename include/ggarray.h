@@ -1,0 +1,177 @@
+/*
+ * ggarray.h -- C ABI of the B200-native GGArray (arXiv 2209.00103).
+ *
+ * A GGArray is S LFVectors ("shards"); shard s stores its elements in
+ * power-of-two buckets, bucket b holding fb*2^b elements, allocated on the
+ * device by a bump allocator over one CUDA-VMM arena and never moved.  A
+ * committed exclusive prefix over the shard sizes is the global directory.
+ *
+ * This header is the drop-in boundary.  The reference has no FFI: its
+ * boundary is the Python class API of growarray.GrowableArray /
+ * ShardVector / baselines.  Each entry point below names the reference
+ * member it replaces (paths relative to /root/reference/pkg/src/growarray).
+ * Pointers named d_* are device pointers, h_* host pointers; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  No torch types cross the ABI.
+ *
+ * Return codes map to the reference's Python exceptions (errors.py):
+ *   GG_OK 0, GG_EVALUE 1 (ValueError), GG_ECAPACITY 2 (CapacityError),
+ *   GG_EINDEX 3 (IndexError), GG_ENOMEM 4 (MemoryError), GG_ECUDA 5,
+ *   GG_EUNPUBLISHED 6 (RuntimeError: bucket unpublished), GG_EPARTIAL 7
+ *   (some shards failed: per-shard codes in h_status -> ShardInsertError).
+ * gg_last_error() returns a message for the calling thread's last failure.
+ */
+#ifndef GGARRAY_H
+#define GGARRAY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  GG_OK = 0, GG_EVALUE = 1, GG_ECAPACITY = 2, GG_EINDEX = 3, GG_ENOMEM = 4,
+  GG_ECUDA = 5, GG_EUNPUBLISHED = 6, GG_EPARTIAL = 7
+};
+
+/* element types (arithmetic of the r/w passes; copies are byte-exact) */
+enum {
+  GG_I8 = 0, GG_U8 = 1, GG_I16 = 2, GG_U16 = 3, GG_I32 = 4, GG_U32 = 5,
+  GG_I64 = 6, GG_U64 = 7, GG_F16 = 8, GG_F32 = 9, GG_F64 = 10
+};
+
+/* r/w traversal modes */
+enum { GG_RW_PER_SHARD = 0, GG_RW_GLOBAL = 1, GG_RW_FUSED = 2 };
+
+/* static-array insertion algorithms (paper section 3-B) */
+enum { GG_ALGO_ATOMIC = 0, GG_ALGO_WARP = 1, GG_ALGO_BLOCK = 2, GG_ALGO_BATCH = 3 };
+
+typedef struct gg_array gg_array;
+
+/* Allocator hook: called on the host, in shard then bucket order, once per
+ * bucket an operation is about to allocate; nonzero = allocation failure.
+ * Replaces the `allocator` callable of ShardVector (bucket_vector.py:130-134,
+ * 194-201) for counting and failure injection; storage always comes from
+ * the device arena. */
+typedef int (*gg_alloc_hook)(void *ctx, uint32_t shard, uint32_t bucket, uint64_t elems);
+
+const char *gg_last_error(void);
+int gg_version(void);
+/* number of kernels this library has launched (process-wide counter) */
+uint64_t gg_kernel_launches(void);
+
+/* GrowableArray(shards, first_bucket_size, dtype, max_buckets, allocator)
+ * sharded_array.py:85-100, bucket_vector.py:84-93,124-137.
+ * arena_va_bytes = virtual reservation of the bucket arena (0 = device
+ * memory size).  max_buckets <= 64. */
+int gg_create(int device, uint32_t shards, uint32_t first_bucket_size, uint32_t dtype,
+              uint32_t max_buckets, uint64_t arena_va_bytes, gg_array **out);
+int gg_destroy(gg_array *a);
+int gg_set_alloc_hook(gg_array *a, gg_alloc_hook hook, void *ctx);
+/* Cap on mapped arena bytes (failure injection: allocations past it fail
+ * with MemoryError, like a failing allocator). 0 = no cap. */
+int gg_set_arena_limit(gg_array *a, uint64_t bytes);
+
+/* insert_parallel / push_back_batch (sharded_array.py:190-211,
+ * bucket_vector.py:216-247): shard s appends d_values[h_offsets[s] ..
+ * h_offsets[s+1]) in argument order.  h_starts == NULL: each non-empty shard
+ * reserves its range with one device atomicAdd on its size; otherwise the
+ * ranges were reserved earlier (ShardVector.size_counter.fetch_add) and only
+ * allocation + write happen.  h_status[S] (may be NULL) receives per-shard
+ * codes; a failing shard keeps its reservation, as in the reference.  Does
+ * not commit. */
+int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+              const uint64_t *h_starts, int32_t *h_status, void *stream);
+/* bench_cli.py:298-307 _insert_duplicate: every shard appends a copy of its
+ * committed contents, read straight from its buckets (no snapshot). */
+int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream);
+/* Paper Alg. 1 with per-lane counts (insert_index.py:84-143 LanePlan /
+ * scan_reserve semantics): lanes [h_lane_offsets[s], h_lane_offsets[s+1])
+ * belong to shard s; lane j appends its first d_counts[j] <= values_per_lane
+ * values d_values[j*values_per_lane ...] (values_per_lane = 1, counts in
+ * {0,1} is the paper's predicated push_back).  Shard s's batch lands in lane
+ * order.  Pass 1 sums the counts per shard (CTA per shard) so the host maps
+ * the arena exactly; pass 2 reserves with ONE atomicAdd per shard, allocates
+ * the buckets, block-scans the counts and scatters. */
+int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
+                    const uint64_t *h_lane_offsets, uint64_t values_per_lane,
+                    int32_t *h_status, void *stream);
+/* commit (sharded_array.py:213-222): prefix = exclusive_scan(sizes)+[total] */
+int gg_commit(gg_array *a, void *stream);
+/* grow / reserve (sharded_array.py:224-240, bucket_vector.py:249-257):
+ * shard by shard, allocate the minimal bucket prefix covering
+ * h_min_capacity[s]; stops at the first failing shard (*h_failed_shard). */
+int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_shard,
+               void *stream);
+/* ShardVector.new_bucket (bucket_vector.py:170-205): *h_won = 1 iff this
+ * call allocated bucket b of shard s. */
+int gg_new_bucket(gg_array *a, uint32_t shard, uint32_t bucket, int32_t *h_won, void *stream);
+/* AtomicCounter.fetch_add on a shard's size (insert_index.py:52-58) */
+int gg_fetch_add(gg_array *a, uint32_t shard, uint64_t count, uint64_t *h_prev, void *stream);
+/* shrink (extension, no reference semantics): size[s] = h_new_sizes[s] <=
+ * size[s]; buckets b >= min_buckets_for(new size) are released to the
+ * arena's per-class free lists (reused by later allocations before the bump
+ * pointer moves); their granules stay mapped.  Commits. */
+int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream);
+
+/* for_each_shard(+c) x passes (sharded_array.py:165-186, bench_cli.py:
+ * 180-183, 323-366).  h_addend points to one element of the array dtype.
+ * mode GG_RW_PER_SHARD walks shard segments (rw_b), GG_RW_GLOBAL resolves
+ * every global index through the directory (rw_g), GG_RW_FUSED applies all
+ * passes in one sweep (reported separately). */
+int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, void *stream);
+/* flatten (sharded_array.py:244-257): d_out[prefix[s]+i] = shard_s[i]. */
+int gg_flatten(gg_array *a, void *d_out, void *stream);
+/* get_global / set_global for index arrays (sharded_array.py:139-158) */
+int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream);
+int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream);
+/* single-element ShardVector.get / set (bucket_vector.py:259-277) */
+int gg_get(gg_array *a, uint32_t shard, uint64_t i, void *h_out, void *stream);
+int gg_set(gg_array *a, uint32_t shard, uint64_t i, const void *h_val, void *stream);
+
+/* Host views of the state (mirrors kept exact by the planner). */
+int gg_info(gg_array *a, uint32_t *h_out4 /* shards, fb, dtype, max_buckets */);
+int gg_host_state(gg_array *a, uint64_t *h_sizes, uint64_t *h_caps, uint64_t *h_flags,
+                  uint64_t *h_prefix, uint64_t *h_ops);
+/* Same quantities read back from DEVICE memory (synchronises `stream`). */
+int gg_device_state(gg_array *a, uint64_t *h_sizes, uint64_t *h_caps, uint64_t *h_flags,
+                    uint64_t *h_prefix, uint64_t *h_ops, void *stream);
+/* bucket base device pointers [S*max_buckets] (0 = unallocated); syncs */
+int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream);
+/* footprint: [0]=capacity bytes (sum of allocated buckets), [1]=mapped
+ * arena bytes, [2]=arena bump top, [3]=needed bytes (sum of sizes),
+ * [4]=device alloc calls, [5]=free-list bytes */
+int gg_mem_stats(gg_array *a, uint64_t *h_out6, void *stream);
+
+/* ---- baselines (baselines.py) on raw device buffers ---- */
+/* StaticArray/DoublingArray/ChunkTableArray.insert_batch (baselines.py:
+ * 63-77, 143-157, 224-236): append d_vals[0..n) at *d_counter using `algo`
+ * (ATOMIC: one atomicAdd per element; WARP: one per warp; BLOCK: one per
+ * CTA after a block scan; BATCH: one reservation, argument order). Elements
+ * landing at index >= capacity are dropped and counted in *d_counter. */
+int gg_flat_insert(void *d_buf, uint64_t capacity, uint64_t *d_counter, const void *d_vals,
+                   uint64_t n, uint32_t elem_bytes, int32_t algo, void *stream);
+/* contiguous +c passes over d_buf[0..n) (static r/w, flattened r/w) */
+int gg_flat_add(void *d_buf, uint64_t n, uint32_t dtype, const void *h_addend,
+                uint32_t passes, int32_t fused, void *stream);
+/* stream-ordered device buffers (semi-static DoublingArray.resize,
+ * baselines.py:127-141: new buffer + D2D copy + free) */
+int gg_buf_alloc(uint64_t bytes, void *stream, void **d_out);
+int gg_buf_free(void *d_ptr, void *stream);
+int gg_buf_copy(void *d_dst, const void *d_src, uint64_t bytes, void *stream);
+/* memMap baseline (paper section 3-A, ChunkTableArray analog): one VA
+ * reservation, physical 2 MiB granules appended with cuMemCreate/cuMemMap. */
+typedef struct gg_vmm gg_vmm;
+int gg_vmm_create(int device, uint64_t va_bytes, gg_vmm **out);
+int gg_vmm_ensure(gg_vmm *v, uint64_t bytes);
+int gg_vmm_info(gg_vmm *v, uint64_t *h_base, uint64_t *h_mapped, uint64_t *h_granule);
+int gg_vmm_destroy(gg_vmm *v);
+
+/* device properties the host layer sizes grids with */
+int gg_device_sms(int device, int32_t *h_sms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GGARRAY_H */

@@ -1,0 +1,1667 @@
+// ggarray.cu -- B200 (sm_100a) GGArray: device tables, VMM bucket arena,
+// bump allocator, and the hot kernels (reserve+allocate, insert, duplicate,
+// commit, r/w, flatten, gather/scatter) behind the C ABI in include/ggarray.h.
+//
+// Layout in HBM (one handle per GPU):
+//   * metadata (plain cudaMalloc, never in the arena): size[S], cap[S],
+//     ops[S], start[S], count[S], prefix[S+1], offsets[S+1], ctl[S],
+//     flag[S*MB] (u32 once-flags: 0 free, 1 allocating, 2 published),
+//     ptr[S*MB] (bucket base pointers), misc[] (arena bump top, alloc calls).
+//   * bucket arena: one cuMemAddressReserve'd VA range; physical 2 MiB
+//     granules are mapped by the host up to the exact bump top the planner
+//     predicts BEFORE a launch; buckets are bump-allocated on the device
+//     with byte-exact packing (16 B alignment; every bucket of fb=32 int32 is
+//     a multiple of 128 B so the packing has zero padding).
+// The host keeps exact mirrors of sizes / flags / capacities / the bump top
+// (every quantity is a deterministic function of the op sequence), which
+// lets it map memory, raise the reference's errors and run the allocator
+// hook without any device round trip per insert.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ggarray.h"
+
+#define GG_VERSION 1
+
+namespace gg {
+
+thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};   // kernels launched by this library
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+// Driver VMM entry points resolved through cudaGetDriverEntryPoint, so the
+// library has no link-time libcuda dependency (it loads on GPU-less hosts).
+struct Drv {
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuGetErrorString) err_string = nullptr;
+  bool ok = false;
+};
+
+Drv &drv() {
+  static Drv d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char *name, void **fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn != nullptr;
+    };
+    d.ok = get("cuMemGetAllocationGranularity", (void **)&d.granularity) &&
+           get("cuMemAddressReserve", (void **)&d.reserve) &&
+           get("cuMemAddressFree", (void **)&d.addr_free) &&
+           get("cuMemCreate", (void **)&d.create) && get("cuMemRelease", (void **)&d.release) &&
+           get("cuMemMap", (void **)&d.map) && get("cuMemUnmap", (void **)&d.unmap) &&
+           get("cuMemSetAccess", (void **)&d.set_access) &&
+           get("cuGetErrorString", (void **)&d.err_string);
+  });
+  return d;
+}
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(GG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define CU_TRY(expr)                                                                   \
+  do {                                                                                 \
+    CUresult r_ = (expr);                                                              \
+    if (r_ != CUDA_SUCCESS) {                                                          \
+      const char *s_ = nullptr;                                                        \
+      if (drv().err_string) drv().err_string(r_, &s_);                                 \
+      return fail(r_ == CUDA_ERROR_OUT_OF_MEMORY ? GG_ENOMEM : GG_ECUDA,               \
+                  std::string(#expr) + ": " + (s_ ? s_ : "?"));                        \
+    }                                                                                  \
+  } while (0)
+
+constexpr int kMaxBuckets = 64;
+constexpr int kThreads = 256;          // CTA size of the streaming kernels
+constexpr int kTileBytes = 32 * 1024;  // bytes of payload per tile
+constexpr uint32_t kFlagPublished = 2;
+
+// ctl word per shard (only uploaded when an op plans a failure)
+constexpr uint32_t kCtlLimitMask = 0xffu;   // allocate buckets < limit
+constexpr uint32_t kCtlWrite = 1u << 8;     // write the values
+constexpr uint32_t kCtlZero = 1u << 9;      // write zeros instead (failed shard)
+
+enum { MISC_TOP = 0, MISC_ALLOCS = 1, MISC_OOM = 2, MISC_N = 4 };
+
+inline uint32_t elem_bytes_of(uint32_t dt) {
+  switch (dt) {
+    case GG_I8: case GG_U8: return 1;
+    case GG_I16: case GG_U16: case GG_F16: return 2;
+    case GG_I32: case GG_U32: case GG_F32: return 4;
+    case GG_I64: case GG_U64: case GG_F64: return 8;
+    default: return 0;
+  }
+}
+
+inline uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+
+inline int ilog2(uint64_t x) { return 63 - __builtin_clzll(x); }
+
+// ------------------------------------------------------------------ device side
+
+struct Tables {
+  uint64_t *size, *cap, *ops, *start, *count, *prefix, *offsets;
+  uint32_t *ctl, *flag, *status;
+  char **ptr;
+  uint64_t *fl;            // [MB*S] per-class free lists of arena offsets (shrink)
+  int *fl_n;               // [MB] entries per class
+  unsigned long long *misc;
+  char *arena;
+  uint64_t arena_mapped;  // device allocations beyond this fail (OOM)
+  uint32_t S, log2fb, MB, esz;
+};
+
+template <int ESZ> struct ElemT;
+template <> struct ElemT<1> { typedef uint8_t T; };
+template <> struct ElemT<2> { typedef uint16_t T; };
+template <> struct ElemT<4> { typedef uint32_t T; };
+template <> struct ElemT<8> { typedef unsigned long long T; };
+
+__device__ __forceinline__ void locate(uint64_t i, uint32_t log2fb, uint32_t &b, uint64_t &off) {
+  // bucket_vector.py:48-59: b = hibit(i/fb + 1), off = i - fb*(2^b - 1)
+  uint64_t q = (i >> log2fb) + 1;
+  b = 63u - (uint32_t)__clzll((long long)q);
+  off = i - (((1ull << b) - 1ull) << log2fb);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Paper Alg. 2 (new_bucket): CAS the once-flag, the winner bump-allocates
+// from the arena and publishes with release order; losers wait for the
+// publication.  Returns 1 if this caller allocated, 0 if it was already
+// there, -1 on arena exhaustion (flag rolled back, like
+// bucket_vector.py:196-201).
+__device__ int alloc_bucket(const Tables &t, uint32_t s, uint32_t b) {
+  uint32_t *f = t.flag + (size_t)s * t.MB + b;
+  for (;;) {
+    uint32_t cur = ld_acquire(f);
+    if (cur == kFlagPublished) return 0;
+    if (cur == 0 && atomicCAS(f, 0u, 1u) == 0u) break;
+    __nanosleep(64);
+  }
+  const uint64_t elems = 1ull << (t.log2fb + b);
+  const uint64_t bytes = (elems * t.esz + 15) & ~15ull;
+  unsigned long long off;
+  int k = atomicSub(&t.fl_n[b], 1);
+  if (k > 0) {
+    off = t.fl[(size_t)b * t.S + (k - 1)];   // reuse a bucket released by shrink
+  } else {
+    atomicAdd(&t.fl_n[b], 1);
+    off = atomicAdd(&t.misc[MISC_TOP], (unsigned long long)bytes);
+  }
+  if (off + bytes > t.arena_mapped) {
+    atomicAdd(&t.misc[MISC_OOM], 1ull);
+    st_release(f, 0);
+    return -1;
+  }
+  t.ptr[(size_t)s * t.MB + b] = t.arena + off;
+  atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
+  atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
+  __threadfence();
+  st_release(f, kFlagPublished);
+  return 1;
+}
+
+// Reservation + bucket allocation, one thread per shard: one atomicAdd on the
+// shard's size per batch (bucket_vector.py:229 via insert_index.py:118-122),
+// then allocate every missing bucket of the reserved range
+// (bucket_vector.py:207-214, 234-238).  Count sources:
+//   mode 0: CSR offsets (insert); mode 1: committed lengths (duplicate);
+//   mode 2: explicit starts + counts already in t.start/t.count (fetch_add'ed)
+__global__ void k_reserve(Tables t, int mode) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= t.S) return;
+  uint64_t c, start;
+  if (mode == 0) c = t.offsets[s + 1] - t.offsets[s];
+  else if (mode == 1) c = t.prefix[s + 1] - t.prefix[s];
+  else c = t.count[s];
+  const uint32_t ctl = t.ctl ? t.ctl[s] : (kCtlWrite | t.MB);
+  if (mode != 2) {
+    t.count[s] = c;
+    if (c == 0) return;
+    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+    t.ops[s] += 1;
+    t.start[s] = start;
+  } else {
+    if (c == 0) return;
+    start = t.start[s];
+  }
+  uint32_t b0, b1;
+  uint64_t o;
+  locate(start, t.log2fb, b0, o);
+  locate(start + c - 1, t.log2fb, b1, o);
+  uint32_t lim = ctl & kCtlLimitMask;
+  if (lim > b1 + 1) lim = b1 + 1;
+  for (uint32_t b = b0; b < lim; ++b)
+    if (alloc_bucket(t, s, b) < 0) atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+}
+
+// grow: thread per shard, allocate buckets [0, lim[s]) (ctl carries lim)
+__global__ void k_grow(Tables t) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= t.S) return;
+  uint32_t lim = t.ctl[s] & kCtlLimitMask;
+  for (uint32_t b = 0; b < lim; ++b)
+    if (alloc_bucket(t, s, b) < 0) atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+}
+
+__global__ void k_new_bucket(Tables t, uint32_t s, uint32_t b, int *won) {
+  *won = alloc_bucket(t, s, b);
+}
+
+__global__ void k_fetch_add(Tables t, uint32_t s, uint64_t c) {
+  atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+  t.ops[s] += 1;
+}
+
+// commit (sharded_array.py:213-222): one CTA, exclusive scan of S sizes.
+__global__ void __launch_bounds__(1024) k_commit(Tables t) {
+  __shared__ uint64_t warp_tot[32];
+  __shared__ uint64_t carry;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < t.S; base += 1024) {
+    uint32_t s = base + tid;
+    uint64_t v = s < t.S ? t.size[s] : 0;
+    uint64_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= (uint32_t)d) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t w = warp_tot[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= (uint32_t)d) w += y;
+      }
+      warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    uint64_t incl = x + (wid ? warp_tot[wid - 1] : 0) + carry;
+    if (s < t.S) {
+      t.prefix[s + 1] = incl;
+      if (s == 0) t.prefix[0] = 0;
+    }
+    __syncthreads();
+    if (tid == 1023) carry = incl;
+    __syncthreads();
+  }
+}
+
+// block-wide exclusive scan of one u64 per thread (blockDim multiple of 32);
+// returns the exclusive prefix, *total gets the block sum.
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t *total,
+                                                         uint64_t *warp_sums /* smem[32] */) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= (uint32_t)d) w += y;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  uint64_t incl = x + (wid ? warp_sums[wid - 1] : 0);
+  *total = warp_sums[nw - 1];
+  __syncthreads();
+  return incl - v;
+}
+
+// Paper Alg. 1 with per-lane counts, pass 1: CTA per shard sums its lanes'
+// counts (so the host can map the arena exactly before pass 2).
+__global__ void __launch_bounds__(1024) k_lanes_count(Tables t, const uint32_t *counts) {
+  __shared__ uint64_t ws[32];
+  const uint32_t s = blockIdx.x;
+  const uint64_t lo = t.offsets[s], hi = t.offsets[s + 1];
+  uint64_t acc = 0;
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) acc += counts[j];
+  uint64_t tot;
+  block_exclusive_scan(acc, &tot, ws);
+  if (threadIdx.x == 0) t.count[s] = tot;
+}
+
+// Pass 2 (paper Alg. 1): the CTA of shard s reserves its whole batch with ONE
+// atomicAdd on the LFVector size, allocates the buckets the range touches
+// (Alg. 2), then block-scans the lane counts chunk by chunk and every lane
+// scatters its values to start + carry + exclusive_scan(lane).
+template <int ESZ>
+__global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *vals,
+                                                       const uint32_t *counts, uint32_t K) {
+  typedef typename ElemT<ESZ>::T E;
+  __shared__ uint64_t ws[32];
+  __shared__ char *bptr[64];
+  __shared__ uint64_t start_s;
+  __shared__ uint32_t ctl_s;
+  const uint32_t s = blockIdx.x, tid = threadIdx.x;
+  const uint64_t c = t.count[s];
+  if (c == 0) return;
+  if (tid == 0) {
+    const uint32_t ctl = t.ctl ? t.ctl[s] : (kCtlWrite | t.MB);
+    const uint64_t start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+    t.ops[s] += 1;
+    uint32_t b0, b1; uint64_t o;
+    locate(start, t.log2fb, b0, o);
+    locate(start + c - 1, t.log2fb, b1, o);
+    uint32_t lim = min(ctl & kCtlLimitMask, b1 + 1);
+    for (uint32_t b = b0; b < lim; ++b)
+      if (alloc_bucket(t, s, b) < 0) atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+    start_s = start;
+    ctl_s = ctl;
+  }
+  __syncthreads();
+  if (tid < t.MB) bptr[tid] = t.flag[(size_t)s * t.MB + tid] == kFlagPublished
+                                  ? t.ptr[(size_t)s * t.MB + tid] : nullptr;
+  __syncthreads();
+  const uint64_t start = start_s;
+  const uint32_t ctl = ctl_s;
+  if (!(ctl & (kCtlWrite | kCtlZero))) return;
+  const uint64_t lo = t.offsets[s], hi = t.offsets[s + 1];
+  uint64_t carry = 0;
+  for (uint64_t base = lo; base < hi; base += blockDim.x) {
+    const uint64_t j = base + tid;
+    const uint32_t cnt = j < hi ? counts[j] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan(cnt, &tot, ws);
+    const E *src = (const E *)vals + j * K;
+    for (uint32_t e = 0; e < cnt; ++e) {
+      uint32_t b; uint64_t o;
+      locate(start + carry + ex + e, t.log2fb, b, o);
+      if (bptr[b]) ((E *)bptr[b])[o] = (ctl & kCtlWrite) ? src[e] : E(0);
+    }
+    carry += tot;
+  }
+}
+
+// shrink (extension): thread per bucket class b walks shards in order and
+// releases bucket b of every shard whose new size needs fewer than b+1
+// buckets onto the class free list (deterministic list order).
+__global__ void k_shrink_release(Tables t, const uint64_t *new_sizes) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= t.MB) return;
+  const uint64_t fbv = 1ull << t.log2fb;
+  int n = t.fl_n[b];
+  for (uint32_t s = 0; s < t.S; ++s) {
+    uint64_t ns = new_sizes[s];
+    uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + fbv - 1) >> t.log2fb))) : 0u;
+    uint32_t *f = t.flag + (size_t)s * t.MB + b;
+    if (b >= keep && *f == kFlagPublished) {
+      t.fl[(size_t)b * t.S + n++] = (uint64_t)(t.ptr[(size_t)s * t.MB + b] - t.arena);
+      t.ptr[(size_t)s * t.MB + b] = nullptr;
+      *f = 0;
+      atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)(0ull - (fbv << b)));
+    }
+  }
+  t.fl_n[b] = n;
+}
+
+__global__ void k_shrink_sizes(Tables t, const uint64_t *new_sizes) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < t.S) t.size[s] = new_sizes[s];
+}
+
+// ---- streaming primitives: a CTA moves one contiguous piece -------------
+
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_rw(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg(uint4 *p, const uint4 &v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// dst[0..n) = src[0..n) (element granular, arbitrary relative alignment), or
+// zeros if src == nullptr.  Stores are 16 B aligned vectors; loads are 16 B
+// vectors when src shares dst's alignment, else element loads.
+template <int ESZ, int UNROLL>
+__device__ __forceinline__ void cta_copy(char *dst, const char *src, uint64_t n, uint32_t tid,
+                                         uint32_t nt) {
+  typedef typename ElemT<ESZ>::T E;
+  constexpr uint32_t VE = 16 / ESZ;
+  const uintptr_t d = (uintptr_t)dst;
+  uint64_t head = ((16 - (d & 15)) & 15) / ESZ;
+  if (head > n) head = n;
+  const uint64_t body = (n - head) / VE;
+  const uint64_t tail0 = head + body * VE;
+  E *de = (E *)dst;
+  const E *se = (const E *)src;
+  for (uint64_t e = tid; e < head; e += nt) de[e] = src ? se[e] : E(0);
+  for (uint64_t e = tail0 + tid; e < n; e += nt) de[e] = src ? se[e] : E(0);
+  uint4 *dv = (uint4 *)(dst + head * ESZ);
+  if (src == nullptr) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (uint64_t v = tid; v < body; v += nt) stg(dv + v, z);
+    return;
+  }
+  const char *sb = src + head * ESZ;
+  if ((((uintptr_t)sb) & 15) == 0) {
+    const uint4 *sv = (const uint4 *)sb;
+    uint64_t v = tid;
+    for (; v + (UNROLL - 1) * (uint64_t)nt < body; v += UNROLL * (uint64_t)nt) {
+      uint4 r[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) r[u] = ldg_stream(sv + v + u * nt);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) stg(dv + v + u * nt, r[u]);
+    }
+    for (; v < body; v += nt) stg(dv + v, ldg_stream(sv + v));
+  } else {
+    const E *s2 = (const E *)sb;
+    for (uint64_t v = tid; v < body; v += nt) {
+      union { uint4 q; E e[VE]; } u;
+#pragma unroll
+      for (uint32_t k = 0; k < VE; ++k) u.e[k] = __ldg(s2 + v * VE + k);
+      stg(dv + v, u.q);
+    }
+  }
+}
+
+// typed wrapping / IEEE add used by the r/w passes
+template <typename T> struct AddOp {
+  __device__ __forceinline__ static T apply(T x, T a) { return (T)(x + a); }
+};
+template <> struct AddOp<int8_t> {
+  __device__ __forceinline__ static int8_t apply(int8_t x, int8_t a) {
+    return (int8_t)(uint8_t)((uint8_t)x + (uint8_t)a);
+  }
+};
+template <> struct AddOp<int16_t> {
+  __device__ __forceinline__ static int16_t apply(int16_t x, int16_t a) {
+    return (int16_t)(uint16_t)((uint16_t)x + (uint16_t)a);
+  }
+};
+template <> struct AddOp<int32_t> {
+  __device__ __forceinline__ static int32_t apply(int32_t x, int32_t a) {
+    return (int32_t)((uint32_t)x + (uint32_t)a);
+  }
+};
+template <> struct AddOp<long long> {
+  __device__ __forceinline__ static long long apply(long long x, long long a) {
+    return (long long)((unsigned long long)x + (unsigned long long)a);
+  }
+};
+template <> struct AddOp<float> {
+  __device__ __forceinline__ static float apply(float x, float a) { return __fadd_rn(x, a); }
+};
+template <> struct AddOp<double> {
+  __device__ __forceinline__ static double apply(double x, double a) { return __dadd_rn(x, a); }
+};
+template <> struct AddOp<__half> {
+  // numpy float16 arithmetic: widen to float32, add, round back (exact RN)
+  __device__ __forceinline__ static __half apply(__half x, __half a) {
+    return __float2half_rn(__half2float(x) + __half2float(a));
+  }
+};
+
+// in-place p[0..n) = p + a (applied `reps` times in registers; reps = 1 for a
+// separate sweep per pass)
+template <typename T, int UNROLL>
+__device__ __forceinline__ void cta_add(char *p, uint64_t n, T a, uint32_t reps, uint32_t tid,
+                                        uint32_t nt) {
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uintptr_t d = (uintptr_t)p;
+  uint64_t head = ((16 - (d & 15)) & 15) / sizeof(T);
+  if (head > n) head = n;
+  const uint64_t body = (n - head) / VE;
+  const uint64_t tail0 = head + body * VE;
+  T *pe = (T *)p;
+  for (uint64_t e = tid; e < head; e += nt) {
+    T x = pe[e];
+    for (uint32_t r = 0; r < reps; ++r) x = AddOp<T>::apply(x, a);
+    pe[e] = x;
+  }
+  for (uint64_t e = tail0 + tid; e < n; e += nt) {
+    T x = pe[e];
+    for (uint32_t r = 0; r < reps; ++r) x = AddOp<T>::apply(x, a);
+    pe[e] = x;
+  }
+  uint4 *pv = (uint4 *)(p + head * sizeof(T));
+  uint64_t v = tid;
+  for (; v + (UNROLL - 1) * (uint64_t)nt < body; v += UNROLL * (uint64_t)nt) {
+    union { uint4 q; T e[VE]; } u[UNROLL];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) u[k].q = ldg_rw(pv + v + k * nt);
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      for (uint32_t r = 0; r < reps; ++r)
+#pragma unroll
+        for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = AddOp<T>::apply(u[k].e[j], a);
+      stg(pv + v + k * nt, u[k].q);
+    }
+  }
+  for (; v < body; v += nt) {
+    union { uint4 q; T e[VE]; } u;
+    u.q = ldg_rw(pv + v);
+    for (uint32_t r = 0; r < reps; ++r)
+#pragma unroll
+      for (uint32_t j = 0; j < VE; ++j) u.e[j] = AddOp<T>::apply(u.e[j], a);
+    stg(pv + v, u.q);
+  }
+}
+
+// ---- tile walker ------------------------------------------------------------
+// The work space is an index range [0, total) partitioned among shards by a
+// directory dir[S+1] (CSR offsets for inserts, the committed prefix for
+// duplicate / flatten / r/w).  A CTA takes tiles of kTileBytes and walks them
+// in pieces over which shard, source bucket and destination bucket are all
+// constant; every thread computes the (uniform) piece bounds itself.
+enum { W_INSERT = 0, W_DUP = 1, W_FLATTEN = 2, W_RW = 3 };
+
+__device__ __forceinline__ uint32_t upper_shard(const uint64_t *dir, uint32_t S, uint64_t g) {
+  // largest s with dir[s] <= g (bisect_right - 1, sharded_array.py:136)
+  uint32_t lo = 0, hi = S;  // dir[0] = 0 <= g
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (dir[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int ESZ, int W, typename T>
+__global__ void __launch_bounds__(kThreads) k_walk(Tables t, const char *flat_src, char *flat_dst,
+                                                   uint64_t total, T addend, uint32_t reps) {
+  constexpr uint64_t TILE = kTileBytes / ESZ;
+  const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
+  const uint64_t ntiles = (total + TILE - 1) / TILE;
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint64_t g = tile * TILE;
+    const uint64_t gend = min(total, g + TILE);
+    uint32_t s = upper_shard(dir, t.S, g);
+    while (g < gend) {
+      uint64_t shard_end = dir[s + 1];
+      while (shard_end <= g) { ++s; shard_end = dir[s + 1]; }
+      const uint64_t k = g - dir[s];
+      uint64_t len = min(gend, shard_end) - g;
+      const uint32_t ctl = (W == W_INSERT || W == W_DUP) && t.ctl ? t.ctl[s] : kCtlWrite;
+      const char *sp = nullptr;
+      char *dp = nullptr;
+      bool dst_ok = true;
+      // source side
+      if constexpr (W == W_INSERT) {
+        sp = flat_src + g * ESZ;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(k, t.log2fb, b, o);
+        len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
+        sp = t.ptr[(size_t)s * t.MB + b] + o * ESZ;
+      }
+      // destination side
+      if constexpr (W == W_FLATTEN) {
+        dp = flat_dst + g * ESZ;
+      } else if constexpr (W == W_RW) {
+        dp = (char *)sp;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(t.start[s] + k, t.log2fb, b, o);
+        len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
+        uint32_t f = t.flag[(size_t)s * t.MB + b];
+        dst_ok = (f == kFlagPublished);
+        dp = t.ptr[(size_t)s * t.MB + b] + o * ESZ;
+      }
+      if constexpr (W == W_RW) {
+        cta_add<T, 4>(dp, len, addend, reps, tid, nt);
+      } else if (dst_ok && (ctl & (kCtlWrite | kCtlZero))) {
+        cta_copy<ESZ, 4>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
+      }
+      g += len;
+    }
+  }
+}
+
+// rw_g: one thread per element resolved through the directory
+// (bench_cli.py:339-366, paper's rw_g): warp-uniform bisect on the smem
+// prefix, per-lane fix-up, clz locate.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total, T addend) {
+  extern __shared__ uint64_t sp[];
+  const bool in_smem = (t.S + 1) <= 4096;
+  const uint64_t *pre = t.prefix;
+  if (in_smem) {
+    for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) sp[i] = t.prefix[i];
+    __syncthreads();
+    pre = sp;
+  }
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (uint64_t base = wid * 32; base < total; base += nwarps * 32) {
+    uint32_t s = upper_shard(pre, t.S, base);  // warp-uniform key: smem broadcast
+    const uint64_t g = base + lane;
+    if (g < total) {
+      while (pre[s + 1] <= g) ++s;               // lanes past a shard boundary
+      uint32_t b; uint64_t o;
+      locate(g - pre[s], t.log2fb, b, o);
+      T *p = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
+      *p = AddOp<T>::apply(*p, addend);
+    }
+  }
+}
+
+template <int ESZ>
+__global__ void k_gather(Tables t, const int64_t *idx, uint64_t n, char *out, const char *vals,
+                         int scatter) {
+  typedef typename ElemT<ESZ>::T E;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t g = (uint64_t)idx[j];
+    uint32_t s = upper_shard(t.prefix, t.S, g);
+    uint32_t b; uint64_t o;
+    locate(g - t.prefix[s], t.log2fb, b, o);
+    E *p = (E *)(t.ptr[(size_t)s * t.MB + b]) + o;
+    if (scatter) *p = ((const E *)vals)[j];
+    else ((E *)out)[j] = *p;
+  }
+}
+
+// zero whole buckets listed as (shard, bucket) pairs (dirty shards only)
+__global__ void k_zero_buckets(Tables t, const uint32_t *pairs, uint32_t npairs) {
+  for (uint32_t k = blockIdx.x; k < npairs; k += gridDim.x) {
+    uint32_t s = pairs[2 * k], b = pairs[2 * k + 1];
+    char *p = t.ptr[(size_t)s * t.MB + b];
+    uint64_t n = (1ull << (t.log2fb + b)) * t.esz;
+    if (t.flag[(size_t)s * t.MB + b] != kFlagPublished) continue;
+    cta_copy<1, 4>(p, nullptr, n, threadIdx.x, blockDim.x);
+  }
+}
+
+// ---- static-array baselines ---------------------------------------------------
+template <int ESZ>
+__global__ void k_flat_insert(char *buf, uint64_t cap, unsigned long long *counter,
+                              const char *vals, uint64_t n, int algo) {
+  typedef typename ElemT<ESZ>::T E;
+  const E *v = (const E *)vals;
+  E *out = (E *)buf;
+  __shared__ unsigned long long base_s;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
+    uint64_t j = j0 + threadIdx.x;
+    bool have = j < n;
+    unsigned long long idx = 0;
+    if (algo == GG_ALGO_ATOMIC) {
+      if (have) idx = atomicAdd(counter, 1ull);  // paper 3-B-1: one atomic per element
+    } else if (algo == GG_ALGO_WARP) {
+      // paper 3-B-2 (warp shuffle scan of 0/1 counts, one atomic per warp)
+      unsigned mask = __ballot_sync(0xffffffffu, have);
+      unsigned lane = threadIdx.x & 31;
+      unsigned long long wb = 0;
+      if (lane == 0 && mask) wb = atomicAdd(counter, (unsigned long long)__popc(mask));
+      wb = __shfl_sync(0xffffffffu, wb, 0);
+      idx = wb + __popc(mask & ((1u << lane) - 1u));
+    } else {  // GG_ALGO_BLOCK: block scan, one atomic per CTA
+      uint64_t cnt = min((uint64_t)blockDim.x, n - j0);
+      if (threadIdx.x == 0) base_s = atomicAdd(counter, (unsigned long long)cnt);
+      __syncthreads();
+      idx = base_s + threadIdx.x;
+      __syncthreads();
+    }
+    if (have && idx < cap) out[idx] = v[j];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_flat_add(char *buf, uint64_t n, T a, uint32_t reps) {
+  // grid-stride over 32 KiB chunks of the contiguous array
+  constexpr uint64_t CH = kTileBytes / sizeof(T);
+  const uint64_t nch = (n + CH - 1) / CH;
+  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    uint64_t lo = c * CH, len = min(n - lo, CH);
+    cta_add<T, 4>(buf + lo * sizeof(T), len, a, reps, threadIdx.x, blockDim.x);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+struct Arena {
+  int dev = 0;
+  CUdeviceptr base = 0;
+  size_t va = 0, gran = 0, mapped = 0;
+  struct Map { size_t off, size; CUmemGenericAllocationHandle h; };
+  std::vector<Map> maps;
+
+  int init(int device, uint64_t va_bytes) {
+    dev = device;
+    if (!drv().ok) return fail(GG_ECUDA, "CUDA driver VMM entry points unavailable");
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = device;
+    CU_TRY(drv().granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+    va = (va_bytes + gran - 1) / gran * gran;
+    CU_TRY(drv().reserve(&base, va, gran, 0, 0));
+    return GG_OK;
+  }
+  // map physical granules so that [0, bytes) is backed
+  int ensure(uint64_t bytes) {
+    if (bytes <= mapped) return GG_OK;
+    size_t want = (bytes + gran - 1) / gran * gran;
+    if (want > va) return fail(GG_ENOMEM, "arena VA reservation exhausted");
+    size_t add = want - mapped;
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = dev;
+    CUmemGenericAllocationHandle h;
+    CU_TRY(drv().create(&h, add, &prop, 0));
+    CUresult r = drv().map(base + mapped, add, 0, h, 0);
+    if (r != CUDA_SUCCESS) {
+      drv().release(h);
+      return fail(GG_ECUDA, "cuMemMap failed");
+    }
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = drv().set_access(base + mapped, add, &acc, 1);
+    if (r != CUDA_SUCCESS) {
+      drv().unmap(base + mapped, add);
+      drv().release(h);
+      return fail(GG_ECUDA, "cuMemSetAccess failed");
+    }
+    maps.push_back({mapped, add, h});
+    mapped = want;
+    return GG_OK;
+  }
+  // release whole mappings lying at or above `keep` bytes
+  void trim(uint64_t keep) {
+    while (!maps.empty() && maps.back().off >= keep) {
+      Map m = maps.back();
+      maps.pop_back();
+      drv().unmap(base + m.off, m.size);
+      drv().release(m.h);
+      mapped = m.off;
+    }
+  }
+  void destroy() {
+    trim(0);
+    if (base) drv().addr_free(base, va);
+    base = 0;
+  }
+};
+
+int g_sms[64] = {0};
+
+int sm_count(int dev) {
+  if (dev < 0 || dev >= 64) return 148;
+  if (!g_sms[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    g_sms[dev] = v;
+  }
+  return g_sms[dev];
+}
+
+// pinned upload ring: small per-op host arrays (offsets, ctl words) travel
+// through pinned slots; a slot is reused only after its copy completed.
+struct Uploader {
+  static constexpr int kSlots = 4;
+  char *host[kSlots] = {nullptr};
+  cudaEvent_t ev[kSlots] = {nullptr};
+  bool used[kSlots] = {false};
+  size_t cap = 0;
+  int next = 0;
+  int init(size_t bytes) {
+    cap = bytes;
+    for (int i = 0; i < kSlots; ++i) {
+      CUDA_TRY(cudaMallocHost(&host[i], cap));
+      CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    return GG_OK;
+  }
+  // copy `n` arrays (dst device ptr, src host ptr, bytes) in one slot
+  int upload(cudaStream_t st, int n, void *const *dst, const void *const *src, const size_t *bytes) {
+    int k = next;
+    next = (next + 1) % kSlots;
+    if (used[k]) CUDA_TRY(cudaEventSynchronize(ev[k]));
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      if (off + bytes[i] > cap) return fail(GG_EVALUE, "upload slot overflow");
+      memcpy(host[k] + off, src[i], bytes[i]);
+      CUDA_TRY(cudaMemcpyAsync(dst[i], host[k] + off, bytes[i], cudaMemcpyHostToDevice, st));
+      off += (bytes[i] + 15) & ~size_t(15);
+    }
+    CUDA_TRY(cudaEventRecord(ev[k], st));
+    used[k] = true;
+    return GG_OK;
+  }
+  void destroy() {
+    for (int i = 0; i < kSlots; ++i) {
+      if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+      if (host[i]) cudaFreeHost(host[i]);
+    }
+  }
+};
+
+}  // namespace gg
+
+using namespace gg;
+
+struct gg_array {
+  int dev;
+  uint32_t S, fb, log2fb, dtype, esz, MB;
+  // exact host mirrors
+  std::vector<uint64_t> size, cap, ops, prefix, flags;  // flags: bitmask per shard
+  std::vector<uint8_t> dirty;                            // shard saw a failed reservation
+  uint64_t top = 0;                                      // arena bump top (bytes)
+  std::vector<uint64_t> fl_count;                        // free-list entries per class
+  uint64_t alloc_calls = 0;
+  uint64_t limit = 0;                                    // mapped-bytes cap (0 = none)
+  gg_alloc_hook hook = nullptr;
+  void *hook_ctx = nullptr;
+  Arena arena;
+  Uploader up;
+  Tables t;          // device pointers (kernel argument)
+  void *dmem = nullptr;
+  int *d_won = nullptr;
+  char *d_scratch = nullptr;   // 64 B element scratch for get/set
+  char *h_scratch = nullptr;   // pinned
+  std::mutex mu;
+};
+
+namespace {
+
+inline uint64_t bucket_elems(const gg_array *a, uint32_t b) { return uint64_t(a->fb) << b; }
+inline uint64_t bucket_bytes(const gg_array *a, uint32_t b) {
+  return round16(bucket_elems(a, b) * a->esz);
+}
+inline void host_locate(const gg_array *a, uint64_t i, uint32_t &b, uint64_t &off) {
+  uint64_t q = (i >> a->log2fb) + 1;
+  b = (uint32_t)ilog2(q);
+  off = i - (((uint64_t(1) << b) - 1) << a->log2fb);
+}
+inline uint32_t min_buckets_for(const gg_array *a, uint64_t n) {
+  if (n == 0) return 0;
+  uint64_t t = (n + a->fb - 1) / a->fb;
+  return (uint32_t)ilog2(t) + 1;
+}
+inline cudaStream_t S_(void *s) { return (cudaStream_t)s; }
+
+int grid_for(const gg_array *a, uint64_t tiles, int per_sm = 8) {
+  uint64_t g = (uint64_t)sm_count(a->dev) * per_sm;
+  if (tiles < g) g = tiles;
+  return (int)std::max<uint64_t>(g, 1);
+}
+
+Tables tables_for_launch(gg_array *a, bool with_ctl) {
+  Tables t = a->t;
+  if (!with_ctl) t.ctl = nullptr;
+  t.arena = (char *)a->arena.base;
+  t.arena_mapped = a->arena.mapped;
+  return t;
+}
+
+// Plan of one allocating operation, computed on the host before launch.
+struct Plan {
+  std::vector<uint64_t> size, cap, flags, fl_count;
+  uint64_t top, alloc_calls;
+  std::vector<uint32_t> ctl;        // per shard
+  std::vector<int32_t> status;      // per shard
+  std::vector<uint32_t> zero_pairs; // (s, b) buckets to zero after allocation
+  bool any_fail = false, any_ctl = false;
+};
+
+void plan_init(const gg_array *a, Plan &p) {
+  p.size = a->size; p.cap = a->cap; p.flags = a->flags; p.fl_count = a->fl_count;
+  p.top = a->top; p.alloc_calls = a->alloc_calls;
+  p.ctl.assign(a->S, kCtlWrite | a->MB);
+  p.status.assign(a->S, GG_OK);
+}
+
+// Try to allocate bucket b of shard s in the plan; false on (hook/arena) failure.
+bool plan_alloc(gg_array *a, Plan &p, uint32_t s, uint32_t b) {
+  if (a->hook && a->hook(a->hook_ctx, s, b, bucket_elems(a, b)) != 0) return false;
+  uint64_t nb = bucket_bytes(a, b);
+  uint64_t cap_bytes = a->arena.va;
+  if (a->limit && a->limit < cap_bytes) cap_bytes = a->limit;
+  if (p.fl_count[b] > 0) {
+    p.fl_count[b] -= 1;                      // device pops the class free list
+  } else {
+    if (p.top + nb > cap_bytes) return false;
+    p.top += nb;
+  }
+  p.flags[s] |= uint64_t(1) << b;
+  p.cap[s] += bucket_elems(a, b);
+  p.alloc_calls += 1;
+  if (a->dirty[s]) { p.zero_pairs.push_back(s); p.zero_pairs.push_back(b); }
+  return true;
+}
+
+// Plan an append of counts[s] at starts (explicit) or at size[s] (reserve).
+void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *starts) {
+  for (uint32_t s = 0; s < a->S; ++s) {
+    uint64_t c = counts[s];
+    if (c == 0) continue;
+    uint64_t start = starts ? starts[s] : p.size[s];
+    if (!starts) p.size[s] += c;
+    uint32_t b0, b1; uint64_t o;
+    host_locate(a, start, b0, o);
+    host_locate(a, start + c - 1, b1, o);
+    if (b1 >= a->MB) {                       // bucket_vector.py:208-211
+      p.status[s] = GG_ECAPACITY;
+      p.ctl[s] = 0;                          // reserve only: no allocation, no write
+      p.any_fail = p.any_ctl = true;
+      continue;
+    }
+    for (uint32_t b = b0; b <= b1; ++b) {
+      if (p.flags[s] >> b & 1) continue;
+      if (!plan_alloc(a, p, s, b)) {         // bucket_vector.py:194-201
+        p.status[s] = GG_ENOMEM;
+        p.ctl[s] = b | kCtlZero;             // keep buckets < b; zero the reserved range
+        p.any_fail = p.any_ctl = true;
+        break;
+      }
+    }
+  }
+}
+
+int commit_plan(gg_array *a, Plan &p) {
+  int rc = a->arena.ensure(p.top);
+  if (rc) return rc;
+  a->size = p.size; a->cap = p.cap; a->flags = p.flags; a->fl_count = p.fl_count;
+  a->top = p.top; a->alloc_calls = p.alloc_calls;
+  for (uint32_t s = 0; s < a->S; ++s)
+    if (p.status[s] != GG_OK) a->dirty[s] = 1;
+  return GG_OK;
+}
+
+template <int W>
+int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
+                cudaStream_t st) {
+  if (total == 0) return GG_OK;
+  const uint64_t tile = kTileBytes / a->esz;
+  int grid = grid_for(a, (total + tile - 1) / tile);
+  switch (a->esz) {
+    case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_walk<4, W, uint32_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+// run an allocating append: upload ctl/zero list if needed, reserve, zero, copy
+int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src,
+               uint64_t total, cudaStream_t st) {
+  int rc = commit_plan(a, p);
+  if (rc) return rc;
+  Tables t = tables_for_launch(a, p.any_ctl);
+  if (p.any_ctl) {
+    void *dst[1] = {a->t.ctl};
+    const void *srcs[1] = {p.ctl.data()};
+    size_t bytes[1] = {a->S * sizeof(uint32_t)};
+    if ((rc = a->up.upload(st, 1, dst, srcs, bytes))) return rc;
+  }
+  { k_reserve<<<(a->S + 255) / 256, 256, 0, st>>>(t, reserve_mode); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  if (!p.zero_pairs.empty()) {
+    uint32_t *d_pairs = nullptr;
+    CUDA_TRY(cudaMallocAsync((void **)&d_pairs, p.zero_pairs.size() * 4, st));
+    CUDA_TRY(cudaMemcpyAsync(d_pairs, p.zero_pairs.data(), p.zero_pairs.size() * 4,
+                             cudaMemcpyHostToDevice, st));
+    uint32_t np = (uint32_t)(p.zero_pairs.size() / 2);
+    { k_zero_buckets<<<std::min<uint32_t>(np, 1024), kThreads, 0, st>>>(t, d_pairs, np); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(d_pairs, st));
+    CUDA_TRY(cudaStreamSynchronize(st));  // zero_pairs host memory is pageable
+  }
+  if (walk == W_INSERT) return launch_walk<W_INSERT>(a, t, src, nullptr, total, st);
+  return launch_walk<W_DUP>(a, t, nullptr, nullptr, total, st);
+}
+
+int finish_status(gg_array *a, const Plan &p, int32_t *h_status) {
+  if (h_status)
+    for (uint32_t s = 0; s < a->S; ++s) h_status[s] = p.status[s];
+  if (!p.any_fail) return GG_OK;
+  return fail(GG_EPARTIAL, "insert failed on some shards; commit withheld");
+}
+
+template <typename T>
+int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode, uint64_t total,
+              cudaStream_t st) {
+  const uint64_t tile = kTileBytes / sizeof(T);
+  if (mode == GG_RW_GLOBAL) {
+    int grid = sm_count(a->dev) * 8;
+    size_t smem = (a->S + 1) <= 4096 ? (a->S + 1) * sizeof(uint64_t) : 0;
+    for (uint32_t p = 0; p < passes; ++p)
+      { k_rw_global<T><<<grid, kThreads, smem, st>>>(t, total, addend); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  } else {
+    int grid = grid_for(a, (total + tile - 1) / tile);
+    if (mode == GG_RW_FUSED)
+      { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, 0, st>>>(t, nullptr, nullptr, total, addend, passes); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    else
+      for (uint32_t p = 0; p < passes; ++p)
+        { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, 0, st>>>(t, nullptr, nullptr, total, addend, 1); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+template <typename T>
+int launch_flat_add(char *buf, uint64_t n, T a, uint32_t passes, int fused, int dev,
+                    cudaStream_t st) {
+  if (n == 0) return GG_OK;
+  const uint64_t ch = kTileBytes / sizeof(T);
+  uint64_t nch = (n + ch - 1) / ch;
+  int grid = (int)std::min<uint64_t>(nch, (uint64_t)sm_count(dev) * 8);
+  if (fused) { k_flat_add<T><<<grid, kThreads, 0, st>>>(buf, n, a, passes); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  else
+    for (uint32_t p = 0; p < passes; ++p) { k_flat_add<T><<<grid, kThreads, 0, st>>>(buf, n, a, 1); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+#define DISPATCH_DTYPE(dt, T, ...)                                          \
+  switch (dt) {                                                             \
+    case GG_I8: { typedef int8_t T; __VA_ARGS__; break; }                   \
+    case GG_U8: { typedef uint8_t T; __VA_ARGS__; break; }                  \
+    case GG_I16: { typedef int16_t T; __VA_ARGS__; break; }                 \
+    case GG_U16: { typedef uint16_t T; __VA_ARGS__; break; }                \
+    case GG_I32: { typedef int32_t T; __VA_ARGS__; break; }                 \
+    case GG_U32: { typedef uint32_t T; __VA_ARGS__; break; }                \
+    case GG_I64: { typedef long long T; __VA_ARGS__; break; }               \
+    case GG_U64: { typedef unsigned long long T; __VA_ARGS__; break; }      \
+    case GG_F16: { typedef __half T; __VA_ARGS__; break; }                  \
+    case GG_F32: { typedef float T; __VA_ARGS__; break; }                   \
+    case GG_F64: { typedef double T; __VA_ARGS__; break; }                  \
+    default: return fail(GG_EVALUE, "bad dtype");                           \
+  }
+
+// the committed range of every shard must lie in published buckets
+// (bucket_vector.py:279-295 raises RuntimeError otherwise)
+int check_committed_published(const gg_array *a) {
+  for (uint32_t s = 0; s < a->S; ++s) {
+    uint64_t n = a->prefix[s + 1] - a->prefix[s];
+    uint32_t k = min_buckets_for(a, n);
+    if (k == 0) continue;
+    uint64_t need = (k >= 64) ? ~uint64_t(0) : ((uint64_t(1) << k) - 1);
+    if ((a->flags[s] & need) != need)
+      return fail(GG_EUNPUBLISHED, "bucket unpublished while walking shard " + std::to_string(s));
+  }
+  return GG_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char *gg_last_error(void) { return g_err.c_str(); }
+int gg_version(void) { return GG_VERSION; }
+uint64_t gg_kernel_launches(void) { return g_launches.load(); }
+
+int gg_device_sms(int device, int32_t *h_sms) {
+  *h_sms = sm_count(device);
+  return GG_OK;
+}
+
+int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t max_buckets,
+              uint64_t arena_va_bytes, gg_array **out) {
+  *out = nullptr;
+  if (shards < 1) return fail(GG_EVALUE, "shards must be >= 1");
+  if (fb < 1 || (fb & (fb - 1))) return fail(GG_EVALUE, "first_bucket_size must be a power of two");
+  if (max_buckets < 1 || max_buckets > kMaxBuckets) return fail(GG_EVALUE, "max_buckets must be in [1, 64]");
+  uint32_t esz = elem_bytes_of(dtype);
+  if (!esz) return fail(GG_EVALUE, "unsupported dtype");
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaFree(0));
+  gg_array *a = new gg_array();
+  a->dev = device; a->S = shards; a->fb = fb; a->log2fb = ilog2(fb); a->dtype = dtype;
+  a->esz = esz; a->MB = max_buckets;
+  a->size.assign(shards, 0); a->cap.assign(shards, 0); a->ops.assign(shards, 0);
+  a->prefix.assign(shards + 1, 0); a->flags.assign(shards, 0); a->dirty.assign(shards, 0);
+  a->fl_count.assign(max_buckets, 0);
+  if (arena_va_bytes == 0) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    arena_va_bytes = tot ? tot : (uint64_t(1) << 36);
+  }
+  int rc = a->arena.init(device, arena_va_bytes);
+  if (rc) { delete a; return rc; }
+  // metadata block
+  const size_t S = shards, T = S * max_buckets;
+  size_t bytes = 0;
+  auto take = [&](size_t n) { size_t o = bytes; bytes += (n + 255) & ~size_t(255); return o; };
+  size_t o_size = take(S * 8), o_cap = take(S * 8), o_ops = take(S * 8), o_start = take(S * 8),
+         o_count = take(S * 8), o_prefix = take((S + 1) * 8), o_off = take((S + 1) * 8),
+         o_ctl = take(S * 4), o_flag = take(T * 4), o_status = take(S * 4), o_ptr = take(T * 8),
+         o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_fl = take(T * 8),
+         o_fln = take(max_buckets * 4);
+  cudaError_t e = cudaMalloc(&a->dmem, bytes);
+  if (e != cudaSuccess) { a->arena.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
+  cudaMemset(a->dmem, 0, bytes);
+  char *base = (char *)a->dmem;
+  Tables &t = a->t;
+  t.size = (uint64_t *)(base + o_size); t.cap = (uint64_t *)(base + o_cap);
+  t.ops = (uint64_t *)(base + o_ops); t.start = (uint64_t *)(base + o_start);
+  t.count = (uint64_t *)(base + o_count); t.prefix = (uint64_t *)(base + o_prefix);
+  t.offsets = (uint64_t *)(base + o_off); t.ctl = (uint32_t *)(base + o_ctl);
+  t.flag = (uint32_t *)(base + o_flag); t.status = (uint32_t *)(base + o_status);
+  t.ptr = (char **)(base + o_ptr); t.misc = (unsigned long long *)(base + o_misc);
+  t.fl = (uint64_t *)(base + o_fl); t.fl_n = (int *)(base + o_fln);
+  t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
+  a->d_won = (int *)(base + o_won);
+  a->d_scratch = base + o_scr;
+  if ((rc = a->up.init(std::max<size_t>(4 * (S + 1) * 8, 4096)))) { gg_destroy(a); return rc; }
+  e = cudaMallocHost(&a->h_scratch, 64);
+  if (e != cudaSuccess) { gg_destroy(a); return fail(GG_ECUDA, cudaGetErrorString(e)); }
+  CUDA_TRY(cudaDeviceSynchronize());
+  *out = a;
+  return GG_OK;
+}
+
+int gg_destroy(gg_array *a) {
+  if (!a) return GG_OK;
+  cudaSetDevice(a->dev);
+  cudaDeviceSynchronize();
+  a->up.destroy();
+  if (a->h_scratch) cudaFreeHost(a->h_scratch);
+  if (a->dmem) cudaFree(a->dmem);
+  a->arena.destroy();
+  delete a;
+  return GG_OK;
+}
+
+int gg_set_alloc_hook(gg_array *a, gg_alloc_hook hook, void *ctx) {
+  a->hook = hook; a->hook_ctx = ctx;
+  return GG_OK;
+}
+
+int gg_set_arena_limit(gg_array *a, uint64_t bytes) {
+  a->limit = bytes;
+  return GG_OK;
+}
+
+int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+              const uint64_t *h_starts, int32_t *h_status, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  if (h_offsets[0] != 0) return fail(GG_EVALUE, "offsets[0] must be 0");
+  std::vector<uint64_t> counts(a->S);
+  for (uint32_t s = 0; s < a->S; ++s) {
+    if (h_offsets[s + 1] < h_offsets[s]) return fail(GG_EVALUE, "offsets must be non-decreasing");
+    counts[s] = h_offsets[s + 1] - h_offsets[s];
+  }
+  const uint64_t total = h_offsets[a->S];
+  Plan p;
+  plan_init(a, p);
+  plan_append(a, p, counts.data(), h_starts);
+  // upload directory (+ explicit starts / counts)
+  int rc;
+  if (h_starts) {
+    std::vector<uint64_t> st0(a->S, 0);
+    for (uint32_t s = 0; s < a->S; ++s) st0[s] = counts[s] ? h_starts[s] : 0;
+    void *dst[3] = {a->t.offsets, a->t.start, a->t.count};
+    const void *src[3] = {h_offsets, st0.data(), counts.data()};
+    size_t bytes[3] = {(a->S + 1) * 8, a->S * 8, a->S * 8};
+    if ((rc = a->up.upload(st, 3, dst, src, bytes))) return rc;
+  } else {
+    void *dst[1] = {a->t.offsets};
+    const void *src[1] = {h_offsets};
+    size_t bytes[1] = {(a->S + 1) * 8};
+    if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
+  }
+  if ((rc = run_append(a, p, h_starts ? 2 : 0, W_INSERT, (const char *)d_values, total, st))) return rc;
+  if (!h_starts)
+    for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
+  return finish_status(a, p, h_status);
+}
+
+int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  int rc = check_committed_published(a);
+  if (rc) return rc;
+  std::vector<uint64_t> counts(a->S);
+  for (uint32_t s = 0; s < a->S; ++s) counts[s] = a->prefix[s + 1] - a->prefix[s];
+  Plan p;
+  plan_init(a, p);
+  plan_append(a, p, counts.data(), nullptr);
+  if ((rc = run_append(a, p, 1, W_DUP, nullptr, a->prefix[a->S], S_(stream)))) return rc;
+  for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
+  return finish_status(a, p, h_status);
+}
+
+int gg_commit(gg_array *a, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  uint64_t acc = 0;
+  a->prefix[0] = 0;
+  for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
+  { k_commit<<<1, 1024, 0, S_(stream)>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_shard, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  if (h_failed_shard) *h_failed_shard = -1;
+  Plan p;
+  plan_init(a, p);
+  std::vector<uint32_t> lim(a->S, 0);
+  int err = GG_OK;
+  bool any = false;
+  for (uint32_t s = 0; s < a->S && err == GG_OK; ++s) {
+    uint32_t k = min_buckets_for(a, h_min_capacity[s]);
+    if (k > a->MB) {                                    // bucket_vector.py:252-255
+      err = fail(GG_ECAPACITY, "capacity needs more buckets than the table holds");
+      if (h_failed_shard) *h_failed_shard = s;
+      break;
+    }
+    for (uint32_t b = 0; b < k; ++b) {
+      if (p.flags[s] >> b & 1) continue;
+      if (!plan_alloc(a, p, s, b)) {
+        err = fail(GG_ENOMEM, "bucket allocation failed");
+        if (h_failed_shard) *h_failed_shard = s;
+        break;
+      }
+      lim[s] = b + 1;
+      any = true;
+    }
+  }
+  if (any) {
+    int rc = commit_plan(a, p);
+    if (rc) return rc;
+    void *dst[1] = {a->t.ctl};
+    const void *src[1] = {lim.data()};
+    size_t bytes[1] = {a->S * 4};
+    if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
+    Tables t = tables_for_launch(a, true);
+    { k_grow<<<(a->S + 255) / 256, 256, 0, st>>>(t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    CUDA_TRY(cudaGetLastError());
+    if (!p.zero_pairs.empty()) {
+      // grow on a dirty shard: zero the new buckets (reference buckets are np.zeros)
+      uint32_t *d_pairs = nullptr;
+      CUDA_TRY(cudaMallocAsync((void **)&d_pairs, p.zero_pairs.size() * 4, st));
+      CUDA_TRY(cudaMemcpyAsync(d_pairs, p.zero_pairs.data(), p.zero_pairs.size() * 4,
+                               cudaMemcpyHostToDevice, st));
+      uint32_t np = (uint32_t)(p.zero_pairs.size() / 2);
+      { k_zero_buckets<<<std::min<uint32_t>(np, 1024), kThreads, 0, st>>>(t, d_pairs, np); g_launches.fetch_add(1, std::memory_order_relaxed); }
+      CUDA_TRY(cudaFreeAsync(d_pairs, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+    }
+  }
+  return err;
+}
+
+int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  *h_won = 0;
+  if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
+  if (b >= a->MB) return fail(GG_ECAPACITY, "bucket outside the table");
+  if (a->flags[s] >> b & 1) return GG_OK;
+  Plan p;
+  plan_init(a, p);
+  if (!plan_alloc(a, p, s, b)) return fail(GG_ENOMEM, "bucket allocation failed");
+  int rc = commit_plan(a, p);
+  if (rc) return rc;
+  Tables t = tables_for_launch(a, false);
+  { k_new_bucket<<<1, 1, 0, st>>>(t, s, b, a->d_won); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  if (!p.zero_pairs.empty()) {
+    uint32_t pair[2] = {s, b};
+    uint32_t *d_pairs = (uint32_t *)a->d_scratch;
+    CUDA_TRY(cudaMemcpyAsync(d_pairs, pair, 8, cudaMemcpyHostToDevice, st));
+    { k_zero_buckets<<<1, kThreads, 0, st>>>(t, d_pairs, 1); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  }
+  int won = 0;
+  CUDA_TRY(cudaMemcpyAsync(a->h_scratch, a->d_won, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(&won, a->h_scratch, sizeof(int));
+  *h_won = won > 0;
+  return GG_OK;
+}
+
+int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
+  *h_prev = a->size[s];
+  a->size[s] += c;
+  a->ops[s] += 1;
+  { k_fetch_add<<<1, 1, 0, S_(stream)>>>(a->t, s, c); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  for (uint32_t s = 0; s < a->S; ++s)
+    if (h_new_sizes[s] > a->size[s]) return fail(GG_EVALUE, "shrink cannot grow a shard");
+  for (uint32_t s = 0; s < a->S; ++s) {
+    uint32_t keep = min_buckets_for(a, h_new_sizes[s]);
+    for (uint32_t b = keep; b < a->MB; ++b)
+      if (a->flags[s] >> b & 1) {
+        a->flags[s] &= ~(uint64_t(1) << b);
+        a->cap[s] -= bucket_elems(a, b);
+        a->fl_count[b] += 1;
+      }
+    a->size[s] = h_new_sizes[s];
+  }
+  void *dst[1] = {a->t.count};
+  const void *src[1] = {h_new_sizes};
+  size_t bytes[1] = {a->S * 8};
+  int rc = a->up.upload(st, 1, dst, src, bytes);
+  if (rc) return rc;
+  Tables t = tables_for_launch(a, false);
+  { k_shrink_release<<<1, 64, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  { k_shrink_sizes<<<(a->S + 255) / 256, 256, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  uint64_t acc = 0;
+  for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
+  { k_commit<<<1, 1024, 0, st>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
+                    const uint64_t *h_lane_offsets, uint64_t values_per_lane,
+                    int32_t *h_status, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  if (h_lane_offsets[0] != 0) return fail(GG_EVALUE, "lane offsets must start at 0");
+  for (uint32_t s = 0; s < a->S; ++s)
+    if (h_lane_offsets[s + 1] < h_lane_offsets[s]) return fail(GG_EVALUE, "lane offsets must be non-decreasing");
+  if (values_per_lane == 0 || values_per_lane > 0xffffffffu) return fail(GG_EVALUE, "bad values_per_lane");
+  void *dst[1] = {a->t.offsets};
+  const void *src[1] = {h_lane_offsets};
+  size_t bytes[1] = {(a->S + 1) * 8};
+  int rc = a->up.upload(st, 1, dst, src, bytes);
+  if (rc) return rc;
+  // pass 1: per-shard totals -> host (one sync per launch, not per insert)
+  { k_lanes_count<<<a->S, 1024, 0, st>>>(a->t, d_counts); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  std::vector<uint64_t> counts(a->S);
+  CUDA_TRY(cudaMemcpyAsync(counts.data(), a->t.count, a->S * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (uint32_t s = 0; s < a->S; ++s)
+    if (counts[s] > (h_lane_offsets[s + 1] - h_lane_offsets[s]) * values_per_lane)
+      return fail(GG_EVALUE, "a lane count exceeds values_per_lane");
+  Plan p;
+  plan_init(a, p);
+  plan_append(a, p, counts.data(), nullptr);
+  if ((rc = commit_plan(a, p))) return rc;
+  Tables t = tables_for_launch(a, p.any_ctl);
+  if (p.any_ctl) {
+    void *d2[1] = {a->t.ctl};
+    const void *s2[1] = {p.ctl.data()};
+    size_t b2[1] = {a->S * sizeof(uint32_t)};
+    if ((rc = a->up.upload(st, 1, d2, s2, b2))) return rc;
+  }
+  if (!p.zero_pairs.empty()) return fail(GG_EVALUE, "lane insert into a shard with failed reservations");
+  switch (a->esz) {
+    case 1: { k_lanes_insert<1><<<a->S, 1024, 0, st>>>(t, (const char *)d_values, d_counts, (uint32_t)values_per_lane); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_lanes_insert<2><<<a->S, 1024, 0, st>>>(t, (const char *)d_values, d_counts, (uint32_t)values_per_lane); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_lanes_insert<4><<<a->S, 1024, 0, st>>>(t, (const char *)d_values, d_counts, (uint32_t)values_per_lane); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_lanes_insert<8><<<a->S, 1024, 0, st>>>(t, (const char *)d_values, d_counts, (uint32_t)values_per_lane); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
+  return finish_status(a, p, h_status);
+}
+
+int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  int rc = check_committed_published(a);
+  if (rc) return rc;
+  const uint64_t total = a->prefix[a->S];
+  if (total == 0 || passes == 0) return GG_OK;
+  Tables t = tables_for_launch(a, false);
+  DISPATCH_DTYPE(a->dtype, T, {
+    T v; memcpy(&v, h_addend, sizeof(T));
+    rc = launch_rw<T>(a, t, v, passes, mode, total, S_(stream));
+  });
+  return rc;
+}
+
+int gg_flatten(gg_array *a, void *d_out, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  int rc = check_committed_published(a);
+  if (rc) return rc;
+  Tables t = tables_for_launch(a, false);
+  return launch_walk<W_FLATTEN>(a, t, nullptr, (char *)d_out, a->prefix[a->S], S_(stream));
+}
+
+int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  if (n == 0) return GG_OK;
+  Tables t = tables_for_launch(a, false);
+  int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
+  switch (a->esz) {
+    case 1: { k_gather<1><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_gather<2><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_gather<4><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_gather<8><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  if (n == 0) return GG_OK;
+  Tables t = tables_for_launch(a, false);
+  int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
+  switch (a->esz) {
+    case 1: { k_gather<1><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_gather<2><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_gather<4><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_gather<8><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+namespace {
+int elem_addr(gg_array *a, uint32_t s, uint64_t i, char **out, cudaStream_t st) {
+  if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
+  if (i >= a->size[s]) return fail(GG_EINDEX, "index outside size");
+  uint32_t b; uint64_t o;
+  host_locate(a, i, b, o);
+  if (b >= a->MB || !(a->flags[s] >> b & 1))
+    return fail(GG_EUNPUBLISHED, "index is reserved but its bucket is unpublished");
+  char *p = nullptr;
+  CUDA_TRY(cudaMemcpyAsync(a->h_scratch, a->t.ptr + (size_t)s * a->MB + b, sizeof(char *),
+                           cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(&p, a->h_scratch, sizeof(char *));
+  *out = p + o * a->esz;
+  return GG_OK;
+}
+}  // namespace
+
+int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  char *p;
+  int rc = elem_addr(a, s, i, &p, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(a->h_scratch, p, a->esz, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(h_out, a->h_scratch, a->esz);
+  return GG_OK;
+}
+
+int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  char *p;
+  int rc = elem_addr(a, s, i, &p, st);
+  if (rc) return rc;
+  memcpy(a->h_scratch, h_val, a->esz);
+  CUDA_TRY(cudaMemcpyAsync(p, a->h_scratch, a->esz, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return GG_OK;
+}
+
+int gg_info(gg_array *a, uint32_t *o) {
+  o[0] = a->S; o[1] = a->fb; o[2] = a->dtype; o[3] = a->MB;
+  return GG_OK;
+}
+
+int gg_host_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint64_t *pre,
+                  uint64_t *ops) {
+  std::lock_guard<std::mutex> g(a->mu);
+  const size_t S = a->S;
+  if (sz) memcpy(sz, a->size.data(), S * 8);
+  if (cp) memcpy(cp, a->cap.data(), S * 8);
+  if (fl) memcpy(fl, a->flags.data(), S * 8);
+  if (pre) memcpy(pre, a->prefix.data(), (S + 1) * 8);
+  if (ops) memcpy(ops, a->ops.data(), S * 8);
+  return GG_OK;
+}
+
+int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint64_t *pre,
+                    uint64_t *ops, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  cudaStream_t st = S_(stream);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const size_t S = a->S;
+  if (sz) CUDA_TRY(cudaMemcpy(sz, a->t.size, S * 8, cudaMemcpyDeviceToHost));
+  if (cp) CUDA_TRY(cudaMemcpy(cp, a->t.cap, S * 8, cudaMemcpyDeviceToHost));
+  if (pre) CUDA_TRY(cudaMemcpy(pre, a->t.prefix, (S + 1) * 8, cudaMemcpyDeviceToHost));
+  if (ops) CUDA_TRY(cudaMemcpy(ops, a->t.ops, S * 8, cudaMemcpyDeviceToHost));
+  if (fl) {
+    std::vector<uint32_t> f(S * a->MB);
+    CUDA_TRY(cudaMemcpy(f.data(), a->t.flag, f.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t s = 0; s < S; ++s) {
+      uint64_t m = 0;
+      for (uint32_t b = 0; b < a->MB; ++b)
+        if (f[s * a->MB + b] == kFlagPublished) m |= uint64_t(1) << b;
+      fl[s] = m;
+    }
+  }
+  return GG_OK;
+}
+
+int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaSetDevice(a->dev);
+  CUDA_TRY(cudaStreamSynchronize(S_(stream)));
+  CUDA_TRY(cudaMemcpy(h_ptrs, a->t.ptr, (size_t)a->S * a->MB * 8, cudaMemcpyDeviceToHost));
+  return GG_OK;
+}
+
+int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
+  (void)stream;
+  std::lock_guard<std::mutex> g(a->mu);
+  uint64_t cap = 0, need = 0;
+  for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
+  o[0] = cap * a->esz; o[1] = a->arena.mapped; o[2] = a->top; o[3] = need * a->esz;
+  uint64_t fl = 0;
+  for (uint32_t b = 0; b < a->MB; ++b) fl += a->fl_count[b] * bucket_bytes(a, b);
+  o[4] = a->alloc_calls; o[5] = fl;
+  return GG_OK;
+}
+
+// ---------------------------------------------------------------- baselines
+int gg_flat_insert(void *d_buf, uint64_t capacity, uint64_t *d_counter, const void *d_vals,
+                   uint64_t n, uint32_t esz, int32_t algo, void *stream) {
+  if (n == 0) return GG_OK;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t st = S_(stream);
+  if (algo == GG_ALGO_BATCH) {
+    // contiguous append at the host-known counter value is done by the caller
+    // with gg_buf_copy; here: device-side single reservation + copy
+    return fail(GG_EVALUE, "BATCH algo is host-side (reserve + gg_buf_copy)");
+  }
+  int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(dev) * 16);
+  switch (esz) {
+    case 1: { k_flat_insert<1><<<grid, 256, 0, st>>>((char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, algo); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_flat_insert<2><<<grid, 256, 0, st>>>((char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, algo); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_flat_insert<4><<<grid, 256, 0, st>>>((char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, algo); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_flat_insert<8><<<grid, 256, 0, st>>>((char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, algo); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    default: return fail(GG_EVALUE, "bad element size");
+  }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_flat_add(void *d_buf, uint64_t n, uint32_t dtype, const void *h_addend, uint32_t passes,
+                int32_t fused, void *stream) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int rc = GG_OK;
+  DISPATCH_DTYPE(dtype, T, {
+    T v; memcpy(&v, h_addend, sizeof(T));
+    rc = launch_flat_add<T>((char *)d_buf, n, v, passes, fused, dev, S_(stream));
+  });
+  return rc;
+}
+
+int gg_buf_alloc(uint64_t bytes, void *stream, void **d_out) {
+  CUDA_TRY(cudaMallocAsync(d_out, bytes ? bytes : 16, S_(stream)));
+  return GG_OK;
+}
+int gg_buf_free(void *d_ptr, void *stream) {
+  CUDA_TRY(cudaFreeAsync(d_ptr, S_(stream)));
+  return GG_OK;
+}
+int gg_buf_copy(void *d_dst, const void *d_src, uint64_t bytes, void *stream) {
+  if (!bytes) return GG_OK;
+  CUDA_TRY(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDeviceToDevice, S_(stream)));
+  return GG_OK;
+}
+
+}  // extern "C"
+
+struct gg_vmm {
+  Arena arena;
+};
+
+extern "C" {
+int gg_vmm_create(int device, uint64_t va_bytes, gg_vmm **out) {
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaFree(0));
+  gg_vmm *v = new gg_vmm();
+  int rc = v->arena.init(device, va_bytes);
+  if (rc) { delete v; return rc; }
+  *out = v;
+  return GG_OK;
+}
+int gg_vmm_ensure(gg_vmm *v, uint64_t bytes) { return v->arena.ensure(bytes); }
+int gg_vmm_info(gg_vmm *v, uint64_t *b, uint64_t *m, uint64_t *g) {
+  *b = (uint64_t)v->arena.base; *m = v->arena.mapped; *g = v->arena.gran;
+  return GG_OK;
+}
+int gg_vmm_destroy(gg_vmm *v) {
+  if (!v) return GG_OK;
+  cudaDeviceSynchronize();
+  v->arena.destroy();
+  delete v;
+  return GG_OK;
+}
+}  // extern "C"

@@ -1,0 +1,174 @@
+"""Parity of the B200 drop-in against the reference-generated goldens and the CPU
+oracle.  Every state compared here is read back from DEVICE memory
+(``_parity_state`` asserts the host mirror agrees with it)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import scenarios
+from oracle import ggoracle as O
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+
+
+@pytest.fixture(scope="module")
+def gg():
+    import paper_2209_00103_b200 as gg
+    return gg
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN["ggarray"]))
+def test_golden_scenario_bit_exact(gg, name):
+    case = GOLDEN["ggarray"][name]
+    got = scenarios.run_scenario(gg, case["ops"])
+    for k, (g, want) in enumerate(zip(got, case["states"])):
+        assert g == want, f"{name} step {k} ({case['ops'][k]})"
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN["baselines"]))
+def test_golden_baselines(gg, name):
+    case = GOLDEN["baselines"][name]
+    got = scenarios.run_baseline_scenario(gg, case["ops"])
+    for k, (g, want) in enumerate(zip(got, case["states"])):
+        assert g == want, f"{name} step {k}"
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_scenarios_vs_oracle(gg, seed):
+    ops = scenarios._random_scenario(500 + seed)
+    assert scenarios.run_scenario(gg, ops) == scenarios.run_scenario(O, ops)
+
+
+@pytest.mark.parametrize("mode", ["per_shard", "global", "fused"])
+@pytest.mark.parametrize("dtype", ["int32", "int64", "float32", "float64", "int8", "uint16", "float16"])
+def test_rw_modes_agree_with_oracle(gg, mode, dtype):
+    rng = np.random.default_rng(3)
+    S, fb = 37, 4
+    sizes = rng.integers(0, 3000, S)
+    sizes[::5] = 0
+    vals = (np.arange(sizes.sum()) % 1000).astype(dtype)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    batches = [vals[off[s]:off[s + 1]] for s in range(S)]
+    a = gg.GrowableArray(S, fb, dtype=dtype)
+    o = O.OracleGGArray(S, fb, dtype=dtype)
+    a.insert_parallel(batches)
+    o.insert_parallel(batches)
+    a.rw_add(3, passes=5, mode=mode)
+    o.rw_add(3, passes=5)
+    assert a.flatten().tobytes() == o.flatten().tobytes()
+
+
+def test_get_many_set_many(gg):
+    a = gg.GrowableArray.from_flat(np.arange(100000, dtype=np.int64), shards=13, first_bucket_size=8)
+    idx = np.random.default_rng(0).integers(0, 100000, 5000)
+    assert np.array_equal(a.get_many(idx).cpu().numpy(), idx)
+    a.set_many(idx, -idx)
+    flat = a.flatten()
+    ref = np.arange(100000)
+    ref[idx] = -idx
+    assert np.array_equal(flat, ref)
+    with pytest.raises(IndexError):
+        a.get_many([100000])
+
+
+def test_lanes_insert_matches_compaction(gg):
+    import torch
+    rng = np.random.default_rng(11)
+    S, K = 19, 3
+    lanes = rng.integers(0, 4000, S)
+    lo = np.concatenate([[0], np.cumsum(lanes)]).astype(np.uint64)
+    L = int(lo[-1])
+    counts = rng.integers(0, K + 1, L).astype(np.int32)
+    vals = np.arange(L * K, dtype=np.int32)
+    a = gg.GrowableArray(S, 32, dtype=np.int32)
+    a.insert_parallel([np.arange(int(x), dtype=np.int32) for x in rng.integers(0, 50, S)])
+    before = [a.shards[s].to_numpy() for s in range(S)]
+    a.insert_lanes(torch.from_numpy(vals).cuda(), counts, lo, values_per_lane=K)
+    for s in range(S):
+        exp = [before[s]]
+        for j in range(int(lo[s]), int(lo[s + 1])):
+            exp.append(vals[j * K: j * K + counts[j]])
+        assert np.array_equal(a.shards[s].to_numpy(), np.concatenate(exp)), s
+    st = a._parity_state()
+    assert st["sizes"] == [len(b) + int(counts[int(lo[s]):int(lo[s + 1])].sum()) for s, b in enumerate(before)]
+
+
+def test_predicated_push_back_one_value_per_lane(gg):
+    # the paper's Alg. 1: each thread pushes its element iff its predicate holds
+    S = 8
+    n = 1 << 16
+    vals = np.arange(n, dtype=np.int32)
+    keep = (vals % 3 == 0).astype(np.int32)
+    lo = np.linspace(0, n, S + 1).astype(np.uint64)
+    a = gg.GrowableArray(S, 32, dtype=np.int32)
+    a.insert_lanes(vals, keep, lo)
+    exp = np.concatenate([vals[int(lo[s]):int(lo[s + 1])][keep[int(lo[s]):int(lo[s + 1])] == 1]
+                          for s in range(S)])
+    assert np.array_equal(a.flatten(), exp)
+
+
+def test_shrink_matches_oracle_model(gg):
+    rng = np.random.default_rng(5)
+    S, fb = 16, 4
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    o = O.OracleGGArray(S, fb, dtype=np.int32)
+    tag = 0
+    for _ in range(12):
+        if rng.random() < 0.5 or not a.committed_size:
+            sizes = rng.integers(0, 400, S)
+            batches = [np.arange(tag + 1000 * s, tag + 1000 * s + k, dtype=np.int32) for s, k in enumerate(sizes)]
+            tag += 7
+            a.insert_parallel(batches)
+            o.insert_parallel(batches)
+        else:
+            cur = np.asarray(o.size)
+            new = (cur * rng.random(S)).astype(np.int64)
+            a.shrink(new)
+            o.shrink(new)
+        assert a._parity_state() == {k: v for k, v in o._parity_state().items() if k != "alloc_calls"}
+        assert a.flatten().tobytes() == o.flatten().tobytes()
+    ms = a.memory_stats()
+    assert ms["capacity_bytes"] == int(o.capacity.sum()) * 4
+
+
+def test_flatten_device_and_views(gg):
+    import torch
+    a = gg.GrowableArray.from_flat(np.arange(5000, dtype=np.float32), shards=3, first_bucket_size=2)
+    f = a.flatten_device()
+    assert f.is_cuda and f.dtype == torch.float32
+    assert torch.equal(f.cpu(), torch.arange(5000, dtype=torch.float32))
+    # for_each_shard hands out writable device views
+    a.for_each_shard(lambda v: v.add_(1))
+    assert np.array_equal(a.flatten(), np.arange(5000, dtype=np.float32) + 1)
+    segs = list(a.shards[1].iter_segments(11, start=3))
+    assert torch.equal(torch.cat(segs).cpu(), torch.arange(1667 + 3, 1667 + 11, dtype=torch.float32) + 1)
+
+
+def test_scan_reserver_rendezvous_on_device_counter(gg):
+    # reference test_bucket_vector.py:228-239: 6 lanes, groups of 4 -> 2 counter ops
+    import threading
+    sv = gg.ShardVector(first_bucket_size=4, dtype=np.int64)
+    reserver = gg.ScanReserver(6, group_size=4)
+    batches = [10_000 * t + np.arange(50 * (t % 3)) for t in range(6)]
+    ops0 = sv.size_counter.op_count
+    ths = [threading.Thread(target=sv.push_back_batch, args=(b, reserver)) for b in batches]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert sv.size_counter.op_count - ops0 == 2
+    assert np.array_equal(np.sort(sv.to_numpy()), np.sort(np.concatenate(batches)))
+
+
+def test_memory_footprint_config1(gg):
+    a = gg.GrowableArray(512, 32, dtype=np.int32)
+    a.insert_parallel(gg.split_batches(np.arange(1 << 20, dtype=np.int32), 512))
+    ms = a.memory_stats()
+    assert ms["capacity_bytes"] == 2_080_768 * 4                 # SURVEY 8c golden
+    assert ms["arena_top_bytes"] == ms["capacity_bytes"]          # zero padding in the arena
+    assert ms["capacity_bytes"] == gg.ggarray_capacity_for(1 << 20, 512, 32, 4)

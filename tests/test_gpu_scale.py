@@ -1,0 +1,116 @@
+"""Full-size parity through size-independent properties (BASELINE configs 1-3):
+closed-form sizes / capacities (memory_model.py:152-166) and closed-form
+contents of the doubling schedule, checked on the device; the oracle checks
+the same schedule bit for bit at reduced size."""
+import numpy as np
+import pytest
+
+from oracle import ggoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gg():
+    import paper_2209_00103_b200 as gg
+    return gg
+
+
+def _expected_schedule_state(S, fb, n0, rounds):
+    per = n0 // S
+    k = O.min_buckets_for(per << rounds, fb)
+    return per << rounds, O.capacity_of(k, fb)
+
+
+def test_config2_reduced_bit_exact_vs_oracle(gg):
+    """2^16 -> 2^22 doubling rounds, S=512: grow(2n), duplicate, +1 -- every round."""
+    S, fb = 512, 32
+    init = np.arange(1 << 16, dtype=np.int32)
+    a = gg.GrowableArray.from_flat(init, S, fb)
+    o = O.OracleGGArray.from_flat(init, S, fb)
+    for r in range(6):
+        n = a.committed_size
+        a.grow(2 * n); o.grow(2 * n)
+        a.insert_duplicate(); o.insert_duplicate()
+        a.rw_add(1); o.rw_add(1)
+        st = a._parity_state()
+        assert st["sizes"] == [int(x) for x in o.size]
+        assert st["caps"] == [int(x) for x in o.capacity]
+        assert st["prefix"] == [int(x) for x in o.prefix]
+    assert a.flatten().tobytes() == o.flatten().tobytes()
+
+
+def test_config2_full_2p30_closed_form(gg):
+    """The BASELINE config-2 schedule at full size: 2^20 -> 2^30 int32, S=512."""
+    import torch
+    S, fb, n0, rounds = 512, 32, 1 << 20, 10
+    a = gg.GrowableArray.from_flat(torch.arange(n0, dtype=torch.int32, device="cuda"), S, fb)
+    for r in range(rounds):
+        n = a.committed_size
+        a.grow(2 * n)
+        a.insert_duplicate()
+        a.rw_add(1)
+        per, cap = _expected_schedule_state(S, fb, n0, r + 1)
+        st = a.device_state()
+        assert np.all(st["sizes"] == per) and np.all(st["caps"] == cap), r
+        ms = a.memory_stats()
+        assert ms["capacity_bytes"] == int(O.sharded_capacity_elements([n0 << (r + 1)], S, fb)[0]) * 4
+        assert ms["arena_top_bytes"] == ms["capacity_bytes"]
+    assert a.committed_size == 1 << 30
+    ms = a.memory_stats()
+    assert ms["capacity_bytes"] == 2_147_467_264 * 4
+    assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"]            # paper's <= 2x claim, mapped
+    flat = a.flatten_device()
+    per = (n0 // S) << rounds
+    g = torch.arange(1 << 30, dtype=torch.int64, device="cuda")
+    exp = ((g // per) * (n0 // S) + (g % (n0 // S)) + rounds).to(torch.int32)
+    del g
+    assert torch.equal(flat, exp)
+
+
+def test_config1_full_vs_reference_hash(gg, golden):
+    """Config 1 (512 LFVectors, 2^20 int32 insert, +1 pass, flatten) against the
+    hash recorded from the reference."""
+    import hashlib
+    a = gg.GrowableArray(512, 32, dtype=np.int32)
+    a.insert_parallel(gg.split_batches(np.arange(1 << 20, dtype=np.int32), 512))
+    a.rw_add(1)
+    want = golden["ggarray"]["config1_2p20"]["states"][-1]["flat"]
+    assert "sha256:" + hashlib.sha256(a.flatten().tobytes()).hexdigest() == want
+
+
+def test_ragged_csr_insert_large_misaligned(gg):
+    """Random ragged batches (odd sizes -> unaligned source/destination) at 2^22."""
+    import torch
+    rng = np.random.default_rng(9)
+    S, fb = 333, 32
+    counts = rng.integers(0, 25000, S)
+    counts[rng.random(S) < 0.1] = 0
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    vals = rng.integers(-2**31, 2**31 - 1, int(off[-1]), dtype=np.int64).astype(np.int32)
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    o = O.OracleGGArray(S, fb, dtype=np.int32)
+    pre = [np.arange(int(k), dtype=np.int32) for k in rng.integers(0, 77, S)]
+    a.insert_parallel(pre); o.insert_parallel(pre)
+    a.insert_csr(torch.from_numpy(vals).cuda(), off)
+    o.insert_parallel([vals[off[s]:off[s + 1]] for s in range(S)])
+    a.insert_duplicate(); o.insert_duplicate()
+    assert a.flatten().tobytes() == o.flatten().tobytes()
+    assert a._parity_state()["caps"] == [int(x) for x in o.capacity]
+
+
+@pytest.mark.parametrize("dtype", ["int8", "int16", "int64", "float64"])
+def test_element_sizes_misaligned_paths(gg, dtype):
+    rng = np.random.default_rng(1)
+    S, fb = 7, 1
+    counts = rng.integers(0, 5000, S)
+    vals = (rng.integers(0, 100, int(counts.sum()))).astype(dtype)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    batches = [vals[off[s]:off[s + 1]] for s in range(S)]
+    a = gg.GrowableArray(S, fb, dtype=dtype)
+    o = O.OracleGGArray(S, fb, dtype=dtype)
+    for _ in range(3):
+        a.insert_parallel(batches); o.insert_parallel(batches)
+        a.insert_duplicate(); o.insert_duplicate()
+        a.rw_add(1, mode="global"); o.rw_add(1)
+    assert a.flatten().tobytes() == o.flatten().tobytes()
