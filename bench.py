@@ -19,7 +19,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 
@@ -44,46 +43,55 @@ def _peaks():
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Polls NVML (SM clock + throttle reasons) every 5 ms on a thread while the
+    timed region runs; falls back to nothing if NVML is unavailable."""
 
-    def __init__(self, index: int):
-        self.index, self.proc, self.path = index, None, f"/tmp/gg_clocks_{os.getpid()}.csv"
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period, self.rows, self._stop = index, period_s, [], None
 
     def __enter__(self):
+        import threading
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
-                stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self._N, self._h = N, N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._N = None
+            return self
+        self._stop = threading.Event()
+
+        def poll():
+            N, h = self._N, self._h
+            while not self._stop.is_set():
+                try:
+                    self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
+                                      N.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(self.period)
+        self._t = threading.Thread(target=poll, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait()
-            self.fh.close()
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join()
 
     def summary(self) -> dict:
-        rows = []
-        try:
-            for line in open(self.path):
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) >= 7 and parts[0].isdigit():
-                    rows.append(parts)
-        except OSError:
-            pass
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = sorted(int(r[0]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None),
+                    "reasons": ["unsampled"], "samples": 0}
+        N = self._N
+        bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({k for _, m in self.rows for k, bit in bits.items() if m & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml (5 ms poll during the timed region)"}
 
 
 # --------------------------------------------------------------------------- device legs
@@ -152,7 +160,9 @@ def run_device(args, rank, world, local_rank):
         t0, t1 = _events(torch)
         torch.cuda.synchronize()
         t0.record()
+        h0 = time.perf_counter()
         evs = [step.run(True) for _ in range(args.steps)]
+        host_ms = (time.perf_counter() - h0) * 1e3
         t1.record()
         torch.cuda.synchronize()
     launches = _lib.lib.gg_kernel_launches() - launches0
@@ -200,6 +210,7 @@ def run_device(args, rank, world, local_rank):
                       "capacity_over_needed": round(mem["capacity_over_needed"], 6),
                       "mapped_over_needed": round(mem["mapped_over_needed"], 6)},
         "clocks": sampler.summary(),
+        "host_enqueue_ms_per_step": round(host_ms / args.steps, 4),
     }
     if not args.quick:
         out.update(secondary(args, gg, torch, device, step, hbm))

@@ -194,6 +194,63 @@ __device__ int alloc_bucket(const Tables &t, uint32_t s, uint32_t b) {
   return 1;
 }
 
+// Host-planned allocation of class-b buckets for every lane with `need`
+// (each (shard, bucket) is requested by exactly one lane, so the once-flags
+// are uncontended): ONE free-list pop and at most ONE bump of the arena top per
+// warp and class -- the paper's "one atomic per group" applied to the
+// allocator.  Slots are handed out in lane rank order.
+__device__ __forceinline__ void warp_alloc_class(const Tables &t, bool need, uint32_t s,
+                                                 uint32_t b) {
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (!m) return;
+  const uint32_t lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  const uint32_t cnt = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
+  const uint64_t elems = 1ull << (t.log2fb + b);
+  const uint64_t bytes = (elems * t.esz + 15) & ~15ull;
+  int k = 0;
+  uint32_t npop = 0;
+  unsigned long long bump = 0;
+  if (lane == leader) {
+    k = atomicSub(&t.fl_n[b], (int)cnt);             // entries [k-cnt, k) are ours if >= 0
+    npop = k > 0 ? min((uint32_t)k, cnt) : 0u;
+    if (npop < cnt) {
+      atomicAdd(&t.fl_n[b], (int)(cnt - npop));       // return the overdraft
+      bump = atomicAdd(&t.misc[MISC_TOP], (unsigned long long)((cnt - npop) * bytes));
+    }
+    atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)cnt);
+  }
+  k = __shfl_sync(0xffffffffu, k, leader);
+  npop = __shfl_sync(0xffffffffu, npop, leader);
+  bump = __shfl_sync(0xffffffffu, bump, leader);
+  if (!need) return;
+  const unsigned long long off =
+      rank < npop ? t.fl[(size_t)b * t.S + (k - 1 - rank)] : bump + (rank - npop) * bytes;
+  if (off + bytes > t.arena_mapped) {                 // cannot happen for planned ops
+    atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+    return;
+  }
+  t.ptr[(size_t)s * t.MB + b] = t.arena + off;
+  atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
+  __threadfence();
+  st_release(t.flag + (size_t)s * t.MB + b, kFlagPublished);
+}
+
+// allocate buckets [lo, hi) of shard s that are not yet published, warp-wide
+// loop over classes (lanes without work pass lo = hi)
+__device__ __forceinline__ void warp_alloc_range(const Tables &t, uint32_t s, uint32_t lo,
+                                                 uint32_t hi) {
+  uint32_t wlo = lo, whi = hi;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) {
+    wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, d));
+    whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, d));
+  }
+  for (uint32_t b = wlo; b < whi; ++b) {
+    bool need = b >= lo && b < hi && t.flag[(size_t)s * t.MB + b] != kFlagPublished;
+    warp_alloc_class(t, need, s, b);
+  }
+}
+
 // Reservation + bucket allocation, one thread per shard: one atomicAdd on the
 // shard's size per batch (bucket_vector.py:229 via insert_index.py:118-122),
 // then allocate every missing bucket of the reserved range
@@ -201,40 +258,44 @@ __device__ int alloc_bucket(const Tables &t, uint32_t s, uint32_t b) {
 //   mode 0: CSR offsets (insert); mode 1: committed lengths (duplicate);
 //   mode 2: explicit starts + counts already in t.start/t.count (fetch_add'ed)
 __global__ void k_reserve(Tables t, int mode) {
-  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= t.S) return;
-  uint64_t c, start;
-  if (mode == 0) c = t.offsets[s + 1] - t.offsets[s];
-  else if (mode == 1) c = t.prefix[s + 1] - t.prefix[s];
-  else c = t.count[s];
-  const uint32_t ctl = t.ctl ? t.ctl[s] : (kCtlWrite | t.MB);
-  if (mode != 2) {
-    t.count[s] = c;
-    if (c == 0) return;
-    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
-    t.ops[s] += 1;
-    t.start[s] = start;
-  } else {
-    if (c == 0) return;
-    start = t.start[s];
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = s < t.S;
+  uint64_t c = 0, start = 0;
+  uint32_t lo = 0, hi = 0;
+  if (live) {
+    if (mode == 0) c = t.offsets[s + 1] - t.offsets[s];
+    else if (mode == 1) c = t.prefix[s + 1] - t.prefix[s];
+    else c = t.count[s];
+    const uint32_t ctl = t.ctl ? t.ctl[s] : (kCtlWrite | t.MB);
+    if (mode != 2) {
+      t.count[s] = c;
+      if (c) {
+        start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+        t.ops[s] += 1;
+        t.start[s] = start;
+      }
+    } else {
+      start = t.start[s];
+    }
+    if (c) {
+      uint32_t b0, b1;
+      uint64_t o;
+      locate(start, t.log2fb, b0, o);
+      locate(start + c - 1, t.log2fb, b1, o);
+      lo = b0;
+      hi = min(ctl & kCtlLimitMask, b1 + 1);
+      if (hi < lo) hi = lo;
+    }
   }
-  uint32_t b0, b1;
-  uint64_t o;
-  locate(start, t.log2fb, b0, o);
-  locate(start + c - 1, t.log2fb, b1, o);
-  uint32_t lim = ctl & kCtlLimitMask;
-  if (lim > b1 + 1) lim = b1 + 1;
-  for (uint32_t b = b0; b < lim; ++b)
-    if (alloc_bucket(t, s, b) < 0) atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+  warp_alloc_range(t, live ? s : 0, lo, hi);
 }
 
 // grow: thread per shard, allocate buckets [0, lim[s]) (ctl carries lim)
 __global__ void k_grow(Tables t) {
-  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= t.S) return;
-  uint32_t lim = t.ctl[s] & kCtlLimitMask;
-  for (uint32_t b = 0; b < lim; ++b)
-    if (alloc_bucket(t, s, b) < 0) atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = s < t.S;
+  const uint32_t lim = live ? (t.ctl[s] & kCtlLimitMask) : 0u;
+  warp_alloc_range(t, live ? s : 0, 0, lim);
 }
 
 __global__ void k_new_bucket(Tables t, uint32_t s, uint32_t b, int *won) {
@@ -379,26 +440,34 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
   }
 }
 
-// shrink (extension): thread per bucket class b walks shards in order and
-// releases bucket b of every shard whose new size needs fewer than b+1
-// buckets onto the class free list (deterministic list order).
-__global__ void k_shrink_release(Tables t, const uint64_t *new_sizes) {
-  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= t.MB) return;
+// shrink (extension): block per bucket class b; a block scan over the shards
+// gives every released bucket its free-list slot in shard order
+// (deterministic), so the whole release is one parallel pass.
+__global__ void __launch_bounds__(1024) k_shrink_release(Tables t, const uint64_t *new_sizes) {
+  __shared__ uint64_t ws[32];
+  const uint32_t b = blockIdx.x;
   const uint64_t fbv = 1ull << t.log2fb;
-  int n = t.fl_n[b];
-  for (uint32_t s = 0; s < t.S; ++s) {
-    uint64_t ns = new_sizes[s];
-    uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + fbv - 1) >> t.log2fb))) : 0u;
-    uint32_t *f = t.flag + (size_t)s * t.MB + b;
-    if (b >= keep && *f == kFlagPublished) {
-      t.fl[(size_t)b * t.S + n++] = (uint64_t)(t.ptr[(size_t)s * t.MB + b] - t.arena);
+  uint64_t base = (uint64_t)t.fl_n[b];
+  for (uint32_t s0 = 0; s0 < t.S; s0 += blockDim.x) {
+    const uint32_t s = s0 + threadIdx.x;
+    bool rel = false;
+    if (s < t.S) {
+      const uint64_t ns = new_sizes[s];
+      const uint32_t keep =
+          ns ? (64u - (uint32_t)__clzll((long long)((ns + fbv - 1) >> t.log2fb))) : 0u;
+      rel = b >= keep && t.flag[(size_t)s * t.MB + b] == kFlagPublished;
+    }
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan(rel ? 1 : 0, &tot, ws);
+    if (rel) {
+      t.fl[(size_t)b * t.S + base + ex] = (uint64_t)(t.ptr[(size_t)s * t.MB + b] - t.arena);
       t.ptr[(size_t)s * t.MB + b] = nullptr;
-      *f = 0;
+      t.flag[(size_t)s * t.MB + b] = 0;
       atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)(0ull - (fbv << b)));
     }
+    base += tot;
   }
-  t.fl_n[b] = n;
+  if (threadIdx.x == 0) t.fl_n[b] = (int)base;
 }
 
 __global__ void k_shrink_sizes(Tables t, const uint64_t *new_sizes) {
@@ -573,16 +642,29 @@ __device__ __forceinline__ uint32_t upper_shard(const uint64_t *dir, uint32_t S,
   return lo;
 }
 
+constexpr uint32_t kSmemDir = 4096;   // directories up to 4096 shards are cached in smem
+constexpr int kUnroll = 8;
+
+// load dir[0..S] into smem when it fits (one pass per CTA of a persistent grid)
+__device__ __forceinline__ const uint64_t *stage_dir(const uint64_t *gdir, uint32_t S,
+                                                     uint64_t *sdir) {
+  if (S + 1 > kSmemDir) return gdir;
+  for (uint32_t i = threadIdx.x; i <= S; i += blockDim.x) sdir[i] = gdir[i];
+  __syncthreads();
+  return sdir;
+}
+
 template <int ESZ, int W, typename T>
 __global__ void __launch_bounds__(kThreads) k_walk(Tables t, const char *flat_src, char *flat_dst,
-                                                   uint64_t total, T addend, uint32_t reps) {
-  constexpr uint64_t TILE = kTileBytes / ESZ;
-  const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
-  const uint64_t ntiles = (total + TILE - 1) / TILE;
+                                                   uint64_t total, T addend, uint32_t reps,
+                                                   uint32_t tile) {
+  extern __shared__ uint64_t sdir[];
+  const uint64_t *dir = stage_dir((W == W_INSERT) ? t.offsets : t.prefix, t.S, sdir);
+  const uint64_t ntiles = (total + tile - 1) / tile;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint64_t g = tile * TILE;
-    const uint64_t gend = min(total, g + TILE);
+  for (uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    uint64_t g = ti * tile;
+    const uint64_t gend = min(total, g + tile);
     uint32_t s = upper_shard(dir, t.S, g);
     while (g < gend) {
       uint64_t shard_end = dir[s + 1];
@@ -616,40 +698,52 @@ __global__ void __launch_bounds__(kThreads) k_walk(Tables t, const char *flat_sr
         dp = t.ptr[(size_t)s * t.MB + b] + o * ESZ;
       }
       if constexpr (W == W_RW) {
-        cta_add<T, 4>(dp, len, addend, reps, tid, nt);
+        cta_add<T, kUnroll>(dp, len, addend, reps, tid, nt);
       } else if (dst_ok && (ctl & (kCtlWrite | kCtlZero))) {
-        cta_copy<ESZ, 4>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
+        cta_copy<ESZ, kUnroll>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
       }
       g += len;
     }
   }
 }
 
-// rw_g: one thread per element resolved through the directory
-// (bench_cli.py:339-366, paper's rw_g): warp-uniform bisect on the smem
-// prefix, per-lane fix-up, clz locate.
+// rw_g (bench_cli.py:339-366, the paper's rw_g): every group of 16 B of
+// consecutive GLOBAL indices is resolved through the directory -- a
+// warp-uniform bisect on the smem prefix, a per-lane fix-up and a clz locate --
+// then updated with one vector access when the group stays inside one
+// aligned bucket run (else element by element).
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total, T addend) {
-  extern __shared__ uint64_t sp[];
-  const bool in_smem = (t.S + 1) <= 4096;
-  const uint64_t *pre = t.prefix;
-  if (in_smem) {
-    for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) sp[i] = t.prefix[i];
-    __syncthreads();
-    pre = sp;
-  }
+  extern __shared__ uint64_t sdir[];
+  const uint64_t *pre = stage_dir(t.prefix, t.S, sdir);
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uint64_t nvec = (total + VE - 1) / VE;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (uint64_t base = wid * 32; base < total; base += nwarps * 32) {
-    uint32_t s = upper_shard(pre, t.S, base);  // warp-uniform key: smem broadcast
-    const uint64_t g = base + lane;
-    if (g < total) {
-      while (pre[s + 1] <= g) ++s;               // lanes past a shard boundary
-      uint32_t b; uint64_t o;
-      locate(g - pre[s], t.log2fb, b, o);
-      T *p = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
-      *p = AddOp<T>::apply(*p, addend);
+  for (uint64_t vbase = wid * 32; vbase < nvec; vbase += nwarps * 32) {
+    uint32_t s = upper_shard(pre, t.S, vbase * VE);       // warp-uniform key
+    const uint64_t v = vbase + lane;
+    if (v >= nvec) continue;
+    const uint64_t g = v * VE;
+    while (pre[s + 1] <= g) ++s;
+    uint32_t b; uint64_t o;
+    locate(g - pre[s], t.log2fb, b, o);
+    T *p = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
+    if (g + VE <= pre[s + 1] && (o % VE) == 0 && o + VE <= (1ull << (t.log2fb + b))) {
+      union { uint4 q; T e[VE]; } u;
+      u.q = ldg_rw((const uint4 *)p);
+#pragma unroll
+      for (uint32_t j = 0; j < VE; ++j) u.e[j] = AddOp<T>::apply(u.e[j], addend);
+      stg((uint4 *)p, u.q);
+    } else {
+      for (uint32_t j = 0; j < VE && g + j < total; ++j) {
+        const uint64_t gj = g + j;
+        while (pre[s + 1] <= gj) ++s;
+        locate(gj - pre[s], t.log2fb, b, o);
+        T *q = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
+        *q = AddOp<T>::apply(*q, addend);
+      }
     }
   }
 }
@@ -722,7 +816,7 @@ __global__ void __launch_bounds__(kThreads) k_flat_add(char *buf, uint64_t n, T 
   const uint64_t nch = (n + CH - 1) / CH;
   for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     uint64_t lo = c * CH, len = min(n - lo, CH);
-    cta_add<T, 4>(buf + lo * sizeof(T), len, a, reps, threadIdx.x, blockDim.x);
+    cta_add<T, kUnroll>(buf + lo * sizeof(T), len, a, reps, threadIdx.x, blockDim.x);
   }
 }
 
@@ -981,17 +1075,29 @@ int commit_plan(gg_array *a, Plan &p) {
   return GG_OK;
 }
 
+// tile of a streaming launch: 32 KiB, shrunk (down to 4 KiB) until the grid
+// has ~8 CTAs per SM, so small rounds still spread over every SM
+uint32_t tile_elems(const gg_array *a, uint64_t total) {
+  uint64_t bytes = total * a->esz;
+  uint64_t want = (uint64_t)sm_count(a->dev) * 8;
+  uint64_t tb = kTileBytes;
+  while (tb > 4096 && bytes / tb < want) tb >>= 1;
+  return (uint32_t)(tb / a->esz);
+}
+size_t dir_smem(const gg_array *a) { return (a->S + 1) <= kSmemDir ? (a->S + 1) * 8 : 0; }
+
 template <int W>
 int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
                 cudaStream_t st) {
   if (total == 0) return GG_OK;
-  const uint64_t tile = kTileBytes / a->esz;
+  const uint32_t tile = tile_elems(a, total);
   int grid = grid_for(a, (total + tile - 1) / tile);
+  const size_t sm = dir_smem(a);
   switch (a->esz) {
-    case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_walk<4, W, uint32_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, 0, st>>>(t, src, dst, total, 0, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_walk<4, W, uint32_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
   }
   CUDA_TRY(cudaGetLastError());
   return GG_OK;
@@ -1036,19 +1142,20 @@ int finish_status(gg_array *a, const Plan &p, int32_t *h_status) {
 template <typename T>
 int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode, uint64_t total,
               cudaStream_t st) {
-  const uint64_t tile = kTileBytes / sizeof(T);
+  const size_t sm = dir_smem(a);
   if (mode == GG_RW_GLOBAL) {
-    int grid = sm_count(a->dev) * 8;
-    size_t smem = (a->S + 1) <= 4096 ? (a->S + 1) * sizeof(uint64_t) : 0;
+    const uint64_t nvec = (total * sizeof(T) + 15) / 16;
+    int grid = (int)std::min<uint64_t>((nvec + kThreads - 1) / kThreads, (uint64_t)sm_count(a->dev) * 8);
     for (uint32_t p = 0; p < passes; ++p)
-      { k_rw_global<T><<<grid, kThreads, smem, st>>>(t, total, addend); g_launches.fetch_add(1, std::memory_order_relaxed); }
+      { k_rw_global<T><<<grid, kThreads, sm, st>>>(t, total, addend); g_launches.fetch_add(1, std::memory_order_relaxed); }
   } else {
+    const uint32_t tile = tile_elems(a, total);
     int grid = grid_for(a, (total + tile - 1) / tile);
     if (mode == GG_RW_FUSED)
-      { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, 0, st>>>(t, nullptr, nullptr, total, addend, passes); g_launches.fetch_add(1, std::memory_order_relaxed); }
+      { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, passes, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
     else
       for (uint32_t p = 0; p < passes; ++p)
-        { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, 0, st>>>(t, nullptr, nullptr, total, addend, 1); g_launches.fetch_add(1, std::memory_order_relaxed); }
+        { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, 1, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
   }
   CUDA_TRY(cudaGetLastError());
   return GG_OK;
@@ -1368,7 +1475,7 @@ int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
   int rc = a->up.upload(st, 1, dst, src, bytes);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
-  { k_shrink_release<<<1, 64, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  { k_shrink_release<<<a->MB, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
   { k_shrink_sizes<<<(a->S + 255) / 256, 256, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
   CUDA_TRY(cudaGetLastError());
   uint64_t acc = 0;
