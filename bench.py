@@ -33,6 +33,23 @@ UNIT = "Gelem/s"
 WORKLOAD = "config2: GGArray-512 doubling 2^20->2^30 int32 (grow + duplicate-insert per round)"
 
 
+def _ncu_traffic():
+    """dram read+write bytes of the dominant kernel's largest launch, from the
+    newest committed ncu summary (profiles/rNN_ncu_summary.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    for f in reversed(files):
+        try:
+            for e in json.load(open(f))["full_capture"]:
+                if "W_DUP" in e.get("label", ""):
+                    return {"bytes_per_launch": e["traffic_bytes"], "algorithmic_bytes": e["algorithmic_bytes"],
+                            "ratio": e["traffic_over_algorithmic"], "source": os.path.relpath(f, ROOT),
+                            "launch": "last doubling round, 2^29 elements"}
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -152,6 +169,26 @@ def run_device(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step.run(False)
     torch.cuda.synchronize()
+    # eager, host-driven steps with per-phase events (phases, dominant kernel)
+    e0, e1 = _events(torch)
+    e0.record()
+    h0 = time.perf_counter()
+    evs = [step.run(True) for _ in range(args.steps)]
+    host_ms = (time.perf_counter() - h0) * 1e3
+    e1.record()
+    torch.cuda.synchronize()
+    eager_ms = e0.elapsed_time(e1)
+    for ev in evs:
+        step.collect(ev)
+    # the same step captured once in a CUDA graph (host planning done at capture;
+    # every kernel of the step runs on each replay)
+    graph = torch.cuda.CUDAGraph()
+    with step.arr.capture_mode():
+        with torch.cuda.graph(graph):
+            step.run(False)
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
     if dist:
         dist.barrier()
     launches0 = _lib.lib.gg_kernel_launches()
@@ -160,15 +197,15 @@ def run_device(args, rank, world, local_rank):
         t0, t1 = _events(torch)
         torch.cuda.synchronize()
         t0.record()
-        h0 = time.perf_counter()
-        evs = [step.run(True) for _ in range(args.steps)]
-        host_ms = (time.perf_counter() - h0) * 1e3
+        for _ in range(args.steps):
+            graph.replay()
         t1.record()
         torch.cuda.synchronize()
-    launches = _lib.lib.gg_kernel_launches() - launches0
+    # graph replays do not pass through the launch counter: count the kernels
+    # the captured step launches (same as one eager step) per replay
+    launches = launches_per_step(step) * args.steps
     ms = t0.elapsed_time(t1)
-    for ev in evs:
-        step.collect(ev)
+    check_state(step, torch)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -178,9 +215,11 @@ def run_device(args, rank, world, local_rank):
         dist.all_gather(sizes, torch.tensor([step.arr.committed_size], device=device))
     inserted_per_step = 1 << 30                        # 2^20 initial + sum of duplicates
     value = world * inserted_per_step * args.steps / (ms * 1e-3) / 1e9
+    eager_value = world * inserted_per_step * args.steps / (eager_ms * 1e-3) / 1e9
 
     a = step.arr
     assert a.committed_size == 1 << 30
+    traffic = _ncu_traffic()
     mem = a.memory_stats()
     dup_bytes = 8 * step.dup_elems                     # read 4 + write 4 per element
     dup_ms = sum(step.dup_ms)
@@ -197,12 +236,18 @@ def run_device(args, rank, world, local_rank):
                    "parallelism": f"lfvector-sharded x{world}",
                    "l2": "inputs larger than L2 (4 GiB live, 8 GiB capacity per GPU)"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "k_walk<4,W_DUP> (duplicate insert)",
+        "roofline": {"bound": "hbm", "kernel": "k_walk<4,W_DUP> (duplicate insert, all 10 rounds)",
                      "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "peak_kind": peaks_kind,
-                     "traffic": None, "algorithmic_bytes_per_elem": 8,
-                     "last_round_2p29_gbs": round(float(last_gbs), 1)},
+                     "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "traffic_detail": traffic, "algorithmic_bytes_per_elem": 8,
+                     "achieved_def": "sum of 8 B x elements duplicated / sum of CUDA-event times of the "
+                                     "insert phases (reserve + walk + commit) over the K eager steps",
+                     "last_round_2p29_gbs": round(float(last_gbs), 1),
+                     "last_round_frac": round(float(last_gbs) / hbm, 4)},
         "phases": {"insert_ms_per_step": round(dup_ms / args.steps, 4),
+                   "insert_ms_by_round": [round(float(np.mean(step.dup_ms[r::ROUNDS])), 4)
+                                          for r in range(ROUNDS)],
                    "grow_ms_per_step": round(sum(step.grow_ms) / args.steps, 4),
                    "insert_only_gelem_s": round(step.dup_elems / (dup_ms * 1e-3) / 1e9, 2)},
         "footprint": {"needed_bytes": mem["needed_bytes"], "capacity_bytes": mem["capacity_bytes"],
@@ -210,7 +255,10 @@ def run_device(args, rank, world, local_rank):
                       "capacity_over_needed": round(mem["capacity_over_needed"], 6),
                       "mapped_over_needed": round(mem["mapped_over_needed"], 6)},
         "clocks": sampler.summary(),
-        "host_enqueue_ms_per_step": round(host_ms / args.steps, 4),
+        "timing": "value: K replays of the step captured once as a CUDA graph; "
+                  "eager: the same K steps issued op by op from Python",
+        "eager": {"value": round(eager_value, 3), "ms_per_step": round(eager_ms / args.steps, 4),
+                  "host_enqueue_ms_per_step": round(host_ms / args.steps, 4)},
     }
     if not args.quick:
         out.update(secondary(args, gg, torch, device, step, hbm))
@@ -218,6 +266,30 @@ def run_device(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args)
     return out
+
+
+def launches_per_step(step) -> int:
+    from paper_2209_00103_b200 import _lib
+    import torch
+    c0 = _lib.lib.gg_kernel_launches()
+    step.run(False)
+    torch.cuda.synchronize()
+    return int(_lib.lib.gg_kernel_launches() - c0)
+
+
+def check_state(step, torch) -> None:
+    """After the replays: device state == host mirror, and the contents equal
+    the closed form of the schedule (element g = (g // 2^21) * 2048 + g % 2048)."""
+    a = step.arr
+    dev, host = a.device_state(), a._host()
+    for k in ("sizes", "caps", "flags", "prefix"):      # ops counts replays: not a fixed point
+        assert np.array_equal(dev[k], host[k]), f"device/host mismatch in {k} after replays"
+    assert int(dev["prefix"][-1]) == 1 << 30
+    idx = torch.randint(0, 1 << 30, (1 << 16,), device="cuda", dtype=torch.int64)
+    got = a.get_many(idx).to(torch.int64)
+    per = (N0 // S) << ROUNDS
+    exp = (idx // per) * (N0 // S) + idx % (N0 // S)
+    assert torch.equal(got, exp), "schedule contents differ from the closed form"
 
 
 def _time(torch, fn, reps=1):

@@ -130,6 +130,21 @@ int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals
 int gg_get(gg_array *a, uint32_t shard, uint64_t i, void *h_out, void *stream);
 int gg_set(gg_array *a, uint32_t shard, uint64_t i, const void *h_val, void *stream);
 
+/* CUDA-graph capture support: while on != 0, per-op host->device uploads use
+ * pinned buffers owned by the captured graph (released by
+ * gg_capture_release) and no call synchronises, so a stream capture of any
+ * op sequence is legal.  A captured sequence that starts and ends in the same
+ * state (e.g. reset + inserts) may be replayed; the host mirrors keep the
+ * state after the captured sequence. */
+int gg_capture_mode(gg_array *a, int32_t on);
+int gg_capture_release(gg_array *a);
+/* Tuning of the 4-byte streaming kernels (for sweeps): cache policy ls
+ * (0 .cg, 1 .nc, 2 default, 3 .cs), unroll (4|8), tile bytes, CTA threads
+ * (256|512); -1 / 0 keep the built-in defaults.  Process-wide. */
+int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads);
+/* committed size, total (reserved) size, total capacity -- host mirrors */
+int gg_summary(gg_array *a, uint64_t *h_out3);
+
 /* Host views of the state (mirrors kept exact by the planner). */
 int gg_info(gg_array *a, uint32_t *h_out4 /* shards, fb, dtype, max_buckets */);
 int gg_host_state(gg_array *a, uint64_t *h_sizes, uint64_t *h_caps, uint64_t *h_flags,

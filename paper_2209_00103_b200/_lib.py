@@ -64,6 +64,10 @@ _SIGS = {
     "gg_get": ([P, U32, U64, P, P], C.c_int),
     "gg_set": ([P, U32, U64, P, P], C.c_int),
     "gg_info": ([P, PU32], C.c_int),
+    "gg_capture_mode": ([P, I32], C.c_int),
+    "gg_set_tuning": ([I32, I32, U32, U32], C.c_int),
+    "gg_capture_release": ([P], C.c_int),
+    "gg_summary": ([P, PU64], C.c_int),
     "gg_host_state": ([P, PU64, PU64, PU64, PU64, PU64], C.c_int),
     "gg_device_state": ([P, PU64, PU64, PU64, PU64, PU64, P], C.c_int),
     "gg_bucket_ptrs": ([P, PU64, P], C.c_int),
@@ -115,6 +119,10 @@ def ptr(a: np.ndarray, ctype=U64):
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
-def stream_handle(device) -> int:
+def stream_handle(device_index: int) -> int:
+    """Raw cudaStream_t of torch's current stream on ``device_index``."""
     import torch
-    return torch.cuda.current_stream(device).cuda_stream
+    try:
+        return torch._C._cuda_getCurrentRawStream(device_index)
+    except AttributeError:  # older torch
+        return torch.cuda.current_stream(device_index).cuda_stream

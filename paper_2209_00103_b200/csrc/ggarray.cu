@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -128,6 +129,7 @@ struct Tables {
   uint64_t *size, *cap, *ops, *start, *count, *prefix, *offsets;
   uint32_t *ctl, *flag, *status;
   char **ptr;
+  unsigned long long *pmask;  // [S] published-bucket bitmask per shard
   uint64_t *fl;            // [MB*S] per-class free lists of arena offsets (shrink)
   int *fl_n;               // [MB] entries per class
   unsigned long long *misc;
@@ -191,6 +193,7 @@ __device__ int alloc_bucket(const Tables &t, uint32_t s, uint32_t b) {
   atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
   __threadfence();
   st_release(f, kFlagPublished);
+  atomicOr(&t.pmask[s], 1ull << b);
   return 1;
 }
 
@@ -233,21 +236,26 @@ __device__ __forceinline__ void warp_alloc_class(const Tables &t, bool need, uin
   atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
   __threadfence();
   st_release(t.flag + (size_t)s * t.MB + b, kFlagPublished);
+  atomicOr(&t.pmask[s], 1ull << b);
 }
 
 // allocate buckets [lo, hi) of shard s that are not yet published, warp-wide
 // loop over classes (lanes without work pass lo = hi)
 __device__ __forceinline__ void warp_alloc_range(const Tables &t, uint32_t s, uint32_t lo,
                                                  uint32_t hi) {
-  uint32_t wlo = lo, whi = hi;
-#pragma unroll
-  for (int d = 16; d; d >>= 1) {
-    wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, d));
-    whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, d));
+  // classes this lane needs = [lo, hi) minus the published ones (one mask load)
+  unsigned long long want = 0;
+  if (hi > lo) {
+    want = (hi >= 64 ? ~0ull : ((1ull << hi) - 1ull)) & ~((1ull << lo) - 1ull);
+    want &= ~t.pmask[s];
   }
-  for (uint32_t b = wlo; b < whi; ++b) {
-    bool need = b >= lo && b < hi && t.flag[(size_t)s * t.MB + b] != kFlagPublished;
-    warp_alloc_class(t, need, s, b);
+  unsigned long long any = want;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, d);
+  while (any) {
+    const uint32_t b = __ffsll((long long)any) - 1;
+    any &= any - 1;
+    warp_alloc_class(t, (want >> b) & 1ull, s, b);
   }
 }
 
@@ -290,11 +298,12 @@ __global__ void k_reserve(Tables t, int mode) {
   warp_alloc_range(t, live ? s : 0, lo, hi);
 }
 
-// grow: thread per shard, allocate buckets [0, lim[s]) (ctl carries lim)
-__global__ void k_grow(Tables t) {
+// grow: thread per shard, allocate buckets [0, lim[s]); lim comes from the
+// ctl words, or (uniform_k != ~0u) is the same for every shard
+__global__ void k_grow(Tables t, uint32_t uniform_k) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = s < t.S;
-  const uint32_t lim = live ? (t.ctl[s] & kCtlLimitMask) : 0u;
+  const uint32_t lim = !live ? 0u : (uniform_k != ~0u ? uniform_k : (t.ctl[s] & kCtlLimitMask));
   warp_alloc_range(t, live ? s : 0, 0, lim);
 }
 
@@ -463,6 +472,7 @@ __global__ void __launch_bounds__(1024) k_shrink_release(Tables t, const uint64_
       t.fl[(size_t)b * t.S + base + ex] = (uint64_t)(t.ptr[(size_t)s * t.MB + b] - t.arena);
       t.ptr[(size_t)s * t.MB + b] = nullptr;
       t.flag[(size_t)s * t.MB + b] = 0;
+      atomicAnd(&t.pmask[s], ~(1ull << b));
       atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)(0ull - (fbv << b)));
     }
     base += tot;
@@ -495,12 +505,36 @@ __device__ __forceinline__ void stg(uint4 *p, const uint4 &v) {
                "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
+// Cache policy of the streaming loads/stores (selected by the tuning sweep):
+// 0 = L2-only (.cg), 1 = read-only path loads (.nc) + default stores,
+// 2 = default loads/stores, 3 = evict-first streaming (.cs).
+template <int LS> struct LdSt;
+template <> struct LdSt<0> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return __ldcg(p); }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { __stcg(p, v); }
+};
+template <> struct LdSt<1> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return __ldg(p); }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { *p = v; }
+};
+template <> struct LdSt<2> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return *p; }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { *p = v; }
+};
+template <> struct LdSt<3> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return __ldcs(p); }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { __stcs(p, v); }
+};
+constexpr int kDefLS = 0;
+constexpr int kDefUnroll = 4;
+
 // dst[0..n) = src[0..n) (element granular, arbitrary relative alignment), or
 // zeros if src == nullptr.  Stores are 16 B aligned vectors; loads are 16 B
 // vectors when src shares dst's alignment, else element loads.
-template <int ESZ, int UNROLL>
+template <int ESZ, int UNROLL, int LS = kDefLS>
 __device__ __forceinline__ void cta_copy(char *dst, const char *src, uint64_t n, uint32_t tid,
                                          uint32_t nt) {
+  typedef LdSt<LS> M;
   typedef typename ElemT<ESZ>::T E;
   constexpr uint32_t VE = 16 / ESZ;
   const uintptr_t d = (uintptr_t)dst;
@@ -515,28 +549,36 @@ __device__ __forceinline__ void cta_copy(char *dst, const char *src, uint64_t n,
   uint4 *dv = (uint4 *)(dst + head * ESZ);
   if (src == nullptr) {
     const uint4 z = make_uint4(0, 0, 0, 0);
-    for (uint64_t v = tid; v < body; v += nt) stg(dv + v, z);
+    for (uint64_t v = tid; v < body; v += nt) M::st(dv + v, z);
     return;
   }
   const char *sb = src + head * ESZ;
   if ((((uintptr_t)sb) & 15) == 0) {
+    // batches of UNROLL independent 16 B loads per thread, all issued before
+    // the stores; loads past the end are clamped (re-read the last vector) so
+    // they stay unconditional and the compiler cannot interleave them
     const uint4 *sv = (const uint4 *)sb;
-    uint64_t v = tid;
-    for (; v + (UNROLL - 1) * (uint64_t)nt < body; v += UNROLL * (uint64_t)nt) {
+    for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
       uint4 r[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) r[u] = ldg_stream(sv + v + u * nt);
+      for (int u = 0; u < UNROLL; ++u) r[u] = M::ld(sv + min(v0 + u * (uint64_t)nt, body - 1));
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) stg(dv + v + u * nt, r[u]);
+      for (int u = 0; u < UNROLL; ++u)
+        if (v0 + u * (uint64_t)nt < body) M::st(dv + v0 + u * nt, r[u]);
     }
-    for (; v < body; v += nt) stg(dv + v, ldg_stream(sv + v));
   } else {
     const E *s2 = (const E *)sb;
-    for (uint64_t v = tid; v < body; v += nt) {
-      union { uint4 q; E e[VE]; } u;
+    for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
+      union { uint4 q; E e[VE]; } u[UNROLL];
 #pragma unroll
-      for (uint32_t k = 0; k < VE; ++k) u.e[k] = __ldg(s2 + v * VE + k);
-      stg(dv + v, u.q);
+      for (int k = 0; k < UNROLL; ++k) {
+        const uint64_t v = min(v0 + k * (uint64_t)nt, body - 1);
+#pragma unroll
+        for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = M::ld(s2 + v * VE + j);
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k)
+        if (v0 + k * (uint64_t)nt < body) M::st(dv + v0 + k * nt, u[k].q);
     }
   }
 }
@@ -580,9 +622,10 @@ template <> struct AddOp<__half> {
 
 // in-place p[0..n) = p + a (applied `reps` times in registers; reps = 1 for a
 // separate sweep per pass)
-template <typename T, int UNROLL>
+template <typename T, int UNROLL, int LS = kDefLS>
 __device__ __forceinline__ void cta_add(char *p, uint64_t n, T a, uint32_t reps, uint32_t tid,
                                         uint32_t nt) {
+  typedef LdSt<LS == 1 ? 2 : LS> M;   // no read-only path for in-place updates
   constexpr uint32_t VE = 16 / sizeof(T);
   const uintptr_t d = (uintptr_t)p;
   uint64_t head = ((16 - (d & 15)) & 15) / sizeof(T);
@@ -601,26 +644,19 @@ __device__ __forceinline__ void cta_add(char *p, uint64_t n, T a, uint32_t reps,
     pe[e] = x;
   }
   uint4 *pv = (uint4 *)(p + head * sizeof(T));
-  uint64_t v = tid;
-  for (; v + (UNROLL - 1) * (uint64_t)nt < body; v += UNROLL * (uint64_t)nt) {
+  for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
     union { uint4 q; T e[VE]; } u[UNROLL];
 #pragma unroll
-    for (int k = 0; k < UNROLL; ++k) u[k].q = ldg_rw(pv + v + k * nt);
+    for (int k = 0; k < UNROLL; ++k) u[k].q = M::ld(pv + min(v0 + k * (uint64_t)nt, body - 1));
 #pragma unroll
     for (int k = 0; k < UNROLL; ++k) {
-      for (uint32_t r = 0; r < reps; ++r)
+      if (v0 + k * (uint64_t)nt < body) {
+        for (uint32_t r = 0; r < reps; ++r)
 #pragma unroll
-        for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = AddOp<T>::apply(u[k].e[j], a);
-      stg(pv + v + k * nt, u[k].q);
+          for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = AddOp<T>::apply(u[k].e[j], a);
+        M::st(pv + v0 + k * nt, u[k].q);
+      }
     }
-  }
-  for (; v < body; v += nt) {
-    union { uint4 q; T e[VE]; } u;
-    u.q = ldg_rw(pv + v);
-    for (uint32_t r = 0; r < reps; ++r)
-#pragma unroll
-      for (uint32_t j = 0; j < VE; ++j) u.e[j] = AddOp<T>::apply(u.e[j], a);
-    stg(pv + v, u.q);
   }
 }
 
@@ -643,7 +679,7 @@ __device__ __forceinline__ uint32_t upper_shard(const uint64_t *dir, uint32_t S,
 }
 
 constexpr uint32_t kSmemDir = 4096;   // directories up to 4096 shards are cached in smem
-constexpr int kUnroll = 8;
+constexpr int kUnroll = kDefUnroll;
 
 // load dir[0..S] into smem when it fits (one pass per CTA of a persistent grid)
 __device__ __forceinline__ const uint64_t *stage_dir(const uint64_t *gdir, uint32_t S,
@@ -654,8 +690,81 @@ __device__ __forceinline__ const uint64_t *stage_dir(const uint64_t *gdir, uint3
   return sdir;
 }
 
-template <int ESZ, int W, typename T>
-__global__ void __launch_bounds__(kThreads) k_walk(Tables t, const char *flat_src, char *flat_dst,
+// Fast path of one tile [g, gend) of the work space lying inside shard s with
+// 16 B-congruent source and destination: every thread resolves each of its
+// vectors' addresses independently (clz locate + bucket-pointer load) and
+// issues all UNROLL loads before any store, so a tile costs one memory round
+// trip however many buckets it touches.  Returns false (tile not handled)
+// when the tile crosses a shard or the alignment does not hold.
+template <int ESZ, int W, typename T, int UNROLL, int LS>
+__device__ __forceinline__ bool vector_tile(const Tables &t, const uint64_t *dir, uint32_t s,
+                                            uint64_t g, uint64_t gend, const char *flat_src,
+                                            char *flat_dst, T addend, uint32_t reps) {
+  constexpr uint32_t VE = 16 / ESZ;
+  const uint64_t lo = dir[s];
+  if (gend > dir[s + 1] || ((g - lo) % VE) || ((gend - g) % VE) || (t.log2fb < 31 && ((1u << t.log2fb) % VE)))
+    return false;
+  uint64_t dbase = 0;                      // destination local index of work index lo
+  if constexpr (W == W_INSERT || W == W_DUP) {
+    if (t.ctl && t.ctl[s] != (kCtlWrite | t.MB))
+      return false;                        // planned failure on this shard: slow path
+    dbase = t.start[s];
+    if (dbase % VE) return false;
+  }
+  if constexpr (W == W_INSERT) {
+    if (((uintptr_t)(flat_src + g * ESZ)) & 15) return false;
+  }
+  if constexpr (W == W_FLATTEN) {
+    if (((uintptr_t)(flat_dst + g * ESZ)) & 15) return false;
+  }
+  typedef LdSt<(W == W_RW && LS == 1) ? 2 : LS> M;
+  char *const *ptr = t.ptr + (size_t)s * t.MB;
+  const uint64_t nvec = (gend - g) / VE;
+  const uint64_t k0 = g - lo;              // work-space offset inside the shard
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  for (uint64_t v0 = tid; v0 < nvec; v0 += UNROLL * (uint64_t)nt) {
+    uint4 r[UNROLL];
+    char *sp[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint64_t v = min(v0 + u * (uint64_t)nt, nvec - 1);
+      if constexpr (W == W_INSERT) {
+        sp[u] = (char *)flat_src + (g + v * VE) * ESZ;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(k0 + v * VE, t.log2fb, b, o);
+        sp[u] = ptr[b] + o * ESZ;
+      }
+      r[u] = M::ld((const uint4 *)sp[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint64_t v = v0 + u * (uint64_t)nt;
+      if (v >= nvec) continue;
+      char *dp;
+      if constexpr (W == W_FLATTEN) {
+        dp = flat_dst + (g + v * VE) * ESZ;
+      } else if constexpr (W == W_RW) {
+        dp = sp[u];
+        union { uint4 q; T e[VE]; } x;
+        x.q = r[u];
+        for (uint32_t rr = 0; rr < reps; ++rr)
+#pragma unroll
+          for (uint32_t j = 0; j < VE; ++j) x.e[j] = AddOp<T>::apply(x.e[j], addend);
+        r[u] = x.q;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(dbase + k0 + v * VE, t.log2fb, b, o);
+        dp = ptr[b] + o * ESZ;
+      }
+      M::st((uint4 *)dp, r[u]);
+    }
+  }
+  return true;
+}
+
+template <int ESZ, int W, typename T, int UNROLL = kDefUnroll, int LS = kDefLS>
+__global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, char *flat_dst,
                                                    uint64_t total, T addend, uint32_t reps,
                                                    uint32_t tile) {
   extern __shared__ uint64_t sdir[];
@@ -666,6 +775,8 @@ __global__ void __launch_bounds__(kThreads) k_walk(Tables t, const char *flat_sr
     uint64_t g = ti * tile;
     const uint64_t gend = min(total, g + tile);
     uint32_t s = upper_shard(dir, t.S, g);
+    if (vector_tile<ESZ, W, T, UNROLL, LS>(t, dir, s, g, gend, flat_src, flat_dst, addend, reps))
+      continue;
     while (g < gend) {
       uint64_t shard_end = dir[s + 1];
       while (shard_end <= g) { ++s; shard_end = dir[s + 1]; }
@@ -698,51 +809,73 @@ __global__ void __launch_bounds__(kThreads) k_walk(Tables t, const char *flat_sr
         dp = t.ptr[(size_t)s * t.MB + b] + o * ESZ;
       }
       if constexpr (W == W_RW) {
-        cta_add<T, kUnroll>(dp, len, addend, reps, tid, nt);
+        cta_add<T, UNROLL, LS>(dp, len, addend, reps, tid, nt);
       } else if (dst_ok && (ctl & (kCtlWrite | kCtlZero))) {
-        cta_copy<ESZ, kUnroll>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
+        cta_copy<ESZ, UNROLL, LS>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
       }
       g += len;
     }
   }
 }
 
-// rw_g (bench_cli.py:339-366, the paper's rw_g): every group of 16 B of
-// consecutive GLOBAL indices is resolved through the directory -- a
-// warp-uniform bisect on the smem prefix, a per-lane fix-up and a clz locate --
-// then updated with one vector access when the group stays inside one
-// aligned bucket run (else element by element).
+// rw_g (bench_cli.py:339-366, the paper's rw_g): every 16 B group of
+// consecutive GLOBAL indices is resolved through the directory on its own --
+// a warp-uniform bisect on the smem prefix for the chunk, a per-lane fix-up
+// and a clz locate -- and each thread keeps kDefUnroll such vectors in flight.
+// Groups that straddle a shard or are not 16 B-aligned inside their bucket
+// are updated element by element.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total, T addend) {
   extern __shared__ uint64_t sdir[];
   const uint64_t *pre = stage_dir(t.prefix, t.S, sdir);
   constexpr uint32_t VE = 16 / sizeof(T);
+  constexpr int U = kDefUnroll;
+  typedef LdSt<kDefLS == 1 ? 2 : kDefLS> M;
   const uint64_t nvec = (total + VE - 1) / VE;
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  for (uint64_t vbase = wid * 32; vbase < nvec; vbase += nwarps * 32) {
-    uint32_t s = upper_shard(pre, t.S, vbase * VE);       // warp-uniform key
-    const uint64_t v = vbase + lane;
-    if (v >= nvec) continue;
-    const uint64_t g = v * VE;
-    while (pre[s + 1] <= g) ++s;
-    uint32_t b; uint64_t o;
-    locate(g - pre[s], t.log2fb, b, o);
-    T *p = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
-    if (g + VE <= pre[s + 1] && (o % VE) == 0 && o + VE <= (1ull << (t.log2fb + b))) {
-      union { uint4 q; T e[VE]; } u;
-      u.q = ldg_rw((const uint4 *)p);
+  for (uint64_t c0 = wid * 32 * U; c0 < nvec; c0 += nwarps * 32 * U) {
+    uint32_t s = upper_shard(pre, t.S, c0 * VE);      // warp-uniform key: smem broadcast
+    uint4 r[U];
+    T *p[U];
+    bool vec[U];
 #pragma unroll
-      for (uint32_t j = 0; j < VE; ++j) u.e[j] = AddOp<T>::apply(u.e[j], addend);
-      stg((uint4 *)p, u.q);
-    } else {
-      for (uint32_t j = 0; j < VE && g + j < total; ++j) {
-        const uint64_t gj = g + j;
-        while (pre[s + 1] <= gj) ++s;
-        locate(gj - pre[s], t.log2fb, b, o);
-        T *q = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
-        *q = AddOp<T>::apply(*q, addend);
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = c0 + lane + 32u * u;
+      const uint64_t g = v * VE;
+      vec[u] = false;
+      p[u] = nullptr;
+      if (v < nvec) {
+        while (pre[s + 1] <= g) ++s;
+        uint32_t b; uint64_t o;
+        locate(g - pre[s], t.log2fb, b, o);
+        p[u] = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
+        vec[u] = g + VE <= pre[s + 1] && (o % VE) == 0 && o + VE <= (1ull << (t.log2fb + b));
+        if (vec[u]) r[u] = M::ld((const uint4 *)p[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = c0 + lane + 32u * u;
+      if (v >= nvec) continue;
+      if (vec[u]) {
+        union { uint4 q; T e[VE]; } x;
+        x.q = r[u];
+#pragma unroll
+        for (uint32_t j = 0; j < VE; ++j) x.e[j] = AddOp<T>::apply(x.e[j], addend);
+        M::st((uint4 *)p[u], x.q);
+      } else {
+        const uint64_t g = v * VE;
+        uint32_t sj = upper_shard(pre, t.S, g);
+        for (uint32_t j = 0; j < VE && g + j < total; ++j) {
+          const uint64_t gj = g + j;
+          while (pre[sj + 1] <= gj) ++sj;
+          uint32_t b; uint64_t o;
+          locate(gj - pre[sj], t.log2fb, b, o);
+          T *q = (T *)(t.ptr[(size_t)sj * t.MB + b]) + o;
+          *q = AddOp<T>::apply(*q, addend);
+        }
       }
     }
   }
@@ -809,14 +942,14 @@ __global__ void k_flat_insert(char *buf, uint64_t cap, unsigned long long *count
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads) k_flat_add(char *buf, uint64_t n, T a, uint32_t reps) {
+template <typename T, int UNROLL = kDefUnroll, int LS = kDefLS>
+__global__ void __launch_bounds__(512) k_flat_add(char *buf, uint64_t n, T a, uint32_t reps) {
   // grid-stride over 32 KiB chunks of the contiguous array
   constexpr uint64_t CH = kTileBytes / sizeof(T);
   const uint64_t nch = (n + CH - 1) / CH;
   for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     uint64_t lo = c * CH, len = min(n - lo, CH);
-    cta_add<T, kUnroll>(buf + lo * sizeof(T), len, a, reps, threadIdx.x, blockDim.x);
+    cta_add<T, UNROLL, LS>(buf + lo * sizeof(T), len, a, reps, threadIdx.x, blockDim.x);
   }
 }
 
@@ -891,6 +1024,10 @@ struct Arena {
 
 int g_sms[64] = {0};
 
+// runtime tuning of the 4-byte streaming kernels (sweep); -1 / 0 = default
+struct Tuning { int ls = -1, unroll = -1; uint32_t tile_bytes = 0, threads = 0; };
+Tuning g_tune;
+
 int sm_count(int dev) {
   if (dev < 0 || dev >= 64) return 148;
   if (!g_sms[dev]) {
@@ -905,22 +1042,49 @@ int sm_count(int dev) {
 // pinned upload ring: small per-op host arrays (offsets, ctl words) travel
 // through pinned slots; a slot is reused only after its copy completed.
 struct Uploader {
-  static constexpr int kSlots = 4;
+  static constexpr int kSlots = 64;
   char *host[kSlots] = {nullptr};
   cudaEvent_t ev[kSlots] = {nullptr};
   bool used[kSlots] = {false};
   size_t cap = 0;
   int next = 0;
+  char *block = nullptr;
   int init(size_t bytes) {
-    cap = bytes;
+    cap = (bytes + 255) & ~size_t(255);
+    CUDA_TRY(cudaMallocHost(&block, cap * kSlots));
     for (int i = 0; i < kSlots; ++i) {
-      CUDA_TRY(cudaMallocHost(&host[i], cap));
+      host[i] = block + cap * i;
       CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
     }
     return GG_OK;
   }
   // copy `n` arrays (dst device ptr, src host ptr, bytes) in one slot
+  // graph capture: uploads are carved from a pinned pool allocated when
+  // capture mode is switched on (allocation is illegal during capture); the
+  // pools stay alive, owned by the captured graphs, until release_captured
+  static constexpr size_t kCapturePool = 4u << 20;
+  bool capturing = false;
+  std::vector<char *> captured;
+  size_t pool_off = 0;
+  int begin_capture() {
+    char *h = nullptr;
+    CUDA_TRY(cudaHostAlloc(&h, kCapturePool, cudaHostAllocDefault));
+    captured.push_back(h);
+    pool_off = 0;
+    capturing = true;
+    return GG_OK;
+  }
   int upload(cudaStream_t st, int n, void *const *dst, const void *const *src, const size_t *bytes) {
+    if (capturing) {
+      char *h = captured.back();
+      for (int i = 0; i < n; ++i) {
+        if (pool_off + bytes[i] > kCapturePool) return fail(GG_EVALUE, "capture upload pool exhausted");
+        memcpy(h + pool_off, src[i], bytes[i]);
+        CUDA_TRY(cudaMemcpyAsync(dst[i], h + pool_off, bytes[i], cudaMemcpyHostToDevice, st));
+        pool_off += (bytes[i] + 15) & ~size_t(15);
+      }
+      return GG_OK;
+    }
     int k = next;
     next = (next + 1) % kSlots;
     if (used[k]) CUDA_TRY(cudaEventSynchronize(ev[k]));
@@ -935,11 +1099,15 @@ struct Uploader {
     used[k] = true;
     return GG_OK;
   }
+  void release_captured() {
+    for (char *h : captured) cudaFreeHost(h);
+    captured.clear();
+  }
   void destroy() {
-    for (int i = 0; i < kSlots; ++i) {
+    for (int i = 0; i < kSlots; ++i)
       if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
-      if (host[i]) cudaFreeHost(host[i]);
-    }
+    if (block) cudaFreeHost(block);
+    release_captured();
   }
 };
 
@@ -986,9 +1154,15 @@ inline uint32_t min_buckets_for(const gg_array *a, uint64_t n) {
   return (uint32_t)ilog2(t) + 1;
 }
 inline cudaStream_t S_(void *s) { return (cudaStream_t)s; }
+// make the handle's device current only when it is not (cheap, capture-safe)
+inline void use_dev(int dev) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) cudaSetDevice(dev);
+}
 
+uint32_t walk_threads();
 int grid_for(const gg_array *a, uint64_t tiles, int per_sm = 8) {
-  uint64_t g = (uint64_t)sm_count(a->dev) * per_sm;
+  uint64_t g = (uint64_t)sm_count(a->dev) * per_sm * kThreads / walk_threads();
   if (tiles < g) g = tiles;
   return (int)std::max<uint64_t>(g, 1);
 }
@@ -1077,14 +1251,39 @@ int commit_plan(gg_array *a, Plan &p) {
 
 // tile of a streaming launch: 32 KiB, shrunk (down to 4 KiB) until the grid
 // has ~8 CTAs per SM, so small rounds still spread over every SM
+uint32_t walk_threads() { return g_tune.threads ? g_tune.threads : kThreads; }
+
 uint32_t tile_elems(const gg_array *a, uint64_t total) {
   uint64_t bytes = total * a->esz;
-  uint64_t want = (uint64_t)sm_count(a->dev) * 8;
-  uint64_t tb = kTileBytes;
+  uint64_t want = (uint64_t)sm_count(a->dev) * 8 * kThreads / walk_threads();
+  uint64_t tb = g_tune.tile_bytes ? g_tune.tile_bytes : kTileBytes;
   while (tb > 4096 && bytes / tb < want) tb >>= 1;
   return (uint32_t)(tb / a->esz);
 }
 size_t dir_smem(const gg_array *a) { return (a->S + 1) <= kSmemDir ? (a->S + 1) * 8 : 0; }
+
+// dispatch of the tuned variants (4-byte elements only)
+template <int W, typename T, int U, int LS>
+void walk4v(int grid, size_t sm, cudaStream_t st, const Tables &t, const char *src, char *dst,
+            uint64_t total, T add, uint32_t reps, uint32_t tile) {
+  { k_walk<4, W, T, U, LS><<<grid, walk_threads(), sm, st>>>(t, src, dst, total, add, reps, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
+}
+template <int W, typename T>
+void walk4(int grid, size_t sm, cudaStream_t st, const Tables &t, const char *src, char *dst,
+           uint64_t total, T add, uint32_t reps, uint32_t tile) {
+  const int ls = g_tune.ls < 0 ? kDefLS : g_tune.ls, u = g_tune.unroll < 0 ? kDefUnroll : g_tune.unroll;
+  switch (ls * 16 + u) {
+    case 0 * 16 + 4: walk4v<W, T, 4, 0>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 1 * 16 + 4: walk4v<W, T, 4, 1>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 2 * 16 + 4: walk4v<W, T, 4, 2>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 3 * 16 + 4: walk4v<W, T, 4, 3>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 0 * 16 + 8: walk4v<W, T, 8, 0>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 1 * 16 + 8: walk4v<W, T, 8, 1>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 2 * 16 + 8: walk4v<W, T, 8, 2>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    case 3 * 16 + 8: walk4v<W, T, 8, 3>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
+    default: walk4v<W, T, kDefUnroll, kDefLS>(grid, sm, st, t, src, dst, total, add, reps, tile);
+  }
+}
 
 template <int W>
 int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
@@ -1096,7 +1295,7 @@ int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64
   switch (a->esz) {
     case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
     case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_walk<4, W, uint32_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: walk4<W, uint32_t>(grid, sm, st, t, src, dst, total, 0u, 1u, tile); break;
     case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
   }
   CUDA_TRY(cudaGetLastError());
@@ -1145,12 +1344,19 @@ int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode,
   const size_t sm = dir_smem(a);
   if (mode == GG_RW_GLOBAL) {
     const uint64_t nvec = (total * sizeof(T) + 15) / 16;
-    int grid = (int)std::min<uint64_t>((nvec + kThreads - 1) / kThreads, (uint64_t)sm_count(a->dev) * 8);
+    int grid = (int)std::min<uint64_t>((nvec + kThreads * kDefUnroll - 1) / (kThreads * kDefUnroll),
+                                       (uint64_t)sm_count(a->dev) * 8);
     for (uint32_t p = 0; p < passes; ++p)
       { k_rw_global<T><<<grid, kThreads, sm, st>>>(t, total, addend); g_launches.fetch_add(1, std::memory_order_relaxed); }
   } else {
     const uint32_t tile = tile_elems(a, total);
     int grid = grid_for(a, (total + tile - 1) / tile);
+    if constexpr (sizeof(T) == 4 && std::is_same<T, int32_t>::value) {
+      if (mode == GG_RW_FUSED) walk4<W_RW, T>(grid, sm, st, t, nullptr, nullptr, total, addend, passes, tile);
+      else for (uint32_t p = 0; p < passes; ++p) walk4<W_RW, T>(grid, sm, st, t, nullptr, nullptr, total, addend, 1, tile);
+      CUDA_TRY(cudaGetLastError());
+      return GG_OK;
+    }
     if (mode == GG_RW_FUSED)
       { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, passes, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
     else
@@ -1250,7 +1456,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
          o_count = take(S * 8), o_prefix = take((S + 1) * 8), o_off = take((S + 1) * 8),
          o_ctl = take(S * 4), o_flag = take(T * 4), o_status = take(S * 4), o_ptr = take(T * 8),
          o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_fl = take(T * 8),
-         o_fln = take(max_buckets * 4);
+         o_fln = take(max_buckets * 4), o_pm = take(S * 8);
   cudaError_t e = cudaMalloc(&a->dmem, bytes);
   if (e != cudaSuccess) { a->arena.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
   cudaMemset(a->dmem, 0, bytes);
@@ -1263,6 +1469,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   t.flag = (uint32_t *)(base + o_flag); t.status = (uint32_t *)(base + o_status);
   t.ptr = (char **)(base + o_ptr); t.misc = (unsigned long long *)(base + o_misc);
   t.fl = (uint64_t *)(base + o_fl); t.fl_n = (int *)(base + o_fln);
+  t.pmask = (unsigned long long *)(base + o_pm);
   t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
   a->d_won = (int *)(base + o_won);
   a->d_scratch = base + o_scr;
@@ -1276,7 +1483,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
 
 int gg_destroy(gg_array *a) {
   if (!a) return GG_OK;
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaDeviceSynchronize();
   a->up.destroy();
   if (a->h_scratch) cudaFreeHost(a->h_scratch);
@@ -1299,7 +1506,7 @@ int gg_set_arena_limit(gg_array *a, uint64_t bytes) {
 int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
               const uint64_t *h_starts, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_offsets[0] != 0) return fail(GG_EVALUE, "offsets[0] must be 0");
   std::vector<uint64_t> counts(a->S);
@@ -1334,7 +1541,7 @@ int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
 
 int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   int rc = check_committed_published(a);
   if (rc) return rc;
   std::vector<uint64_t> counts(a->S);
@@ -1349,7 +1556,7 @@ int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
 
 int gg_commit(gg_array *a, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   uint64_t acc = 0;
   a->prefix[0] = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
@@ -1360,7 +1567,7 @@ int gg_commit(gg_array *a, void *stream) {
 
 int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_shard, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_failed_shard) *h_failed_shard = -1;
   Plan p;
@@ -1389,12 +1596,18 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
   if (any) {
     int rc = commit_plan(a, p);
     if (rc) return rc;
-    void *dst[1] = {a->t.ctl};
-    const void *src[1] = {lim.data()};
-    size_t bytes[1] = {a->S * 4};
-    if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
+    // uniform target without failures: every shard allocates [0, k) -- no upload
+    bool uniform = err == GG_OK;
+    for (uint32_t s = 1; s < a->S && uniform; ++s) uniform = h_min_capacity[s] == h_min_capacity[0];
+    uint32_t uk = uniform ? min_buckets_for(a, h_min_capacity[0]) : ~0u;
+    if (!uniform) {
+      void *dst[1] = {a->t.ctl};
+      const void *src[1] = {lim.data()};
+      size_t bytes[1] = {a->S * 4};
+      if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
+    }
     Tables t = tables_for_launch(a, true);
-    { k_grow<<<(a->S + 255) / 256, 256, 0, st>>>(t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    { k_grow<<<(a->S + 255) / 256, 256, 0, st>>>(t, uk); g_launches.fetch_add(1, std::memory_order_relaxed); }
     CUDA_TRY(cudaGetLastError());
     if (!p.zero_pairs.empty()) {
       // grow on a dirty shard: zero the new buckets (reference buckets are np.zeros)
@@ -1413,7 +1626,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
 
 int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   *h_won = 0;
   if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
@@ -1443,7 +1656,7 @@ int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *str
 
 int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
   *h_prev = a->size[s];
   a->size[s] += c;
@@ -1455,7 +1668,7 @@ int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *st
 
 int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_new_sizes[s] > a->size[s]) return fail(GG_EVALUE, "shrink cannot grow a shard");
@@ -1489,7 +1702,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
                     const uint64_t *h_lane_offsets, uint64_t values_per_lane,
                     int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_lane_offsets[0] != 0) return fail(GG_EVALUE, "lane offsets must start at 0");
   for (uint32_t s = 0; s < a->S; ++s)
@@ -1534,7 +1747,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
 
 int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   int rc = check_committed_published(a);
   if (rc) return rc;
   const uint64_t total = a->prefix[a->S];
@@ -1549,7 +1762,7 @@ int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, 
 
 int gg_flatten(gg_array *a, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   int rc = check_committed_published(a);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
@@ -1558,7 +1771,7 @@ int gg_flatten(gg_array *a, void *d_out, void *stream) {
 
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   if (n == 0) return GG_OK;
   Tables t = tables_for_launch(a, false);
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
@@ -1574,7 +1787,7 @@ int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *
 
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   if (n == 0) return GG_OK;
   Tables t = tables_for_launch(a, false);
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
@@ -1608,7 +1821,7 @@ int elem_addr(gg_array *a, uint32_t s, uint64_t i, char **out, cudaStream_t st) 
 
 int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
@@ -1621,7 +1834,7 @@ int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
 
 int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
@@ -1629,6 +1842,36 @@ int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream)
   memcpy(a->h_scratch, h_val, a->esz);
   CUDA_TRY(cudaMemcpyAsync(p, a->h_scratch, a->esz, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return GG_OK;
+}
+
+int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads) {
+  if (ls > 3 || (unroll != -1 && unroll != 4 && unroll != 8) || (threads && threads != 256 && threads != 512))
+    return fail(GG_EVALUE, "bad tuning");
+  g_tune.ls = ls; g_tune.unroll = unroll; g_tune.tile_bytes = tile_bytes; g_tune.threads = threads;
+  return GG_OK;
+}
+
+int gg_capture_mode(gg_array *a, int32_t on) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  if (on && !a->up.capturing) return a->up.begin_capture();
+  if (!on) a->up.capturing = false;
+  return GG_OK;
+}
+
+int gg_capture_release(gg_array *a) {
+  std::lock_guard<std::mutex> g(a->mu);
+  cudaDeviceSynchronize();
+  a->up.release_captured();
+  return GG_OK;
+}
+
+int gg_summary(gg_array *a, uint64_t *o) {
+  std::lock_guard<std::mutex> g(a->mu);
+  uint64_t sz = 0, cp = 0;
+  for (uint32_t s = 0; s < a->S; ++s) { sz += a->size[s]; cp += a->cap[s]; }
+  o[0] = a->prefix[a->S]; o[1] = sz; o[2] = cp;
   return GG_OK;
 }
 
@@ -1652,7 +1895,7 @@ int gg_host_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint64_
 int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint64_t *pre,
                     uint64_t *ops, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   cudaStream_t st = S_(stream);
   CUDA_TRY(cudaStreamSynchronize(st));
   const size_t S = a->S;
@@ -1675,7 +1918,7 @@ int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint6
 
 int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
-  cudaSetDevice(a->dev);
+  use_dev(a->dev);
   CUDA_TRY(cudaStreamSynchronize(S_(stream)));
   CUDA_TRY(cudaMemcpy(h_ptrs, a->t.ptr, (size_t)a->S * a->MB * 8, cudaMemcpyDeviceToHost));
   return GG_OK;

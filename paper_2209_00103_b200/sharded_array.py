@@ -10,6 +10,7 @@ concurrency lives inside the kernels (CTA = actor).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import threading
 from bisect import bisect_right
@@ -98,17 +99,36 @@ class GrowableArray:
             L.lib.gg_set_alloc_hook(self._h, self._hook_fn, None)
         self._cache = None
         self._ptrs = None
+        self._summary = np.zeros(3, np.uint64)
+        self._status = np.zeros(shards, np.int32)
+        self._caps = np.zeros(shards, np.uint64)
+        self._dev_index = self.device.index
         self._mu = threading.Lock()
         self.shards = [ShardVector._bind(self, s) for s in range(shards)]
 
     # ------------------------------------------------------------ plumbing
     def _stream(self):
-        import torch
-        return torch.cuda.current_stream(self.device).cuda_stream
+        return L.stream_handle(self._dev_index)
 
     def _dirty(self):
         self._cache = None
         self._ptrs = None
+
+    def _totals(self):
+        L.lib.gg_summary(self._h, L.ptr(self._summary))
+        return self._summary
+
+    @contextlib.contextmanager
+    def capture_mode(self):
+        """Make every operation inside the block legal under CUDA stream capture
+        (``torch.cuda.graph``): per-op uploads use graph-owned pinned buffers
+        and nothing synchronises.  A captured sequence that starts and ends in
+        the same state (e.g. ``shrink(0)`` + inserts) can be replayed."""
+        L.check(L.lib.gg_capture_mode(self._h, 1), "capture_mode")
+        try:
+            yield self
+        finally:
+            L.lib.gg_capture_mode(self._h, 0)
 
     def _host(self) -> dict:
         if self._cache is None:
@@ -248,15 +268,15 @@ class GrowableArray:
 
     @property
     def committed_size(self) -> int:
-        return int(self._host()["prefix"][-1])
+        return int(self._totals()[0])
 
     @property
     def total_size(self) -> int:
-        return int(self._host()["sizes"].sum())
+        return int(self._totals()[1])
 
     @property
     def total_capacity(self) -> int:
-        return int(self._host()["caps"].sum())
+        return int(self._totals()[2])
 
     def __len__(self) -> int:
         return self.committed_size
@@ -425,7 +445,7 @@ class GrowableArray:
     def insert_duplicate(self, commit: bool = True) -> None:
         """Every shard appends a copy of its committed contents, read directly from
         its buckets (the bench's _insert_duplicate, bench_cli.py:298-307)."""
-        status = np.zeros(self._S, np.int32)
+        status = self._status
         self._hook_exc.clear()
         rc = L.lib.gg_insert_duplicate(self._h, L.ptr(status, C.c_int32), self._stream())
         self._dirty()
@@ -445,7 +465,8 @@ class GrowableArray:
     def grow(self, target_total_capacity: int, distribution: Sequence | None = None) -> None:
         if distribution is None:
             per = -(-int(target_total_capacity) // self._S)
-            caps = np.full(self._S, max(per, 0), np.uint64)
+            caps = self._caps
+            caps.fill(max(per, 0))
         else:
             if len(distribution) != self._S:
                 raise ValueError(f"distribution needs {self._S} entries, got {len(distribution)}")
