@@ -1,0 +1,92 @@
+"""World-size-2 gloo tests of the multi-GPU host logic on CPU: every
+rank owns a contiguous LFVector range (the oracle array stands in for the
+device array); the all-gather directory and the gather-to-root flatten must
+reproduce the single-array flatten of the concatenated shards."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import ggoracle as O
+    from paper_2209_00103_b200.multigpu import DistributedGrowableArray
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        S_total, per_rank = 8, 4
+        rng = np.random.default_rng(0)
+        sizes = rng.integers(0, 50, S_total)
+        vals = np.arange(int(sizes.sum()), dtype=np.int32)
+        off = np.concatenate([[0], np.cumsum(sizes)])
+        lo, hi = rank * per_rank, (rank + 1) * per_rank
+        local = O.OracleGGArray(per_rank, 4, dtype=np.int32)
+        local.insert_parallel([vals[off[s]:off[s + 1]] for s in range(lo, hi)])
+        for _ in range(2):                               # local growth, no communication
+            local.grow(2 * local.committed_size)
+            local.insert_duplicate()
+            local.rw_add(1)
+        d = DistributedGrowableArray(local)
+        pre = d.global_prefix()
+        flat = d.flatten_global(root=0)
+        allg = d.allgather_flat().numpy()
+        loc = d.locate_global(pre[-1] - 1, pre)
+        q.put((rank, pre, None if flat is None else flat.numpy(), allg, loc))
+    finally:
+        dist.destroy_process_group()
+
+
+def _single_array_reference():
+    from oracle import ggoracle as O
+    S_total = 8
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(0, 50, S_total)
+    vals = np.arange(int(sizes.sum()), dtype=np.int32)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    # the two ranks grow independently: reproduce per rank, then concatenate
+    parts = []
+    for r in range(2):
+        a = O.OracleGGArray(4, 4, dtype=np.int32)
+        a.insert_parallel([vals[off[s]:off[s + 1]] for s in range(4 * r, 4 * r + 4)])
+        for _ in range(2):
+            a.grow(2 * a.committed_size)
+            a.insert_duplicate()
+            a.rw_add(1)
+        parts.append(a.flatten())
+    return np.concatenate(parts), [0, len(parts[0]), len(parts[0]) + len(parts[1])]
+
+
+def test_two_rank_directory_and_gather():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        rank, pre, flat, allg, loc = q.get(timeout=120)
+        res[rank] = (pre, flat, allg, loc)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want, want_pre = _single_array_reference()
+    assert res[0][0] == res[1][0] == want_pre
+    assert np.array_equal(res[0][1], want)
+    assert res[1][1] is None
+    assert np.array_equal(res[0][2], want) and np.array_equal(res[1][2], want)
+    assert res[0][3] == (1, want_pre[2] - want_pre[1] - 1)
