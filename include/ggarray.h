@@ -83,6 +83,15 @@ int gg_set_arena_limit(gg_array *a, uint64_t bytes);
  * not commit. */
 int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
               const uint64_t *h_starts, int32_t *h_status, void *stream);
+/* flags of the _ex variants: GG_F_COMMIT commits (prefix rebuild) in the same
+ * launch when no shard fails -- insert_parallel's insert-then-commit
+ * (sharded_array.py:207-211); GG_F_UNFUSED forces the separate
+ * reserve / copy kernels.  By default reservation, bucket allocation and the
+ * copy run as ONE persistent launch. */
+enum { GG_F_COMMIT = 1, GG_F_UNFUSED = 2 };
+int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+                 const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream);
+int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream);
 /* bench_cli.py:298-307 _insert_duplicate: every shard appends a copy of its
  * committed contents, read straight from its buckets (no snapshot). */
 int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream);

@@ -26,6 +26,7 @@ lib = C.CDLL(LIB_PATH)
 GG_OK, GG_EVALUE, GG_ECAPACITY, GG_EINDEX, GG_ENOMEM, GG_ECUDA, GG_EUNPUBLISHED, GG_EPARTIAL = range(8)
 GG_RW_PER_SHARD, GG_RW_GLOBAL, GG_RW_FUSED = 0, 1, 2
 GG_ALGO_ATOMIC, GG_ALGO_WARP, GG_ALGO_BLOCK, GG_ALGO_BATCH = 0, 1, 2, 3
+GG_F_COMMIT, GG_F_UNFUSED = 1, 2
 
 # numpy dtype -> GG dtype code (include/ggarray.h)
 DTYPE_CODES = {
@@ -51,6 +52,8 @@ _SIGS = {
     "gg_set_arena_limit": ([P, U64], C.c_int),
     "gg_insert": ([P, P, PU64, PU64, PI32, P], C.c_int),
     "gg_insert_duplicate": ([P, PI32, P], C.c_int),
+    "gg_insert_ex": ([P, P, PU64, PU64, U32, PI32, P], C.c_int),
+    "gg_insert_duplicate_ex": ([P, U32, PI32, P], C.c_int),
     "gg_insert_lanes": ([P, P, P, PU64, U64, PI32, P], C.c_int),
     "gg_commit": ([P, P], C.c_int),
     "gg_reserve": ([P, PU64, PI64, P], C.c_int),

@@ -107,7 +107,10 @@ constexpr uint32_t kCtlLimitMask = 0xffu;   // allocate buckets < limit
 constexpr uint32_t kCtlWrite = 1u << 8;     // write the values
 constexpr uint32_t kCtlZero = 1u << 9;      // write zeros instead (failed shard)
 
-enum { MISC_TOP = 0, MISC_ALLOCS = 1, MISC_OOM = 2, MISC_N = 4 };
+// launch-coordination counters live on their own 128 B lines, away from the
+// allocator's bump top (pollers would otherwise contend with its atomics)
+enum { MISC_TOP = 0, MISC_ALLOCS = 1, MISC_OOM = 2, MISC_DONE = 16, MISC_RSV = 32, MISC_TICKET = 48,
+       MISC_N = 64 };
 
 inline uint32_t elem_bytes_of(uint32_t dt) {
   switch (dt) {
@@ -154,6 +157,11 @@ __device__ __forceinline__ void locate(uint64_t i, uint32_t log2fb, uint32_t &b,
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire64(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
@@ -265,9 +273,7 @@ __device__ __forceinline__ void warp_alloc_range(const Tables &t, uint32_t s, ui
 // (bucket_vector.py:207-214, 234-238).  Count sources:
 //   mode 0: CSR offsets (insert); mode 1: committed lengths (duplicate);
 //   mode 2: explicit starts + counts already in t.start/t.count (fetch_add'ed)
-__global__ void k_reserve(Tables t, int mode) {
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = s < t.S;
+__device__ __forceinline__ void reserve_shards(const Tables &t, uint32_t s, bool live, int mode) {
   uint64_t c = 0, start = 0;
   uint32_t lo = 0, hi = 0;
   if (live) {
@@ -296,6 +302,11 @@ __global__ void k_reserve(Tables t, int mode) {
     }
   }
   warp_alloc_range(t, live ? s : 0, lo, hi);
+}
+
+__global__ void k_reserve(Tables t, int mode) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  reserve_shards(t, s, s < t.S, mode);
 }
 
 // grow: thread per shard, allocate buckets [0, lim[s]); lim comes from the
@@ -763,15 +774,66 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, const uint64_t *dir
   return true;
 }
 
-template <int ESZ, int W, typename T, int UNROLL = kDefUnroll, int LS = kDefLS>
+// Fused append (FUSE): ONE launch reserves + allocates (the first ceil(S/nt)
+// CTAs, thread per shard: one atomicAdd per LFVector, warp-aggregated bucket
+// allocation), then every CTA waits once (acquire on a global counter the
+// reserving CTAs bump after a fence) and copies its tiles; the last CTA to
+// finish resets the counters and, if asked, rebuilds the prefix (commit).
+// Reserving CTAs are chosen by start-time tickets, so they are running
+// before any CTA waits: no deadlock whatever the dispatch order.
+struct Fuse { int rmode; uint32_t epoch; int commit; };
+
+__device__ void commit_block(const Tables &t) {
+  __shared__ uint64_t ws[32];
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const uint64_t v = s < t.S ? ld_acquire64(t.size + s) : 0;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan(v, &tot, ws);
+    if (s < t.S) t.prefix[s + 1] = carry + ex + v;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) t.prefix[0] = 0;
+}
+
+template <int ESZ, int W, typename T, int UNROLL = kDefUnroll, int LS = kDefLS, bool FUSE = false>
 __global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, char *flat_dst,
                                                    uint64_t total, T addend, uint32_t reps,
-                                                   uint32_t tile) {
+                                                   uint32_t tile, Fuse fz) {
   extern __shared__ uint64_t sdir[];
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  uint32_t vblock = blockIdx.x;
+  if constexpr (FUSE) {
+    // a CTA's virtual index is a ticket taken when it STARTS running, so the
+    // reserving CTAs (tickets < n_rsv) are always resident before anyone waits
+    __shared__ uint32_t ticket;
+    if (tid == 0) ticket = (uint32_t)atomicAdd(&t.misc[MISC_TICKET], 1ull);
+    __syncthreads();
+    vblock = ticket;
+    // phase 1: the first ceil(S/nt) tickets reserve + allocate (thread per shard)
+    const uint32_t n_rsv = min(gridDim.x, (t.S + nt - 1) / nt);
+    if (vblock < n_rsv) {
+      for (uint32_t base = vblock * nt; base < t.S; base += n_rsv * nt) {
+        const uint32_t s = base + tid;
+        reserve_shards(t, s, s < t.S, fz.rmode);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(&t.misc[MISC_RSV], 1ull);
+      }
+    }
+    // every CTA waits ONCE for all reservations (acquire by thread 0, then the
+    // CTA barrier orders the other threads' loads after it)
+    if (tid == 0) {
+      while (ld_acquire64((const uint64_t *)&t.misc[MISC_RSV]) < n_rsv) __nanosleep(256);
+    }
+    __syncthreads();
+  }
   const uint64_t *dir = stage_dir((W == W_INSERT) ? t.offsets : t.prefix, t.S, sdir);
   const uint64_t ntiles = (total + tile - 1) / tile;
-  const uint32_t tid = threadIdx.x, nt = blockDim.x;
-  for (uint64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+  for (uint64_t ti = vblock; ti < ntiles; ti += gridDim.x) {
     uint64_t g = ti * tile;
     const uint64_t gend = min(total, g + tile);
     uint32_t s = upper_shard(dir, t.S, g);
@@ -814,6 +876,25 @@ __global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, ch
         cta_copy<ESZ, UNROLL, LS>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
       }
       g += len;
+    }
+  }
+  if constexpr (FUSE) {
+    // the last CTA to finish resets the launch counters and, if asked, commits
+    __shared__ bool is_last;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      is_last = atomicAdd(&t.misc[MISC_DONE], 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      if (fz.commit) commit_block(t);
+      if (tid == 0) {
+        t.misc[MISC_DONE] = 0;
+        t.misc[MISC_RSV] = 0;
+        t.misc[MISC_TICKET] = 0;
+      }
     }
   }
 }
@@ -1122,6 +1203,7 @@ struct gg_array {
   std::vector<uint64_t> size, cap, ops, prefix, flags;  // flags: bitmask per shard
   std::vector<uint8_t> dirty;                            // shard saw a failed reservation
   uint64_t top = 0;                                      // arena bump top (bytes)
+  uint32_t epoch = 0;                                    // fused-launch ready-flag epoch
   std::vector<uint64_t> fl_count;                        // free-list entries per class
   uint64_t alloc_calls = 0;
   uint64_t limit = 0;                                    // mapped-bytes cap (0 = none)
@@ -1266,7 +1348,7 @@ size_t dir_smem(const gg_array *a) { return (a->S + 1) <= kSmemDir ? (a->S + 1) 
 template <int W, typename T, int U, int LS>
 void walk4v(int grid, size_t sm, cudaStream_t st, const Tables &t, const char *src, char *dst,
             uint64_t total, T add, uint32_t reps, uint32_t tile) {
-  { k_walk<4, W, T, U, LS><<<grid, walk_threads(), sm, st>>>(t, src, dst, total, add, reps, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  { k_walk<4, W, T, U, LS><<<grid, walk_threads(), sm, st>>>(t, src, dst, total, add, reps, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); }
 }
 template <int W, typename T>
 void walk4(int grid, size_t sm, cudaStream_t st, const Tables &t, const char *src, char *dst,
@@ -1293,18 +1375,61 @@ int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64
   int grid = grid_for(a, (total + tile - 1) / tile);
   const size_t sm = dir_smem(a);
   switch (a->esz) {
-    case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
     case 4: walk4<W, uint32_t>(grid, sm, st, t, src, dst, total, 0u, 1u, tile); break;
-    case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
   }
   CUDA_TRY(cudaGetLastError());
   return GG_OK;
 }
 
-// run an allocating append: upload ctl/zero list if needed, reserve, zero, copy
+// fused append launch (same persistent grid as the unfused walk; the ticket
+// scheme makes the reservation wait safe under oversubscription)
+template <int ESZ, int W, typename E>
+int launch_fused(gg_array *a, const Tables &t, const char *src, uint64_t total, Fuse fz,
+                 cudaStream_t st) {
+  auto kern = k_walk<ESZ, W, E, kDefUnroll, kDefLS, true>;
+  static int per_sm = 0;
+  const size_t sm = dir_smem(a);
+  if (!per_sm) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, sm) != cudaSuccess || n < 1) n = 1;
+    per_sm = n;
+  }
+  const uint32_t tile = total ? tile_elems(a, total) : 1;
+  uint64_t grid = total ? (total + tile - 1) / tile : 1;
+  (void)per_sm;
+  grid = std::min<uint64_t>(grid, (uint64_t)sm_count(a->dev) * 8);
+  grid = std::max<uint64_t>(grid, 1);
+  { kern<<<(int)grid, kThreads, sm, st>>>(t, src, nullptr, total, E(0), 0u, tile, fz); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+template <int W>
+int launch_fused_esz(gg_array *a, const Tables &t, const char *src, uint64_t total, Fuse fz,
+                     cudaStream_t st) {
+  switch (a->esz) {
+    case 1: return launch_fused<1, W, uint8_t>(a, t, src, total, fz, st);
+    case 2: return launch_fused<2, W, uint16_t>(a, t, src, total, fz, st);
+    case 4: return launch_fused<4, W, uint32_t>(a, t, src, total, fz, st);
+    default: return launch_fused<8, W, uint64_t>(a, t, src, total, fz, st);
+  }
+}
+
+void host_commit(gg_array *a) {
+  uint64_t acc = 0;
+  a->prefix[0] = 0;
+  for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
+}
+
+// run an allocating append: upload ctl/zero list if needed, then either one
+// fused launch (reserve + allocate + copy [+ commit]) or the unfused
+// reserve / zero / copy sequence (failure paths that must zero buckets).
 int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src,
-               uint64_t total, cudaStream_t st) {
+               uint64_t total, cudaStream_t st, uint32_t flags, bool *committed) {
+  *committed = false;
   int rc = commit_plan(a, p);
   if (rc) return rc;
   Tables t = tables_for_launch(a, p.any_ctl);
@@ -1313,6 +1438,22 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src
     const void *srcs[1] = {p.ctl.data()};
     size_t bytes[1] = {a->S * sizeof(uint32_t)};
     if ((rc = a->up.upload(st, 1, dst, srcs, bytes))) return rc;
+  }
+  // Fused single launch by default.  Under CUDA-graph capture inter-kernel
+  // gaps are ~1 us, and the measured A/B (r01) favours the separate
+  // reserve / copy / commit kernels there (680 vs 663 Gelem/s on config 2),
+  // while eager issue favours the fused launch (604 vs 597).
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if (p.zero_pairs.empty() && !(flags & GG_F_UNFUSED) && cap == cudaStreamCaptureStatusNone) {
+    const bool commit = (flags & GG_F_COMMIT) && !p.any_fail;
+    if (++a->epoch == 0) ++a->epoch;
+    Fuse fz{reserve_mode, a->epoch, commit ? 1 : 0};
+    rc = walk == W_INSERT ? launch_fused_esz<W_INSERT>(a, t, src, total, fz, st)
+                          : launch_fused_esz<W_DUP>(a, t, nullptr, total, fz, st);
+    if (rc) return rc;
+    if (commit) { host_commit(a); *committed = true; }
+    return GG_OK;
   }
   { k_reserve<<<(a->S + 255) / 256, 256, 0, st>>>(t, reserve_mode); g_launches.fetch_add(1, std::memory_order_relaxed); }
   CUDA_TRY(cudaGetLastError());
@@ -1327,8 +1468,16 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src
     CUDA_TRY(cudaFreeAsync(d_pairs, st));
     CUDA_TRY(cudaStreamSynchronize(st));  // zero_pairs host memory is pageable
   }
-  if (walk == W_INSERT) return launch_walk<W_INSERT>(a, t, src, nullptr, total, st);
-  return launch_walk<W_DUP>(a, t, nullptr, nullptr, total, st);
+  rc = walk == W_INSERT ? launch_walk<W_INSERT>(a, t, src, nullptr, total, st)
+                        : launch_walk<W_DUP>(a, t, nullptr, nullptr, total, st);
+  if (rc) return rc;
+  if ((flags & GG_F_COMMIT) && !p.any_fail) {
+    host_commit(a);
+    { k_commit<<<1, 1024, 0, st>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    CUDA_TRY(cudaGetLastError());
+    *committed = true;
+  }
+  return GG_OK;
 }
 
 int finish_status(gg_array *a, const Plan &p, int32_t *h_status) {
@@ -1358,10 +1507,10 @@ int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode,
       return GG_OK;
     }
     if (mode == GG_RW_FUSED)
-      { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, passes, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
+      { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, passes, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); }
     else
       for (uint32_t p = 0; p < passes; ++p)
-        { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, 1, tile); g_launches.fetch_add(1, std::memory_order_relaxed); }
+        { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, 1, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); }
   }
   CUDA_TRY(cudaGetLastError());
   return GG_OK;
@@ -1503,8 +1652,8 @@ int gg_set_arena_limit(gg_array *a, uint64_t bytes) {
   return GG_OK;
 }
 
-int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
-              const uint64_t *h_starts, int32_t *h_status, void *stream) {
+int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+                 const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
@@ -1533,13 +1682,16 @@ int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
     size_t bytes[1] = {(a->S + 1) * 8};
     if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
   }
-  if ((rc = run_append(a, p, h_starts ? 2 : 0, W_INSERT, (const char *)d_values, total, st))) return rc;
+  bool committed;
+  if ((rc = run_append(a, p, h_starts ? 2 : 0, W_INSERT, (const char *)d_values, total, st, flags,
+                       &committed)))
+    return rc;
   if (!h_starts)
     for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
   return finish_status(a, p, h_status);
 }
 
-int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
+int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   int rc = check_committed_published(a);
@@ -1549,9 +1701,20 @@ int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
   Plan p;
   plan_init(a, p);
   plan_append(a, p, counts.data(), nullptr);
-  if ((rc = run_append(a, p, 1, W_DUP, nullptr, a->prefix[a->S], S_(stream)))) return rc;
+  bool committed;
+  const uint64_t total = a->prefix[a->S];
+  if ((rc = run_append(a, p, 1, W_DUP, nullptr, total, S_(stream), flags, &committed))) return rc;
   for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
   return finish_status(a, p, h_status);
+}
+
+int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+              const uint64_t *h_starts, int32_t *h_status, void *stream) {
+  return gg_insert_ex(a, d_values, h_offsets, h_starts, 0, h_status, stream);
+}
+
+int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
+  return gg_insert_duplicate_ex(a, 0, h_status, stream);
 }
 
 int gg_commit(gg_array *a, void *stream) {

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import contextlib
 import ctypes as C
+import os
 import threading
 from bisect import bisect_right
 from typing import Callable, Sequence
@@ -29,6 +30,8 @@ DEFAULT_SHARDS = 32
 RW_MODES = {"per_shard": L.GG_RW_PER_SHARD, "global": L.GG_RW_GLOBAL, "fused": L.GG_RW_FUSED}
 
 _INT_OF_SIZE = {1: np.int8, 2: np.int16, 4: np.int32, 8: np.int64}
+# GG_UNFUSED=1 forces the separate reserve / copy / commit kernels (A/B runs)
+_EXTRA_FLAGS = L.GG_F_UNFUSED if os.environ.get("GG_UNFUSED") == "1" else 0
 
 
 def split_batches(values, shards: int) -> list:
@@ -172,18 +175,23 @@ class GrowableArray:
             return self._hook_exc.pop(s, None) or MemoryError(f"shard {s}: bucket arena exhausted")
         return RuntimeError(f"shard {s}: status {code}")
 
-    def _insert_device(self, vals, offsets: np.ndarray, starts: np.ndarray | None = None) -> dict:
-        """gg_insert; returns {shard: exception} for failed shards (no commit)."""
+    def _insert_device(self, vals, offsets: np.ndarray, starts: np.ndarray | None = None,
+                       commit: bool = False) -> dict:
+        """gg_insert_ex; returns {shard: exception} for failed shards.  With
+        ``commit`` the prefix is rebuilt in the same launch iff nothing failed."""
         offsets = L.u64_array(offsets)
-        status = np.zeros(self._S, np.int32)
+        status = self._status
         self._hook_exc.clear()
         starts = None if starts is None else L.u64_array(starts)
         st = None if starts is None else L.ptr(starts)
-        rc = L.lib.gg_insert(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
-                             L.ptr(offsets), st, L.ptr(status, C.c_int32), self._stream())
+        flags = (L.GG_F_COMMIT if commit else 0) | _EXTRA_FLAGS
+        rc = L.lib.gg_insert_ex(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
+                                L.ptr(offsets), st, flags, L.ptr(status, C.c_int32), self._stream())
         self._dirty()
         if rc not in (L.GG_OK, L.GG_EPARTIAL):
             L.check(rc, "insert")
+        if rc == L.GG_OK:
+            return {}
         return {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
 
     def _write_ranges(self, ranges: dict) -> None:
@@ -373,7 +381,10 @@ class GrowableArray:
             failures, ok = self._insert_with_reserver(per_shard_batches, reserver)
         else:
             vals, offsets = self._pack(per_shard_batches)
-            failures = self._insert_device(vals, offsets)
+            failures = self._insert_device(vals, offsets, commit=True)   # commit fused on success
+            if not failures:
+                self._cache = None
+                return
             counts = np.diff(offsets.astype(np.int64))
             ok = [s for s in range(self._S) if counts[s] and s not in failures]
         if failures:
@@ -406,12 +417,10 @@ class GrowableArray:
         offsets = L.u64_array(offsets)
         if offsets.shape != (self._S + 1,) or int(offsets[-1]) != vals.numel():
             raise ValueError("offsets must have S+1 entries ending at len(values)")
-        failures = self._insert_device(vals, offsets)
+        failures = self._insert_device(vals, offsets, commit=commit)
         if failures:
             counts = np.diff(offsets.astype(np.int64))
             raise ShardInsertError(failures, [s for s in range(self._S) if counts[s] and s not in failures])
-        if commit:
-            self.commit()
 
     def insert_lanes(self, values, counts, lane_offsets, values_per_lane: int = 1,
                      commit: bool = True) -> None:
@@ -447,7 +456,8 @@ class GrowableArray:
         its buckets (the bench's _insert_duplicate, bench_cli.py:298-307)."""
         status = self._status
         self._hook_exc.clear()
-        rc = L.lib.gg_insert_duplicate(self._h, L.ptr(status, C.c_int32), self._stream())
+        flags = (L.GG_F_COMMIT if commit else 0) | _EXTRA_FLAGS
+        rc = L.lib.gg_insert_duplicate_ex(self._h, flags, L.ptr(status, C.c_int32), self._stream())
         self._dirty()
         if rc not in (L.GG_OK, L.GG_EPARTIAL):
             L.check(rc, "insert_duplicate")
@@ -455,8 +465,6 @@ class GrowableArray:
             failures = {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
             cl = np.diff(self._host()["prefix"].astype(np.int64))
             raise ShardInsertError(failures, [s for s in range(self._S) if cl[s] and s not in failures])
-        if commit:
-            self.commit()
 
     def commit(self) -> None:
         L.check(L.lib.gg_commit(self._h, self._stream()), "commit")
@@ -517,10 +525,9 @@ class GrowableArray:
         arr = cls(shards, first_bucket_size, dtype=dtype, max_buckets=max_buckets,
                   allocator=allocator, device=device, arena_va_bytes=arena_va_bytes)
         vals = arr._device_values(values)
-        failures = arr._insert_device(vals, split_offsets(n, shards))
+        failures = arr._insert_device(vals, split_offsets(n, shards), commit=True)
         if failures:
             raise failures[min(failures)]
-        arr.commit()
         return arr
 
     # ------------------------------------------------------------ stats / parity
