@@ -124,6 +124,23 @@ int gg_fetch_add(gg_array *a, uint32_t shard, uint64_t count, uint64_t *h_prev, 
  * pointer moves); their granules stay mapped.  Commits. */
 int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream);
 
+/* Device-side appends from user kernels (include/ggarray_device.cuh, paper
+ * Alg. 1/2).  gg_device_view_get maps `headroom_bytes` of arena beyond the
+ * current bump top and copies the device tables' view (a gg::gg_device_view,
+ * view_bytes = sizeof) to h_view for passing to a kernel by value;
+ * gg_device_view_sync waits for `stream`, refreshes the host mirrors from the
+ * device (sizes, capacities, flags, bump top), releases unused headroom and
+ * reports per-shard failures (GG_EPARTIAL).  Neither commits. */
+uint64_t gg_device_view_bytes(void);
+int gg_device_view_get(gg_array *a, uint64_t headroom_bytes, void *h_view, uint64_t view_bytes);
+int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream);
+/* Example user kernel of that API: block b of a `grid`-block launch (0 =
+ * auto) appends d_vals[i] for every i of its slices with d_pred[i] != 0 to
+ * shard b % S; mode 0 = warp_push_back (one atomicAdd per warp), 1 =
+ * block_push_back (block scan, one atomicAdd per block). */
+int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t n, int32_t mode,
+               uint32_t grid, int32_t *h_status, void *stream);
+
 /* for_each_shard(+c) x passes (sharded_array.py:165-186, bench_cli.py:
  * 180-183, 323-366).  h_addend points to one element of the array dtype.
  * mode GG_RW_PER_SHARD walks shard segments (rw_b), GG_RW_GLOBAL resolves

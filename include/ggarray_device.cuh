@@ -1,0 +1,217 @@
+/*
+ * ggarray_device.cuh -- device-side GGArray API for user kernels (sm_100a).
+ *
+ * The paper's point (arXiv 2209.00103 Alg. 1/2): threads of a running kernel
+ * append to an LFVector, the block computing per-thread offsets with a
+ * warp-shuffle / shared-memory scan, reserving with ONE atomicAdd on the
+ * LFVector size and allocating the buckets its range touches on the fly (CAS
+ * once-flag; the winner allocates, losers wait for publication).  This header
+ * exposes exactly that to any kernel:
+ *
+ *   gg::gg_device_view v = ...;          // from gg_device_view_get() (host)
+ *   gg::warp_push_back(v, shard, pred, value);        // one atomicAdd per warp
+ *   gg::block_push_back<BLOCK>(v, shard, count, vals, scratch);  // one per block
+ *
+ * The view's arena has `arena_mapped` bytes of physical memory behind it (the
+ * host maps headroom before the launch: device code cannot map memory);
+ * allocations beyond it fail, set status[shard] |= GG_ENOMEM, and the
+ * reservation is kept, like a failing allocator in the reference
+ * (bucket_vector.py:194-201).  After the kernel, gg_device_view_sync()
+ * refreshes the host's mirrors from the device tables.
+ *
+ * The same structures and allocator back the library's own kernels
+ * (paper_2209_00103_b200/csrc/ggarray.cu), so there is one implementation.
+ */
+#ifndef GGARRAY_DEVICE_CUH
+#define GGARRAY_DEVICE_CUH
+
+#include <cstdint>
+
+namespace gg {
+
+// Device tables of one GGArray (all pointers are device memory).
+struct gg_device_view {
+  uint64_t *size, *cap, *ops, *start, *count, *prefix, *offsets;
+  uint32_t *ctl, *flag, *status;
+  char **ptr;                 // [S*MB] bucket base pointers
+  unsigned long long *pmask;  // [S] published-bucket bitmask per shard
+  uint64_t *fl;               // [MB*S] per-class free lists of arena offsets (shrink)
+  int *fl_n;                  // [MB] entries per class
+  unsigned long long *misc;   // arena bump top, alloc count, launch counters
+  char *arena;                // base of the VMM bucket arena
+  uint64_t arena_mapped;      // bytes of the arena backed by physical memory
+  uint32_t S, log2fb, MB, esz;
+};
+
+constexpr uint32_t kFlagPublished = 2;   // once-flag states: 0 free, 1 allocating, 2 published
+constexpr uint32_t kStatusNoMem = 4;     // == GG_ENOMEM
+
+// launch-coordination counters live on their own 128 B lines, away from the
+// allocator's bump top (pollers would otherwise contend with its atomics)
+enum { MISC_TOP = 0, MISC_ALLOCS = 1, MISC_OOM = 2, MISC_DONE = 16, MISC_RSV = 32, MISC_TICKET = 48,
+       MISC_N = 64 };
+
+// bucket_vector.py:48-59: b = hibit(i/fb + 1), off = i - fb*(2^b - 1)
+__device__ __forceinline__ void locate(uint64_t i, uint32_t log2fb, uint32_t &b, uint64_t &off) {
+  uint64_t q = (i >> log2fb) + 1;
+  b = 63u - (uint32_t)__clzll((long long)q);
+  off = i - (((1ull << b) - 1ull) << log2fb);
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_acquire64(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Paper Alg. 2 (new_bucket): CAS the once-flag; the winner takes a bucket from
+// the class free list or bumps the arena top and publishes it with release
+// order; losers wait for the publication (or retry after a rollback).
+// Returns 1 if this caller allocated, 0 if the bucket was already there, -1 on
+// arena exhaustion (flag rolled back, like bucket_vector.py:196-201).
+__device__ inline int alloc_bucket(const gg_device_view &t, uint32_t s, uint32_t b) {
+  uint32_t *f = t.flag + (size_t)s * t.MB + b;
+  for (;;) {
+    uint32_t cur = ld_acquire(f);
+    if (cur == kFlagPublished) return 0;
+    if (cur == 0 && atomicCAS(f, 0u, 1u) == 0u) break;
+    __nanosleep(64);
+  }
+  const uint64_t elems = 1ull << (t.log2fb + b);
+  const uint64_t bytes = (elems * t.esz + 15) & ~15ull;
+  unsigned long long off;
+  int k = atomicSub(&t.fl_n[b], 1);
+  if (k > 0) {
+    off = t.fl[(size_t)b * t.S + (k - 1)];   // reuse a bucket released by shrink
+  } else {
+    atomicAdd(&t.fl_n[b], 1);
+    off = atomicAdd(&t.misc[MISC_TOP], (unsigned long long)bytes);
+  }
+  if (off + bytes > t.arena_mapped) {
+    atomicAdd(&t.misc[MISC_OOM], 1ull);
+    st_release(f, 0);
+    return -1;
+  }
+  t.ptr[(size_t)s * t.MB + b] = t.arena + off;
+  atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
+  atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
+  __threadfence();
+  st_release(f, kFlagPublished);
+  atomicOr(&t.pmask[s], 1ull << b);
+  return 1;
+}
+
+// Allocate every bucket covering local indices [start, start + n) of shard s
+// (bucket_vector.py:207-214).  Returns false if a bucket could not be had.
+__device__ inline bool ensure_buckets(const gg_device_view &t, uint32_t s, uint64_t start,
+                                      uint64_t n) {
+  if (!n) return true;
+  uint32_t b0, b1;
+  uint64_t o;
+  locate(start, t.log2fb, b0, o);
+  locate(start + n - 1, t.log2fb, b1, o);
+  bool ok = b1 < t.MB;
+  for (uint32_t b = b0; ok && b <= b1; ++b)
+    if (!((t.pmask[s] >> b) & 1ull) && alloc_bucket(t, s, b) < 0) ok = false;
+  if (!ok) atomicOr(&t.status[s], kStatusNoMem);
+  return ok;
+}
+
+// Store one element at local index i of shard s (bucket must be published).
+template <typename T>
+__device__ __forceinline__ void store_local(const gg_device_view &t, uint32_t s, uint64_t i,
+                                            const T &v) {
+  uint32_t b;
+  uint64_t o;
+  locate(i, t.log2fb, b, o);
+  if (b < t.MB && (t.flag[(size_t)s * t.MB + b] == kFlagPublished || ld_acquire(t.flag + (size_t)s * t.MB + b) == kFlagPublished))
+    reinterpret_cast<T *>(t.ptr[(size_t)s * t.MB + b])[o] = v;
+}
+
+// Paper Alg. 1, warp flavour: every lane with `pred` appends `value` to shard s
+// (s warp-uniform).  The 0/1 counts are scanned with a ballot (the warp
+// shuffle scan of a predicate), the warp reserves with ONE atomicAdd on the
+// LFVector size, lane 0 allocates the touched buckets, values land in lane
+// order.  Must be called by all 32 lanes.  Returns the lane's local index or
+// ~0ull.
+template <typename T>
+__device__ inline uint64_t warp_push_back(const gg_device_view &t, uint32_t s, bool pred,
+                                          const T &value) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (!m) return ~0ull;
+  const uint32_t lane = threadIdx.x & 31, cnt = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
+  unsigned long long start = 0;
+  int ok = 1;
+  if (lane == 0) {
+    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)cnt);
+    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+    ok = ensure_buckets(t, s, start, cnt);
+  }
+  start = __shfl_sync(0xffffffffu, start, 0);
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  __syncwarp();
+  if (!pred || !ok) return ~0ull;
+  store_local(t, s, start + rank, value);
+  return start + rank;
+}
+
+// Paper Alg. 1, block flavour: thread j contributes vals[0..count_j); a
+// shared-memory scan of the counts gives each thread its offset, thread 0
+// reserves the block total with ONE atomicAdd and allocates the buckets, the
+// values land in thread order.  `scratch` is 34 u64 of shared memory; BLOCK is
+// blockDim.x (multiple of 32).  Returns the block's start index.
+template <int BLOCK, typename T>
+__device__ inline uint64_t block_push_back(const gg_device_view &t, uint32_t s, uint32_t count,
+                                           const T *vals, unsigned long long *scratch) {
+  static_assert(BLOCK % 32 == 0 && BLOCK <= 1024, "BLOCK must be a multiple of 32, <= 1024");
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned long long x = count;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < BLOCK / 32 ? scratch[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= (uint32_t)d) w += y;
+    }
+    scratch[lane] = w;
+  }
+  __syncthreads();
+  const unsigned long long excl = x - count + (wid ? scratch[wid - 1] : 0);
+  const unsigned long long total = scratch[BLOCK / 32 - 1];
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long start = 0;
+    int ok = 1;
+    if (total) {
+      start = atomicAdd((unsigned long long *)&t.size[s], total);
+      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+      ok = ensure_buckets(t, s, start, total);
+    }
+    scratch[32] = start;
+    scratch[33] = ok;
+  }
+  __syncthreads();
+  const unsigned long long start = scratch[32];
+  if (scratch[33])
+    for (uint32_t e = 0; e < count; ++e) store_local(t, s, start + excl + e, vals[e]);
+  return start;
+}
+
+}  // namespace gg
+
+#endif  // GGARRAY_DEVICE_CUH

@@ -31,10 +31,13 @@
 #include <vector>
 
 #include "../../include/ggarray.h"
+#include "../../include/ggarray_device.cuh"
 
 #define GG_VERSION 1
 
 namespace gg {
+
+typedef gg_device_view Tables;
 
 thread_local std::string g_err;
 std::atomic<unsigned long long> g_launches{0};   // kernels launched by this library
@@ -100,17 +103,11 @@ Drv &drv() {
 constexpr int kMaxBuckets = 64;
 constexpr int kThreads = 256;          // CTA size of the streaming kernels
 constexpr int kTileBytes = 32 * 1024;  // bytes of payload per tile
-constexpr uint32_t kFlagPublished = 2;
 
 // ctl word per shard (only uploaded when an op plans a failure)
 constexpr uint32_t kCtlLimitMask = 0xffu;   // allocate buckets < limit
 constexpr uint32_t kCtlWrite = 1u << 8;     // write the values
 constexpr uint32_t kCtlZero = 1u << 9;      // write zeros instead (failed shard)
-
-// launch-coordination counters live on their own 128 B lines, away from the
-// allocator's bump top (pollers would otherwise contend with its atomics)
-enum { MISC_TOP = 0, MISC_ALLOCS = 1, MISC_OOM = 2, MISC_DONE = 16, MISC_RSV = 32, MISC_TICKET = 48,
-       MISC_N = 64 };
 
 inline uint32_t elem_bytes_of(uint32_t dt) {
   switch (dt) {
@@ -128,82 +125,11 @@ inline int ilog2(uint64_t x) { return 63 - __builtin_clzll(x); }
 
 // ------------------------------------------------------------------ device side
 
-struct Tables {
-  uint64_t *size, *cap, *ops, *start, *count, *prefix, *offsets;
-  uint32_t *ctl, *flag, *status;
-  char **ptr;
-  unsigned long long *pmask;  // [S] published-bucket bitmask per shard
-  uint64_t *fl;            // [MB*S] per-class free lists of arena offsets (shrink)
-  int *fl_n;               // [MB] entries per class
-  unsigned long long *misc;
-  char *arena;
-  uint64_t arena_mapped;  // device allocations beyond this fail (OOM)
-  uint32_t S, log2fb, MB, esz;
-};
-
 template <int ESZ> struct ElemT;
 template <> struct ElemT<1> { typedef uint8_t T; };
 template <> struct ElemT<2> { typedef uint16_t T; };
 template <> struct ElemT<4> { typedef uint32_t T; };
 template <> struct ElemT<8> { typedef unsigned long long T; };
-
-__device__ __forceinline__ void locate(uint64_t i, uint32_t log2fb, uint32_t &b, uint64_t &off) {
-  // bucket_vector.py:48-59: b = hibit(i/fb + 1), off = i - fb*(2^b - 1)
-  uint64_t q = (i >> log2fb) + 1;
-  b = 63u - (uint32_t)__clzll((long long)q);
-  off = i - (((1ull << b) - 1ull) << log2fb);
-}
-
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_acquire64(const uint64_t *p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// Paper Alg. 2 (new_bucket): CAS the once-flag, the winner bump-allocates
-// from the arena and publishes with release order; losers wait for the
-// publication.  Returns 1 if this caller allocated, 0 if it was already
-// there, -1 on arena exhaustion (flag rolled back, like
-// bucket_vector.py:196-201).
-__device__ int alloc_bucket(const Tables &t, uint32_t s, uint32_t b) {
-  uint32_t *f = t.flag + (size_t)s * t.MB + b;
-  for (;;) {
-    uint32_t cur = ld_acquire(f);
-    if (cur == kFlagPublished) return 0;
-    if (cur == 0 && atomicCAS(f, 0u, 1u) == 0u) break;
-    __nanosleep(64);
-  }
-  const uint64_t elems = 1ull << (t.log2fb + b);
-  const uint64_t bytes = (elems * t.esz + 15) & ~15ull;
-  unsigned long long off;
-  int k = atomicSub(&t.fl_n[b], 1);
-  if (k > 0) {
-    off = t.fl[(size_t)b * t.S + (k - 1)];   // reuse a bucket released by shrink
-  } else {
-    atomicAdd(&t.fl_n[b], 1);
-    off = atomicAdd(&t.misc[MISC_TOP], (unsigned long long)bytes);
-  }
-  if (off + bytes > t.arena_mapped) {
-    atomicAdd(&t.misc[MISC_OOM], 1ull);
-    st_release(f, 0);
-    return -1;
-  }
-  t.ptr[(size_t)s * t.MB + b] = t.arena + off;
-  atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
-  atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
-  __threadfence();
-  st_release(f, kFlagPublished);
-  atomicOr(&t.pmask[s], 1ull << b);
-  return 1;
-}
 
 // Host-planned allocation of class-b buckets for every lane with `need`
 // (each (shard, bucket) is requested by exactly one lane, so the once-flags
@@ -1055,12 +981,20 @@ struct Arena {
     CU_TRY(drv().reserve(&base, va, gran, 0, 0));
     return GG_OK;
   }
-  // map physical granules so that [0, bytes) is backed
+  // map physical granules so that [0, bytes) is backed, in pieces of at most
+  // kMapChunk so a later trim() can release unused headroom
+  static constexpr size_t kMapChunk = size_t(64) << 20;
   int ensure(uint64_t bytes) {
-    if (bytes <= mapped) return GG_OK;
-    size_t want = (bytes + gran - 1) / gran * gran;
-    if (want > va) return fail(GG_ENOMEM, "arena VA reservation exhausted");
-    size_t add = want - mapped;
+    while (mapped < bytes) {
+      size_t want = (bytes + gran - 1) / gran * gran;
+      if (want > va) return fail(GG_ENOMEM, "arena VA reservation exhausted");
+      size_t add = std::min(want - mapped, std::max(kMapChunk, gran));
+      int rc = map_piece(add);
+      if (rc) return rc;
+    }
+    return GG_OK;
+  }
+  int map_piece(size_t add) {
     CUmemAllocationProp prop = {};
     prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -1083,11 +1017,12 @@ struct Arena {
       return fail(GG_ECUDA, "cuMemSetAccess failed");
     }
     maps.push_back({mapped, add, h});
-    mapped = want;
+    mapped += add;
     return GG_OK;
   }
   // release whole mappings lying at or above `keep` bytes
   void trim(uint64_t keep) {
+    cudaDeviceSynchronize();
     while (!maps.empty() && maps.back().off >= keep) {
       Map m = maps.back();
       maps.pop_back();
@@ -1254,6 +1189,7 @@ Tables tables_for_launch(gg_array *a, bool with_ctl) {
   if (!with_ctl) t.ctl = nullptr;
   t.arena = (char *)a->arena.base;
   t.arena_mapped = a->arena.mapped;
+  if (a->limit && a->limit < t.arena_mapped) t.arena_mapped = a->limit;   // failure injection
   return t;
 }
 
@@ -1561,6 +1497,27 @@ int check_committed_published(const gg_array *a) {
 }
 
 }  // namespace
+
+namespace gg {
+// Example user kernel of the device API (paper Alg. 1): block b appends the
+// elements i of its slice with pred[i] != 0 to shard b % S, warp- or
+// block-aggregated.
+template <int ESZ, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char *vals,
+                                                   const uint8_t *pred, uint64_t n, int block_mode) {
+  typedef typename ElemT<ESZ>::T E;
+  __shared__ unsigned long long scratch[34];
+  const uint32_t s = blockIdx.x % t.S;
+  for (uint64_t base = (uint64_t)blockIdx.x * BLOCK; base < n; base += (uint64_t)gridDim.x * BLOCK) {
+    const uint64_t i = base + threadIdx.x;
+    const bool p = i < n && pred[i];
+    const E v = p ? reinterpret_cast<const E *>(vals)[i] : E(0);
+    if (block_mode) block_push_back<BLOCK, E>(t, s, p ? 1u : 0u, &v, scratch);
+    else warp_push_back<E>(t, s, p, v);
+  }
+}
+
+}  // namespace gg
 
 // =================================================================== C ABI
 extern "C" {
@@ -2006,6 +1963,91 @@ int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream)
   CUDA_TRY(cudaMemcpyAsync(p, a->h_scratch, a->esz, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return GG_OK;
+}
+
+uint64_t gg_device_view_bytes(void) { return sizeof(gg_device_view); }
+
+int gg_device_view_get(gg_array *a, uint64_t headroom_bytes, void *h_view, uint64_t view_bytes) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  if (view_bytes != sizeof(gg_device_view)) return fail(GG_EVALUE, "view size mismatch (ggarray_device.cuh)");
+  uint64_t want = a->top + headroom_bytes;
+  if (a->limit && want > a->limit) want = std::max<uint64_t>(a->top, a->limit);
+  int rc = a->arena.ensure(want);
+  if (rc) return rc;
+  gg_device_view v = tables_for_launch(a, false);
+  memcpy(h_view, &v, sizeof v);
+  return GG_OK;
+}
+
+// refresh the host mirrors from the device after user kernels appended
+int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  cudaStream_t st = S_(stream);
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const size_t S = a->S;
+  std::vector<uint32_t> f(S * a->MB), status(S);
+  std::vector<unsigned long long> misc(MISC_N);
+  std::vector<int> fln(a->MB);
+  CUDA_TRY(cudaMemcpy(a->size.data(), a->t.size, S * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(a->cap.data(), a->t.cap, S * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(a->ops.data(), a->t.ops, S * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(f.data(), a->t.flag, f.size() * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(status.data(), a->t.status, S * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(misc.data(), a->t.misc, MISC_N * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(fln.data(), a->t.fl_n, a->MB * 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemset(a->t.status, 0, S * 4));
+  bool any = false;
+  for (size_t s = 0; s < S; ++s) {
+    uint64_t m = 0;
+    for (uint32_t b = 0; b < a->MB; ++b)
+      if (f[s * a->MB + b] == kFlagPublished) m |= uint64_t(1) << b;
+    a->flags[s] = m;
+    if (h_status) h_status[s] = (int32_t)status[s];
+    if (status[s]) { any = true; a->dirty[s] = 1; }
+  }
+  a->top = misc[MISC_TOP];
+  a->alloc_calls = misc[MISC_ALLOCS];
+  for (uint32_t b = 0; b < a->MB; ++b) a->fl_count[b] = (uint64_t)std::max(fln[b], 0);
+  a->arena.trim(a->top);          // release mapped headroom the kernel did not use
+  return any ? fail(GG_EPARTIAL, "device-side appends failed on some shards") : GG_OK;
+}
+
+int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t n, int32_t mode,
+               uint32_t grid, int32_t *h_status, void *stream) {
+  cudaStream_t st = S_(stream);
+  if (n == 0) return GG_OK;
+  const uint32_t B = 256;
+  if (!grid) grid = (uint32_t)std::min<uint64_t>((n + B - 1) / B, (uint64_t)a->S * 64);
+  // worst-case headroom: every candidate of shard s appended
+  uint64_t headroom = 0;
+  {
+    std::lock_guard<std::mutex> g(a->mu);
+    std::vector<uint64_t> cand(a->S, 0);
+    const uint64_t per_round = (uint64_t)grid * B;
+    for (uint32_t blk = 0; blk < grid; ++blk) {
+      uint64_t lo = (uint64_t)blk * B, c = 0;
+      for (uint64_t base = lo; base < n; base += per_round) c += std::min<uint64_t>(B, n - base);
+      cand[blk % a->S] += c;
+    }
+    for (uint32_t s = 0; s < a->S; ++s) {
+      uint32_t k = std::min<uint32_t>(min_buckets_for(a, a->size[s] + cand[s]), a->MB);
+      for (uint32_t b = 0; b < k; ++b)
+        if (!(a->flags[s] >> b & 1)) headroom += bucket_bytes(a, b);
+    }
+  }
+  gg_device_view v;
+  int rc = gg_device_view_get(a, headroom, &v, sizeof v);
+  if (rc) return rc;
+  switch (a->esz) {
+    case 1: { k_push_if<1, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_push_if<2, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_push_if<4, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_push_if<8, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+  }
+  CUDA_TRY(cudaGetLastError());
+  return gg_device_view_sync(a, h_status, stream);
 }
 
 int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads) {

@@ -451,6 +451,53 @@ class GrowableArray:
         if commit:
             self.commit()
 
+    # ------------------------------------------------------------ device-side appends
+    def device_view(self, headroom_bytes: int = 0) -> bytes:
+        """Raw ``gg::gg_device_view`` (include/ggarray_device.cuh) for a user kernel
+        that appends with ``warp_push_back`` / ``block_push_back``; maps
+        ``headroom_bytes`` of arena beyond the bump top first.  Call
+        :meth:`device_sync` after the kernel."""
+        n = int(L.lib.gg_device_view_bytes())
+        buf = C.create_string_buffer(n)
+        L.check(L.lib.gg_device_view_get(self._h, int(headroom_bytes), buf, n), "device_view")
+        return buf.raw
+
+    def device_sync(self) -> None:
+        """Refresh the host mirrors after device-side appends; ShardInsertError on
+        shards whose appends failed (reservations kept, as in the reference)."""
+        status = self._status
+        rc = L.lib.gg_device_view_sync(self._h, L.ptr(status, C.c_int32), self._stream())
+        self._dirty()
+        if rc == L.GG_EPARTIAL:
+            failures = {int(s): MemoryError(f"shard {s}: bucket arena exhausted in a device append")
+                        for s in np.flatnonzero(status)}
+            raise ShardInsertError(failures, [])
+        L.check(rc, "device_sync")
+
+    def push_if(self, values, pred, mode: str = "block", grid: int = 0, commit: bool = True) -> None:
+        """Paper Alg. 1 from inside a kernel: block b appends values[i] for the
+        i of its slices with pred[i] to shard b % S (block-scan or warp-ballot
+        offsets, one atomicAdd per block / warp, on-demand bucket allocation)."""
+        import torch
+        vals = self._device_values(values)
+        p = pred if isinstance(pred, torch.Tensor) else torch.from_numpy(np.asarray(pred))
+        p = p.to(device=self.device, dtype=torch.uint8).contiguous()
+        if p.numel() != vals.numel():
+            raise ValueError("values and pred differ in length")
+        status = self._status
+        rc = L.lib.gg_push_if(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
+                              C.c_void_p(p.data_ptr() if p.numel() else 0), vals.numel(),
+                              1 if mode == "block" else 0, int(grid), L.ptr(status, C.c_int32),
+                              self._stream())
+        self._dirty()
+        if rc == L.GG_EPARTIAL:
+            failures = {int(s): MemoryError(f"shard {s}: bucket arena exhausted in a device append")
+                        for s in np.flatnonzero(status)}
+            raise ShardInsertError(failures, [])
+        L.check(rc, "push_if")
+        if commit:
+            self.commit()
+
     def insert_duplicate(self, commit: bool = True) -> None:
         """Every shard appends a copy of its committed contents, read directly from
         its buckets (the bench's _insert_duplicate, bench_cli.py:298-307)."""

@@ -172,3 +172,38 @@ def test_memory_footprint_config1(gg):
     assert ms["capacity_bytes"] == 2_080_768 * 4                 # SURVEY 8c golden
     assert ms["arena_top_bytes"] == ms["capacity_bytes"]          # zero padding in the arena
     assert ms["capacity_bytes"] == gg.ggarray_capacity_for(1 << 20, 512, 32, 4)
+
+
+def test_phased_insert_shrink_vs_oracle_model(gg):
+    """Config 4 at reduced size: uniform(0,2) total-size factors, even split,
+    insert or shrink; state and contents vs the oracle's (unpinned) shrink model."""
+    rng = np.random.default_rng(0)
+    S, fb = 64, 32
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    o = O.OracleGGArray(S, fb, dtype=np.int32)
+    n = 1 << 14
+    vals = np.arange(1 << 17, dtype=np.int32)
+    off = np.minimum(np.arange(S + 1) * (-(-n // S)), n)
+    a.insert_parallel([vals[off[s]:off[s + 1]] for s in range(S)])
+    o.insert_parallel([vals[off[s]:off[s + 1]] for s in range(S)])
+    for _ in range(30):
+        target = int(min(1 << 16, round(rng.uniform(0, 2) * (1 << 14))))
+        q, r = divmod(target, S)
+        new = np.full(S, q, np.int64)
+        new[:r] += 1
+        cur = np.asarray(o.size)
+        if target >= n:
+            d = new - cur
+            offs = np.concatenate([[0], np.cumsum(d)])
+            batches = [vals[offs[s]:offs[s + 1]] for s in range(S)]
+            a.insert_parallel(batches)
+            o.insert_parallel(batches)
+        else:
+            a.shrink(new)
+            o.shrink(new)
+        n = target
+        st = a._parity_state()
+        assert st["sizes"] == [int(x) for x in o.size] and st["caps"] == [int(x) for x in o.capacity]
+        ms = a.memory_stats()
+        assert ms["capacity_bytes"] <= 2 * ms["needed_bytes"] + S * fb * 4
+    assert a.flatten().tobytes() == o.flatten().tobytes()
