@@ -18,7 +18,9 @@ FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-li
 def build(verbose: bool = False) -> str:
     src = os.path.join(PKG, "csrc", "ggarray.cu")
     out = os.path.join(PKG, "_ggarray.so")
-    deps = [src, os.path.join(ROOT, "include", "ggarray.h")]
+    import glob
+    deps = [src, __file__] + glob.glob(os.path.join(ROOT, "include", "*")) + \
+        glob.glob(os.path.join(PKG, "csrc", "*"))
     if os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out
     cmd = [NVCC, *FLAGS, "-o", out + ".tmp", src]

@@ -125,15 +125,24 @@ __device__ inline bool ensure_buckets(const gg_device_view &t, uint32_t s, uint6
   return ok;
 }
 
-// Store one element at local index i of shard s (bucket must be published).
+// Bucket base of (s, b) read with acquire order: the flag load synchronises
+// with the allocator's release, so the pointer read after it is current even
+// if another SM allocated the bucket (plain loads could hit a stale L1 line).
+__device__ __forceinline__ char *bucket_acquire(const gg_device_view &t, uint32_t s, uint32_t b) {
+  if (b >= t.MB || ld_acquire(t.flag + (size_t)s * t.MB + b) != kFlagPublished) return nullptr;
+  char *p;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(p) : "l"(t.ptr + (size_t)s * t.MB + b) : "memory");
+  return p;
+}
+
+// Element store that bypasses L1 (st.global.cg): appended data must survive
+// other warps' acquire loads on this SM, which invalidate its L1.
 template <typename T>
-__device__ __forceinline__ void store_local(const gg_device_view &t, uint32_t s, uint64_t i,
-                                            const T &v) {
-  uint32_t b;
-  uint64_t o;
-  locate(i, t.log2fb, b, o);
-  if (b < t.MB && (t.flag[(size_t)s * t.MB + b] == kFlagPublished || ld_acquire(t.flag + (size_t)s * t.MB + b) == kFlagPublished))
-    reinterpret_cast<T *>(t.ptr[(size_t)s * t.MB + b])[o] = v;
+__device__ __forceinline__ void store_cg(T *p, const T &v) {
+  if constexpr (sizeof(T) == 1) { unsigned char x; memcpy(&x, &v, 1); __stcg((unsigned char *)p, x); }
+  else if constexpr (sizeof(T) == 2) { unsigned short x; memcpy(&x, &v, 2); __stcg((unsigned short *)p, x); }
+  else if constexpr (sizeof(T) == 4) { unsigned int x; memcpy(&x, &v, 4); __stcg((unsigned int *)p, x); }
+  else { unsigned long long x; memcpy(&x, &v, 8); __stcg((unsigned long long *)p, x); }
 }
 
 // Paper Alg. 1, warp flavour: every lane with `pred` appends `value` to shard s
@@ -157,9 +166,16 @@ __device__ inline uint64_t warp_push_back(const gg_device_view &t, uint32_t s, b
   }
   start = __shfl_sync(0xffffffffu, start, 0);
   ok = __shfl_sync(0xffffffffu, ok, 0);
-  __syncwarp();
-  if (!pred || !ok) return ~0ull;
-  store_local(t, s, start + rank, value);
+  if (!ok) return ~0ull;
+  if (!pred) return ~0ull;
+  // each lane resolves its own bucket with an acquire load (no shuffle: a
+  // full-mask shuffle next to the predicated return can be sunk into a
+  // divergent branch by the compiler)
+  uint32_t b;
+  uint64_t o;
+  locate(start + rank, t.log2fb, b, o);
+  char *base = bucket_acquire(t, s, b);
+  if (base) store_cg(reinterpret_cast<T *>(base) + o, value);
   return start + rank;
 }
 
@@ -207,8 +223,24 @@ __device__ inline uint64_t block_push_back(const gg_device_view &t, uint32_t s, 
   }
   __syncthreads();
   const unsigned long long start = scratch[32];
-  if (scratch[33])
-    for (uint32_t e = 0; e < count; ++e) store_local(t, s, start + excl + e, vals[e]);
+  const bool ok = scratch[33] != 0;
+  __shared__ char *bptr[64];
+  if (ok && total) {
+    uint32_t b0, b1;
+    uint64_t o;
+    locate(start, t.log2fb, b0, o);
+    locate(start + total - 1, t.log2fb, b1, o);
+    if (tid <= b1 - b0) bptr[b0 + tid] = bucket_acquire(t, s, b0 + tid);
+  }
+  __syncthreads();
+  if (ok)
+    for (uint32_t e = 0; e < count; ++e) {
+      uint32_t b;
+      uint64_t o;
+      locate(start + excl + e, t.log2fb, b, o);
+      if (bptr[b]) store_cg(reinterpret_cast<T *>(bptr[b]) + o, vals[e]);
+    }
+  __syncthreads();
   return start;
 }
 

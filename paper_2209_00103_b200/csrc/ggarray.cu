@@ -754,6 +754,7 @@ __global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, ch
     // CTA barrier orders the other threads' loads after it)
     if (tid == 0) {
       while (ld_acquire64((const uint64_t *)&t.misc[MISC_RSV]) < n_rsv) __nanosleep(256);
+      __threadfence();   // as in cooperative-groups grid sync: fence after the spin
     }
     __syncthreads();
   }
