@@ -128,7 +128,7 @@ class Step:
 
     def run(self, timed_phases: bool):
         a, torch = self.arr, self.torch
-        a.shrink(0)                                   # reset: buckets -> free lists
+        a.shrink(0, release=False)                    # reset: buckets cached in place
         a.insert_csr(self.vals, self.offsets)         # 2^20 initial elements
         ev = []
         for _ in range(ROUNDS):
@@ -431,7 +431,8 @@ def phased_leg(args, gg, torch, device):
             "mapped_over_needed_final": round(map_ratio[-1], 4),
             "ratios_over": "rounds with total >= base/8",
             "note": "capacity = allocated buckets (reference semantics, <= 2x + fb per shard); "
-                    "mapped = arena high-water mark (released buckets stay mapped on free lists)"}
+                    "mapped = physical slab chunks (shrink(release=True) unmaps chunks left "
+                    "without a live bucket; map/unmap cost is inside ms)"}
 
 
 def split_off(n):
@@ -448,7 +449,7 @@ def e2e_leg(args, gg, torch, device, world, dist):
     res = torch.empty(S, dtype=torch.int64).pin_memory()
 
     def one():
-        arr.shrink(0)
+        arr.shrink(0, release=False)
         arr.insert_csr(host.to(device, non_blocking=True), offs)
         for _ in range(ROUNDS):
             arr.grow(2 * arr.committed_size)

@@ -3,8 +3,11 @@
  *
  * A GGArray is S LFVectors ("shards"); shard s stores its elements in
  * power-of-two buckets, bucket b holding fb*2^b elements, allocated on the
- * device by a bump allocator over one CUDA-VMM arena and never moved.  A
- * committed exclusive prefix over the shard sizes is the global directory.
+ * device (CAS once-flag) in a per-class slab -- bucket (s, b) sits in slot s of
+ * class b's CUDA-VMM region -- and never moved.  Physical memory is mapped
+ * in refcounted chunks as buckets appear and unmapped when a shrink empties
+ * them.  A committed exclusive prefix over the shard sizes is the global
+ * directory.
  *
  * This header is the drop-in boundary.  The reference has no FFI: its
  * boundary is the Python class API of growarray.GrowableArray /
@@ -63,13 +66,14 @@ uint64_t gg_kernel_launches(void);
 
 /* GrowableArray(shards, first_bucket_size, dtype, max_buckets, allocator)
  * sharded_array.py:85-100, bucket_vector.py:84-93,124-137.
- * arena_va_bytes = virtual reservation of the bucket arena (0 = device
- * memory size).  max_buckets <= 64. */
+ * arena_va_bytes = virtual-address budget of the bucket slabs (0 = 16 TiB;
+ * class regions are reserved lazily, S * bucket bytes each).  max_buckets
+ * <= 64. */
 int gg_create(int device, uint32_t shards, uint32_t first_bucket_size, uint32_t dtype,
               uint32_t max_buckets, uint64_t arena_va_bytes, gg_array **out);
 int gg_destroy(gg_array *a);
 int gg_set_alloc_hook(gg_array *a, gg_alloc_hook hook, void *ctx);
-/* Cap on mapped arena bytes (failure injection: allocations past it fail
+/* Cap on live bucket bytes (failure injection: allocations past it fail
  * with MemoryError, like a failing allocator). 0 = no cap. */
 int gg_set_arena_limit(gg_array *a, uint64_t bytes);
 
@@ -119,20 +123,28 @@ int gg_new_bucket(gg_array *a, uint32_t shard, uint32_t bucket, int32_t *h_won, 
 /* AtomicCounter.fetch_add on a shard's size (insert_index.py:52-58) */
 int gg_fetch_add(gg_array *a, uint32_t shard, uint64_t count, uint64_t *h_prev, void *stream);
 /* shrink (extension, no reference semantics): size[s] = h_new_sizes[s] <=
- * size[s]; buckets b >= min_buckets_for(new size) are released to the
- * arena's per-class free lists (reused by later allocations before the bump
- * pointer moves); their granules stay mapped.  Commits. */
+ * size[s]; buckets b >= min_buckets_for(new size) are released.  With
+ * GG_SHRINK_RELEASE the slab chunks left without a live bucket are unmapped
+ * at once (the call then waits for the device); without it they stay mapped
+ * ("cached", reused in place when the buckets come back) until gg_trim.
+ * gg_shrink = gg_shrink_ex(.., GG_SHRINK_RELEASE, ..).  Commits. */
+enum { GG_SHRINK_RELEASE = 1 };
+int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint32_t flags, void *stream);
 int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream);
+/* unmap every cached chunk (waits for the device) */
+int gg_trim(gg_array *a);
 
 /* Device-side appends from user kernels (include/ggarray_device.cuh, paper
- * Alg. 1/2).  gg_device_view_get maps `headroom_bytes` of arena beyond the
- * current bump top and copies the device tables' view (a gg::gg_device_view,
- * view_bytes = sizeof) to h_view for passing to a kernel by value;
- * gg_device_view_sync waits for `stream`, refreshes the host mirrors from the
- * device (sizes, capacities, flags, bump top), releases unused headroom and
- * reports per-shard failures (GG_EPARTIAL).  Neither commits. */
+ * Alg. 1/2).  gg_device_view_get backs the slots of every bucket shard s
+ * needs to reach h_max_sizes[s] elements (NULL = no headroom: appends only
+ * into published buckets) and copies the device tables' view (a
+ * gg::gg_device_view, view_bytes = sizeof) to h_view for passing to a kernel
+ * by value; gg_device_view_sync waits for `stream`, refreshes the host
+ * mirrors from the device (sizes, capacities, flags), unmaps the headroom no
+ * bucket took and reports per-shard failures (GG_EPARTIAL).  Neither
+ * commits; one view at a time per array. */
 uint64_t gg_device_view_bytes(void);
-int gg_device_view_get(gg_array *a, uint64_t headroom_bytes, void *h_view, uint64_t view_bytes);
+int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, uint64_t view_bytes);
 int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream);
 /* Example user kernel of that API: block b of a `grid`-block launch (0 =
  * auto) appends d_vals[i] for every i of its slices with d_pred[i] != 0 to
@@ -180,9 +192,11 @@ int gg_device_state(gg_array *a, uint64_t *h_sizes, uint64_t *h_caps, uint64_t *
                     uint64_t *h_prefix, uint64_t *h_ops, void *stream);
 /* bucket base device pointers [S*max_buckets] (0 = unallocated); syncs */
 int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream);
-/* footprint: [0]=capacity bytes (sum of allocated buckets), [1]=mapped
- * arena bytes, [2]=arena bump top, [3]=needed bytes (sum of sizes),
- * [4]=device alloc calls, [5]=free-list bytes */
+/* footprint: [0]=capacity bytes (elements of allocated buckets x element
+ * size, the reference's capacity), [1]=mapped slab bytes (physical),
+ * [2]=live bucket bytes (16 B rounded), [3]=needed bytes (sum of sizes),
+ * [4]=device alloc calls, [5]=cached bytes (mapped chunks without a live
+ * bucket) */
 int gg_mem_stats(gg_array *a, uint64_t *h_out6, void *stream);
 
 /* ---- baselines (baselines.py) on raw device buffers ---- */

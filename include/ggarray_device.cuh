@@ -12,12 +12,13 @@
  *   gg::warp_push_back(v, shard, pred, value);        // one atomicAdd per warp
  *   gg::block_push_back<BLOCK>(v, shard, count, vals, scratch);  // one per block
  *
- * The view's arena has `arena_mapped` bytes of physical memory behind it (the
- * host maps headroom before the launch: device code cannot map memory);
- * allocations beyond it fail, set status[shard] |= GG_ENOMEM, and the
+ * Device code cannot map memory, so the host backs the slots a launch may
+ * need before it (gg_device_view_get with per-shard worst-case sizes);
+ * allocations of unbacked slots fail, set status[shard] |= GG_ENOMEM, and the
  * reservation is kept, like a failing allocator in the reference
  * (bucket_vector.py:194-201).  After the kernel, gg_device_view_sync()
- * refreshes the host's mirrors from the device tables.
+ * refreshes the host's mirrors from the device tables and unmaps the
+ * headroom no bucket took.
  *
  * The same structures and allocator back the library's own kernels
  * (paper_2209_00103_b200/csrc/ggarray.cu), so there is one implementation.
@@ -30,16 +31,24 @@
 namespace gg {
 
 // Device tables of one GGArray (all pointers are device memory).
+//
+// Bucket storage is a slab per bucket class: class b owns a region of S
+// slots of bucket_bytes(b), slot s belonging to shard s, so bucket (s, b)
+// lives at cbase[b] + s * bucket_bytes(b) for its whole life (address
+// stability, bucket_vector.py:249-255).  Allocation is the CAS once-flag plus
+// that address computation -- no device malloc, no bump pointer.  The host
+// backs slots with physical memory (CUDA VMM chunks, refcounted by live
+// buckets) before any kernel can publish them, and unmaps chunks whose
+// buckets were all released by a shrink.
 struct gg_device_view {
   uint64_t *size, *cap, *ops, *start, *count, *prefix, *offsets;
   uint32_t *ctl, *flag, *status;
-  char **ptr;                 // [S*MB] bucket base pointers
+  char **ptr;                 // [S*MB] bucket base pointers (0 = unallocated)
   unsigned long long *pmask;  // [S] published-bucket bitmask per shard
-  uint64_t *fl;               // [MB*S] per-class free lists of arena offsets (shrink)
-  int *fl_n;                  // [MB] entries per class
-  unsigned long long *misc;   // arena bump top, alloc count, launch counters
-  char *arena;                // base of the VMM bucket arena
-  uint64_t arena_mapped;      // bytes of the arena backed by physical memory
+  unsigned long long *amask;  // [S] slots the host has backed; nullptr = every
+                              // allocation of the launch was planned (and backed)
+  char **cbase;               // [MB] base of class b's slot region
+  unsigned long long *misc;   // alloc count, OOM count, launch counters
   uint32_t S, log2fb, MB, esz;
 };
 
@@ -48,7 +57,7 @@ constexpr uint32_t kStatusNoMem = 4;     // == GG_ENOMEM
 
 // launch-coordination counters live on their own 128 B lines, away from the
 // allocator's bump top (pollers would otherwise contend with its atomics)
-enum { MISC_TOP = 0, MISC_ALLOCS = 1, MISC_OOM = 2, MISC_DONE = 16, MISC_RSV = 32, MISC_TICKET = 48,
+enum { MISC_ALLOCS = 1, MISC_OOM = 2, MISC_DONE = 16, MISC_RSV = 32, MISC_TICKET = 48,
        MISC_N = 64 };
 
 // bucket_vector.py:48-59: b = hibit(i/fb + 1), off = i - fb*(2^b - 1)
@@ -72,11 +81,20 @@ __device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Paper Alg. 2 (new_bucket): CAS the once-flag; the winner takes a bucket from
-// the class free list or bumps the arena top and publishes it with release
+__device__ __forceinline__ uint64_t bucket_bytes(const gg_device_view &t, uint32_t b) {
+  return ((1ull << (t.log2fb + b)) * t.esz + 15) & ~15ull;
+}
+// the fixed slot of bucket (s, b) in class b's slab
+__device__ __forceinline__ char *bucket_slot(const gg_device_view &t, uint32_t s, uint32_t b) {
+  return t.cbase[b] + (uint64_t)s * bucket_bytes(t, b);
+}
+
+// Paper Alg. 2 (new_bucket): CAS the once-flag; the winner takes the shard's
+// slot of class b (if the host backed it) and publishes it with release
 // order; losers wait for the publication (or retry after a rollback).
-// Returns 1 if this caller allocated, 0 if the bucket was already there, -1 on
-// arena exhaustion (flag rolled back, like bucket_vector.py:196-201).
+// Returns 1 if this caller allocated, 0 if the bucket was already there, -1 if
+// the slot has no physical memory behind it (flag rolled back, like
+// bucket_vector.py:196-201).
 __device__ inline int alloc_bucket(const gg_device_view &t, uint32_t s, uint32_t b) {
   uint32_t *f = t.flag + (size_t)s * t.MB + b;
   for (;;) {
@@ -85,23 +103,13 @@ __device__ inline int alloc_bucket(const gg_device_view &t, uint32_t s, uint32_t
     if (cur == 0 && atomicCAS(f, 0u, 1u) == 0u) break;
     __nanosleep(64);
   }
-  const uint64_t elems = 1ull << (t.log2fb + b);
-  const uint64_t bytes = (elems * t.esz + 15) & ~15ull;
-  unsigned long long off;
-  int k = atomicSub(&t.fl_n[b], 1);
-  if (k > 0) {
-    off = t.fl[(size_t)b * t.S + (k - 1)];   // reuse a bucket released by shrink
-  } else {
-    atomicAdd(&t.fl_n[b], 1);
-    off = atomicAdd(&t.misc[MISC_TOP], (unsigned long long)bytes);
-  }
-  if (off + bytes > t.arena_mapped) {
+  if (t.amask && !((t.amask[s] >> b) & 1ull)) {
     atomicAdd(&t.misc[MISC_OOM], 1ull);
     st_release(f, 0);
     return -1;
   }
-  t.ptr[(size_t)s * t.MB + b] = t.arena + off;
-  atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
+  t.ptr[(size_t)s * t.MB + b] = bucket_slot(t, s, b);
+  atomicAdd((unsigned long long *)&t.cap[s], 1ull << (t.log2fb + b));
   atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
   __threadfence();
   st_release(f, kFlagPublished);

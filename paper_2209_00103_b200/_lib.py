@@ -60,9 +60,11 @@ _SIGS = {
     "gg_new_bucket": ([P, U32, U32, PI32, P], C.c_int),
     "gg_fetch_add": ([P, U32, U64, PU64, P], C.c_int),
     "gg_shrink": ([P, PU64, P], C.c_int),
+    "gg_shrink_ex": ([P, PU64, U32, P], C.c_int),
+    "gg_trim": ([P], C.c_int),
     "gg_rw_add": ([P, P, U32, I32, P], C.c_int),
     "gg_device_view_bytes": ([], U64),
-    "gg_device_view_get": ([P, U64, P, U64], C.c_int),
+    "gg_device_view_get": ([P, PU64, P, U64], C.c_int),
     "gg_device_view_sync": ([P, PI32, P], C.c_int),
     "gg_push_if": ([P, P, P, U64, I32, U32, PI32, P], C.c_int),
     "gg_flatten": ([P, P, P], C.c_int),

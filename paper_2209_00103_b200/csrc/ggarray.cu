@@ -3,19 +3,21 @@
 // commit, r/w, flatten, gather/scatter) behind the C ABI in include/ggarray.h.
 //
 // Layout in HBM (one handle per GPU):
-//   * metadata (plain cudaMalloc, never in the arena): size[S], cap[S],
+//   * metadata (plain cudaMalloc, never in the slabs): size[S], cap[S],
 //     ops[S], start[S], count[S], prefix[S+1], offsets[S+1], ctl[S],
 //     flag[S*MB] (u32 once-flags: 0 free, 1 allocating, 2 published),
-//     ptr[S*MB] (bucket base pointers), misc[] (arena bump top, alloc calls).
-//   * bucket arena: one cuMemAddressReserve'd VA range; physical 2 MiB
-//     granules are mapped by the host up to the exact bump top the planner
-//     predicts BEFORE a launch; buckets are bump-allocated on the device
-//     with byte-exact packing (16 B alignment; every bucket of fb=32 int32 is
-//     a multiple of 128 B so the packing has zero padding).
-// The host keeps exact mirrors of sizes / flags / capacities / the bump top
-// (every quantity is a deterministic function of the op sequence), which
-// lets it map memory, raise the reference's errors and run the allocator
-// hook without any device round trip per insert.
+//     ptr[S*MB] (bucket base pointers), pmask/amask[S], cbase[MB], misc[].
+//   * bucket slabs: class b owns a VA region of S slots of bucket_bytes(b)
+//     (classes whose region is below one 2 MiB granule share one packed
+//     region), so bucket (s, b) always lives at cbase[b] + s*bytes(b).  The
+//     host backs slots with physical memory in chunks (cuMemCreate/cuMemMap,
+//     refcounted by live buckets) before a launch can publish them, and a
+//     shrink unmaps chunks none of whose buckets is live any more -- the
+//     footprint follows the live capacity (<= 2x the needed bytes) both ways.
+// The host keeps exact mirrors of sizes / flags / capacities (every quantity
+// is a deterministic function of the op sequence), which lets it back
+// memory, raise the reference's errors and run the allocator hook without
+// any device round trip per insert.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -101,6 +103,7 @@ Drv &drv() {
   } while (0)
 
 constexpr int kMaxBuckets = 64;
+constexpr uint64_t kDefaultVaBudget = uint64_t(16) << 40;   // slab VA per array (16 TiB)
 constexpr int kThreads = 256;          // CTA size of the streaming kernels
 constexpr int kTileBytes = 32 * 1024;  // bytes of payload per tile
 
@@ -133,41 +136,16 @@ template <> struct ElemT<8> { typedef unsigned long long T; };
 
 // Host-planned allocation of class-b buckets for every lane with `need`
 // (each (shard, bucket) is requested by exactly one lane, so the once-flags
-// are uncontended): ONE free-list pop and at most ONE bump of the arena top per
-// warp and class -- the paper's "one atomic per group" applied to the
-// allocator.  Slots are handed out in lane rank order.
+// are uncontended and the slot is the shard's own: no address atomics at
+// all; one counter update per warp and class).
 __device__ __forceinline__ void warp_alloc_class(const Tables &t, bool need, uint32_t s,
                                                  uint32_t b) {
   const unsigned m = __ballot_sync(0xffffffffu, need);
   if (!m) return;
-  const uint32_t lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-  const uint32_t cnt = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
-  const uint64_t elems = 1ull << (t.log2fb + b);
-  const uint64_t bytes = (elems * t.esz + 15) & ~15ull;
-  int k = 0;
-  uint32_t npop = 0;
-  unsigned long long bump = 0;
-  if (lane == leader) {
-    k = atomicSub(&t.fl_n[b], (int)cnt);             // entries [k-cnt, k) are ours if >= 0
-    npop = k > 0 ? min((uint32_t)k, cnt) : 0u;
-    if (npop < cnt) {
-      atomicAdd(&t.fl_n[b], (int)(cnt - npop));       // return the overdraft
-      bump = atomicAdd(&t.misc[MISC_TOP], (unsigned long long)((cnt - npop) * bytes));
-    }
-    atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)cnt);
-  }
-  k = __shfl_sync(0xffffffffu, k, leader);
-  npop = __shfl_sync(0xffffffffu, npop, leader);
-  bump = __shfl_sync(0xffffffffu, bump, leader);
+  if ((threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)__popc(m));
   if (!need) return;
-  const unsigned long long off =
-      rank < npop ? t.fl[(size_t)b * t.S + (k - 1 - rank)] : bump + (rank - npop) * bytes;
-  if (off + bytes > t.arena_mapped) {                 // cannot happen for planned ops
-    atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
-    return;
-  }
-  t.ptr[(size_t)s * t.MB + b] = t.arena + off;
-  atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)elems);
+  t.ptr[(size_t)s * t.MB + b] = bucket_slot(t, s, b);
+  atomicAdd((unsigned long long *)&t.cap[s], 1ull << (t.log2fb + b));
   __threadfence();
   st_release(t.flag + (size_t)s * t.MB + b, kFlagPublished);
   atomicOr(&t.pmask[s], 1ull << b);
@@ -386,40 +364,25 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
   }
 }
 
-// shrink (extension): block per bucket class b; a block scan over the shards
-// gives every released bucket its free-list slot in shard order
-// (deterministic), so the whole release is one parallel pass.
-__global__ void __launch_bounds__(1024) k_shrink_release(Tables t, const uint64_t *new_sizes) {
-  __shared__ uint64_t ws[32];
-  const uint32_t b = blockIdx.x;
-  const uint64_t fbv = 1ull << t.log2fb;
-  uint64_t base = (uint64_t)t.fl_n[b];
-  for (uint32_t s0 = 0; s0 < t.S; s0 += blockDim.x) {
-    const uint32_t s = s0 + threadIdx.x;
-    bool rel = false;
-    if (s < t.S) {
-      const uint64_t ns = new_sizes[s];
-      const uint32_t keep =
-          ns ? (64u - (uint32_t)__clzll((long long)((ns + fbv - 1) >> t.log2fb))) : 0u;
-      rel = b >= keep && t.flag[(size_t)s * t.MB + b] == kFlagPublished;
-    }
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_scan(rel ? 1 : 0, &tot, ws);
-    if (rel) {
-      t.fl[(size_t)b * t.S + base + ex] = (uint64_t)(t.ptr[(size_t)s * t.MB + b] - t.arena);
+// shrink (extension): thread per shard; size[s] = new size, buckets
+// b >= min_buckets_for(new size) unpublished (their slots stay reserved for
+// the shard; the host unmaps chunks that lost their last live bucket).
+__global__ void k_shrink(Tables t, const uint64_t *new_sizes) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= t.S) return;
+  const uint64_t ns = new_sizes[s];
+  const uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + (1ull << t.log2fb) - 1) >> t.log2fb))) : 0u;
+  unsigned long long m = t.pmask[s], freed = 0;
+  for (uint32_t b = keep; b < t.MB; ++b)
+    if ((m >> b) & 1ull) {
       t.ptr[(size_t)s * t.MB + b] = nullptr;
       t.flag[(size_t)s * t.MB + b] = 0;
-      atomicAnd(&t.pmask[s], ~(1ull << b));
-      atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)(0ull - (fbv << b)));
+      freed += 1ull << (t.log2fb + b);
     }
-    base += tot;
-  }
-  if (threadIdx.x == 0) t.fl_n[b] = (int)base;
-}
-
-__global__ void k_shrink_sizes(Tables t, const uint64_t *new_sizes) {
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < t.S) t.size[s] = new_sizes[s];
+  if (keep < 64) m &= (1ull << keep) - 1ull;
+  t.pmask[s] = m;
+  t.cap[s] -= freed;
+  t.size[s] = ns;
 }
 
 // ---- streaming primitives: a CTA moves one contiguous piece -------------
@@ -1039,6 +1002,191 @@ struct Arena {
   }
 };
 
+// Slab store of one GGArray: a VA region per bucket class, slot s of class b
+// = bucket (s, b).  Physical memory is mapped per chunk (a gran-multiple
+// piece of a region) and refcounted by the live buckets overlapping it, so
+// releasing buckets returns memory as soon as a chunk empties.  Classes whose
+// region is smaller than one granule share one packed region ("small"), so a
+// tiny array costs one granule, not one per class.
+struct Slab {
+  struct Chunk { uint32_t refs = 0; bool mapped = false; CUmemGenericAllocationHandle h = 0; };
+  struct Region { CUdeviceptr base = 0; size_t va = 0, chunk = 0; std::vector<Chunk> chunks; };
+  static constexpr size_t kChunk = size_t(64) << 20;   // mapping unit of large regions
+  int dev = 0;
+  size_t gran = 0;
+  uint32_t S = 0, MB = 0;
+  uint64_t va_budget = 0, va_used = 0, mapped = 0, cached = 0;  // cached: mapped, 0 refs
+  std::vector<uint64_t> bytes;        // bucket bytes per class (powers of two >= 16)
+  std::vector<uint64_t> small_off;    // offset in the small region, ~0 = own region
+  Region small;
+  std::vector<Region> big;
+
+  int init(int device, uint32_t shards, uint32_t mb, const std::vector<uint64_t> &bb, uint64_t budget) {
+    dev = device; S = shards; MB = mb; bytes = bb; va_budget = budget;
+    if (!drv().ok) return fail(GG_ECUDA, "CUDA driver VMM entry points unavailable");
+    CUmemAllocationProp prop = props();
+    CU_TRY(drv().granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+    small_off.assign(MB, ~uint64_t(0));
+    big.assign(MB, Region());
+    uint64_t off = 0;
+    for (uint32_t b = 0; b < MB; ++b) {
+      const long double r = (long double)S * bytes[b];
+      if (r >= gran) break;
+      small_off[b] = off;
+      off += S * bytes[b];
+    }
+    if (off) {
+      small.va = round_up(off, gran);
+      small.chunk = gran;
+      small.chunks.assign(small.va / gran, Chunk());
+      int rc = reserve_va(small);
+    if (rc) return rc;
+    }
+    return GG_OK;
+  }
+  static size_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+  CUmemAllocationProp props() const {
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = dev;
+    return prop;
+  }
+  int reserve_va(Region &r) {
+    if (va_used + r.va > va_budget) return fail(GG_ENOMEM, "slab VA budget exhausted");
+    CUresult e = drv().reserve(&r.base, r.va, r.chunk, 0, 0);
+    if (e != CUDA_SUCCESS) { r.base = 0; return fail(GG_ENOMEM, "cuMemAddressReserve failed (VA exhausted)"); }
+    va_used += r.va;
+    return GG_OK;
+  }
+  // mapping unit of class b's region: a power of two >= one granule and >=
+  // one bucket, about 1/16 of the region (so a partly live top class -- an
+  // uneven split -- strands at most one chunk), at most kChunk otherwise
+  uint64_t chunk_for(uint32_t b) const {
+    if (bytes[b] >= kChunk) return bytes[b];
+    const uint64_t R = S * bytes[b];
+    uint64_t c = gran;
+    while (c < kChunk && c * 32 <= R) c <<= 1;
+    return std::max<uint64_t>(c, bytes[b]);
+  }
+  Region &region(uint32_t b) { return small_off[b] != ~uint64_t(0) ? small : big[b]; }
+  // reserve class b's region on first use; *created = true if it is new
+  int ensure_region(uint32_t b, bool *created) {
+    *created = false;
+    if (small_off[b] != ~uint64_t(0)) return GG_OK;
+    Region &r = big[b];
+    if (r.base) return GG_OK;
+    const long double want = (long double)S * bytes[b];
+    if (want > (long double)va_budget) return fail(GG_ENOMEM, "bucket class region exceeds the VA budget");
+    const uint64_t R = S * bytes[b];
+    r.chunk = chunk_for(b);
+    r.va = round_up(R, r.chunk);
+    r.chunks.assign(r.va / r.chunk, Chunk());
+    int rc = reserve_va(r);
+    if (rc) { r = Region(); return rc; }
+    *created = true;
+    return GG_OK;
+  }
+  uint64_t class_base(uint32_t b) const {
+    if (small_off[b] != ~uint64_t(0)) return (uint64_t)small.base + small_off[b];
+    return (uint64_t)big[b].base;
+  }
+  void span(uint32_t s, uint32_t b, Region *&r, size_t &c0, size_t &c1) {
+    r = &region(b);
+    const uint64_t off = (small_off[b] != ~uint64_t(0) ? small_off[b] : 0) + (uint64_t)s * bytes[b];
+    c0 = off / r->chunk;
+    c1 = (off + bytes[b] - 1) / r->chunk;
+  }
+  int map_chunk(Region &r, size_t c) {
+    Chunk &k = r.chunks[c];
+    if (k.mapped) { if (!k.refs) cached -= r.chunk; return GG_OK; }
+    CUmemAllocationProp prop = props();
+    CU_TRY(drv().create(&k.h, r.chunk, &prop, 0));
+    const CUdeviceptr at = r.base + c * r.chunk;
+    if (drv().map(at, r.chunk, 0, k.h, 0) != CUDA_SUCCESS) {
+      drv().release(k.h);
+      return fail(GG_ENOMEM, "cuMemMap failed");
+    }
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (drv().set_access(at, r.chunk, &acc, 1) != CUDA_SUCCESS) {
+      drv().unmap(at, r.chunk);
+      drv().release(k.h);
+      return fail(GG_ENOMEM, "cuMemSetAccess failed");
+    }
+    k.mapped = true;
+    mapped += r.chunk;
+    return GG_OK;
+  }
+  void unmap_chunk(Region &r, size_t c) {
+    Chunk &k = r.chunks[c];
+    drv().unmap(r.base + c * r.chunk, r.chunk);
+    drv().release(k.h);
+    k.mapped = false;
+    k.h = 0;
+    mapped -= r.chunk;
+    cached -= r.chunk;
+  }
+  // back bucket (s, b) with physical memory (region must exist)
+  int back(uint32_t s, uint32_t b) {
+    Region *r; size_t c0, c1;
+    span(s, b, r, c0, c1);
+    for (size_t c = c0; c <= c1; ++c) {
+      int rc = map_chunk(*r, c);
+      if (rc) {                                  // undo this bucket's earlier chunks
+        for (size_t d = c0; d < c; ++d) drop(*r, d);
+        return rc;
+      }
+      r->chunks[c].refs += 1;
+    }
+    return GG_OK;
+  }
+  void drop(Region &r, size_t c) {
+    Chunk &k = r.chunks[c];
+    if (--k.refs == 0) cached += r.chunk;      // stays mapped until trim()
+  }
+  // bucket (s, b) is no longer live
+  void unback(uint32_t s, uint32_t b) {
+    Region *r; size_t c0, c1;
+    span(s, b, r, c0, c1);
+    for (size_t c = c0; c <= c1; ++c) drop(*r, c);
+  }
+  // bytes backing (s, b) would newly map
+  uint64_t new_bytes(uint32_t s, uint32_t b) {
+    if (small_off[b] == ~uint64_t(0) && !big[b].base) return chunk_for(b);
+    Region *r; size_t c0, c1;
+    span(s, b, r, c0, c1);
+    uint64_t n = 0;
+    for (size_t c = c0; c <= c1; ++c) if (!r->chunks[c].mapped) n += r->chunk;
+    return n;
+  }
+  // unmap every chunk without live buckets (caller synchronised the device)
+  void trim() {
+    auto go = [&](Region &r) {
+      for (size_t c = 0; c < r.chunks.size(); ++c)
+        if (r.chunks[c].mapped && r.chunks[c].refs == 0) unmap_chunk(r, c);
+    };
+    go(small);
+    for (auto &r : big) go(r);
+  }
+  void destroy() {
+    auto go = [&](Region &r) {
+      for (size_t c = 0; c < r.chunks.size(); ++c)
+        if (r.chunks[c].mapped) {
+          drv().unmap(r.base + c * r.chunk, r.chunk);
+          drv().release(r.chunks[c].h);
+        }
+      if (r.base) drv().addr_free(r.base, r.va);
+      r = Region();
+    };
+    go(small);
+    for (auto &r : big) go(r);
+    mapped = cached = va_used = 0;
+  }
+};
+
 int g_sms[64] = {0};
 
 // runtime tuning of the 4-byte streaming kernels (sweep); -1 / 0 = default
@@ -1138,14 +1286,15 @@ struct gg_array {
   // exact host mirrors
   std::vector<uint64_t> size, cap, ops, prefix, flags;  // flags: bitmask per shard
   std::vector<uint8_t> dirty;                            // shard saw a failed reservation
-  uint64_t top = 0;                                      // arena bump top (bytes)
+  uint64_t live = 0;                                     // bytes of live buckets
   uint32_t epoch = 0;                                    // fused-launch ready-flag epoch
-  std::vector<uint64_t> fl_count;                        // free-list entries per class
+  std::vector<uint32_t> headroom;                        // (s, b) backed for a device view
+  bool cbase_dirty = false;                              // a class region appeared
   uint64_t alloc_calls = 0;
-  uint64_t limit = 0;                                    // mapped-bytes cap (0 = none)
+  uint64_t limit = 0;                                    // live-bytes cap (0 = none)
   gg_alloc_hook hook = nullptr;
   void *hook_ctx = nullptr;
-  Arena arena;
+  Slab slab;
   Uploader up;
   Tables t;          // device pointers (kernel argument)
   void *dmem = nullptr;
@@ -1158,8 +1307,10 @@ struct gg_array {
 namespace {
 
 inline uint64_t bucket_elems(const gg_array *a, uint32_t b) { return uint64_t(a->fb) << b; }
+// saturates at 2^63 for classes no device could hold (max_buckets up to 64)
 inline uint64_t bucket_bytes(const gg_array *a, uint32_t b) {
-  return round16(bucket_elems(a, b) * a->esz);
+  const uint32_t lg = a->log2fb + b + (uint32_t)ilog2(a->esz);
+  return lg >= 63 ? (uint64_t(1) << 63) : round16(bucket_elems(a, b) * a->esz);
 }
 inline void host_locate(const gg_array *a, uint64_t i, uint32_t &b, uint64_t &off) {
   uint64_t q = (i >> a->log2fb) + 1;
@@ -1188,16 +1339,17 @@ int grid_for(const gg_array *a, uint64_t tiles, int per_sm = 8) {
 Tables tables_for_launch(gg_array *a, bool with_ctl) {
   Tables t = a->t;
   if (!with_ctl) t.ctl = nullptr;
-  t.arena = (char *)a->arena.base;
-  t.arena_mapped = a->arena.mapped;
-  if (a->limit && a->limit < t.arena_mapped) t.arena_mapped = a->limit;   // failure injection
+  t.amask = nullptr;          // library launches only publish host-backed buckets
   return t;
 }
 
 // Plan of one allocating operation, computed on the host before launch.
+// Backing (physical mapping) happens while planning, so a real out-of-memory
+// fails exactly the shard whose bucket could not be had, like a failing
+// allocator in the reference (bucket_vector.py:194-201).
 struct Plan {
-  std::vector<uint64_t> size, cap, flags, fl_count;
-  uint64_t top, alloc_calls;
+  std::vector<uint64_t> size, cap, flags;
+  uint64_t live, alloc_calls;
   std::vector<uint32_t> ctl;        // per shard
   std::vector<int32_t> status;      // per shard
   std::vector<uint32_t> zero_pairs; // (s, b) buckets to zero after allocation
@@ -1205,24 +1357,28 @@ struct Plan {
 };
 
 void plan_init(const gg_array *a, Plan &p) {
-  p.size = a->size; p.cap = a->cap; p.flags = a->flags; p.fl_count = a->fl_count;
-  p.top = a->top; p.alloc_calls = a->alloc_calls;
+  p.size = a->size; p.cap = a->cap; p.flags = a->flags;
+  p.live = a->live; p.alloc_calls = a->alloc_calls;
   p.ctl.assign(a->S, kCtlWrite | a->MB);
   p.status.assign(a->S, GG_OK);
 }
 
-// Try to allocate bucket b of shard s in the plan; false on (hook/arena) failure.
+// reserve class b's region if needed and back slot (s, b)
+int back_bucket(gg_array *a, uint32_t s, uint32_t b) {
+  bool created = false;
+  int rc = a->slab.ensure_region(b, &created);
+  if (rc) return rc;
+  if (created) a->cbase_dirty = true;
+  return a->slab.back(s, b);
+}
+
+// Try to allocate bucket b of shard s in the plan; false on (hook/memory) failure.
 bool plan_alloc(gg_array *a, Plan &p, uint32_t s, uint32_t b) {
   if (a->hook && a->hook(a->hook_ctx, s, b, bucket_elems(a, b)) != 0) return false;
-  uint64_t nb = bucket_bytes(a, b);
-  uint64_t cap_bytes = a->arena.va;
-  if (a->limit && a->limit < cap_bytes) cap_bytes = a->limit;
-  if (p.fl_count[b] > 0) {
-    p.fl_count[b] -= 1;                      // device pops the class free list
-  } else {
-    if (p.top + nb > cap_bytes) return false;
-    p.top += nb;
-  }
+  const uint64_t nb = bucket_bytes(a, b);
+  if (a->limit && p.live + nb > a->limit) return false;
+  if (back_bucket(a, s, b) != GG_OK) return false;
+  p.live += nb;
   p.flags[s] |= uint64_t(1) << b;
   p.cap[s] += bucket_elems(a, b);
   p.alloc_calls += 1;
@@ -1258,14 +1414,26 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
   }
 }
 
-int commit_plan(gg_array *a, Plan &p) {
-  int rc = a->arena.ensure(p.top);
+// class bases travel to the device when a new class region was reserved
+int push_cbase(gg_array *a, cudaStream_t st) {
+  if (!a->cbase_dirty) return GG_OK;
+  std::vector<uint64_t> cb(a->MB);
+  for (uint32_t b = 0; b < a->MB; ++b) cb[b] = a->slab.class_base(b);
+  void *dst[1] = {a->t.cbase};
+  const void *src[1] = {cb.data()};
+  size_t bytes[1] = {a->MB * sizeof(uint64_t)};
+  int rc = a->up.upload(st, 1, dst, src, bytes);
   if (rc) return rc;
-  a->size = p.size; a->cap = p.cap; a->flags = p.flags; a->fl_count = p.fl_count;
-  a->top = p.top; a->alloc_calls = p.alloc_calls;
+  a->cbase_dirty = false;
+  return GG_OK;
+}
+
+int commit_plan(gg_array *a, Plan &p, cudaStream_t st) {
+  a->size = p.size; a->cap = p.cap; a->flags = p.flags;
+  a->live = p.live; a->alloc_calls = p.alloc_calls;
   for (uint32_t s = 0; s < a->S; ++s)
     if (p.status[s] != GG_OK) a->dirty[s] = 1;
-  return GG_OK;
+  return push_cbase(a, st);
 }
 
 // tile of a streaming launch: 32 KiB, shrunk (down to 4 KiB) until the grid
@@ -1367,7 +1535,7 @@ void host_commit(gg_array *a) {
 int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src,
                uint64_t total, cudaStream_t st, uint32_t flags, bool *committed) {
   *committed = false;
-  int rc = commit_plan(a, p);
+  int rc = commit_plan(a, p, st);
   if (rc) return rc;
   Tables t = tables_for_launch(a, p.any_ctl);
   if (p.any_ctl) {
@@ -1547,14 +1715,11 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   a->esz = esz; a->MB = max_buckets;
   a->size.assign(shards, 0); a->cap.assign(shards, 0); a->ops.assign(shards, 0);
   a->prefix.assign(shards + 1, 0); a->flags.assign(shards, 0); a->dirty.assign(shards, 0);
-  a->fl_count.assign(max_buckets, 0);
-  if (arena_va_bytes == 0) {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    arena_va_bytes = tot ? tot : (uint64_t(1) << 36);
-  }
-  int rc = a->arena.init(device, arena_va_bytes);
-  if (rc) { delete a; return rc; }
+  if (arena_va_bytes == 0) arena_va_bytes = kDefaultVaBudget;
+  std::vector<uint64_t> bb(max_buckets);
+  for (uint32_t b = 0; b < max_buckets; ++b) bb[b] = bucket_bytes(a, b);
+  int rc = a->slab.init(device, shards, max_buckets, bb, arena_va_bytes);
+  if (rc) { a->slab.destroy(); delete a; return rc; }
   // metadata block
   const size_t S = shards, T = S * max_buckets;
   size_t bytes = 0;
@@ -1562,10 +1727,10 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   size_t o_size = take(S * 8), o_cap = take(S * 8), o_ops = take(S * 8), o_start = take(S * 8),
          o_count = take(S * 8), o_prefix = take((S + 1) * 8), o_off = take((S + 1) * 8),
          o_ctl = take(S * 4), o_flag = take(T * 4), o_status = take(S * 4), o_ptr = take(T * 8),
-         o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_fl = take(T * 8),
-         o_fln = take(max_buckets * 4), o_pm = take(S * 8);
+         o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_am = take(S * 8),
+         o_cb = take(max_buckets * 8), o_pm = take(S * 8);
   cudaError_t e = cudaMalloc(&a->dmem, bytes);
-  if (e != cudaSuccess) { a->arena.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
+  if (e != cudaSuccess) { a->slab.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
   cudaMemset(a->dmem, 0, bytes);
   char *base = (char *)a->dmem;
   Tables &t = a->t;
@@ -1575,7 +1740,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   t.offsets = (uint64_t *)(base + o_off); t.ctl = (uint32_t *)(base + o_ctl);
   t.flag = (uint32_t *)(base + o_flag); t.status = (uint32_t *)(base + o_status);
   t.ptr = (char **)(base + o_ptr); t.misc = (unsigned long long *)(base + o_misc);
-  t.fl = (uint64_t *)(base + o_fl); t.fl_n = (int *)(base + o_fln);
+  t.amask = (unsigned long long *)(base + o_am); t.cbase = (char **)(base + o_cb);
   t.pmask = (unsigned long long *)(base + o_pm);
   t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
   a->d_won = (int *)(base + o_won);
@@ -1583,6 +1748,11 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   if ((rc = a->up.init(std::max<size_t>(4 * (S + 1) * 8, 4096)))) { gg_destroy(a); return rc; }
   e = cudaMallocHost(&a->h_scratch, 64);
   if (e != cudaSuccess) { gg_destroy(a); return fail(GG_ECUDA, cudaGetErrorString(e)); }
+  if (a->slab.small.base) {           // the packed small-class region exists from the start
+    std::vector<uint64_t> cb(max_buckets);
+    for (uint32_t b = 0; b < max_buckets; ++b) cb[b] = a->slab.class_base(b);
+    CUDA_TRY(cudaMemcpy(t.cbase, cb.data(), max_buckets * 8, cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(cudaDeviceSynchronize());
   *out = a;
   return GG_OK;
@@ -1595,7 +1765,7 @@ int gg_destroy(gg_array *a) {
   a->up.destroy();
   if (a->h_scratch) cudaFreeHost(a->h_scratch);
   if (a->dmem) cudaFree(a->dmem);
-  a->arena.destroy();
+  a->slab.destroy();
   delete a;
   return GG_OK;
 }
@@ -1715,7 +1885,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
     }
   }
   if (any) {
-    int rc = commit_plan(a, p);
+    int rc = commit_plan(a, p, st);
     if (rc) return rc;
     // uniform target without failures: every shard allocates [0, k) -- no upload
     bool uniform = err == GG_OK;
@@ -1756,7 +1926,7 @@ int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *str
   Plan p;
   plan_init(a, p);
   if (!plan_alloc(a, p, s, b)) return fail(GG_ENOMEM, "bucket allocation failed");
-  int rc = commit_plan(a, p);
+  int rc = commit_plan(a, p, st);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
   { k_new_bucket<<<1, 1, 0, st>>>(t, s, b, a->d_won); g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -1787,7 +1957,7 @@ int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *st
   return GG_OK;
 }
 
-int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
+int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint32_t flags, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
@@ -1799,7 +1969,8 @@ int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
       if (a->flags[s] >> b & 1) {
         a->flags[s] &= ~(uint64_t(1) << b);
         a->cap[s] -= bucket_elems(a, b);
-        a->fl_count[b] += 1;
+        a->live -= bucket_bytes(a, b);
+        a->slab.unback(s, b);
       }
     a->size[s] = h_new_sizes[s];
   }
@@ -1809,13 +1980,34 @@ int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
   int rc = a->up.upload(st, 1, dst, src, bytes);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
-  { k_shrink_release<<<a->MB, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
-  { k_shrink_sizes<<<(a->S + 255) / 256, 256, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  { k_shrink<<<(a->S + 255) / 256, 256, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
   CUDA_TRY(cudaGetLastError());
   uint64_t acc = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
   { k_commit<<<1, 1024, 0, st>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
   CUDA_TRY(cudaGetLastError());
+  // GG_SHRINK_RELEASE: unmap emptied chunks now (waits for the device: queued
+  // work may still read the released buckets).  Not under graph capture,
+  // where the chunks stay cached until gg_trim.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  if ((flags & GG_SHRINK_RELEASE) && cap == cudaStreamCaptureStatusNone && a->slab.cached) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    a->slab.trim();
+  }
+  return GG_OK;
+}
+
+int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
+  return gg_shrink_ex(a, h_new_sizes, GG_SHRINK_RELEASE, stream);
+}
+
+int gg_trim(gg_array *a) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  if (!a->slab.cached) return GG_OK;
+  CUDA_TRY(cudaDeviceSynchronize());
+  a->slab.trim();
   return GG_OK;
 }
 
@@ -1846,7 +2038,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
   Plan p;
   plan_init(a, p);
   plan_append(a, p, counts.data(), nullptr);
-  if ((rc = commit_plan(a, p))) return rc;
+  if ((rc = commit_plan(a, p, st))) return rc;
   Tables t = tables_for_launch(a, p.any_ctl);
   if (p.any_ctl) {
     void *d2[1] = {a->t.ctl};
@@ -1968,15 +2160,36 @@ int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream)
 
 uint64_t gg_device_view_bytes(void) { return sizeof(gg_device_view); }
 
-int gg_device_view_get(gg_array *a, uint64_t headroom_bytes, void *h_view, uint64_t view_bytes) {
+int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, uint64_t view_bytes) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   if (view_bytes != sizeof(gg_device_view)) return fail(GG_EVALUE, "view size mismatch (ggarray_device.cuh)");
-  uint64_t want = a->top + headroom_bytes;
-  if (a->limit && want > a->limit) want = std::max<uint64_t>(a->top, a->limit);
-  int rc = a->arena.ensure(want);
+  if (!a->headroom.empty()) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
+  // back every slot the launch may take: buckets [0, min_buckets_for(max)) per
+  // shard, in shard then bucket order, while the live-bytes cap allows
+  std::vector<unsigned long long> am(a->S);
+  uint64_t live = a->live;
+  bool stop = false;
+  for (uint32_t s = 0; s < a->S; ++s) {
+    am[s] = a->flags[s];
+    if (!h_max_sizes || stop) continue;
+    const uint32_t k = std::min<uint32_t>(min_buckets_for(a, h_max_sizes[s]), a->MB);
+    for (uint32_t b = 0; b < k; ++b) {
+      if (a->flags[s] >> b & 1) continue;
+      const uint64_t nb = bucket_bytes(a, b);
+      if ((a->limit && live + nb > a->limit) || back_bucket(a, s, b) != GG_OK) { stop = true; break; }
+      live += nb;
+      am[s] |= 1ull << b;
+      a->headroom.push_back(s);
+      a->headroom.push_back(b);
+    }
+  }
+  int rc = push_cbase(a, 0);
   if (rc) return rc;
-  gg_device_view v = tables_for_launch(a, false);
+  CUDA_TRY(cudaMemcpy(a->t.amask, am.data(), a->S * 8, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaDeviceSynchronize());
+  gg_device_view v = a->t;
+  v.ctl = nullptr;                          // amask gates the device allocator
   memcpy(h_view, &v, sizeof v);
   return GG_OK;
 }
@@ -1990,14 +2203,12 @@ int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
   const size_t S = a->S;
   std::vector<uint32_t> f(S * a->MB), status(S);
   std::vector<unsigned long long> misc(MISC_N);
-  std::vector<int> fln(a->MB);
   CUDA_TRY(cudaMemcpy(a->size.data(), a->t.size, S * 8, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(a->cap.data(), a->t.cap, S * 8, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(a->ops.data(), a->t.ops, S * 8, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(f.data(), a->t.flag, f.size() * 4, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(status.data(), a->t.status, S * 4, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemcpy(misc.data(), a->t.misc, MISC_N * 8, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(fln.data(), a->t.fl_n, a->MB * 4, cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemset(a->t.status, 0, S * 4));
   bool any = false;
   for (size_t s = 0; s < S; ++s) {
@@ -2008,10 +2219,15 @@ int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
     if (h_status) h_status[s] = (int32_t)status[s];
     if (status[s]) { any = true; a->dirty[s] = 1; }
   }
-  a->top = misc[MISC_TOP];
   a->alloc_calls = misc[MISC_ALLOCS];
-  for (uint32_t b = 0; b < a->MB; ++b) a->fl_count[b] = (uint64_t)std::max(fln[b], 0);
-  a->arena.trim(a->top);          // release mapped headroom the kernel did not use
+  // headroom the kernel took becomes live; the rest is unmapped again
+  for (size_t i = 0; i < a->headroom.size(); i += 2) {
+    const uint32_t s = a->headroom[i], b = a->headroom[i + 1];
+    if (a->flags[s] >> b & 1) a->live += bucket_bytes(a, b);
+    else a->slab.unback(s, b);
+  }
+  a->headroom.clear();
+  if (a->slab.cached) a->slab.trim();
   return any ? fail(GG_EPARTIAL, "device-side appends failed on some shards") : GG_OK;
 }
 
@@ -2021,25 +2237,20 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   if (n == 0) return GG_OK;
   const uint32_t B = 256;
   if (!grid) grid = (uint32_t)std::min<uint64_t>((n + B - 1) / B, (uint64_t)a->S * 64);
-  // worst-case headroom: every candidate of shard s appended
-  uint64_t headroom = 0;
+  // worst case: every candidate of shard s appended
+  std::vector<uint64_t> maxsz(a->S, 0);
   {
     std::lock_guard<std::mutex> g(a->mu);
-    std::vector<uint64_t> cand(a->S, 0);
     const uint64_t per_round = (uint64_t)grid * B;
     for (uint32_t blk = 0; blk < grid; ++blk) {
       uint64_t lo = (uint64_t)blk * B, c = 0;
       for (uint64_t base = lo; base < n; base += per_round) c += std::min<uint64_t>(B, n - base);
-      cand[blk % a->S] += c;
+      maxsz[blk % a->S] += c;
     }
-    for (uint32_t s = 0; s < a->S; ++s) {
-      uint32_t k = std::min<uint32_t>(min_buckets_for(a, a->size[s] + cand[s]), a->MB);
-      for (uint32_t b = 0; b < k; ++b)
-        if (!(a->flags[s] >> b & 1)) headroom += bucket_bytes(a, b);
-    }
+    for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += a->size[s];
   }
   gg_device_view v;
-  int rc = gg_device_view_get(a, headroom, &v, sizeof v);
+  int rc = gg_device_view_get(a, maxsz.data(), &v, sizeof v);
   if (rc) return rc;
   switch (a->esz) {
     case 1: { k_push_if<1, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
@@ -2135,10 +2346,8 @@ int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   uint64_t cap = 0, need = 0;
   for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
-  o[0] = cap * a->esz; o[1] = a->arena.mapped; o[2] = a->top; o[3] = need * a->esz;
-  uint64_t fl = 0;
-  for (uint32_t b = 0; b < a->MB; ++b) fl += a->fl_count[b] * bucket_bytes(a, b);
-  o[4] = a->alloc_calls; o[5] = fl;
+  o[0] = cap * a->esz; o[1] = a->slab.mapped; o[2] = a->live; o[3] = need * a->esz;
+  o[4] = a->alloc_calls; o[5] = a->slab.cached;
   return GG_OK;
 }
 

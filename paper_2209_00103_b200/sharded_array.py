@@ -452,14 +452,17 @@ class GrowableArray:
             self.commit()
 
     # ------------------------------------------------------------ device-side appends
-    def device_view(self, headroom_bytes: int = 0) -> bytes:
+    def device_view(self, max_sizes=None) -> bytes:
         """Raw ``gg::gg_device_view`` (include/ggarray_device.cuh) for a user kernel
-        that appends with ``warp_push_back`` / ``block_push_back``; maps
-        ``headroom_bytes`` of arena beyond the bump top first.  Call
+        that appends with ``warp_push_back`` / ``block_push_back``.  The slots of
+        every bucket shard s needs to reach ``max_sizes[s]`` elements (scalar or
+        per shard; None = no headroom) are backed with memory first.  Call
         :meth:`device_sync` after the kernel."""
         n = int(L.lib.gg_device_view_bytes())
         buf = C.create_string_buffer(n)
-        L.check(L.lib.gg_device_view_get(self._h, int(headroom_bytes), buf, n), "device_view")
+        mx = None if max_sizes is None else L.u64_array(np.broadcast_to(np.asarray(max_sizes), (self._S,)))
+        L.check(L.lib.gg_device_view_get(self._h, L.ptr(mx) if mx is not None else None, buf, n),
+                "device_view")
         return buf.raw
 
     def device_sync(self) -> None:
@@ -528,12 +531,18 @@ class GrowableArray:
             caps = np.asarray([max(int(x), 0) for x in distribution], np.uint64)
         self._reserve(caps)
 
-    def shrink(self, new_sizes) -> None:
+    def shrink(self, new_sizes, release: bool = True) -> None:
         """Extension (no reference semantics): pop shards to ``new_sizes`` and release
-        buckets beyond the minimal prefix; commits."""
+        buckets beyond the minimal prefix; commits.  ``release`` unmaps the slab
+        chunks left without a live bucket at once (waits for the device);
+        ``release=False`` keeps them mapped for reuse until :meth:`trim`."""
         ns = L.u64_array(np.broadcast_to(np.asarray(new_sizes), (self._S,)))
-        L.check(L.lib.gg_shrink(self._h, L.ptr(ns), self._stream()), "shrink")
+        L.check(L.lib.gg_shrink_ex(self._h, L.ptr(ns), 1 if release else 0, self._stream()), "shrink")
         self._dirty()
+
+    def trim(self) -> None:
+        """Unmap every cached slab chunk (mapped memory without a live bucket)."""
+        L.check(L.lib.gg_trim(self._h), "trim")
 
     # ------------------------------------------------------------ flattening
     def flatten_device(self, out=None):
@@ -581,9 +590,9 @@ class GrowableArray:
     def memory_stats(self) -> dict:
         o = np.zeros(6, np.uint64)
         L.check(L.lib.gg_mem_stats(self._h, L.ptr(o), self._stream()), "mem_stats")
-        cap, mapped, top, need, allocs, free = (int(x) for x in o)
-        return {"capacity_bytes": cap, "mapped_bytes": mapped, "arena_top_bytes": top,
-                "needed_bytes": need, "alloc_calls": allocs, "free_list_bytes": free,
+        cap, mapped, live, need, allocs, cached = (int(x) for x in o)
+        return {"capacity_bytes": cap, "mapped_bytes": mapped, "bucket_bytes": live,
+                "needed_bytes": need, "alloc_calls": allocs, "cached_bytes": cached,
                 "capacity_over_needed": cap / need if need else None,
                 "mapped_over_needed": mapped / need if need else None}
 

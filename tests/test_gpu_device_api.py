@@ -45,8 +45,8 @@ def test_push_if_multiset_and_layout(gg, mode, S, fb, grid):
         assert st["flags"][s] == (1 << k) - 1
     ms = a.memory_stats()
     if fb * 4 % 16 == 0:                                                 # no 16 B padding
-        assert ms["arena_top_bytes"] == ms["capacity_bytes"]
-    assert ms["mapped_bytes"] - ms["arena_top_bytes"] < 64 << 20        # headroom trimmed
+        assert ms["bucket_bytes"] == ms["capacity_bytes"]
+    assert ms["mapped_bytes"] - ms["bucket_bytes"] < 64 << 20        # headroom trimmed
 
 
 def test_block_order_within_a_block(gg):

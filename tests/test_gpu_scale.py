@@ -55,7 +55,7 @@ def test_config2_full_2p30_closed_form(gg):
         assert np.all(st["sizes"] == per) and np.all(st["caps"] == cap), r
         ms = a.memory_stats()
         assert ms["capacity_bytes"] == int(O.sharded_capacity_elements([n0 << (r + 1)], S, fb)[0]) * 4
-        assert ms["arena_top_bytes"] == ms["capacity_bytes"]
+        assert ms["bucket_bytes"] == ms["capacity_bytes"]
     assert a.committed_size == 1 << 30
     ms = a.memory_stats()
     assert ms["capacity_bytes"] == 2_147_467_264 * 4
@@ -114,3 +114,72 @@ def test_element_sizes_misaligned_paths(gg, dtype):
         a.insert_duplicate(); o.insert_duplicate()
         a.rw_add(1, mode="global"); o.rw_add(1)
     assert a.flatten().tobytes() == o.flatten().tobytes()
+
+
+def test_slab_release_and_cache(gg):
+    """Shrink unmaps slab chunks that lost their last live bucket (footprint
+    follows the live capacity down), release=False keeps them cached for
+    in-place reuse, trim() returns the cache; contents survive throughout."""
+    import torch
+    S, fb, n = 512, 32, 1 << 24
+    a = gg.GrowableArray.from_flat(torch.arange(n, dtype=torch.int32, device="cuda"), S, fb)
+    o_per = n // S
+    ms0 = a.memory_stats()
+    assert ms0["mapped_bytes"] <= 2 * ms0["needed_bytes"]
+    small = n >> 6
+    a.shrink(small // S)
+    ms = a.memory_stats()
+    assert ms["cached_bytes"] == 0
+    assert ms["capacity_bytes"] == int(O.sharded_capacity_elements([small], S, fb)[0]) * 4
+    assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"] + (2 << 20)      # + the packed small-class granule
+    a.grow(n)
+    a.insert_duplicate()                                                   # regrow into fresh chunks
+    per = small // S
+    g = torch.arange(2 * small, dtype=torch.int64, device="cuda")
+    s_, i_ = g // (2 * per), g % (2 * per)
+    exp = (s_ * o_per + (i_ % per)).to(torch.int32)
+    assert torch.equal(a.flatten_device(), exp)
+    mapped_before = a.memory_stats()["mapped_bytes"]
+    a.shrink(0, release=False)
+    ms = a.memory_stats()
+    assert ms["mapped_bytes"] == mapped_before and ms["cached_bytes"] > 0
+    a.insert_csr(torch.arange(n, dtype=torch.int32, device="cuda"),
+                 np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(o_per), np.uint64(n)))
+    assert a.memory_stats()["mapped_bytes"] == mapped_before               # reused in place
+    assert torch.equal(a.flatten_device(), torch.arange(n, dtype=torch.int32, device="cuda"))
+    a.shrink(0, release=False)
+    a.trim()
+    ms = a.memory_stats()
+    assert ms["cached_bytes"] == 0 and ms["mapped_bytes"] <= 2 << 20
+
+
+def test_phased_footprint_follows_live_capacity(gg):
+    """Config 4 shape at 2^22: after every insert/shrink round the mapped slab
+    bytes stay within 2x needed plus one chunk per partly live class."""
+    import torch
+    rng = np.random.default_rng(0)
+    S, fb, n0 = 512, 32, 1 << 22
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    src = torch.arange(4 * n0, dtype=torch.int32, device="cuda")
+    off = np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(n0 // S), np.uint64(n0))
+    a.insert_csr(src[:n0], off)
+    n, worst = n0, 0.0
+    for _ in range(40):
+        target = int(round(rng.uniform(0, 2) * n0))
+        q, r = divmod(target, S)
+        new = np.full(S, q, np.int64)
+        new[:r] += 1
+        cur = a._host()["sizes"].astype(np.int64)
+        if target >= n:
+            d = new - cur
+            offs = np.concatenate([[0], np.cumsum(d)]).astype(np.uint64)
+            a.insert_csr(src[:int(offs[-1])], offs)
+        else:
+            a.shrink(new)
+        n = target
+        ms = a.memory_stats()
+        assert ms["cached_bytes"] == 0
+        if target >= n0 // 8:
+            worst = max(worst, ms["mapped_bytes"] / ms["needed_bytes"])
+            assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"] + (8 << 20)
+    assert worst <= 2.5

@@ -30,7 +30,7 @@ def t_dup(reps=5):
     for _ in range(reps):
         e0, e1 = ev()
         e0.record(); a.insert_duplicate(commit=False); e1.record()
-        a.shrink(half)
+        a.shrink(half, release=False)
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     return min(ts)
@@ -56,7 +56,7 @@ full = np.full(S, 1 << 21, np.uint64)
 res = []
 for ls, un, tile, thr in itertools.product([0, 1, 2, 3], [4, 8], [16384, 32768, 65536], [256, 512]):
     _lib.check(_lib.lib.gg_set_tuning(ls, un, tile, thr))
-    a.shrink(half)
+    a.shrink(half, release=False)
     d = t_dup()
     a.insert_duplicate()
     f = t_op(lambda: a.flatten_device(out=out))
