@@ -391,48 +391,66 @@ def phased_leg(args, gg, torch, device):
     """Config 4: 100 rounds; each draws a total size uniform in [0, 2] x the
     base size (2^26), spread evenly over 512 LFVectors, and inserts or shrinks
     to it; footprint sampled after every round.  Shrink has no reference
-    semantics (parity unpinned)."""
-    rng = np.random.default_rng(0)
+    semantics (parity unpinned).  Run twice: shrink(release=True) (chunks left
+    without a live bucket are unmapped at once -- the footprint policy) and
+    release=False (chunks cached in place, the caching-allocator policy)."""
     n0 = 1 << 26
     cap_elems = 1 << 28
-    a = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
     src = torch.arange(cap_elems, dtype=torch.int32, device=device)
-    a.insert_csr(src[:n0], split_off(n0))
-    n = n0
-    cap_ratio, map_ratio, moved = [], [], 0
-    e0, e1 = _events(torch)
-    e0.record()
-    for _ in range(100):
-        target = int(min(cap_elems, round(rng.uniform(0, 2) * n0)))
-        q, r = divmod(target, S)
-        new = np.full(S, q, np.int64)
-        new[:r] += 1
-        cur = a._host()["sizes"].astype(np.int64)
-        if target >= n:
-            delta = new - cur
-            off = np.concatenate([[0], np.cumsum(delta)]).astype(np.uint64)
-            a.insert_csr(src[:int(off[-1])], off)
-            moved += int(off[-1])
-        else:
-            a.shrink(new)
-        n = target
-        ms = a.memory_stats()
-        if target >= n0 // 8:              # ratios of near-empty arrays are dominated by S*fb
-            cap_ratio.append(ms["capacity_bytes"] / ms["needed_bytes"])
-            map_ratio.append(ms["mapped_bytes"] / ms["needed_bytes"])
-    e1.record()
-    torch.cuda.synchronize()
-    ms_tot = e0.elapsed_time(e1)
-    return {"rounds": 100, "seed": 0, "start_elements": n0, "max_elements": cap_elems,
-            "inserted_elements": moved, "ms": round(ms_tot, 3),
-            "capacity_over_needed_max": round(max(cap_ratio), 4),
-            "capacity_over_needed_mean": round(float(np.mean(cap_ratio)), 4),
-            "mapped_over_needed_max": round(max(map_ratio), 4),
-            "mapped_over_needed_final": round(map_ratio[-1], 4),
-            "ratios_over": "rounds with total >= base/8",
-            "note": "capacity = allocated buckets (reference semantics, <= 2x + fb per shard); "
-                    "mapped = physical slab chunks (shrink(release=True) unmaps chunks left "
-                    "without a live bucket; map/unmap cost is inside ms)"}
+
+    def run(release):
+        rng = np.random.default_rng(0)
+        a = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+        a.insert_csr(src[:n0], split_off(n0))
+        n = n0
+        cap_ratio, map_ratio, moved = [], [], 0
+        sl0 = a.slab_stats()
+        torch.cuda.synchronize()
+        e0, e1 = _events(torch)
+        e0.record()
+        for _ in range(100):
+            target = int(min(cap_elems, round(rng.uniform(0, 2) * n0)))
+            q, r = divmod(target, S)
+            new = np.full(S, q, np.int64)
+            new[:r] += 1
+            cur = a._host()["sizes"].astype(np.int64)
+            if target >= n:
+                delta = new - cur
+                off = np.concatenate([[0], np.cumsum(delta)]).astype(np.uint64)
+                a.insert_csr(src[:int(off[-1])], off)
+                moved += int(off[-1])
+            else:
+                a.shrink(new, release=release)
+            n = target
+            ms = a.memory_stats()
+            if target >= n0 // 8:          # ratios of near-empty arrays are dominated by S*fb
+                cap_ratio.append(ms["capacity_bytes"] / ms["needed_bytes"])
+                map_ratio.append(ms["mapped_bytes"] / ms["needed_bytes"])
+        e1.record()
+        torch.cuda.synchronize()
+        ms_tot = e0.elapsed_time(e1)
+        sl = a.slab_stats()
+        return {"ms": round(ms_tot, 3), "inserted_elements": moved,
+                "capacity_over_needed_max": round(max(cap_ratio), 4),
+                "capacity_over_needed_mean": round(float(np.mean(cap_ratio)), 4),
+                "mapped_over_needed_max": round(max(map_ratio), 4),
+                "mapped_over_needed_mean": round(float(np.mean(map_ratio)), 4),
+                "mapped_over_needed_final": round(map_ratio[-1], 4),
+                "slab": {"chunks_mapped": sl["chunks_mapped"] - sl0["chunks_mapped"],
+                         "chunks_unmapped": sl["chunks_unmapped"] - sl0["chunks_unmapped"],
+                         "map_ms": round((sl["map_ns"] - sl0["map_ns"]) / 1e6, 3),
+                         "unmap_ms": round((sl["unmap_ns"] - sl0["unmap_ns"]) / 1e6, 3)}}
+
+    out = {"rounds": 100, "seed": 0, "start_elements": n0, "max_elements": cap_elems,
+           "ratios_over": "rounds with total >= base/8"}
+    out.update(run(True))
+    out["cached_policy"] = run(False)
+    out["note"] = ("capacity = allocated buckets (reference semantics, <= 2x + fb per shard); "
+                   "mapped = physical slab chunks; release=True unmaps chunks left without a "
+                   "live bucket (map/unmap cost inside ms), cached_policy keeps them mapped")
+    del src
+    torch.cuda.empty_cache()
+    return out
 
 
 def split_off(n):

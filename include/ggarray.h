@@ -198,6 +198,10 @@ int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream);
  * [4]=device alloc calls, [5]=cached bytes (mapped chunks without a live
  * bucket) */
 int gg_mem_stats(gg_array *a, uint64_t *h_out6, void *stream);
+/* slab mapping cost: [0]=mapped bytes, [1]=cached bytes, [2]=chunks mapped
+ * (cumulative), [3]=chunks unmapped, [4]=ns in cuMemCreate/Map/SetAccess,
+ * [5]=ns in cuMemUnmap/Release, [6]=class regions reserved, [7]=VA bytes */
+int gg_slab_stats(gg_array *a, uint64_t *h_out8);
 
 /* ---- baselines (baselines.py) on raw device buffers ---- */
 /* StaticArray/DoublingArray/ChunkTableArray.insert_batch (baselines.py:

@@ -10,7 +10,8 @@ structures with CUDA-event phase timing, plus roofline columns.
 Every benchmark checks its end state against the sequential oracle of the
 reference harness (multiset of tags + passes, bench_cli.py:170-177) before a
 row is written; timing columns are informational.  ``memory-model`` is the
-reference's analytic section-5 model (host-only, out of scope here).
+reference's section-5 sizing model; ``--measure N`` realises N demands per
+sigma as GGArrays on the GPU and appends measured capacity / mapped columns.
 """
 
 from __future__ import annotations
@@ -440,18 +441,34 @@ def build_parser() -> argparse.ArgumentParser:
     c.add_argument("--out", default="-")
     c.add_argument("--csv-header", action=argparse.BooleanOptionalAction, default=True)
     c.add_argument("--rw-grain", type=int, default=65536)
-    for name in ("insert-algos", "shard-sweep", "grow-insert-rw", "two-phase", "memory-model"):
+    for name in ("insert-algos", "shard-sweep", "grow-insert-rw", "two-phase"):
         sub.add_parser(name, parents=[c])
+    mm = sub.add_parser("memory-model", parents=[c])
+    mm.add_argument("--samples", type=int, default=100_000)
+    mm.add_argument("--base-size", type=int, default=1_000_000)
+    mm.add_argument("--element-size", type=int, default=4)
+    mm.add_argument("--measure", type=int, default=0,
+                    help="demands per sigma realised as GGArrays on the GPU (0 = model only)")
     return p
 
 
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
-    if args.command == "memory-model":
-        raise SystemExit("memory-model is the reference's analytic section-5 model (host-only, "
-                         "out of scope); run growarray-bench memory-model")
     if args.command != "shard-sweep" and len(args.shards) != 1:
         raise SystemExit(f"{args.command}: --shards takes a single value")
+    if args.command == "memory-model":          # bench_cli.py:725-738 in the reference
+        from . import memory_model as mmod
+        params = mmod.MemoryModelParams(base_size=args.base_size, samples=args.samples, seed=args.seed)
+        reports = mmod.run_model(params, shards=args.shards[0], first_bucket_size=args.first_bucket,
+                                 element_size=args.element_size)
+        measured = None
+        if args.measure:
+            measured = mmod.measure_device(params, args.measure, shards=args.shards[0],
+                                           first_bucket_size=args.first_bucket,
+                                           element_size=args.element_size)
+        mmod.write_report_csv(reports, sys.stdout if args.out == "-" else args.out,
+                              header=args.csv_header, measured=measured)
+        return 0
     cfg = BenchConfig(structure=args.structure, shards=args.shards[0], first_bucket=args.first_bucket,
                       workers=args.workers, initial_size=args.initial_size,
                       iterations=args.iterations, algo=args.algo, rw_mode=args.rw_mode,

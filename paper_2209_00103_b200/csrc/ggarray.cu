@@ -28,6 +28,7 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1016,6 +1017,11 @@ struct Slab {
   size_t gran = 0;
   uint32_t S = 0, MB = 0;
   uint64_t va_budget = 0, va_used = 0, mapped = 0, cached = 0;  // cached: mapped, 0 refs
+  uint64_t n_map = 0, n_unmap = 0, ns_map = 0, ns_unmap = 0, n_regions = 0;  // cost counters
+  static uint64_t now_ns() {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+        std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
   std::vector<uint64_t> bytes;        // bucket bytes per class (powers of two >= 16)
   std::vector<uint64_t> small_off;    // offset in the small region, ~0 = own region
   Region small;
@@ -1057,6 +1063,7 @@ struct Slab {
     CUresult e = drv().reserve(&r.base, r.va, r.chunk, 0, 0);
     if (e != CUDA_SUCCESS) { r.base = 0; return fail(GG_ENOMEM, "cuMemAddressReserve failed (VA exhausted)"); }
     va_used += r.va;
+    n_regions += 1;
     return GG_OK;
   }
   // mapping unit of class b's region: a power of two >= one granule and >=
@@ -1100,6 +1107,7 @@ struct Slab {
   int map_chunk(Region &r, size_t c) {
     Chunk &k = r.chunks[c];
     if (k.mapped) { if (!k.refs) cached -= r.chunk; return GG_OK; }
+    const uint64_t t0 = now_ns();
     CUmemAllocationProp prop = props();
     CU_TRY(drv().create(&k.h, r.chunk, &prop, 0));
     const CUdeviceptr at = r.base + c * r.chunk;
@@ -1118,16 +1126,21 @@ struct Slab {
     }
     k.mapped = true;
     mapped += r.chunk;
+    n_map += 1;
+    ns_map += now_ns() - t0;
     return GG_OK;
   }
   void unmap_chunk(Region &r, size_t c) {
     Chunk &k = r.chunks[c];
+    const uint64_t t0 = now_ns();
     drv().unmap(r.base + c * r.chunk, r.chunk);
     drv().release(k.h);
     k.mapped = false;
     k.h = 0;
     mapped -= r.chunk;
     cached -= r.chunk;
+    n_unmap += 1;
+    ns_unmap += now_ns() - t0;
   }
   // back bucket (s, b) with physical memory (region must exist)
   int back(uint32_t s, uint32_t b) {
@@ -2348,6 +2361,14 @@ int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
   for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
   o[0] = cap * a->esz; o[1] = a->slab.mapped; o[2] = a->live; o[3] = need * a->esz;
   o[4] = a->alloc_calls; o[5] = a->slab.cached;
+  return GG_OK;
+}
+
+int gg_slab_stats(gg_array *a, uint64_t *o) {
+  std::lock_guard<std::mutex> g(a->mu);
+  const Slab &sl = a->slab;
+  o[0] = sl.mapped; o[1] = sl.cached; o[2] = sl.n_map; o[3] = sl.n_unmap;
+  o[4] = sl.ns_map; o[5] = sl.ns_unmap; o[6] = sl.n_regions; o[7] = sl.va_used;
   return GG_OK;
 }
 

@@ -596,6 +596,14 @@ class GrowableArray:
                 "capacity_over_needed": cap / need if need else None,
                 "mapped_over_needed": mapped / need if need else None}
 
+    def slab_stats(self) -> dict:
+        """Cost of the slab's physical mapping (cumulative counters)."""
+        o = np.zeros(8, np.uint64)
+        L.check(L.lib.gg_slab_stats(self._h, L.ptr(o)), "slab_stats")
+        keys = ("mapped_bytes", "cached_bytes", "chunks_mapped", "chunks_unmapped", "map_ns",
+                "unmap_ns", "regions", "va_bytes")
+        return {k: int(v) for k, v in zip(keys, o)}
+
     def device_state(self) -> dict:
         S = self._S
         st = {k: np.zeros(S + (k == "prefix"), np.uint64) for k in ("sizes", "caps", "flags", "prefix", "ops")}
