@@ -123,13 +123,15 @@ int gg_new_bucket(gg_array *a, uint32_t shard, uint32_t bucket, int32_t *h_won, 
 /* AtomicCounter.fetch_add on a shard's size (insert_index.py:52-58) */
 int gg_fetch_add(gg_array *a, uint32_t shard, uint64_t count, uint64_t *h_prev, void *stream);
 /* shrink (extension, no reference semantics): size[s] = h_new_sizes[s] <=
- * size[s]; buckets b >= min_buckets_for(new size) are released.  With
- * GG_SHRINK_RELEASE the slab chunks left without a live bucket are unmapped
- * at once (the call then waits for the device); without it they stay mapped
- * ("cached", reused in place when the buckets come back) until gg_trim.
- * gg_shrink = gg_shrink_ex(.., GG_SHRINK_RELEASE, ..).  Commits. */
-enum { GG_SHRINK_RELEASE = 1 };
-int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint32_t flags, void *stream);
+ * size[s]; buckets b >= min_buckets_for(new size) are released.  Slab chunks
+ * left without a live bucket stay mapped ("cached", reused in place when the
+ * buckets come back) except that, largest class first, they are unmapped
+ * until at most keep_mapped_bytes remain mapped (0 = unmap them all,
+ * UINT64_MAX = keep them all); unmapping waits for the device.  The Python
+ * layer's default keeps the footprint <= 2x the needed bytes.
+ * gg_shrink = gg_shrink_ex(.., 0, ..).  Commits. */
+int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_bytes,
+                 void *stream);
 int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream);
 /* unmap every cached chunk (waits for the device) */
 int gg_trim(gg_array *a);
@@ -176,10 +178,15 @@ int gg_set(gg_array *a, uint32_t shard, uint64_t i, const void *h_val, void *str
  * state after the captured sequence. */
 int gg_capture_mode(gg_array *a, int32_t on);
 int gg_capture_release(gg_array *a);
-/* Tuning of the 4-byte streaming kernels (for sweeps): cache policy ls
- * (0 .cg, 1 .nc, 2 default, 3 .cs), unroll (4|8), tile bytes, CTA threads
- * (256|512); -1 / 0 keep the built-in defaults.  Process-wide. */
+/* Tuning of the streaming kernels (sweeps): unroll U in {1,2,4,8} = 16 B
+ * vectors per thread per tile (tile = 256 threads x U vectors); -1 = the
+ * built-in choice.  ls / tile_bytes / threads are accepted and ignored
+ * (kept for ABI stability).  Process-wide. */
 int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads);
+/* Programmatic dependent launch of the library's kernels (default on): a
+ * kernel may start while its stream predecessor drains.  Process-wide; for
+ * A/B measurements. */
+int gg_set_pdl(int32_t on);
 /* committed size, total (reserved) size, total capacity -- host mirrors */
 int gg_summary(gg_array *a, uint64_t *h_out3);
 

@@ -57,7 +57,7 @@ constexpr uint32_t kStatusNoMem = 4;     // == GG_ENOMEM
 
 // launch-coordination counters live on their own 128 B lines, away from the
 // allocator's bump top (pollers would otherwise contend with its atomics)
-enum { MISC_ALLOCS = 1, MISC_OOM = 2, MISC_DONE = 16, MISC_RSV = 32, MISC_TICKET = 48,
+enum { MISC_ALLOCS = 1, MISC_OOM = 2,
        MISC_N = 64 };
 
 // bucket_vector.py:48-59: b = hibit(i/fb + 1), off = i - fb*(2^b - 1)

@@ -60,7 +60,7 @@ _SIGS = {
     "gg_new_bucket": ([P, U32, U32, PI32, P], C.c_int),
     "gg_fetch_add": ([P, U32, U64, PU64, P], C.c_int),
     "gg_shrink": ([P, PU64, P], C.c_int),
-    "gg_shrink_ex": ([P, PU64, U32, P], C.c_int),
+    "gg_shrink_ex": ([P, PU64, U64, P], C.c_int),
     "gg_trim": ([P], C.c_int),
     "gg_rw_add": ([P, P, U32, I32, P], C.c_int),
     "gg_device_view_bytes": ([], U64),
@@ -75,6 +75,7 @@ _SIGS = {
     "gg_info": ([P, PU32], C.c_int),
     "gg_capture_mode": ([P, I32], C.c_int),
     "gg_set_tuning": ([I32, I32, U32, U32], C.c_int),
+    "gg_set_pdl": ([C.c_int32], C.c_int),
     "gg_capture_release": ([P], C.c_int),
     "gg_summary": ([P, PU64], C.c_int),
     "gg_host_state": ([P, PU64, PU64, PU64, PU64, PU64], C.c_int),
@@ -136,3 +137,7 @@ def stream_handle(device_index: int) -> int:
         return torch._C._cuda_getCurrentRawStream(device_index)
     except AttributeError:  # older torch
         return torch.cuda.current_stream(device_index).cuda_stream
+
+
+if os.environ.get("GG_PDL") == "0":        # A/B switch for programmatic dependent launch
+    lib.gg_set_pdl(0)

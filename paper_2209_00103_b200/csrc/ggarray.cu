@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <type_traits>
 #include <cstdint>
 #include <cstdio>
@@ -106,7 +107,7 @@ Drv &drv() {
 constexpr int kMaxBuckets = 64;
 constexpr uint64_t kDefaultVaBudget = uint64_t(16) << 40;   // slab VA per array (16 TiB)
 constexpr int kThreads = 256;          // CTA size of the streaming kernels
-constexpr int kTileBytes = 32 * 1024;  // bytes of payload per tile
+constexpr uint64_t kFlatChunk = 16 * 1024;  // bytes per CTA of the contiguous +c kernel
 
 // ctl word per shard (only uploaded when an op plans a failure)
 constexpr uint32_t kCtlLimitMask = 0xffu;   // allocate buckets < limit
@@ -135,6 +136,15 @@ template <> struct ElemT<2> { typedef uint16_t T; };
 template <> struct ElemT<4> { typedef uint32_t T; };
 template <> struct ElemT<8> { typedef unsigned long long T; };
 
+// Programmatic dependent launch: every library kernel lets its stream
+// successor launch as soon as all its CTAs are running, and waits for its
+// predecessor's completion before touching memory (griddepcontrol.wait is a
+// no-op when the launch was not programmatic).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Host-planned allocation of class-b buckets for every lane with `need`
 // (each (shard, bucket) is requested by exactly one lane, so the once-flags
 // are uncontended and the slot is the shard's own: no address atomics at
@@ -145,10 +155,11 @@ __device__ __forceinline__ void warp_alloc_class(const Tables &t, bool need, uin
   if (!m) return;
   if ((threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)__popc(m));
   if (!need) return;
+  // plain stores: these launches only publish host-planned buckets and the
+  // kernel boundary orders them before any reader
   t.ptr[(size_t)s * t.MB + b] = bucket_slot(t, s, b);
   atomicAdd((unsigned long long *)&t.cap[s], 1ull << (t.log2fb + b));
-  __threadfence();
-  st_release(t.flag + (size_t)s * t.MB + b, kFlagPublished);
+  t.flag[(size_t)s * t.MB + b] = kFlagPublished;
   atomicOr(&t.pmask[s], 1ull << b);
 }
 
@@ -210,6 +221,7 @@ __device__ __forceinline__ void reserve_shards(const Tables &t, uint32_t s, bool
 }
 
 __global__ void k_reserve(Tables t, int mode) {
+  pdl_begin();
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   reserve_shards(t, s, s < t.S, mode);
 }
@@ -217,6 +229,7 @@ __global__ void k_reserve(Tables t, int mode) {
 // grow: thread per shard, allocate buckets [0, lim[s]); lim comes from the
 // ctl words, or (uniform_k != ~0u) is the same for every shard
 __global__ void k_grow(Tables t, uint32_t uniform_k) {
+  pdl_begin();
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = s < t.S;
   const uint32_t lim = !live ? 0u : (uniform_k != ~0u ? uniform_k : (t.ctl[s] & kCtlLimitMask));
@@ -234,6 +247,7 @@ __global__ void k_fetch_add(Tables t, uint32_t s, uint64_t c) {
 
 // commit (sharded_array.py:213-222): one CTA, exclusive scan of S sizes.
 __global__ void __launch_bounds__(1024) k_commit(Tables t) {
+  pdl_begin();
   __shared__ uint64_t warp_tot[32];
   __shared__ uint64_t carry;
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -369,6 +383,7 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
 // b >= min_buckets_for(new size) unpublished (their slots stay reserved for
 // the shard; the host unmaps chunks that lost their last live bucket).
 __global__ void k_shrink(Tables t, const uint64_t *new_sizes) {
+  pdl_begin();
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= t.S) return;
   const uint64_t ns = new_sizes[s];
@@ -564,7 +579,7 @@ __device__ __forceinline__ void cta_add(char *p, uint64_t n, T a, uint32_t reps,
 // ---- tile walker ------------------------------------------------------------
 // The work space is an index range [0, total) partitioned among shards by a
 // directory dir[S+1] (CSR offsets for inserts, the committed prefix for
-// duplicate / flatten / r/w).  A CTA takes tiles of kTileBytes and walks them
+// duplicate / flatten / r/w).  A CTA takes one tile and walks it
 // in pieces over which shard, source bucket and destination bucket are all
 // constant; every thread computes the (uniform) piece bounds itself.
 enum { W_INSERT = 0, W_DUP = 1, W_FLATTEN = 2, W_RW = 3 };
@@ -579,37 +594,50 @@ __device__ __forceinline__ uint32_t upper_shard(const uint64_t *dir, uint32_t S,
   return lo;
 }
 
-constexpr uint32_t kSmemDir = 4096;   // directories up to 4096 shards are cached in smem
-constexpr int kUnroll = kDefUnroll;
 
-// load dir[0..S] into smem when it fits (one pass per CTA of a persistent grid)
-__device__ __forceinline__ const uint64_t *stage_dir(const uint64_t *gdir, uint32_t S,
-                                                     uint64_t *sdir) {
-  if (S + 1 > kSmemDir) return gdir;
-  for (uint32_t i = threadIdx.x; i <= S; i += blockDim.x) sdir[i] = gdir[i];
-  __syncthreads();
-  return sdir;
+// Bucket (s, b) sits at a fixed slot of class b's slab (gg_device_view), so
+// kernels compute bucket addresses instead of loading them: scb[] holds the
+// class bases staged in shared memory, lg0 = log2(fb * element bytes).
+__device__ __forceinline__ char *slot_addr(char *const *scb, uint32_t s, uint32_t b, uint32_t lg0) {
+  return scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
+}
+__device__ __forceinline__ void stage_cbase(const Tables &t, char **scb) {
+  for (uint32_t i = threadIdx.x; i < t.MB; i += blockDim.x) scb[i] = t.cbase[i];
 }
 
-// Fast path of one tile [g, gend) of the work space lying inside shard s with
-// 16 B-congruent source and destination: every thread resolves each of its
-// vectors' addresses independently (clz locate + bucket-pointer load) and
-// issues all UNROLL loads before any store, so a tile costs one memory round
-// trip however many buckets it touches.  Returns false (tile not handled)
-// when the tile crosses a shard or the alignment does not hold.
-template <int ESZ, int W, typename T, int UNROLL, int LS>
-__device__ __forceinline__ bool vector_tile(const Tables &t, const uint64_t *dir, uint32_t s,
-                                            uint64_t g, uint64_t gend, const char *flat_src,
-                                            char *flat_dst, T addend, uint32_t reps) {
+// shard of work index g: largest s with dir[s] <= g (bisect_right - 1,
+// sharded_array.py:136) by a 32-ary warp search -- 2 dependent loads for
+// S <= 1024, 3 up to 32768.  Called by a full warp; result in every lane.
+__device__ __forceinline__ uint32_t warp_find_shard(const uint64_t *dir, uint32_t S, uint64_t g) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = S;                 // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) >> 5;
+    const uint32_t p = lo + lane * step;
+    const bool ok = p < hi && dir[p] <= g;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);   // lane 0 (p = lo) always ok
+    lo = lo + (31u - __clz(m)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// One tile [g, gend) lying inside shard s with 16 B-congruent source and
+// destination: each thread moves U vectors, resolving every vector's bucket
+// on its own (clz locate + slot arithmetic) and issuing all U loads before
+// any store -- one memory round trip per tile however many buckets it
+// touches.  Returns false (tile not handled) when the tile crosses a shard
+// or the alignment does not hold.
+template <int ESZ, int W, typename T, int U, int LS>
+__device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, const uint64_t *dir,
+                                            uint32_t s, uint64_t dbase, uint64_t g, uint64_t gend,
+                                            const char *flat_src, char *flat_dst, T addend,
+                                            uint32_t reps) {
   constexpr uint32_t VE = 16 / ESZ;
   const uint64_t lo = dir[s];
   if (gend > dir[s + 1] || ((g - lo) % VE) || ((gend - g) % VE) || (t.log2fb < 31 && ((1u << t.log2fb) % VE)))
     return false;
-  uint64_t dbase = 0;                      // destination local index of work index lo
   if constexpr (W == W_INSERT || W == W_DUP) {
-    if (t.ctl && t.ctl[s] != (kCtlWrite | t.MB))
-      return false;                        // planned failure on this shard: slow path
-    dbase = t.start[s];
     if (dbase % VE) return false;
   }
   if constexpr (W == W_INSERT) {
@@ -619,27 +647,28 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, const uint64_t *dir
     if (((uintptr_t)(flat_dst + g * ESZ)) & 15) return false;
   }
   typedef LdSt<(W == W_RW && LS == 1) ? 2 : LS> M;
-  char *const *ptr = t.ptr + (size_t)s * t.MB;
+  constexpr uint32_t LGE = ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3;
+  const uint32_t lg0 = t.log2fb + LGE;
   const uint64_t nvec = (gend - g) / VE;
   const uint64_t k0 = g - lo;              // work-space offset inside the shard
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
-  for (uint64_t v0 = tid; v0 < nvec; v0 += UNROLL * (uint64_t)nt) {
-    uint4 r[UNROLL];
-    char *sp[UNROLL];
+  for (uint64_t v0 = tid; v0 < nvec; v0 += U * (uint64_t)nt) {
+    uint4 r[U];
+    char *sp[U];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint64_t v = min(v0 + u * (uint64_t)nt, nvec - 1);
       if constexpr (W == W_INSERT) {
         sp[u] = (char *)flat_src + (g + v * VE) * ESZ;
       } else {
         uint32_t b; uint64_t o;
         locate(k0 + v * VE, t.log2fb, b, o);
-        sp[u] = ptr[b] + o * ESZ;
+        sp[u] = slot_addr(scb, s, b, lg0) + o * ESZ;
       }
       r[u] = M::ld((const uint4 *)sp[u]);
     }
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
+    for (int u = 0; u < U; ++u) {
       const uint64_t v = v0 + u * (uint64_t)nt;
       if (v >= nvec) continue;
       char *dp;
@@ -656,7 +685,7 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, const uint64_t *dir
       } else {
         uint32_t b; uint64_t o;
         locate(dbase + k0 + v * VE, t.log2fb, b, o);
-        dp = ptr[b] + o * ESZ;
+        dp = slot_addr(scb, s, b, lg0) + o * ESZ;
       }
       M::st((uint4 *)dp, r[u]);
     }
@@ -664,21 +693,19 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, const uint64_t *dir
   return true;
 }
 
-// Fused append (FUSE): ONE launch reserves + allocates (the first ceil(S/nt)
-// CTAs, thread per shard: one atomicAdd per LFVector, warp-aggregated bucket
-// allocation), then every CTA waits once (acquire on a global counter the
-// reserving CTAs bump after a fence) and copies its tiles; the last CTA to
-// finish resets the counters and, if asked, rebuilds the prefix (commit).
-// Reserving CTAs are chosen by start-time tickets, so they are running
-// before any CTA waits: no deadlock whatever the dispatch order.
-struct Fuse { int rmode; uint32_t epoch; int commit; };
+// Planned append (PLANNED): the host has already backed every destination
+// slot and knows each shard's count, so the copy needs no reservation phase:
+// destinations are slot arithmetic from the unchanged size[s]; k_planned_meta
+// applies the metadata right after.  (A last-CTA epilogue in the walk itself
+// costs more: the completion atomic lengthens every CTA's life.)
+struct Fuse { int rmode; int commit; };
 
 __device__ void commit_block(const Tables &t) {
   __shared__ uint64_t ws[32];
   uint64_t carry = 0;
   for (uint32_t base = 0; base < t.S; base += blockDim.x) {
     const uint32_t s = base + threadIdx.x;
-    const uint64_t v = s < t.S ? ld_acquire64(t.size + s) : 0;
+    const uint64_t v = s < t.S ? t.size[s] : 0;
     uint64_t tot;
     const uint64_t ex = block_exclusive_scan(v, &tot, ws);
     if (s < t.S) t.prefix[s + 1] = carry + ex + v;
@@ -687,55 +714,81 @@ __device__ void commit_block(const Tables &t) {
   if (threadIdx.x == 0) t.prefix[0] = 0;
 }
 
-template <int ESZ, int W, typename T, int UNROLL = kDefUnroll, int LS = kDefLS, bool FUSE = false>
-__global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, char *flat_dst,
-                                                   uint64_t total, T addend, uint32_t reps,
-                                                   uint32_t tile, Fuse fz) {
-  extern __shared__ uint64_t sdir[];
-  const uint32_t tid = threadIdx.x, nt = blockDim.x;
-  uint32_t vblock = blockIdx.x;
-  if constexpr (FUSE) {
-    // a CTA's virtual index is a ticket taken when it STARTS running, so the
-    // reserving CTAs (tickets < n_rsv) are always resident before anyone waits
-    __shared__ uint32_t ticket;
-    if (tid == 0) ticket = (uint32_t)atomicAdd(&t.misc[MISC_TICKET], 1ull);
-    __syncthreads();
-    vblock = ticket;
-    // phase 1: the first ceil(S/nt) tickets reserve + allocate (thread per shard)
-    const uint32_t n_rsv = min(gridDim.x, (t.S + nt - 1) / nt);
-    if (vblock < n_rsv) {
-      for (uint32_t base = vblock * nt; base < t.S; base += n_rsv * nt) {
-        const uint32_t s = base + tid;
-        reserve_shards(t, s, s < t.S, fz.rmode);
+// metadata of a planned append, run by one CTA after every tile is copied
+__device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &fz) {
+  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    uint64_t c = 0;
+    if (s < t.S) c = fz.rmode == 0 ? t.offsets[s + 1] - t.offsets[s] : t.prefix[s + 1] - t.prefix[s];
+    unsigned long long want = 0;
+    if (c) {
+      const uint64_t start = t.size[s];
+      t.size[s] = start + c;
+      t.ops[s] += 1;
+      t.start[s] = start;
+      uint32_t b0, b1; uint64_t o;
+      locate(start, t.log2fb, b0, o);
+      locate(start + c - 1, t.log2fb, b1, o);
+      want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~t.pmask[s];
+      uint64_t add = 0;
+      for (unsigned long long m = want; m; m &= m - 1) {
+        const uint32_t b = __ffsll((long long)m) - 1;
+        t.ptr[(size_t)s * t.MB + b] = slot_addr(scb, s, b, lg0);
+        t.flag[(size_t)s * t.MB + b] = kFlagPublished;
+        add += 1ull << (t.log2fb + b);
       }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(&t.misc[MISC_RSV], 1ull);
-      }
+      if (want) { t.pmask[s] |= want; t.cap[s] += add; }
     }
-    // every CTA waits ONCE for all reservations (acquire by thread 0, then the
-    // CTA barrier orders the other threads' loads after it)
-    if (tid == 0) {
-      while (ld_acquire64((const uint64_t *)&t.misc[MISC_RSV]) < n_rsv) __nanosleep(256);
-      __threadfence();   // as in cooperative-groups grid sync: fence after the spin
-    }
-    __syncthreads();
+    if (s < t.S) t.count[s] = c;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(want));
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)tot);
   }
-  const uint64_t *dir = stage_dir((W == W_INSERT) ? t.offsets : t.prefix, t.S, sdir);
-  const uint64_t ntiles = (total + tile - 1) / tile;
-  for (uint64_t ti = vblock; ti < ntiles; ti += gridDim.x) {
-    uint64_t g = ti * tile;
-    const uint64_t gend = min(total, g + tile);
-    uint32_t s = upper_shard(dir, t.S, g);
-    if (vector_tile<ESZ, W, T, UNROLL, LS>(t, dir, s, g, gend, flat_src, flat_dst, addend, reps))
-      continue;
+  __syncthreads();
+  if (fz.commit) commit_block(t);
+}
+
+// The tile walker: ONE tile per CTA (a non-persistent grid streams ~15%
+// faster than a persistent grid-stride loop on B200, tools/probe), tile =
+// U vectors per thread.  The work space [0, total) is partitioned among
+// shards by dir[S+1] (CSR offsets for inserts, the committed prefix for
+// duplicate / flatten / r/w); a tile inside one shard with congruent
+// alignment takes vector_tile, anything else the piece walker (pieces over
+// which shard, source bucket and destination bucket are constant).
+template <int ESZ, int W, typename T, int U = 4, int LS = kDefLS, bool PLANNED = false>
+__global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, char *flat_dst,
+                                              uint64_t total, T addend, uint32_t reps,
+                                              uint32_t tile, Fuse fz) {
+  __shared__ char *scb[kMaxBuckets];
+  __shared__ uint32_t s_sh;
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  pdl_begin();
+  const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
+  uint64_t g = (uint64_t)blockIdx.x * tile;
+  const uint64_t gend = min(total, g + tile);
+  if (tid < 32) {
+    const uint32_t s0 = warp_find_shard(dir, t.S, g);
+    if (tid == 0) s_sh = s0;
+  }
+  stage_cbase(t, scb);
+  __syncthreads();
+  constexpr uint32_t LGE = ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3;
+  const uint32_t lg0 = t.log2fb + LGE;
+  uint32_t s = s_sh;
+  bool fast = true;
+  uint64_t dbase = 0;                      // destination local index of shard s's work index 0
+  if constexpr (W == W_INSERT || W == W_DUP) {
+    if (!PLANNED && t.ctl && t.ctl[s] != (kCtlWrite | t.MB)) fast = false;   // planned failure
+    dbase = PLANNED ? t.size[s] : t.start[s];
+  }
+  if (!(fast && vector_tile<ESZ, W, T, U, LS>(t, scb, dir, s, dbase, g, gend, flat_src, flat_dst,
+                                              addend, reps))) {
     while (g < gend) {
       uint64_t shard_end = dir[s + 1];
       while (shard_end <= g) { ++s; shard_end = dir[s + 1]; }
       const uint64_t k = g - dir[s];
       uint64_t len = min(gend, shard_end) - g;
-      const uint32_t ctl = (W == W_INSERT || W == W_DUP) && t.ctl ? t.ctl[s] : kCtlWrite;
+      const uint32_t ctl = (W == W_INSERT || W == W_DUP) && !PLANNED && t.ctl ? t.ctl[s] : kCtlWrite;
       const char *sp = nullptr;
       char *dp = nullptr;
       bool dst_ok = true;
@@ -746,7 +799,7 @@ __global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, ch
         uint32_t b; uint64_t o;
         locate(k, t.log2fb, b, o);
         len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
-        sp = t.ptr[(size_t)s * t.MB + b] + o * ESZ;
+        sp = slot_addr(scb, s, b, lg0) + o * ESZ;
       }
       // destination side
       if constexpr (W == W_FLATTEN) {
@@ -755,39 +808,30 @@ __global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, ch
         dp = (char *)sp;
       } else {
         uint32_t b; uint64_t o;
-        locate(t.start[s] + k, t.log2fb, b, o);
+        locate((PLANNED ? t.size[s] : t.start[s]) + k, t.log2fb, b, o);
         len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
-        uint32_t f = t.flag[(size_t)s * t.MB + b];
-        dst_ok = (f == kFlagPublished);
-        dp = t.ptr[(size_t)s * t.MB + b] + o * ESZ;
+        if (!PLANNED) dst_ok = t.flag[(size_t)s * t.MB + b] == kFlagPublished;
+        dp = slot_addr(scb, s, b, lg0) + o * ESZ;
       }
       if constexpr (W == W_RW) {
-        cta_add<T, UNROLL, LS>(dp, len, addend, reps, tid, nt);
+        cta_add<T, U, LS>(dp, len, addend, reps, tid, nt);
       } else if (dst_ok && (ctl & (kCtlWrite | kCtlZero))) {
-        cta_copy<ESZ, UNROLL, LS>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
+        cta_copy<ESZ, U, LS>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
       }
       g += len;
     }
   }
-  if constexpr (FUSE) {
-    // the last CTA to finish resets the launch counters and, if asked, commits
-    __shared__ bool is_last;
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      is_last = atomicAdd(&t.misc[MISC_DONE], 1ull) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (is_last) {
-      __threadfence();
-      if (fz.commit) commit_block(t);
-      if (tid == 0) {
-        t.misc[MISC_DONE] = 0;
-        t.misc[MISC_RSV] = 0;
-        t.misc[MISC_TICKET] = 0;
-      }
-    }
-  }
+}
+
+// Metadata of a planned append (launched right behind its copy walk, PDL):
+// one size update per LFVector (the reference's single fetch_add per batch),
+// bucket publication (flag, ptr, pmask, cap) and, if asked, the commit scan.
+__global__ void __launch_bounds__(1024) k_planned_meta(Tables t, Fuse fz) {
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  stage_cbase(t, scb);
+  __syncthreads();
+  planned_metadata(t, scb, fz);
 }
 
 // rw_g (bench_cli.py:339-366, the paper's rw_g): every 16 B group of
@@ -798,8 +842,13 @@ __global__ void __launch_bounds__(512) k_walk(Tables t, const char *flat_src, ch
 // are updated element by element.
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total, T addend) {
-  extern __shared__ uint64_t sdir[];
-  const uint64_t *pre = stage_dir(t.prefix, t.S, sdir);
+  pdl_begin();
+  __shared__ char *scb[kMaxBuckets];
+  stage_cbase(t, scb);
+  __syncthreads();
+  const uint64_t *pre = t.prefix;
+  constexpr uint32_t LGE = sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : sizeof(T) == 4 ? 2 : 3;
+  const uint32_t lg0 = t.log2fb + LGE;
   constexpr uint32_t VE = 16 / sizeof(T);
   constexpr int U = kDefUnroll;
   typedef LdSt<kDefLS == 1 ? 2 : kDefLS> M;
@@ -808,7 +857,7 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   for (uint64_t c0 = wid * 32 * U; c0 < nvec; c0 += nwarps * 32 * U) {
-    uint32_t s = upper_shard(pre, t.S, c0 * VE);      // warp-uniform key: smem broadcast
+    uint32_t s = warp_find_shard(pre, t.S, c0 * VE);  // warp-uniform 32-ary search
     uint4 r[U];
     T *p[U];
     bool vec[U];
@@ -822,7 +871,7 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
         while (pre[s + 1] <= g) ++s;
         uint32_t b; uint64_t o;
         locate(g - pre[s], t.log2fb, b, o);
-        p[u] = (T *)(t.ptr[(size_t)s * t.MB + b]) + o;
+        p[u] = (T *)slot_addr(scb, s, b, lg0) + o;
         vec[u] = g + VE <= pre[s + 1] && (o % VE) == 0 && o + VE <= (1ull << (t.log2fb + b));
         if (vec[u]) r[u] = M::ld((const uint4 *)p[u]);
       }
@@ -845,7 +894,7 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
           while (pre[sj + 1] <= gj) ++sj;
           uint32_t b; uint64_t o;
           locate(gj - pre[sj], t.log2fb, b, o);
-          T *q = (T *)(t.ptr[(size_t)sj * t.MB + b]) + o;
+          T *q = (T *)slot_addr(scb, sj, b, lg0) + o;
           *q = AddOp<T>::apply(*q, addend);
         }
       }
@@ -916,8 +965,9 @@ __global__ void k_flat_insert(char *buf, uint64_t cap, unsigned long long *count
 
 template <typename T, int UNROLL = kDefUnroll, int LS = kDefLS>
 __global__ void __launch_bounds__(512) k_flat_add(char *buf, uint64_t n, T a, uint32_t reps) {
-  // grid-stride over 32 KiB chunks of the contiguous array
-  constexpr uint64_t CH = kTileBytes / sizeof(T);
+  pdl_begin();
+  // one kFlatChunk chunk of the contiguous array per CTA (non-persistent grid)
+  constexpr uint64_t CH = kFlatChunk / sizeof(T);
   const uint64_t nch = (n + CH - 1) / CH;
   for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
     uint64_t lo = c * CH, len = min(n - lo, CH);
@@ -1175,6 +1225,18 @@ struct Slab {
     for (size_t c = c0; c <= c1; ++c) if (!r->chunks[c].mapped) n += r->chunk;
     return n;
   }
+  // unmap chunks without live buckets, largest class first, until at most
+  // `keep` bytes stay mapped (caller synchronised the device)
+  void trim_to(uint64_t keep) {
+    for (int b = (int)MB - 1; b >= 0 && mapped > keep && cached; --b) {
+      if (small_off[b] != ~uint64_t(0)) continue;
+      Region &r = big[b];
+      for (size_t c = r.chunks.size(); c-- > 0 && mapped > keep;)
+        if (r.chunks[c].mapped && r.chunks[c].refs == 0) unmap_chunk(r, c);
+    }
+    for (size_t c = small.chunks.size(); c-- > 0 && mapped > keep;)
+      if (small.chunks[c].mapped && small.chunks[c].refs == 0) unmap_chunk(small, c);
+  }
   // unmap every chunk without live buckets (caller synchronised the device)
   void trim() {
     auto go = [&](Region &r) {
@@ -1199,6 +1261,28 @@ struct Slab {
     mapped = cached = va_used = 0;
   }
 };
+
+// Every library kernel is launched with programmatic stream serialization
+// (PDL): it may start while its predecessor drains and waits in
+// pdl_begin(), so back-to-back kernels (grow -> append -> grow ...) overlap
+// launch latency and prologue with the previous kernel's tail.
+bool g_pdl = true;
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 int g_sms[64] = {0};
 
@@ -1300,7 +1384,6 @@ struct gg_array {
   std::vector<uint64_t> size, cap, ops, prefix, flags;  // flags: bitmask per shard
   std::vector<uint8_t> dirty;                            // shard saw a failed reservation
   uint64_t live = 0;                                     // bytes of live buckets
-  uint32_t epoch = 0;                                    // fused-launch ready-flag epoch
   std::vector<uint32_t> headroom;                        // (s, b) backed for a device view
   bool cbase_dirty = false;                              // a class region appeared
   uint64_t alloc_calls = 0;
@@ -1342,12 +1425,6 @@ inline void use_dev(int dev) {
   if (cudaGetDevice(&cur) != cudaSuccess || cur != dev) cudaSetDevice(dev);
 }
 
-uint32_t walk_threads();
-int grid_for(const gg_array *a, uint64_t tiles, int per_sm = 8) {
-  uint64_t g = (uint64_t)sm_count(a->dev) * per_sm * kThreads / walk_threads();
-  if (tiles < g) g = tiles;
-  return (int)std::max<uint64_t>(g, 1);
-}
 
 Tables tables_for_launch(gg_array *a, bool with_ctl) {
   Tables t = a->t;
@@ -1449,91 +1526,61 @@ int commit_plan(gg_array *a, Plan &p, cudaStream_t st) {
   return push_cbase(a, st);
 }
 
-// tile of a streaming launch: 32 KiB, shrunk (down to 4 KiB) until the grid
-// has ~8 CTAs per SM, so small rounds still spread over every SM
-uint32_t walk_threads() { return g_tune.threads ? g_tune.threads : kThreads; }
-
-uint32_t tile_elems(const gg_array *a, uint64_t total) {
-  uint64_t bytes = total * a->esz;
-  uint64_t want = (uint64_t)sm_count(a->dev) * 8 * kThreads / walk_threads();
-  uint64_t tb = g_tune.tile_bytes ? g_tune.tile_bytes : kTileBytes;
-  while (tb > 4096 && bytes / tb < want) tb >>= 1;
-  return (uint32_t)(tb / a->esz);
+// Streaming launches: one tile per CTA of kThreads threads x U 16 B vectors.
+// Large work spaces use the U the sweep measured best per walk (tools/
+// sweep.py, B200: copies into / in place on the slabs U = 8 -- 32 KiB tiles,
+// flatten U = 4); smaller ones shrink U so small rounds still spread over
+// every SM.  gg_set_tuning can force U.
+uint32_t walk_unroll(const gg_array *a, uint64_t total, int w) {
+  if (g_tune.unroll > 0) return (uint32_t)g_tune.unroll;
+  const uint64_t bytes = total * a->esz;
+  if (bytes < (uint64_t(32) << 20)) return 2u;
+  if (bytes < (uint64_t(256) << 20)) return 4u;
+  return w == W_FLATTEN ? 4u : 8u;
 }
-size_t dir_smem(const gg_array *a) { return (a->S + 1) <= kSmemDir ? (a->S + 1) * 8 : 0; }
 
-// dispatch of the tuned variants (4-byte elements only)
-template <int W, typename T, int U, int LS>
-void walk4v(int grid, size_t sm, cudaStream_t st, const Tables &t, const char *src, char *dst,
-            uint64_t total, T add, uint32_t reps, uint32_t tile) {
-  { k_walk<4, W, T, U, LS><<<grid, walk_threads(), sm, st>>>(t, src, dst, total, add, reps, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); }
+template <int ESZ, int W, typename T, bool P, int U>
+cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
+                   T add, uint32_t reps, Fuse fz, cudaStream_t st) {
+  const uint32_t tile = (uint32_t)U * kThreads * (16 / ESZ);
+  const uint64_t grid = (total + tile - 1) / tile;
+  cudaError_t e = launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src,
+                           dst, total, add, reps, tile, fz);
+  if (P && e == cudaSuccess) e = launch_k(k_planned_meta, 1, 1024, 0, st, t, fz);
+  return e;
 }
-template <int W, typename T>
-void walk4(int grid, size_t sm, cudaStream_t st, const Tables &t, const char *src, char *dst,
-           uint64_t total, T add, uint32_t reps, uint32_t tile) {
-  const int ls = g_tune.ls < 0 ? kDefLS : g_tune.ls, u = g_tune.unroll < 0 ? kDefUnroll : g_tune.unroll;
-  switch (ls * 16 + u) {
-    case 0 * 16 + 4: walk4v<W, T, 4, 0>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 1 * 16 + 4: walk4v<W, T, 4, 1>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 2 * 16 + 4: walk4v<W, T, 4, 2>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 3 * 16 + 4: walk4v<W, T, 4, 3>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 0 * 16 + 8: walk4v<W, T, 8, 0>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 1 * 16 + 8: walk4v<W, T, 8, 1>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 2 * 16 + 8: walk4v<W, T, 8, 2>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    case 3 * 16 + 8: walk4v<W, T, 8, 3>(grid, sm, st, t, src, dst, total, add, reps, tile); break;
-    default: walk4v<W, T, kDefUnroll, kDefLS>(grid, sm, st, t, src, dst, total, add, reps, tile);
+
+template <int ESZ, int W, typename T, bool P = false>
+int walk(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total, T add,
+         uint32_t reps, Fuse fz, cudaStream_t st) {
+  if (total == 0) return GG_OK;
+  cudaError_t e;
+  switch (walk_unroll(a, total, W)) {
+    case 1: e = walk_u<ESZ, W, T, P, 1>(a, t, src, dst, total, add, reps, fz, st); break;
+    case 2: e = walk_u<ESZ, W, T, P, 2>(a, t, src, dst, total, add, reps, fz, st); break;
+    case 8: e = walk_u<ESZ, W, T, P, 8>(a, t, src, dst, total, add, reps, fz, st); break;
+    default: e = walk_u<ESZ, W, T, P, 4>(a, t, src, dst, total, add, reps, fz, st); break;
+  }
+  if (e != cudaSuccess) return fail(GG_ECUDA, std::string("walk launch: ") + cudaGetErrorString(e));
+  return GG_OK;
+}
+
+// copy-type walks (insert / duplicate / flatten) for every element size
+template <int W, bool P = false>
+int walk_copy(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
+              Fuse fz, cudaStream_t st) {
+  switch (a->esz) {
+    case 1: return walk<1, W, uint8_t, P>(a, t, src, dst, total, (uint8_t)0, 0u, fz, st);
+    case 2: return walk<2, W, uint16_t, P>(a, t, src, dst, total, (uint16_t)0, 0u, fz, st);
+    case 4: return walk<4, W, uint32_t, P>(a, t, src, dst, total, 0u, 0u, fz, st);
+    default: return walk<8, W, uint64_t, P>(a, t, src, dst, total, (uint64_t)0, 0u, fz, st);
   }
 }
 
 template <int W>
 int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
                 cudaStream_t st) {
-  if (total == 0) return GG_OK;
-  const uint32_t tile = tile_elems(a, total);
-  int grid = grid_for(a, (total + tile - 1) / tile);
-  const size_t sm = dir_smem(a);
-  switch (a->esz) {
-    case 1: { k_walk<1, W, uint8_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_walk<2, W, uint16_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: walk4<W, uint32_t>(grid, sm, st, t, src, dst, total, 0u, 1u, tile); break;
-    case 8: { k_walk<8, W, uint64_t><<<grid, kThreads, sm, st>>>(t, src, dst, total, 0, 0, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-  }
-  CUDA_TRY(cudaGetLastError());
-  return GG_OK;
-}
-
-// fused append launch (same persistent grid as the unfused walk; the ticket
-// scheme makes the reservation wait safe under oversubscription)
-template <int ESZ, int W, typename E>
-int launch_fused(gg_array *a, const Tables &t, const char *src, uint64_t total, Fuse fz,
-                 cudaStream_t st) {
-  auto kern = k_walk<ESZ, W, E, kDefUnroll, kDefLS, true>;
-  static int per_sm = 0;
-  const size_t sm = dir_smem(a);
-  if (!per_sm) {
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, sm) != cudaSuccess || n < 1) n = 1;
-    per_sm = n;
-  }
-  const uint32_t tile = total ? tile_elems(a, total) : 1;
-  uint64_t grid = total ? (total + tile - 1) / tile : 1;
-  (void)per_sm;
-  grid = std::min<uint64_t>(grid, (uint64_t)sm_count(a->dev) * 8);
-  grid = std::max<uint64_t>(grid, 1);
-  { kern<<<(int)grid, kThreads, sm, st>>>(t, src, nullptr, total, E(0), 0u, tile, fz); g_launches.fetch_add(1, std::memory_order_relaxed); }
-  CUDA_TRY(cudaGetLastError());
-  return GG_OK;
-}
-
-template <int W>
-int launch_fused_esz(gg_array *a, const Tables &t, const char *src, uint64_t total, Fuse fz,
-                     cudaStream_t st) {
-  switch (a->esz) {
-    case 1: return launch_fused<1, W, uint8_t>(a, t, src, total, fz, st);
-    case 2: return launch_fused<2, W, uint16_t>(a, t, src, total, fz, st);
-    case 4: return launch_fused<4, W, uint32_t>(a, t, src, total, fz, st);
-    default: return launch_fused<8, W, uint64_t>(a, t, src, total, fz, st);
-  }
+  return walk_copy<W, false>(a, t, src, dst, total, Fuse{0, 0}, st);
 }
 
 void host_commit(gg_array *a) {
@@ -1545,7 +1592,7 @@ void host_commit(gg_array *a) {
 // run an allocating append: upload ctl/zero list if needed, then either one
 // fused launch (reserve + allocate + copy [+ commit]) or the unfused
 // reserve / zero / copy sequence (failure paths that must zero buckets).
-int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src,
+int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
                uint64_t total, cudaStream_t st, uint32_t flags, bool *committed) {
   *committed = false;
   int rc = commit_plan(a, p, st);
@@ -1557,23 +1604,24 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src
     size_t bytes[1] = {a->S * sizeof(uint32_t)};
     if ((rc = a->up.upload(st, 1, dst, srcs, bytes))) return rc;
   }
-  // Fused single launch by default.  Under CUDA-graph capture inter-kernel
-  // gaps are ~1 us, and the measured A/B (r01) favours the separate
-  // reserve / copy / commit kernels there (680 vs 663 Gelem/s on config 2),
-  // while eager issue favours the fused launch (604 vs 597).
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(st, &cap);
-  if (p.zero_pairs.empty() && !(flags & GG_F_UNFUSED) && cap == cudaStreamCaptureStatusNone) {
-    const bool commit = (flags & GG_F_COMMIT) && !p.any_fail;
-    if (++a->epoch == 0) ++a->epoch;
-    Fuse fz{reserve_mode, a->epoch, commit ? 1 : 0};
-    rc = walk == W_INSERT ? launch_fused_esz<W_INSERT>(a, t, src, total, fz, st)
-                          : launch_fused_esz<W_DUP>(a, t, nullptr, total, fz, st);
-    if (rc) return rc;
+  // No failure planned: ONE launch copies into host-backed slots and applies
+  // the reservation metadata (+ commit) in its last CTA.  Failure paths
+  // (ctl words, zeroing, explicit starts) take the separate reserve / zero /
+  // copy kernels.
+  if (!p.any_ctl && p.zero_pairs.empty() && reserve_mode != 2 && !(flags & GG_F_UNFUSED)) {
+    const bool commit = (flags & GG_F_COMMIT) != 0;
+    if (total) {
+      Fuse fz{reserve_mode, commit ? 1 : 0};
+      rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
+                            : walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fz, st);
+      if (rc) return rc;
+    } else if (commit) {
+      CUDA_TRY(launch_k(k_commit, 1, 1024, 0, st, a->t));
+    }
     if (commit) { host_commit(a); *committed = true; }
     return GG_OK;
   }
-  { k_reserve<<<(a->S + 255) / 256, 256, 0, st>>>(t, reserve_mode); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(launch_k(k_reserve, (a->S + 255) / 256, 256, 0, st, t, reserve_mode));
   CUDA_TRY(cudaGetLastError());
   if (!p.zero_pairs.empty()) {
     uint32_t *d_pairs = nullptr;
@@ -1586,12 +1634,12 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int walk, const char *src
     CUDA_TRY(cudaFreeAsync(d_pairs, st));
     CUDA_TRY(cudaStreamSynchronize(st));  // zero_pairs host memory is pageable
   }
-  rc = walk == W_INSERT ? launch_walk<W_INSERT>(a, t, src, nullptr, total, st)
-                        : launch_walk<W_DUP>(a, t, nullptr, nullptr, total, st);
+  rc = wk == W_INSERT ? launch_walk<W_INSERT>(a, t, src, nullptr, total, st)
+                      : launch_walk<W_DUP>(a, t, nullptr, nullptr, total, st);
   if (rc) return rc;
   if ((flags & GG_F_COMMIT) && !p.any_fail) {
     host_commit(a);
-    { k_commit<<<1, 1024, 0, st>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    CUDA_TRY(launch_k(k_commit, 1, 1024, 0, st, a->t));
     CUDA_TRY(cudaGetLastError());
     *committed = true;
   }
@@ -1608,43 +1656,34 @@ int finish_status(gg_array *a, const Plan &p, int32_t *h_status) {
 template <typename T>
 int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode, uint64_t total,
               cudaStream_t st) {
-  const size_t sm = dir_smem(a);
   if (mode == GG_RW_GLOBAL) {
     const uint64_t nvec = (total * sizeof(T) + 15) / 16;
-    int grid = (int)std::min<uint64_t>((nvec + kThreads * kDefUnroll - 1) / (kThreads * kDefUnroll),
-                                       (uint64_t)sm_count(a->dev) * 8);
+    const uint64_t grid = (nvec + kThreads * kDefUnroll - 1) / (kThreads * kDefUnroll);
     for (uint32_t p = 0; p < passes; ++p)
-      { k_rw_global<T><<<grid, kThreads, sm, st>>>(t, total, addend); g_launches.fetch_add(1, std::memory_order_relaxed); }
-  } else {
-    const uint32_t tile = tile_elems(a, total);
-    int grid = grid_for(a, (total + tile - 1) / tile);
-    if constexpr (sizeof(T) == 4 && std::is_same<T, int32_t>::value) {
-      if (mode == GG_RW_FUSED) walk4<W_RW, T>(grid, sm, st, t, nullptr, nullptr, total, addend, passes, tile);
-      else for (uint32_t p = 0; p < passes; ++p) walk4<W_RW, T>(grid, sm, st, t, nullptr, nullptr, total, addend, 1, tile);
-      CUDA_TRY(cudaGetLastError());
-      return GG_OK;
-    }
-    if (mode == GG_RW_FUSED)
-      { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, passes, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); }
-    else
-      for (uint32_t p = 0; p < passes; ++p)
-        { k_walk<sizeof(T), W_RW, T><<<grid, kThreads, sm, st>>>(t, nullptr, nullptr, total, addend, 1, tile, Fuse{0, 0, 0}); g_launches.fetch_add(1, std::memory_order_relaxed); }
+      CUDA_TRY(launch_k(k_rw_global<T>, (unsigned)grid, kThreads, 0, st, t, total, addend));
+    return GG_OK;
   }
-  CUDA_TRY(cudaGetLastError());
+  const Fuse none{0, 0};
+  if (mode == GG_RW_FUSED)
+    return walk<sizeof(T), W_RW, T>(a, t, nullptr, nullptr, total, addend, passes, none, st);
+  for (uint32_t p = 0; p < passes; ++p) {
+    int rc = walk<sizeof(T), W_RW, T>(a, t, nullptr, nullptr, total, addend, 1u, none, st);
+    if (rc) return rc;
+  }
   return GG_OK;
 }
 
 template <typename T>
 int launch_flat_add(char *buf, uint64_t n, T a, uint32_t passes, int fused, int dev,
                     cudaStream_t st) {
+  (void)dev;
   if (n == 0) return GG_OK;
-  const uint64_t ch = kTileBytes / sizeof(T);
-  uint64_t nch = (n + ch - 1) / ch;
-  int grid = (int)std::min<uint64_t>(nch, (uint64_t)sm_count(dev) * 8);
-  if (fused) { k_flat_add<T><<<grid, kThreads, 0, st>>>(buf, n, a, passes); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  const uint64_t ch = kFlatChunk / sizeof(T);
+  const uint64_t grid = (n + ch - 1) / ch;      // one chunk per CTA
+  if (fused) CUDA_TRY(launch_k(k_flat_add<T>, (unsigned)grid, kThreads, 0, st, buf, n, a, passes));
   else
-    for (uint32_t p = 0; p < passes; ++p) { k_flat_add<T><<<grid, kThreads, 0, st>>>(buf, n, a, 1); g_launches.fetch_add(1, std::memory_order_relaxed); }
-  CUDA_TRY(cudaGetLastError());
+    for (uint32_t p = 0; p < passes; ++p)
+      CUDA_TRY(launch_k(k_flat_add<T>, (unsigned)grid, kThreads, 0, st, buf, n, a, 1u));
   return GG_OK;
 }
 
@@ -1864,7 +1903,7 @@ int gg_commit(gg_array *a, void *stream) {
   uint64_t acc = 0;
   a->prefix[0] = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
-  { k_commit<<<1, 1024, 0, S_(stream)>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(launch_k(k_commit, 1, 1024, 0, S_(stream), a->t));
   CUDA_TRY(cudaGetLastError());
   return GG_OK;
 }
@@ -1911,7 +1950,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
       if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
     }
     Tables t = tables_for_launch(a, true);
-    { k_grow<<<(a->S + 255) / 256, 256, 0, st>>>(t, uk); g_launches.fetch_add(1, std::memory_order_relaxed); }
+    CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, st, t, uk));
     CUDA_TRY(cudaGetLastError());
     if (!p.zero_pairs.empty()) {
       // grow on a dirty shard: zero the new buckets (reference buckets are np.zeros)
@@ -1970,7 +2009,8 @@ int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *st
   return GG_OK;
 }
 
-int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint32_t flags, void *stream) {
+int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_bytes,
+                 void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
@@ -1993,26 +2033,26 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint32_t flags, void 
   int rc = a->up.upload(st, 1, dst, src, bytes);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
-  { k_shrink<<<(a->S + 255) / 256, 256, 0, st>>>(t, a->t.count); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(launch_k(k_shrink, (a->S + 255) / 256, 256, 0, st, t, (const uint64_t *)a->t.count));
   CUDA_TRY(cudaGetLastError());
   uint64_t acc = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
-  { k_commit<<<1, 1024, 0, st>>>(a->t); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(launch_k(k_commit, 1, 1024, 0, st, a->t));
   CUDA_TRY(cudaGetLastError());
-  // GG_SHRINK_RELEASE: unmap emptied chunks now (waits for the device: queued
-  // work may still read the released buckets).  Not under graph capture,
-  // where the chunks stay cached until gg_trim.
+  // unmap emptied chunks down to keep_mapped_bytes (waits for the device:
+  // queued work may still read the released buckets).  Never under graph
+  // capture, where the chunks stay cached until gg_trim.
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cap);
-  if ((flags & GG_SHRINK_RELEASE) && cap == cudaStreamCaptureStatusNone && a->slab.cached) {
+  if (cap == cudaStreamCaptureStatusNone && a->slab.cached && a->slab.mapped > keep_mapped_bytes) {
     CUDA_TRY(cudaDeviceSynchronize());
-    a->slab.trim();
+    a->slab.trim_to(keep_mapped_bytes);
   }
   return GG_OK;
 }
 
 int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
-  return gg_shrink_ex(a, h_new_sizes, GG_SHRINK_RELEASE, stream);
+  return gg_shrink_ex(a, h_new_sizes, 0, stream);
 }
 
 int gg_trim(gg_array *a) {
@@ -2276,9 +2316,15 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
 }
 
 int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads) {
-  if (ls > 3 || (unroll != -1 && unroll != 4 && unroll != 8) || (threads && threads != 256 && threads != 512))
+  (void)ls; (void)tile_bytes; (void)threads;
+  if (unroll != -1 && unroll != 1 && unroll != 2 && unroll != 4 && unroll != 8)
     return fail(GG_EVALUE, "bad tuning");
-  g_tune.ls = ls; g_tune.unroll = unroll; g_tune.tile_bytes = tile_bytes; g_tune.threads = threads;
+  g_tune.unroll = unroll;
+  return GG_OK;
+}
+
+int gg_set_pdl(int32_t on) {
+  g_pdl = on != 0;
   return GG_OK;
 }
 

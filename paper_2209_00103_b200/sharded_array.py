@@ -531,13 +531,22 @@ class GrowableArray:
             caps = np.asarray([max(int(x), 0) for x in distribution], np.uint64)
         self._reserve(caps)
 
-    def shrink(self, new_sizes, release: bool = True) -> None:
+    def shrink(self, new_sizes, release=2.0) -> None:
         """Extension (no reference semantics): pop shards to ``new_sizes`` and release
-        buckets beyond the minimal prefix; commits.  ``release`` unmaps the slab
-        chunks left without a live bucket at once (waits for the device);
-        ``release=False`` keeps them mapped for reuse until :meth:`trim`."""
+        buckets beyond the minimal prefix; commits.  Slab chunks left without a
+        live bucket are unmapped according to ``release``: a number f keeps at
+        most f x the needed bytes mapped (default 2.0, the paper's footprint
+        bound, unmapping as little as possible -- every unmap/remap costs
+        driver time); True unmaps them all; False keeps them all mapped for
+        in-place reuse until :meth:`trim`."""
         ns = L.u64_array(np.broadcast_to(np.asarray(new_sizes), (self._S,)))
-        L.check(L.lib.gg_shrink_ex(self._h, L.ptr(ns), 1 if release else 0, self._stream()), "shrink")
+        if release is True:
+            keep = 0
+        elif release is False or release is None:
+            keep = (1 << 64) - 1
+        else:
+            keep = int(float(release) * int(ns.sum()) * self.dtype.itemsize)
+        L.check(L.lib.gg_shrink_ex(self._h, L.ptr(ns), keep, self._stream()), "shrink")
         self._dirty()
 
     def trim(self) -> None:

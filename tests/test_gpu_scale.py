@@ -127,7 +127,7 @@ def test_slab_release_and_cache(gg):
     ms0 = a.memory_stats()
     assert ms0["mapped_bytes"] <= 2 * ms0["needed_bytes"]
     small = n >> 6
-    a.shrink(small // S)
+    a.shrink(small // S, release=True)
     ms = a.memory_stats()
     assert ms["cached_bytes"] == 0
     assert ms["capacity_bytes"] == int(O.sharded_capacity_elements([small], S, fb)[0]) * 4
@@ -175,10 +175,9 @@ def test_phased_footprint_follows_live_capacity(gg):
             offs = np.concatenate([[0], np.cumsum(d)]).astype(np.uint64)
             a.insert_csr(src[:int(offs[-1])], offs)
         else:
-            a.shrink(new)
+            a.shrink(new)                       # default policy: keep mapped <= 2x needed
         n = target
         ms = a.memory_stats()
-        assert ms["cached_bytes"] == 0
         if target >= n0 // 8:
             worst = max(worst, ms["mapped_bytes"] / ms["needed_bytes"])
             assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"] + (8 << 20)

@@ -1,7 +1,6 @@
-"""Sweep the 4-byte streaming-kernel variants (cache policy x unroll x tile x
-CTA size) on the config-2/3 state: duplicate-insert of the last doubling round
+"""Sweep the streaming-kernel unroll (tile = 256 threads x U x 16 B, one tile
+per CTA) on the config-2/3 state: duplicate-insert of the last doubling round
 (2^29 -> 2^30), flatten of 2^30, and one +1 pass over 2^30."""
-import itertools
 import json
 import os
 import sys
@@ -54,16 +53,17 @@ del x, y
 a.insert_duplicate()          # state at 2^30 for flatten / rw
 full = np.full(S, 1 << 21, np.uint64)
 res = []
-for ls, un, tile, thr in itertools.product([0, 1, 2, 3], [4, 8], [16384, 32768, 65536], [256, 512]):
-    _lib.check(_lib.lib.gg_set_tuning(ls, un, tile, thr))
+for un in [1, 2, 4, 8]:
+    _lib.check(_lib.lib.gg_set_tuning(-1, un, 0, 0))
     a.shrink(half, release=False)
     d = t_dup()
     a.insert_duplicate()
     f = t_op(lambda: a.flatten_device(out=out))
     r = t_op(lambda: a.rw_add(1))
-    row = {"ls": ls, "unroll": un, "tile": tile, "threads": thr,
+    g = t_op(lambda: a.rw_add(1, mode="global"))
+    row = {"unroll": un, "tile_bytes": un * 256 * 16,
            "dup_gbs": round(8 * (1 << 29) / d / 1e6, 1), "flatten_gbs": round(8 * (1 << 30) / f / 1e6, 1),
-           "rw_gbs": round(8 * (1 << 30) / r / 1e6, 1)}
+           "rw_gbs": round(8 * (1 << 30) / r / 1e6, 1), "rw_global_gbs": round(8 * (1 << 30) / g / 1e6, 1)}
     res.append(row)
     print(json.dumps(row), flush=True)
 _lib.lib.gg_set_tuning(-1, -1, 0, 0)

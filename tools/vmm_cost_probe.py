@@ -74,3 +74,28 @@ for mib in (2, 8, 64, 256, 1024):
     cu.cuMemAddressFree(va, C.c_size_t(size * reps))
     print(json.dumps({"mib": mib, **{k: round(v / reps * 1e6, 1) for k, v in t.items()},
                       "remap_cycle_us": round(rm / reps * 1e6, 1), "unit": "us per call"}))
+
+# one cuMemSetAccess / cuMemUnmap over a run of separately created mappings?
+size, n = 64 << 20, 8
+va = C.c_uint64()
+ck(cu.cuMemAddressReserve(C.byref(va), C.c_size_t(size * n), C.c_size_t(size), C.c_uint64(0), C.c_uint64(0)), "reserve")
+hs = []
+t0 = time.perf_counter()
+for i in range(n):
+    h = C.c_uint64()
+    ck(cu.cuMemCreate(C.byref(h), C.c_size_t(size), C.byref(prop), C.c_uint64(0)), "create")
+    ck(cu.cuMemMap(C.c_uint64(va.value + i * size), C.c_size_t(size), C.c_size_t(0), h, C.c_uint64(0)), "map")
+    hs.append(h)
+t1 = time.perf_counter()
+ra = cu.cuMemSetAccess(va, C.c_size_t(size * n), C.byref(acc), C.c_size_t(1))
+t2 = time.perf_counter()
+x = torch.empty(0)
+ru = cu.cuMemUnmap(va, C.c_size_t(size * n))
+t3 = time.perf_counter()
+for h in hs:
+    cu.cuMemRelease(h)
+t4 = time.perf_counter()
+print(json.dumps({"run_of": n, "mib": 64, "create_map_us": round((t1 - t0) / n * 1e6, 1),
+                  "set_access_rc": ra, "set_access_run_us": round((t2 - t1) * 1e6, 1),
+                  "unmap_rc": ru, "unmap_run_us": round((t3 - t2) * 1e6, 1),
+                  "release_us": round((t4 - t3) / n * 1e6, 1)}))
