@@ -242,7 +242,8 @@ def run_device(args, rank, world, local_rank):
                      "traffic": (traffic or {}).get("bytes_per_launch"),
                      "traffic_detail": traffic, "algorithmic_bytes_per_elem": 8,
                      "achieved_def": "sum of 8 B x elements duplicated / sum of CUDA-event times of the "
-                                     "insert phases (reserve + walk + commit) over the K eager steps",
+                                     "insert phases (planned copy walk + metadata kernel) over the "
+                                     "K eager steps",
                      "last_round_2p29_gbs": round(float(last_gbs), 1),
                      "last_round_frac": round(float(last_gbs) / hbm, 4)},
         "phases": {"insert_ms_per_step": round(dup_ms / args.steps, 4),
@@ -260,6 +261,8 @@ def run_device(args, rank, world, local_rank):
         "eager": {"value": round(eager_value, 3), "ms_per_step": round(eager_ms / args.steps, 4),
                   "host_enqueue_ms_per_step": round(host_ms / args.steps, 4)},
     }
+    if dist:
+        out["gather_flatten"] = gather_leg(args, torch, device, step, dist, world)
     if not args.quick:
         out.update(secondary(args, gg, torch, device, step, hbm))
         out["phased_config4"] = phased_leg(args, gg, torch, device)
@@ -267,6 +270,45 @@ def run_device(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args)
     return out
+
+
+def gather_leg(args, torch, device, step, dist, world):
+    """Config 5's exchange step: every GPU's 2^30-element array gathered into
+    rank 0 by the fused flatten into peer memory (CUDA IPC over NVLink /
+    NVSwitch, multigpu.PeerGather).  Device time = max over ranks of the
+    flatten launch; bytes over NVLink = all slices but the root's own."""
+    try:
+        from paper_2209_00103_b200.multigpu import DistributedGrowableArray, PeerGather
+        d = DistributedGrowableArray(step.arr, device=device)
+        g = PeerGather(d, 0)
+        g.run(); g.wait()
+        k = 3
+        e0, e1 = _events(torch)
+        dist.barrier()
+        e0.record()
+        for _ in range(k):
+            g.run()
+        e1.record()
+        g.wait()
+        t = torch.tensor([e0.elapsed_time(e1) / k], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        total = g.prefix[-1] * 4
+        nvlink = total - (g.prefix[1] - g.prefix[0]) * 4
+        ok = True
+        if dist.get_rank() == 0:
+            flat = g.result()
+            per = step.arr.committed_size
+            ok = bool(torch.equal(flat[:per], step.arr.flatten_device()))
+            del flat
+        g.close()
+        del g
+        torch.cuda.empty_cache()
+        return {"ms": round(ms, 4), "bytes_total": total, "bytes_over_nvlink": nvlink,
+                "nvlink_gbs_into_root": round(nvlink / (ms * 1e-3) / 1e9, 1),
+                "root_slice_ok": ok, "method": "fused K-flatten into the root buffer (CUDA IPC)"}
+    except Exception as exc:                          # report, never lose the bench line
+        return {"error": repr(exc)[:300]}
 
 
 def launches_per_step(step) -> int:

@@ -226,6 +226,18 @@ int gg_flat_add(void *d_buf, uint64_t n, uint32_t dtype, const void *h_addend,
 int gg_buf_alloc(uint64_t bytes, void *stream, void **d_out);
 int gg_buf_free(void *d_ptr, void *stream);
 int gg_buf_copy(void *d_dst, const void *d_src, uint64_t bytes, void *stream);
+/* ---- multi-GPU gather: the root allocates the global flat
+ * buffer with gg_ipc_alloc, publishes its handle (gg_ipc_get_handle, 64 B),
+ * every other rank maps it with gg_ipc_open and runs gg_flatten straight
+ * into it at its global base -- the flatten kernel's stores cross NVLink /
+ * NVSwitch, so the gather is fused into the flatten (no staging copy, no
+ * NCCL call on the data path). */
+int gg_ipc_alloc(uint64_t bytes, void **d_out);
+int gg_ipc_free(void *d_ptr);
+int gg_ipc_handle_bytes(void);
+int gg_ipc_get_handle(void *d_ptr, void *h_handle);
+int gg_ipc_open(const void *h_handle, void **d_out);
+int gg_ipc_close(void *d_ptr);
 /* memMap baseline (paper section 3-A, ChunkTableArray analog): one VA
  * reservation, physical 2 MiB granules appended with cuMemCreate/cuMemMap. */
 typedef struct gg_vmm gg_vmm;

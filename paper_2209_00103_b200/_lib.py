@@ -85,6 +85,12 @@ _SIGS = {
     "gg_slab_stats": ([P, PU64], C.c_int),
     "gg_flat_insert": ([P, U64, P, P, U64, U32, I32, P], C.c_int),
     "gg_flat_add": ([P, U64, U32, P, U32, I32, P], C.c_int),
+    "gg_ipc_alloc": ([U64, C.POINTER(C.c_void_p)], C.c_int),
+    "gg_ipc_free": ([P], C.c_int),
+    "gg_ipc_handle_bytes": ([], C.c_int),
+    "gg_ipc_get_handle": ([P, P], C.c_int),
+    "gg_ipc_open": ([P, C.POINTER(C.c_void_p)], C.c_int),
+    "gg_ipc_close": ([P], C.c_int),
     "gg_buf_alloc": ([U64, P, C.POINTER(P)], C.c_int),
     "gg_buf_free": ([P, P], C.c_int),
     "gg_buf_copy": ([P, P, U64, P], C.c_int),

@@ -2454,6 +2454,35 @@ int gg_flat_add(void *d_buf, uint64_t n, uint32_t dtype, const void *h_addend, u
   return rc;
 }
 
+// ---- peer memory for the multi-GPU gather (CUDA IPC over NVLink / NVSwitch)
+int gg_ipc_alloc(uint64_t bytes, void **d_out) {
+  *d_out = nullptr;
+  CUDA_TRY(cudaMalloc(d_out, bytes ? bytes : 16));   // IPC needs a plain cudaMalloc allocation
+  return GG_OK;
+}
+int gg_ipc_free(void *d_ptr) {
+  CUDA_TRY(cudaFree(d_ptr));
+  return GG_OK;
+}
+int gg_ipc_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+int gg_ipc_get_handle(void *d_ptr, void *h_handle) {
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, d_ptr));
+  memcpy(h_handle, &h, sizeof h);
+  return GG_OK;
+}
+int gg_ipc_open(const void *h_handle, void **d_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle, sizeof h);
+  *d_out = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(d_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return GG_OK;
+}
+int gg_ipc_close(void *d_ptr) {
+  CUDA_TRY(cudaIpcCloseMemHandle(d_ptr));
+  return GG_OK;
+}
+
 int gg_buf_alloc(uint64_t bytes, void *stream, void **d_out) {
   CUDA_TRY(cudaMallocAsync(d_out, bytes ? bytes : 16, S_(stream)));
   return GG_OK;

@@ -7,9 +7,15 @@ exchange steps are
     int64 per rank) whose exclusive scan gives each GPU's global base, so
     global order = GPU-major, then shard-major -- exactly the single-array
     ``flatten()`` order of the concatenated shard list;
-  * the global flatten / gather: every rank flattens locally (K-flatten) and
-    ships its slice to the root, which places it at the rank's global base
-    (NCCL point-to-point over NVLink/NVSwitch when the backend is nccl).
+  * the global flatten / gather.  ``method="peer"`` (device arrays): the
+    root allocates the global buffer (cudaMalloc), publishes its CUDA IPC
+    handle, and every rank runs its K-flatten STRAIGHT INTO the root's buffer
+    at its global base -- the flatten kernel's 16 B stores cross NVLink /
+    NVSwitch, so the gather is fused into the flatten tile by tile, with no
+    staging copy and no collective on the data path.  ``all_gather_flat(
+    method="peer")`` does the same into every rank's buffer.  ``method=
+    "nccl"``: local K-flatten, then point-to-point sends into the root buffer
+    (also the CPU/gloo path the tests use with the oracle array).
 
 The class only needs the local array's ``committed_size`` / ``flatten_device``
 (or ``flatten``) / ``get_many`` surface, so the host logic is exercised on CPU
@@ -18,7 +24,82 @@ with the gloo backend and the oracle array (tests/test_multigpu_gloo.py).
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
+
+_TORCH_DT = None
+
+
+def _torch_dtype(np_dtype):
+    import torch
+    global _TORCH_DT
+    if _TORCH_DT is None:
+        _TORCH_DT = {np.dtype(k): v for k, v in [
+            (np.int8, torch.int8), (np.uint8, torch.uint8), (np.int16, torch.int16),
+            (np.uint16, torch.uint16), (np.int32, torch.int32), (np.uint32, torch.uint32),
+            (np.int64, torch.int64), (np.uint64, torch.uint64), (np.float16, torch.float16),
+            (np.float32, torch.float32), (np.float64, torch.float64)]}
+    return _TORCH_DT[np.dtype(np_dtype)]
+
+
+class PeerBuffer:
+    """A cudaMalloc'd device buffer other processes can map (CUDA IPC).  Exposes
+    ``__cuda_array_interface__`` so ``torch.as_tensor(buf, device=...)`` views
+    it without a copy; freed when the last reference goes."""
+
+    _TYPESTR = {np.dtype(t): np.dtype(t).str for t in (np.int8, np.uint8, np.int16, np.uint16,
+                                                        np.int32, np.uint32, np.int64, np.uint64,
+                                                        np.float16, np.float32, np.float64)}
+
+    def __init__(self, n: int, dtype):
+        from . import _lib as L
+        self.L, self.n, self.dtype = L, int(n), np.dtype(dtype)
+        p = C.c_void_p()
+        L.check(L.lib.gg_ipc_alloc(max(1, self.n) * self.dtype.itemsize, C.byref(p)), "ipc_alloc")
+        self.ptr = int(p.value)
+
+    def handle(self) -> bytes:
+        buf = C.create_string_buffer(int(self.L.lib.gg_ipc_handle_bytes()))
+        self.L.check(self.L.lib.gg_ipc_get_handle(C.c_void_p(self.ptr), buf), "ipc_get_handle")
+        return buf.raw
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.n,), "typestr": self._TYPESTR[self.dtype], "data": (self.ptr, False),
+                "version": 3, "strides": None}
+
+    def tensor(self, device):
+        import torch
+        t = torch.as_tensor(self, device=device)
+        t._peer_buffer_owner = self          # keep the allocation alive with the view
+        return t
+
+    def __del__(self):
+        if getattr(self, "ptr", 0):
+            self.L.lib.gg_ipc_free(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+class PeerMapping:
+    """A peer's PeerBuffer opened in this process (cudaIpcOpenMemHandle with
+    lazy peer access): a device address this GPU's kernels store to over
+    NVLink."""
+
+    def __init__(self, handle: bytes):
+        from . import _lib as L
+        self.L = L
+        p = C.c_void_p()
+        L.check(L.lib.gg_ipc_open(C.create_string_buffer(handle, len(handle)), C.byref(p)), "ipc_open")
+        self.ptr = int(p.value)
+
+    def close(self):
+        if self.ptr:
+            self.L.lib.gg_ipc_close(C.c_void_p(self.ptr))
+            self.ptr = 0
+
+    def __del__(self):
+        self.close()
 
 
 class DistributedGrowableArray:
@@ -63,9 +144,55 @@ class DistributedGrowableArray:
             return self.local.flatten_device()
         return torch.from_numpy(np.ascontiguousarray(self.local.flatten()))
 
-    def flatten_global(self, root: int = 0):
+    def _peer_ok(self) -> bool:
+        return hasattr(self.local, "flatten_to")
+
+    def _sync_local(self):
+        import torch
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def flatten_global(self, root: int = 0, method: str = "auto"):
         """Gather every rank's committed contents into one array on ``root``
-        (global order).  Returns the tensor on root, None elsewhere."""
+        (global order).  Returns the tensor on root, None elsewhere.
+        ``method``: "peer" (fused flatten into the root's buffer over CUDA
+        IPC), "nccl" (local flatten + point-to-point), "auto" = peer for
+        device arrays."""
+        if method == "auto":
+            method = "peer" if self._peer_ok() else "nccl"
+        if method == "peer":
+            return self._flatten_global_peer(root)
+        return self._flatten_global_p2p(root)
+
+    def _flatten_global_peer(self, root: int):
+        g = PeerGather(self, root)
+        g.run()
+        g.wait()
+        out = g.result()
+        g.close()
+        return out
+
+    def all_gather_flat_peer(self):
+        """Every rank receives the whole flattened array: each rank's K-flatten
+        stores its slice into EVERY rank's buffer (one fused flatten per
+        destination, over CUDA IPC)."""
+        p = self.global_prefix()
+        esz = np.dtype(self.local.dtype).itemsize
+        buf = PeerBuffer(p[-1], self.local.dtype)
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, buf.handle(), group=self.group)
+        maps = [None if r == self.rank else PeerMapping(handles[r]) for r in range(self.world)]
+        if p[self.rank + 1] > p[self.rank]:
+            for r in range(self.world):
+                dst = buf.ptr if r == self.rank else maps[r].ptr
+                self.local.flatten_to(dst + p[self.rank] * esz)
+        self._sync_local()
+        self.dist.barrier(group=self.group)
+        for m in maps:
+            if m is not None:
+                m.close()
+        return buf.tensor(self.device)
+
+    def _flatten_global_p2p(self, root: int):
         import torch
         p = self.global_prefix()
         mine = self._local_flat()
@@ -94,3 +221,50 @@ class DistributedGrowableArray:
         parts = [torch.empty_like(buf) for _ in range(self.world)]
         self.dist.all_gather(parts, buf, group=self.group)
         return torch.cat([parts[r][:p[r + 1] - p[r]] for r in range(self.world)])
+
+
+class PeerGather:
+    """Reusable fused gather-flatten to ``root`` (collective setup once): the
+    root's global buffer is allocated and its IPC handle broadcast; every
+    other rank maps it.  ``run()`` launches this rank's K-flatten straight into
+    the root buffer at the rank's global base (stream-ordered, no sync);
+    ``wait()`` = local stream sync + barrier.  The directory must not change
+    between setup and the runs."""
+
+    def __init__(self, d: "DistributedGrowableArray", root: int = 0):
+        self.d, self.root = d, root
+        self.prefix = d.global_prefix()
+        self.esz = np.dtype(d.local.dtype).itemsize
+        handle = [None]
+        self.buf = self.mapping = None
+        if d.rank == root:
+            self.buf = PeerBuffer(self.prefix[-1], d.local.dtype)
+            handle[0] = self.buf.handle()
+        d.dist.broadcast_object_list(handle, src=root, group=d.group)
+        if d.rank == root:
+            self.dst = self.buf.ptr
+        else:
+            self.mapping = PeerMapping(handle[0])
+            self.dst = self.mapping.ptr
+
+    @property
+    def my_bytes(self) -> int:
+        r = self.d.rank
+        return (self.prefix[r + 1] - self.prefix[r]) * self.esz
+
+    def run(self):
+        r = self.d.rank
+        if self.prefix[r + 1] > self.prefix[r]:
+            self.d.local.flatten_to(self.dst + self.prefix[r] * self.esz)
+
+    def wait(self):
+        self.d._sync_local()
+        self.d.dist.barrier(group=self.d.group)
+
+    def result(self):
+        return self.buf.tensor(self.d.device) if self.buf is not None else None
+
+    def close(self):
+        if self.mapping is not None:
+            self.mapping.close()
+            self.mapping = None

@@ -565,6 +565,15 @@ class GrowableArray:
         L.check(L.lib.gg_flatten(self._h, C.c_void_p(out.data_ptr()), self._stream()), "flatten")
         return out[:n]
 
+    def flatten_to(self, dev_ptr: int) -> int:
+        """K-flatten into raw device memory at ``dev_ptr`` (committed_size
+        elements) -- any address the GPU can store to, e.g. a peer GPU's
+        buffer mapped with CUDA IPC (multigpu.py).  Stream-ordered; returns
+        the element count."""
+        n = self.committed_size
+        L.check(L.lib.gg_flatten(self._h, C.c_void_p(int(dev_ptr)), self._stream()), "flatten")
+        return n
+
     def flatten(self) -> np.ndarray:
         """Host copy of the committed contents (the reference returns numpy)."""
         return self._to_numpy(self.flatten_device())
