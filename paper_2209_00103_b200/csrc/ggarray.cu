@@ -145,6 +145,10 @@ __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+__device__ __forceinline__ void stage_cbase(const Tables &t, char **scb) {
+  for (uint32_t i = threadIdx.x; i < t.MB; i += blockDim.x) scb[i] = t.cbase[i];
+}
+
 // Host-planned allocation of class-b buckets for every lane with `need`
 // (each (shard, bucket) is requested by exactly one lane, so the once-flags
 // are uncontended and the slot is the shard's own: no address atomics at
@@ -181,6 +185,29 @@ __device__ __forceinline__ void warp_alloc_range(const Tables &t, uint32_t s, ui
     any &= any - 1;
     warp_alloc_class(t, (want >> b) & 1ull, s, b);
   }
+}
+
+// Publish buckets `want` of shard s (host-planned, slots already backed) from
+// the one thread that owns s in this launch: slot pointer + once-flag per
+// bucket, the shard's pmask (pm = its value at kernel start) and capacity,
+// and one allocation-count update per warp.  Plain stores: the kernel
+// boundary orders them before any reader.  Call with the full warp.
+__device__ __forceinline__ void publish_buckets(const Tables &t, char *const *scb, uint32_t s,
+                                                unsigned long long pm, unsigned long long want,
+                                                uint32_t lg0) {
+  uint64_t add = 0;
+  for (unsigned long long m = want; m; m &= m - 1) {
+    const uint32_t b = __ffsll((long long)m) - 1;
+    t.ptr[(size_t)s * t.MB + b] = scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
+    t.flag[(size_t)s * t.MB + b] = kFlagPublished;
+    add += 1ull << (t.log2fb + b);
+  }
+  if (want) {
+    t.pmask[s] = pm | want;
+    atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)add);
+  }
+  const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(want));
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)tot);
 }
 
 // Reservation + bucket allocation, one thread per shard: one atomicAdd on the
@@ -227,13 +254,20 @@ __global__ void k_reserve(Tables t, int mode) {
 }
 
 // grow: thread per shard, allocate buckets [0, lim[s]); lim comes from the
-// ctl words, or (uniform_k != ~0u) is the same for every shard
-__global__ void k_grow(Tables t, uint32_t uniform_k) {
+// ctl words, or (uniform_k != ~0u) is the same for every shard.  Latency
+// shaped: every global load (class bases, pmask, ctl) is issued up front, then
+// one round of stores (publish_buckets).
+__global__ void __launch_bounds__(256) k_grow(Tables t, uint32_t uniform_k) {
+  __shared__ char *scb[kMaxBuckets];
   pdl_begin();
+  stage_cbase(t, scb);
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = s < t.S;
+  const unsigned long long pm = live ? t.pmask[s] : 0ull;
   const uint32_t lim = !live ? 0u : (uniform_k != ~0u ? uniform_k : (t.ctl[s] & kCtlLimitMask));
-  warp_alloc_range(t, live ? s : 0, 0, lim);
+  __syncthreads();
+  const unsigned long long want = (lim >= 64 ? ~0ull : ((1ull << lim) - 1ull)) & ~pm;
+  publish_buckets(t, scb, live ? s : 0u, pm, live ? want : 0ull, t.log2fb + (31u - __clz(t.esz)));
 }
 
 __global__ void k_new_bucket(Tables t, uint32_t s, uint32_t b, int *won) {
@@ -379,26 +413,39 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
   }
 }
 
-// shrink (extension): thread per shard; size[s] = new size, buckets
+// shrink (extension): one CTA; per shard size[s] = new size, buckets
 // b >= min_buckets_for(new size) unpublished (their slots stay reserved for
-// the shard; the host unmaps chunks that lost their last live bucket).
-__global__ void k_shrink(Tables t, const uint64_t *new_sizes) {
+// the shard; the host unmaps chunks that lost their last live bucket), then
+// the commit scan over the new sizes.  All loads issued up front.
+__global__ void __launch_bounds__(1024) k_shrink(Tables t, const uint64_t *new_sizes) {
+  __shared__ uint64_t ws[32];
   pdl_begin();
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= t.S) return;
-  const uint64_t ns = new_sizes[s];
-  const uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + (1ull << t.log2fb) - 1) >> t.log2fb))) : 0u;
-  unsigned long long m = t.pmask[s], freed = 0;
-  for (uint32_t b = keep; b < t.MB; ++b)
-    if ((m >> b) & 1ull) {
-      t.ptr[(size_t)s * t.MB + b] = nullptr;
-      t.flag[(size_t)s * t.MB + b] = 0;
-      freed += 1ull << (t.log2fb + b);
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const bool live = s < t.S;
+    uint64_t ns = 0, cap = 0;
+    unsigned long long m = 0;
+    if (live) { ns = new_sizes[s]; m = t.pmask[s]; cap = t.cap[s]; }
+    if (live) {
+      const uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + (1ull << t.log2fb) - 1) >> t.log2fb))) : 0u;
+      const unsigned long long drop = keep < 64 ? (m & ~((1ull << keep) - 1ull)) : 0ull;
+      uint64_t freed = 0;
+      for (unsigned long long d = drop; d; d &= d - 1) {
+        const uint32_t b = __ffsll((long long)d) - 1;
+        t.ptr[(size_t)s * t.MB + b] = nullptr;
+        t.flag[(size_t)s * t.MB + b] = 0;
+        freed += 1ull << (t.log2fb + b);
+      }
+      if (drop) { t.pmask[s] = m & ~drop; t.cap[s] = cap - freed; }
+      t.size[s] = ns;
     }
-  if (keep < 64) m &= (1ull << keep) - 1ull;
-  t.pmask[s] = m;
-  t.cap[s] -= freed;
-  t.size[s] = ns;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan(ns, &tot, ws);
+    if (live) t.prefix[s + 1] = carry + ex + ns;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) t.prefix[0] = 0;
 }
 
 // ---- streaming primitives: a CTA moves one contiguous piece -------------
@@ -601,9 +648,6 @@ __device__ __forceinline__ uint32_t upper_shard(const uint64_t *dir, uint32_t S,
 __device__ __forceinline__ char *slot_addr(char *const *scb, uint32_t s, uint32_t b, uint32_t lg0) {
   return scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
 }
-__device__ __forceinline__ void stage_cbase(const Tables &t, char **scb) {
-  for (uint32_t i = threadIdx.x; i < t.MB; i += blockDim.x) scb[i] = t.cbase[i];
-}
 
 // shard of work index g: largest s with dir[s] <= g (bisect_right - 1,
 // sharded_array.py:136) by a 32-ary warp search -- 2 dependent loads for
@@ -700,52 +744,42 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, c
 // costs more: the completion atomic lengthens every CTA's life.)
 struct Fuse { int rmode; int commit; };
 
-__device__ void commit_block(const Tables &t) {
+// metadata of a planned append, run by one CTA after every tile is copied.
+// Latency shaped: all loads (directory pair, size, pmask) issued up front,
+// counters updated with fire-and-forget reductions, the commit scan runs on
+// the new sizes held in registers (no reload).
+__device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &fz) {
   __shared__ uint64_t ws[32];
+  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+  const uint64_t *dir = fz.rmode == 0 ? t.offsets : t.prefix;
   uint64_t carry = 0;
   for (uint32_t base = 0; base < t.S; base += blockDim.x) {
     const uint32_t s = base + threadIdx.x;
-    const uint64_t v = s < t.S ? t.size[s] : 0;
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_scan(v, &tot, ws);
-    if (s < t.S) t.prefix[s + 1] = carry + ex + v;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) t.prefix[0] = 0;
-}
-
-// metadata of a planned append, run by one CTA after every tile is copied
-__device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &fz) {
-  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
-  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
-    const uint32_t s = base + threadIdx.x;
-    uint64_t c = 0;
-    if (s < t.S) c = fz.rmode == 0 ? t.offsets[s + 1] - t.offsets[s] : t.prefix[s + 1] - t.prefix[s];
+    const bool live = s < t.S;
+    uint64_t lo = 0, hi = 0, start = 0;
+    unsigned long long pm = 0;
+    if (live) { lo = dir[s]; hi = dir[s + 1]; start = t.size[s]; pm = t.pmask[s]; }
+    const uint64_t c = hi - lo, nsz = start + c;
     unsigned long long want = 0;
     if (c) {
-      const uint64_t start = t.size[s];
-      t.size[s] = start + c;
-      t.ops[s] += 1;
+      t.size[s] = nsz;
+      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
       t.start[s] = start;
       uint32_t b0, b1; uint64_t o;
       locate(start, t.log2fb, b0, o);
-      locate(start + c - 1, t.log2fb, b1, o);
-      want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~t.pmask[s];
-      uint64_t add = 0;
-      for (unsigned long long m = want; m; m &= m - 1) {
-        const uint32_t b = __ffsll((long long)m) - 1;
-        t.ptr[(size_t)s * t.MB + b] = slot_addr(scb, s, b, lg0);
-        t.flag[(size_t)s * t.MB + b] = kFlagPublished;
-        add += 1ull << (t.log2fb + b);
-      }
-      if (want) { t.pmask[s] |= want; t.cap[s] += add; }
+      locate(nsz - 1, t.log2fb, b1, o);
+      want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~pm;
     }
-    if (s < t.S) t.count[s] = c;
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(want));
-    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)tot);
+    if (live) t.count[s] = c;
+    publish_buckets(t, scb, live ? s : 0u, pm, want, lg0);
+    if (fz.commit) {
+      uint64_t tot;
+      const uint64_t ex = block_exclusive_scan(live ? nsz : 0, &tot, ws);
+      if (live) t.prefix[s + 1] = carry + ex + nsz;
+      carry += tot;
+    }
   }
-  __syncthreads();
-  if (fz.commit) commit_block(t);
+  if (fz.commit && threadIdx.x == 0) t.prefix[0] = 0;
 }
 
 // The tile walker: ONE tile per CTA (a non-persistent grid streams ~15%
@@ -1546,7 +1580,8 @@ cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *ds
   const uint64_t grid = (total + tile - 1) / tile;
   cudaError_t e = launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src,
                            dst, total, add, reps, tile, fz);
-  if (P && e == cudaSuccess) e = launch_k(k_planned_meta, 1, 1024, 0, st, t, fz);
+  if (P && e == cudaSuccess)
+    e = launch_k(k_planned_meta, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t, fz);
   return e;
 }
 
@@ -2033,12 +2068,10 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
   int rc = a->up.upload(st, 1, dst, src, bytes);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
-  CUDA_TRY(launch_k(k_shrink, (a->S + 255) / 256, 256, 0, st, t, (const uint64_t *)a->t.count));
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(launch_k(k_shrink, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t,
+                    (const uint64_t *)a->t.count));
   uint64_t acc = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
-  CUDA_TRY(launch_k(k_commit, 1, 1024, 0, st, a->t));
-  CUDA_TRY(cudaGetLastError());
   // unmap emptied chunks down to keep_mapped_bytes (waits for the device:
   // queued work may still read the released buckets).  Never under graph
   // capture, where the chunks stay cached until gg_trim.
