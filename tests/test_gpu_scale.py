@@ -182,3 +182,34 @@ def test_phased_footprint_follows_live_capacity(gg):
             worst = max(worst, ms["mapped_bytes"] / ms["needed_bytes"])
             assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"] + (8 << 20)
     assert worst <= 2.5
+
+
+@pytest.mark.parametrize("unroll", [1, 2, 4, 8])
+def test_walk_tile_sizes_ragged_parity(gg, unroll):
+    """Every tile size of the one-tile-per-CTA walker (U = 1..8 vectors per
+    thread) on ragged, misaligned shards: CSR insert, duplicate, rw (per shard
+    and global), flatten -- bit-exact against the oracle."""
+    import torch
+    from paper_2209_00103_b200 import _lib
+    rng = np.random.default_rng(100 + unroll)
+    S, fb = 97, 8
+    counts = rng.integers(0, 40000, S)
+    counts[rng.random(S) < 0.15] = 0
+    counts[5] = 1
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    vals = rng.integers(-2**31, 2**31 - 1, int(off[-1]), dtype=np.int64).astype(np.int32)
+    _lib.check(_lib.lib.gg_set_tuning(-1, unroll, 0, 0))
+    try:
+        a = gg.GrowableArray(S, fb, dtype=np.int32)
+        o = O.OracleGGArray(S, fb, dtype=np.int32)
+        pre = [np.arange(int(k), dtype=np.int32) for k in rng.integers(0, 33, S)]
+        a.insert_parallel(pre); o.insert_parallel(pre)
+        a.insert_csr(torch.from_numpy(vals).cuda(), off)
+        o.insert_parallel([vals[off[s]:off[s + 1]] for s in range(S)])
+        a.insert_duplicate(); o.insert_duplicate()
+        a.rw_add(3); o.rw_add(3)
+        a.rw_add(-1, mode="global"); o.rw_add(-1)
+        assert a.flatten().tobytes() == o.flatten().tobytes()
+        assert a._parity_state()["sizes"] == [int(x) for x in o.size]
+    finally:
+        _lib.lib.gg_set_tuning(-1, -1, 0, 0)
