@@ -197,6 +197,9 @@ int gg_host_state(gg_array *a, uint64_t *h_sizes, uint64_t *h_caps, uint64_t *h_
 /* Same quantities read back from DEVICE memory (synchronises `stream`). */
 int gg_device_state(gg_array *a, uint64_t *h_sizes, uint64_t *h_caps, uint64_t *h_flags,
                     uint64_t *h_prefix, uint64_t *h_ops, void *stream);
+/* committed directory prefix[S+1] (u64) copied to device memory d_out,
+ * stream-ordered (capture-safe; the global-index map of the array) */
+int gg_prefix_copy(gg_array *a, void *d_out, void *stream);
 /* bucket base device pointers [S*max_buckets] (0 = unallocated); syncs */
 int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream);
 /* footprint: [0]=capacity bytes (elements of allocated buckets x element

@@ -82,6 +82,7 @@ _SIGS = {
     "gg_device_state": ([P, PU64, PU64, PU64, PU64, PU64, P], C.c_int),
     "gg_bucket_ptrs": ([P, PU64, P], C.c_int),
     "gg_mem_stats": ([P, PU64, P], C.c_int),
+    "gg_prefix_copy": ([P, P, P], C.c_int),
     "gg_slab_stats": ([P, PU64], C.c_int),
     "gg_flat_insert": ([P, U64, P, P, U64, U32, I32, P], C.c_int),
     "gg_flat_add": ([P, U64, U32, P, U32, I32, P], C.c_int),

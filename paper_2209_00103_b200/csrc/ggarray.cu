@@ -2430,6 +2430,13 @@ int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint6
   return GG_OK;
 }
 
+int gg_prefix_copy(gg_array *a, void *d_out, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  CUDA_TRY(cudaMemcpyAsync(d_out, a->t.prefix, (a->S + 1) * 8, cudaMemcpyDeviceToDevice, S_(stream)));
+  return GG_OK;
+}
+
 int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);

@@ -105,6 +105,10 @@ class GrowableArray:
         self._summary = np.zeros(3, np.uint64)
         self._status = np.zeros(shards, np.int32)
         self._caps = np.zeros(shards, np.uint64)
+        self._status_p = L.ptr(self._status, C.c_int32)     # cached ctypes views (hot paths)
+        self._caps_p = L.ptr(self._caps)
+        self._failed = C.c_int64(-1)
+        self._failed_p = C.byref(self._failed)
         self._dev_index = self.device.index
         self._mu = threading.Lock()
         self.shards = [ShardVector._bind(self, s) for s in range(shards)]
@@ -235,10 +239,16 @@ class GrowableArray:
         return vals, offsets
 
     def _reserve(self, caps: np.ndarray) -> None:
-        caps = L.u64_array(caps)
-        failed = C.c_int64(-1)
-        self._hook_exc.clear()
-        rc = L.lib.gg_reserve(self._h, L.ptr(caps), C.byref(failed), self._stream())
+        if caps is self._caps:
+            cp = self._caps_p
+        else:
+            caps = L.u64_array(caps)
+            cp = L.ptr(caps)
+        failed = self._failed
+        failed.value = -1
+        if self._hook_exc:
+            self._hook_exc.clear()
+        rc = L.lib.gg_reserve(self._h, cp, self._failed_p, self._stream())
         self._dirty()
         if rc == L.GG_ENOMEM and failed.value in self._hook_exc:
             raise self._hook_exc.pop(failed.value)
@@ -505,9 +515,10 @@ class GrowableArray:
         """Every shard appends a copy of its committed contents, read directly from
         its buckets (the bench's _insert_duplicate, bench_cli.py:298-307)."""
         status = self._status
-        self._hook_exc.clear()
+        if self._hook_exc:
+            self._hook_exc.clear()
         flags = (L.GG_F_COMMIT if commit else 0) | _EXTRA_FLAGS
-        rc = L.lib.gg_insert_duplicate_ex(self._h, flags, L.ptr(status, C.c_int32), self._stream())
+        rc = L.lib.gg_insert_duplicate_ex(self._h, flags, self._status_p, self._stream())
         self._dirty()
         if rc not in (L.GG_OK, L.GG_EPARTIAL):
             L.check(rc, "insert_duplicate")
@@ -621,6 +632,17 @@ class GrowableArray:
         keys = ("mapped_bytes", "cached_bytes", "chunks_mapped", "chunks_unmapped", "map_ns",
                 "unmap_ns", "regions", "va_bytes")
         return {k: int(v) for k, v in zip(keys, o)}
+
+    def prefix_device(self, out=None):
+        """The committed directory prefix[S+1] as an int64 CUDA tensor (a device
+        copy, stream-ordered and capture-safe)."""
+        import torch
+        if out is None:
+            out = torch.empty(self._S + 1, dtype=torch.int64, device=self.device)
+        elif out.numel() < self._S + 1 or out.dtype != torch.int64 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous int64 device tensor of shards + 1 elements")
+        L.check(L.lib.gg_prefix_copy(self._h, C.c_void_p(out.data_ptr()), self._stream()), "prefix_device")
+        return out
 
     def device_state(self) -> dict:
         S = self._S
