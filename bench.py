@@ -712,11 +712,18 @@ def main():
         if out is not None:
             print(json.dumps(out), flush=True)
         return
+    if os.environ.get("GG_BENCH_SAME_GPU") == "1":
+        # test hook: run the N > 1 code path with every rank on GPU 0 (gloo
+        # control plane; NCCL refuses two ranks on one GPU)
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("GG_BENCH_SAME_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_device(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
