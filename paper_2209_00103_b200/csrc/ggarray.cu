@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(1024) k_planned_meta(Tables t, Fuse fz) {
 // and a clz locate -- and each thread keeps kDefUnroll such vectors in flight.
 // Groups that straddle a shard or are not 16 B-aligned inside their bucket
 // are updated element by element.
-template <typename T>
+template <typename T, int U = kDefUnroll>
 __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total, T addend) {
   pdl_begin();
   __shared__ char *scb[kMaxBuckets];
@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
   constexpr uint32_t LGE = sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : sizeof(T) == 4 ? 2 : 3;
   const uint32_t lg0 = t.log2fb + LGE;
   constexpr uint32_t VE = 16 / sizeof(T);
-  constexpr int U = kDefUnroll;
+  
   typedef LdSt<kDefLS == 1 ? 2 : kDefLS> M;
   const uint64_t nvec = (total + VE - 1) / VE;
   const uint32_t lane = threadIdx.x & 31;
@@ -1698,9 +1698,20 @@ int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode,
               cudaStream_t st) {
   if (mode == GG_RW_GLOBAL) {
     const uint64_t nvec = (total * sizeof(T) + 15) / 16;
-    const uint64_t grid = (nvec + kThreads * kDefUnroll - 1) / (kThreads * kDefUnroll);
-    for (uint32_t p = 0; p < passes; ++p)
-      CUDA_TRY(launch_k(k_rw_global<T>, (unsigned)grid, kThreads, 0, st, t, total, addend));
+    // sweep (tools/sweep.py): rw_g peaks at U = 4 (U = 8 spills the per-vector
+    // pointers / masks into a lower occupancy)
+    const uint32_t U = std::min<uint32_t>(walk_unroll(a, total, W_RW), 4u);
+    const uint64_t grid = (nvec + kThreads * U - 1) / (kThreads * U);
+    for (uint32_t p = 0; p < passes; ++p) {
+      cudaError_t e;
+      switch (U) {
+        case 2: e = launch_k(k_rw_global<T, 2>, (unsigned)grid, kThreads, 0, st, t, total, addend); break;
+        case 8: e = launch_k(k_rw_global<T, 8>, (unsigned)grid, kThreads, 0, st, t, total, addend); break;
+        case 1: e = launch_k(k_rw_global<T, 1>, (unsigned)grid, kThreads, 0, st, t, total, addend); break;
+        default: e = launch_k(k_rw_global<T, 4>, (unsigned)grid, kThreads, 0, st, t, total, addend); break;
+      }
+      CUDA_TRY(e);
+    }
     return GG_OK;
   }
   const Fuse none{0, 0};
