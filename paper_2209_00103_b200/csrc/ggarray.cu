@@ -1255,6 +1255,50 @@ struct Slab {
     span(s, b, r, c0, c1);
     for (size_t c = c0; c <= c1; ++c) drop(*r, c);
   }
+  // chunks [c0, c1] overlapped by slots [s0, s1) of class b, with the number
+  // of those slots touching each chunk (batched refcounting of uniform ops)
+  template <typename F>
+  void for_range(uint32_t b, uint32_t s0, uint32_t s1, F f) {
+    Region &r = region(b);
+    const uint64_t base = small_off[b] != ~uint64_t(0) ? small_off[b] : 0, bb = bytes[b];
+    const uint64_t lo = base + (uint64_t)s0 * bb, hi = base + (uint64_t)s1 * bb;   // [lo, hi)
+    for (size_t c = lo / r.chunk; c <= (hi - 1) / r.chunk; ++c) {
+      const uint64_t clo = std::max<uint64_t>(lo, c * r.chunk), chi = std::min<uint64_t>(hi, (c + 1) * r.chunk);
+      // slots with [base + s*bb, base + (s+1)*bb) intersecting [clo, chi)
+      const uint64_t first = (clo - base) / bb, last = (chi - 1 - base) / bb;
+      f(r, c, (uint32_t)(last - first + 1));
+    }
+  }
+  // back slots [s0, s1) of class b (region must exist); all-or-nothing
+  int back_range(uint32_t b, uint32_t s0, uint32_t s1) {
+    if (s1 <= s0) return GG_OK;
+    int rc = GG_OK;
+    std::vector<std::pair<Region *, size_t>> done;
+    for_range(b, s0, s1, [&](Region &r, size_t c, uint32_t n) {
+      if (rc) return;
+      if ((rc = map_chunk(r, c))) return;
+      r.chunks[c].refs += n;
+      done.push_back({&r, c});
+    });
+    if (rc) {                                   // roll back this call's refs
+      size_t i = 0;
+      for_range(b, s0, s1, [&](Region &r, size_t c, uint32_t n) {
+        if (i < done.size() && done[i].first == &r && done[i].second == c) {
+          r.chunks[c].refs -= n;
+          if (!r.chunks[c].refs) cached += r.chunk;
+          ++i;
+        }
+      });
+    }
+    return rc;
+  }
+  void unback_range(uint32_t b, uint32_t s0, uint32_t s1) {
+    if (s1 <= s0) return;
+    for_range(b, s0, s1, [&](Region &r, size_t c, uint32_t n) {
+      r.chunks[c].refs -= n;
+      if (!r.chunks[c].refs) cached += r.chunk;
+    });
+  }
   // bytes backing (s, b) would newly map
   uint64_t new_bytes(uint32_t s, uint32_t b) {
     if (small_off[b] == ~uint64_t(0) && !big[b].base) return chunk_for(b);
@@ -1925,6 +1969,61 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
 int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  cudaStream_t st = S_(stream);
+  {
+    // uniform fast path: every shard has the same committed length, size and
+    // buckets, no hook / cap / failed shard -> plan shard 0 once
+    const uint64_t c = a->prefix[1] - a->prefix[0];
+    bool uni = !a->hook && !a->limit && !(flags & GG_F_UNFUSED);
+    for (uint32_t s = 0; s < a->S && uni; ++s)
+      uni = a->prefix[s + 1] - a->prefix[s] == c && a->size[s] == a->size[0] &&
+            a->flags[s] == a->flags[0] && !a->dirty[s];
+    if (uni && c) {
+      const uint32_t kc = min_buckets_for(a, c);
+      const uint64_t need = kc >= 64 ? ~uint64_t(0) : ((uint64_t(1) << kc) - 1);
+      if ((a->flags[0] & need) != need)
+        return fail(GG_EUNPUBLISHED, "bucket unpublished while walking shard 0");
+      const uint64_t start = a->size[0];
+      uint32_t b0, b1; uint64_t o;
+      host_locate(a, start, b0, o);
+      host_locate(a, start + c - 1, b1, o);
+      if (b1 < a->MB) {
+        uint64_t want = 0;
+        for (uint32_t b = b0; b <= b1; ++b) if (!(a->flags[0] >> b & 1)) want |= uint64_t(1) << b;
+        int rc = GG_OK;
+        uint64_t got = 0;
+        for (uint32_t b = b0; b <= b1 && !rc; ++b) {
+          if (!(want >> b & 1)) continue;
+          bool created = false;
+          if (!(rc = a->slab.ensure_region(b, &created)) && !(rc = a->slab.back_range(b, 0, a->S))) {
+            if (created) a->cbase_dirty = true;
+            got |= uint64_t(1) << b;
+          }
+        }
+        if (!rc) {
+          uint64_t elems = 0, bytes = 0;
+          for (uint32_t b = b0; b <= b1; ++b)
+            if (want >> b & 1) { elems += bucket_elems(a, b); bytes += bucket_bytes(a, b); }
+          for (uint32_t s = 0; s < a->S; ++s) {
+            a->size[s] += c; a->ops[s] += 1; a->flags[s] |= want; a->cap[s] += elems;
+          }
+          a->live += bytes * a->S;
+          a->alloc_calls += (uint64_t)__builtin_popcountll(want) * a->S;
+          if ((rc = push_cbase(a, st))) return rc;
+          const bool commit = (flags & GG_F_COMMIT) != 0;
+          Tables t = tables_for_launch(a, false);
+          if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S],
+                                           Fuse{1, commit ? 1 : 0}, st)))
+            return rc;
+          if (commit) host_commit(a);
+          if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
+          return GG_OK;
+        }
+        for (uint32_t b = b0; b <= b1; ++b)     // out of memory: undo, take the exact path
+          if (got >> b & 1) a->slab.unback_range(b, 0, a->S);
+      }
+    }
+  }
   int rc = check_committed_published(a);
   if (rc) return rc;
   std::vector<uint64_t> counts(a->S);
@@ -1934,7 +2033,7 @@ int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void 
   plan_append(a, p, counts.data(), nullptr);
   bool committed;
   const uint64_t total = a->prefix[a->S];
-  if ((rc = run_append(a, p, 1, W_DUP, nullptr, total, S_(stream), flags, &committed))) return rc;
+  if ((rc = run_append(a, p, 1, W_DUP, nullptr, total, st, flags, &committed))) return rc;
   for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
   return finish_status(a, p, h_status);
 }
@@ -1964,6 +2063,42 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_failed_shard) *h_failed_shard = -1;
+  {
+    // uniform fast path (every shard the same target and bucket set, no hook,
+    // no cap, no failed shard): class-batched backing, no per-shard planning
+    bool uni = !a->hook && !a->limit;
+    for (uint32_t s = 0; s < a->S && uni; ++s)
+      uni = h_min_capacity[s] == h_min_capacity[0] && a->flags[s] == a->flags[0] && !a->dirty[s];
+    const uint32_t k = uni ? min_buckets_for(a, h_min_capacity[0]) : 0;
+    if (uni && k <= a->MB) {
+      const uint64_t want = (k >= 64 ? ~uint64_t(0) : ((uint64_t(1) << k) - 1)) & ~a->flags[0];
+      if (!want) return GG_OK;
+      int rc = GG_OK;
+      uint64_t got = 0;
+      for (uint32_t b = 0; b < k && !rc; ++b) {
+        if (!(want >> b & 1)) continue;
+        bool created = false;
+        if (!(rc = a->slab.ensure_region(b, &created)) && !(rc = a->slab.back_range(b, 0, a->S))) {
+          if (created) a->cbase_dirty = true;
+          got |= uint64_t(1) << b;
+        }
+      }
+      if (!rc) {
+        uint64_t elems = 0, bytes = 0;
+        for (uint32_t b = 0; b < k; ++b)
+          if (want >> b & 1) { elems += bucket_elems(a, b); bytes += bucket_bytes(a, b); }
+        for (uint32_t s = 0; s < a->S; ++s) { a->flags[s] |= want; a->cap[s] += elems; }
+        a->live += bytes * a->S;
+        a->alloc_calls += (uint64_t)__builtin_popcountll(want) * a->S;
+        if ((rc = push_cbase(a, st))) return rc;
+        Tables t = tables_for_launch(a, true);
+        CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, st, t, k));
+        return GG_OK;
+      }
+      for (uint32_t b = 0; b < k; ++b)            // out of memory: undo, take the exact path
+        if (got >> b & 1) a->slab.unback_range(b, 0, a->S);
+    }
+  }
   Plan p;
   plan_init(a, p);
   std::vector<uint32_t> lim(a->S, 0);
@@ -2067,16 +2202,37 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
   cudaStream_t st = S_(stream);
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_new_sizes[s] > a->size[s]) return fail(GG_EVALUE, "shrink cannot grow a shard");
-  for (uint32_t s = 0; s < a->S; ++s) {
-    uint32_t keep = min_buckets_for(a, h_new_sizes[s]);
-    for (uint32_t b = keep; b < a->MB; ++b)
-      if (a->flags[s] >> b & 1) {
-        a->flags[s] &= ~(uint64_t(1) << b);
-        a->cap[s] -= bucket_elems(a, b);
-        a->live -= bucket_bytes(a, b);
-        a->slab.unback(s, b);
+  bool uni = true;                             // same size and buckets everywhere: class-batched
+  for (uint32_t s = 0; s < a->S && uni; ++s)
+    uni = h_new_sizes[s] == h_new_sizes[0] && a->flags[s] == a->flags[0];
+  if (uni) {
+    const uint32_t keep = min_buckets_for(a, h_new_sizes[0]);
+    const uint64_t drop = keep >= 64 ? 0 : (a->flags[0] & ~((uint64_t(1) << keep) - 1));
+    uint64_t elems = 0, bytes = 0;
+    for (uint32_t b = 0; b < a->MB; ++b)
+      if (drop >> b & 1) {
+        elems += bucket_elems(a, b);
+        bytes += bucket_bytes(a, b);
+        a->slab.unback_range(b, 0, a->S);
       }
-    a->size[s] = h_new_sizes[s];
+    for (uint32_t s = 0; s < a->S; ++s) {
+      a->flags[s] &= ~drop;
+      a->cap[s] -= elems;
+      a->size[s] = h_new_sizes[s];
+    }
+    a->live -= bytes * a->S;
+  } else {
+    for (uint32_t s = 0; s < a->S; ++s) {
+      uint32_t keep = min_buckets_for(a, h_new_sizes[s]);
+      for (uint32_t b = keep; b < a->MB; ++b)
+        if (a->flags[s] >> b & 1) {
+          a->flags[s] &= ~(uint64_t(1) << b);
+          a->cap[s] -= bucket_elems(a, b);
+          a->live -= bucket_bytes(a, b);
+          a->slab.unback(s, b);
+        }
+      a->size[s] = h_new_sizes[s];
+    }
   }
   void *dst[1] = {a->t.count};
   const void *src[1] = {h_new_sizes};
