@@ -187,6 +187,12 @@ int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t thre
  * kernel may start while its stream predecessor drains.  Process-wide; for
  * A/B measurements. */
 int gg_set_pdl(int32_t on);
+/* Deferred metadata (default on): the metadata pass of an append issued
+ * eagerly is launched with the next device-touching call, fused into the
+ * next grow when that comes first (one launch instead of two).  Host-only
+ * queries (summary, host state, memory stats) see the up-to-date host
+ * mirrors either way.  Process-wide; for A/B measurements. */
+int gg_set_defer(int32_t on);
 /* committed size, total (reserved) size, total capacity -- host mirrors */
 int gg_summary(gg_array *a, uint64_t *h_out3);
 

@@ -76,6 +76,7 @@ _SIGS = {
     "gg_capture_mode": ([P, I32], C.c_int),
     "gg_set_tuning": ([I32, I32, U32, U32], C.c_int),
     "gg_set_pdl": ([C.c_int32], C.c_int),
+    "gg_set_defer": ([C.c_int32], C.c_int),
     "gg_capture_release": ([P], C.c_int),
     "gg_summary": ([P, PU64], C.c_int),
     "gg_host_state": ([P, PU64, PU64, PU64, PU64, PU64], C.c_int),
@@ -148,3 +149,5 @@ def stream_handle(device_index: int) -> int:
 
 if os.environ.get("GG_PDL") == "0":        # A/B switch for programmatic dependent launch
     lib.gg_set_pdl(0)
+if os.environ.get("GG_DEFER") == "0":      # A/B switch for the deferred metadata pass
+    lib.gg_set_defer(0)

@@ -868,6 +868,26 @@ __global__ void __launch_bounds__(1024) k_planned_meta(Tables t, Fuse fz) {
   planned_metadata(t, scb, fz);
 }
 
+// A deferred planned-append metadata pass fused with the grow that follows it
+// (the doubling schedule's grow(2n) after every duplicate): one launch, the
+// metadata first, then buckets [0, uk) of every shard published.
+__global__ void __launch_bounds__(1024) k_meta_grow(Tables t, Fuse fz, uint32_t uk) {
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  stage_cbase(t, scb);
+  __syncthreads();
+  planned_metadata(t, scb, fz);
+  __syncthreads();
+  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+  const unsigned long long all = uk >= 64 ? ~0ull : ((1ull << uk) - 1ull);
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const bool live = s < t.S;
+    const unsigned long long pm = live ? t.pmask[s] : 0ull;
+    publish_buckets(t, scb, live ? s : 0u, pm, live ? (all & ~pm) : 0ull, lg0);
+  }
+}
+
 // rw_g (bench_cli.py:339-366, the paper's rw_g): every 16 B group of
 // consecutive GLOBAL indices is resolved through the directory on its own --
 // a warp-uniform bisect on the smem prefix for the chunk, a per-lane fix-up
@@ -1469,6 +1489,11 @@ struct gg_array {
   uint64_t live = 0;                                     // bytes of live buckets
   std::vector<uint32_t> headroom;                        // (s, b) backed for a device view
   bool cbase_dirty = false;                              // a class region appeared
+  // metadata pass of the last planned append, not launched yet (eager issue
+  // only): fused into the next grow, launched by any other device-touching call
+  bool pend = false;
+  Fuse pend_fz{0, 0};
+  cudaStream_t pend_st = nullptr;
   uint64_t alloc_calls = 0;
   uint64_t limit = 0;                                    // live-bytes cap (0 = none)
   gg_alloc_hook hook = nullptr;
@@ -1627,11 +1652,8 @@ cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *ds
                    T add, uint32_t reps, Fuse fz, cudaStream_t st) {
   const uint32_t tile = (uint32_t)U * kThreads * (16 / ESZ);
   const uint64_t grid = (total + tile - 1) / tile;
-  cudaError_t e = launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src,
-                           dst, total, add, reps, tile, fz);
-  if (P && e == cudaSuccess)
-    e = launch_k(k_planned_meta, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t, fz);
-  return e;
+  return launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src, dst,
+                  total, add, reps, tile, fz);
 }
 
 template <int ESZ, int W, typename T, bool P = false>
@@ -1667,6 +1689,35 @@ int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64
   return walk_copy<W, false>(a, t, src, dst, total, Fuse{0, 0}, st);
 }
 
+bool g_defer = true;            // defer + fuse planned metadata (GG_DEFER=0 disables)
+
+uint32_t meta_threads(const gg_array *a) { return std::min<uint32_t>(1024, (a->S + 31) / 32 * 32); }
+
+// launch a deferred metadata pass, if any (on the stream of its walk)
+int flush_pending(gg_array *a) {
+  if (!a->pend) return GG_OK;
+  a->pend = false;
+  Tables t = tables_for_launch(a, false);
+  CUDA_TRY(launch_k(k_planned_meta, 1, meta_threads(a), 0, a->pend_st, t, a->pend_fz));
+  return GG_OK;
+}
+
+// after a planned walk: its metadata pass now, or deferred (eager issue) so
+// that a following grow can run both in one launch
+int finish_planned(gg_array *a, Fuse fz, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (g_defer && !a->up.capturing && cudaStreamIsCapturing(st, &cap) == cudaSuccess &&
+      cap == cudaStreamCaptureStatusNone) {
+    a->pend = true;
+    a->pend_fz = fz;
+    a->pend_st = st;
+    return GG_OK;
+  }
+  Tables t = tables_for_launch(a, false);
+  CUDA_TRY(launch_k(k_planned_meta, 1, meta_threads(a), 0, st, t, fz));
+  return GG_OK;
+}
+
 void host_commit(gg_array *a) {
   uint64_t acc = 0;
   a->prefix[0] = 0;
@@ -1699,6 +1750,7 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
       rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
                             : walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fz, st);
       if (rc) return rc;
+      if ((rc = finish_planned(a, fz, st))) return rc;
     } else if (commit) {
       CUDA_TRY(launch_k(k_commit, 1, 1024, 0, st, a->t));
     }
@@ -1931,6 +1983,7 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   if (h_offsets[0] != 0) return fail(GG_EVALUE, "offsets[0] must be 0");
   std::vector<uint64_t> counts(a->S);
@@ -1969,6 +2022,7 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
 int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   {
     // uniform fast path: every shard has the same committed length, size and
@@ -2015,6 +2069,7 @@ int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void 
           if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S],
                                            Fuse{1, commit ? 1 : 0}, st)))
             return rc;
+          if ((rc = finish_planned(a, Fuse{1, commit ? 1 : 0}, st))) return rc;
           if (commit) host_commit(a);
           if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
           return GG_OK;
@@ -2050,6 +2105,7 @@ int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
 int gg_commit(gg_array *a, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   uint64_t acc = 0;
   a->prefix[0] = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
@@ -2063,6 +2119,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_failed_shard) *h_failed_shard = -1;
+  if (a->pend && a->pend_st != st) { int frc_ = flush_pending(a); if (frc_) return frc_; }
   {
     // uniform fast path (every shard the same target and bucket set, no hook,
     // no cap, no failed shard): class-batched backing, no per-shard planning
@@ -2072,7 +2129,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
     const uint32_t k = uni ? min_buckets_for(a, h_min_capacity[0]) : 0;
     if (uni && k <= a->MB) {
       const uint64_t want = (k >= 64 ? ~uint64_t(0) : ((uint64_t(1) << k) - 1)) & ~a->flags[0];
-      if (!want) return GG_OK;
+      if (!want) return GG_OK;             // (a deferred metadata pass stays deferred)
       int rc = GG_OK;
       uint64_t got = 0;
       for (uint32_t b = 0; b < k && !rc; ++b) {
@@ -2092,13 +2149,19 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
         a->alloc_calls += (uint64_t)__builtin_popcountll(want) * a->S;
         if ((rc = push_cbase(a, st))) return rc;
         Tables t = tables_for_launch(a, true);
-        CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, st, t, k));
+        if (a->pend) {                         // metadata of the last append + this grow: one launch
+          a->pend = false;
+          CUDA_TRY(launch_k(k_meta_grow, 1, meta_threads(a), 0, st, t, a->pend_fz, k));
+        } else {
+          CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, st, t, k));
+        }
         return GG_OK;
       }
       for (uint32_t b = 0; b < k; ++b)            // out of memory: undo, take the exact path
         if (got >> b & 1) a->slab.unback_range(b, 0, a->S);
     }
   }
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   Plan p;
   plan_init(a, p);
   std::vector<uint32_t> lim(a->S, 0);
@@ -2156,6 +2219,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
 int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   *h_won = 0;
   if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
@@ -2186,6 +2250,7 @@ int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *str
 int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
   *h_prev = a->size[s];
   a->size[s] += c;
@@ -2199,6 +2264,7 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
                  void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_new_sizes[s] > a->size[s]) return fail(GG_EVALUE, "shrink cannot grow a shard");
@@ -2263,6 +2329,7 @@ int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
 int gg_trim(gg_array *a) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (!a->slab.cached) return GG_OK;
   CUDA_TRY(cudaDeviceSynchronize());
   a->slab.trim();
@@ -2274,6 +2341,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
                     int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   if (h_lane_offsets[0] != 0) return fail(GG_EVALUE, "lane offsets must start at 0");
   for (uint32_t s = 0; s < a->S; ++s)
@@ -2319,6 +2387,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
 int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   int rc = check_committed_published(a);
   if (rc) return rc;
   const uint64_t total = a->prefix[a->S];
@@ -2334,6 +2403,7 @@ int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, 
 int gg_flatten(gg_array *a, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   int rc = check_committed_published(a);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
@@ -2343,6 +2413,7 @@ int gg_flatten(gg_array *a, void *d_out, void *stream) {
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
   Tables t = tables_for_launch(a, false);
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
@@ -2359,6 +2430,7 @@ int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
   Tables t = tables_for_launch(a, false);
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
@@ -2393,6 +2465,7 @@ int elem_addr(gg_array *a, uint32_t s, uint64_t i, char **out, cudaStream_t st) 
 int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
@@ -2406,6 +2479,7 @@ int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
 int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
@@ -2421,6 +2495,7 @@ uint64_t gg_device_view_bytes(void) { return sizeof(gg_device_view); }
 int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, uint64_t view_bytes) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (view_bytes != sizeof(gg_device_view)) return fail(GG_EVALUE, "view size mismatch (ggarray_device.cuh)");
   if (!a->headroom.empty()) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
   // back every slot the launch may take: buckets [0, min_buckets_for(max)) per
@@ -2456,6 +2531,7 @@ int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, u
 int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   CUDA_TRY(cudaStreamSynchronize(st));
   const size_t S = a->S;
@@ -2533,9 +2609,15 @@ int gg_set_pdl(int32_t on) {
   return GG_OK;
 }
 
+int gg_set_defer(int32_t on) {
+  g_defer = on != 0;
+  return GG_OK;
+}
+
 int gg_capture_mode(gg_array *a, int32_t on) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (on && !a->up.capturing) return a->up.begin_capture();
   if (!on) a->up.capturing = false;
   return GG_OK;
@@ -2577,6 +2659,7 @@ int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint6
                     uint64_t *ops, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   CUDA_TRY(cudaStreamSynchronize(st));
   const size_t S = a->S;
@@ -2600,6 +2683,7 @@ int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint6
 int gg_prefix_copy(gg_array *a, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   CUDA_TRY(cudaMemcpyAsync(d_out, a->t.prefix, (a->S + 1) * 8, cudaMemcpyDeviceToDevice, S_(stream)));
   return GG_OK;
 }
@@ -2607,6 +2691,7 @@ int gg_prefix_copy(gg_array *a, void *d_out, void *stream) {
 int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
   CUDA_TRY(cudaStreamSynchronize(S_(stream)));
   CUDA_TRY(cudaMemcpy(h_ptrs, a->t.ptr, (size_t)a->S * a->MB * 8, cudaMemcpyDeviceToHost));
   return GG_OK;
