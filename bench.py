@@ -305,9 +305,23 @@ def gather_leg(args, torch, device, step, dist, world):
         g.close()
         del g
         torch.cuda.empty_cache()
+        # even rebalance: every rank ends with N/G of the global flat array
+        d.rebalance_flat_peer()
+        dist.barrier()
+        e0.record()
+        part, (lo, hi) = d.rebalance_flat_peer()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rb_ms = float(t.item())
+        del part
+        torch.cuda.empty_cache()
         return {"ms": round(ms, 4), "bytes_total": total, "bytes_over_nvlink": nvlink,
                 "nvlink_gbs_into_root": round(nvlink / (ms * 1e-3) / 1e9, 1),
-                "root_slice_ok": ok, "method": "fused K-flatten into the root buffer (CUDA IPC)"}
+                "root_slice_ok": ok, "method": "fused K-flatten into the root buffer (CUDA IPC)",
+                "rebalance_ms_incl_setup": round(rb_ms, 3),
+                "rebalance": "even slices N/G per rank, K-flatten ranges into the owners' buffers"}
     except Exception as exc:                          # report, never lose the bench line
         return {"error": repr(exc)[:300]}
 

@@ -163,6 +163,9 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
 int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, void *stream);
 /* flatten (sharded_array.py:244-257): d_out[prefix[s]+i] = shard_s[i]. */
 int gg_flatten(gg_array *a, void *d_out, void *stream);
+/* the committed elements with global index in [lo, hi) to d_out[0 .. hi-lo)
+ * (a slice of flatten(): pieces of a rebalance, bounded staging) */
+int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *stream);
 /* get_global / set_global for index arrays (sharded_array.py:139-158) */
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream);
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream);

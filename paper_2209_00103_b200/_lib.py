@@ -68,6 +68,7 @@ _SIGS = {
     "gg_device_view_sync": ([P, PI32, P], C.c_int),
     "gg_push_if": ([P, P, P, U64, I32, U32, PI32, P], C.c_int),
     "gg_flatten": ([P, P, P], C.c_int),
+    "gg_flatten_range": ([P, U64, U64, P, P], C.c_int),
     "gg_gather": ([P, P, U64, P, P], C.c_int),
     "gg_scatter": ([P, P, U64, P, P], C.c_int),
     "gg_get": ([P, U32, U64, P, P], C.c_int),

@@ -742,7 +742,7 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, c
 // destinations are slot arithmetic from the unchanged size[s]; k_planned_meta
 // applies the metadata right after.  (A last-CTA epilogue in the walk itself
 // costs more: the completion atomic lengthens every CTA's life.)
-struct Fuse { int rmode; int commit; };
+struct Fuse { int rmode; int commit; uint64_t g0 = 0; };   // g0: first work index (ranges)
 
 // metadata of a planned append, run by one CTA after every tile is copied.
 // Latency shaped: all loads (directory pair, size, pmask) issued up front,
@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   pdl_begin();
   const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
-  uint64_t g = (uint64_t)blockIdx.x * tile;
+  uint64_t g = fz.g0 + (uint64_t)blockIdx.x * tile;
   const uint64_t gend = min(total, g + tile);
   if (tid < 32) {
     const uint32_t s0 = warp_find_shard(dir, t.S, g);
@@ -1651,7 +1651,7 @@ template <int ESZ, int W, typename T, bool P, int U>
 cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
                    T add, uint32_t reps, Fuse fz, cudaStream_t st) {
   const uint32_t tile = (uint32_t)U * kThreads * (16 / ESZ);
-  const uint64_t grid = (total + tile - 1) / tile;
+  const uint64_t grid = (total - fz.g0 + tile - 1) / tile;
   return launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src, dst,
                   total, add, reps, tile, fz);
 }
@@ -2408,6 +2408,23 @@ int gg_flatten(gg_array *a, void *d_out, void *stream) {
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
   return launch_walk<W_FLATTEN>(a, t, nullptr, (char *)d_out, a->prefix[a->S], S_(stream));
+}
+
+int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  if (lo > hi || hi > a->prefix[a->S]) return fail(GG_EINDEX, "flatten range outside the committed size");
+  if (lo == hi) return GG_OK;
+  int rc = check_committed_published(a);
+  if (rc) return rc;
+  Tables t = tables_for_launch(a, false);
+  Fuse fz{0, 0};
+  fz.g0 = lo;
+  // the walk stores element g at flat_dst + g * esz: shift the base so that
+  // element lo lands at d_out (never dereferenced below lo)
+  char *base = (char *)d_out - lo * a->esz;
+  return walk_copy<W_FLATTEN, false>(a, t, nullptr, base, hi, fz, S_(stream));
 }
 
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {

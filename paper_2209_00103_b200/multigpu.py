@@ -192,6 +192,34 @@ class DistributedGrowableArray:
                 m.close()
         return buf.tensor(self.device)
 
+    def rebalance_flat_peer(self):
+        """Even flat slices across ranks: rank r ends with global indices
+        [r*q, min((r+1)*q, N)), q = ceil(N / G).  Each rank flattens the pieces
+        of its committed range straight into the owning ranks' buffers
+        (gg_flatten_range into CUDA-IPC mapped peer memory): the rebalance is
+        the flatten, with no staging copy and no collective on the data path."""
+        p = self.global_prefix()
+        n, G, me = p[-1], self.world, self.rank
+        q = -(-n // G) if n else 0
+        lo = [min(r * q, n) for r in range(G)]
+        hi = [min((r + 1) * q, n) for r in range(G)]
+        esz = np.dtype(self.local.dtype).itemsize
+        buf = PeerBuffer(hi[me] - lo[me], self.local.dtype)
+        handles = [None] * G
+        self.dist.all_gather_object(handles, buf.handle(), group=self.group)
+        maps = [None if r == me else PeerMapping(handles[r]) for r in range(G)]
+        for r in range(G):
+            a, b = max(lo[r], p[me]), min(hi[r], p[me + 1])
+            if a < b:
+                dst = buf.ptr if r == me else maps[r].ptr
+                self.local.flatten_range_to(a - p[me], b - p[me], dst + (a - lo[r]) * esz)
+        self._sync_local()
+        self.dist.barrier(group=self.group)
+        for m in maps:
+            if m is not None:
+                m.close()
+        return buf.tensor(self.device), (lo[me], hi[me])
+
     def _flatten_global_p2p(self, root: int):
         import torch
         p = self.global_prefix()

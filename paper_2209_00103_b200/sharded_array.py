@@ -585,6 +585,20 @@ class GrowableArray:
         L.check(L.lib.gg_flatten(self._h, C.c_void_p(int(dev_ptr)), self._stream()), "flatten")
         return n
 
+    def flatten_range_to(self, lo: int, hi: int, dev_ptr: int) -> int:
+        """Committed elements with global index in [lo, hi) to raw device memory
+        at ``dev_ptr`` (a slice of flatten(); e.g. into a peer GPU's buffer)."""
+        L.check(L.lib.gg_flatten_range(self._h, int(lo), int(hi), C.c_void_p(int(dev_ptr)),
+                                       self._stream()), "flatten_range")
+        return int(hi) - int(lo)
+
+    def flatten_range(self, lo: int, hi: int):
+        """Device tensor of the committed elements with global index in [lo, hi)."""
+        import torch
+        out = torch.empty(max(0, int(hi) - int(lo)), dtype=self._torch_dtype, device=self.device)
+        self.flatten_range_to(lo, hi, out.data_ptr())
+        return out
+
     def flatten(self) -> np.ndarray:
         """Host copy of the committed contents (the reference returns numpy)."""
         return self._to_numpy(self.flatten_device())

@@ -53,7 +53,10 @@ def _worker(rank, world, port, q):
         d = DistributedGrowableArray(a, device=torch.device("cuda", 0))
         flat = d.flatten_global(root=0, method="peer")
         allg = d.all_gather_flat_peer()
-        q.put((rank, None if flat is None else flat.cpu().numpy(), allg.cpu().numpy(), a.flatten()))
+        reb, rng_ = d.rebalance_flat_peer()
+        part = a.flatten_range(3, max(3, a.committed_size - 5)).cpu().numpy()
+        q.put((rank, None if flat is None else flat.cpu().numpy(), allg.cpu().numpy(), a.flatten(),
+               reb.cpu().numpy(), rng_, part))
         dist.barrier()
     finally:
         dist.destroy_process_group()
@@ -68,8 +71,8 @@ def test_peer_gather_flatten_two_processes():
         p.start()
     res = {}
     for _ in range(world):
-        r, flat, allg, local = q.get(timeout=300)
-        res[r] = (flat, allg, local)
+        r, flat, allg, local, reb, rng_, part = q.get(timeout=300)
+        res[r] = (flat, allg, local, reb, rng_, part)
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -78,3 +81,8 @@ def test_peer_gather_flatten_two_processes():
     assert res[1][0] is None
     for r in range(world):
         assert res[r][1].tobytes() == want.tobytes()
+        lo, hi = res[r][4]
+        assert res[r][3].tobytes() == want[lo:hi].tobytes()          # even rebalance slice
+        local = res[r][2]
+        assert res[r][5].tobytes() == local[3:max(3, len(local) - 5)].tobytes()   # flatten_range
+    assert sum(res[r][4][1] - res[r][4][0] for r in range(world)) == len(want)

@@ -213,3 +213,27 @@ def test_walk_tile_sizes_ragged_parity(gg, unroll):
         assert a._parity_state()["sizes"] == [int(x) for x in o.size]
     finally:
         _lib.lib.gg_set_tuning(-1, -1, 0, 0)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "int8", "float64"])
+def test_flatten_range_slices(gg, dtype):
+    """flatten_range(lo, hi) == flatten()[lo:hi] for random (misaligned) ranges,
+    including empty, single-element and full ranges; IndexError past the end."""
+    import torch
+    rng = np.random.default_rng(7)
+    S, fb = 29, 4
+    counts = rng.integers(0, 3000, S)
+    counts[::7] = 0
+    vals = (rng.integers(0, 120, int(counts.sum()))).astype(dtype)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    a = gg.GrowableArray(S, fb, dtype=dtype)
+    a.insert_parallel([vals[off[s]:off[s + 1]] for s in range(S)])
+    a.insert_duplicate()
+    full = a.flatten()
+    n = len(full)
+    cases = [(0, n), (0, 0), (n, n), (5, 6), (n - 1, n)] + [tuple(sorted(rng.integers(0, n + 1, 2))) for _ in range(20)]
+    for lo, hi in cases:
+        got = a.flatten_range(int(lo), int(hi)).cpu().numpy()
+        assert got.tobytes() == full[lo:hi].tobytes(), (lo, hi)
+    with pytest.raises(IndexError):
+        a.flatten_range(0, n + 1)
