@@ -1390,7 +1390,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 int g_sms[64] = {0};
 
 // runtime tuning of the 4-byte streaming kernels (sweep); -1 / 0 = default
-struct Tuning { int ls = -1, unroll = -1; uint32_t tile_bytes = 0, threads = 0; };
+struct Tuning { int unroll = -1; };   // streaming-kernel U forced by gg_set_tuning (-1 = built in)
 Tuning g_tune;
 
 int sm_count(int dev) {
