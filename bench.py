@@ -182,10 +182,7 @@ def run_device(args, rank, world, local_rank):
         step.collect(ev)
     # the same step captured once in a CUDA graph (host planning done at capture;
     # every kernel of the step runs on each replay)
-    graph = torch.cuda.CUDAGraph()
-    with step.arr.capture_mode():
-        with torch.cuda.graph(graph):
-            step.run(False)
+    graph = step.arr.capture(lambda: step.run(False))
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
@@ -655,10 +652,7 @@ def e2e_leg(args, gg, torch, device, world, dist):
             arr.prefix_device(out=pre_d)
             res_h.copy_(pre_d, non_blocking=True)
 
-        g = torch.cuda.CUDAGraph()
-        with arr.capture_mode():
-            with torch.cuda.graph(g):
-                one_graph()
+        g = arr.capture(one_graph)
         for _ in range(3):
             g.replay()
         torch.cuda.synchronize()
@@ -679,8 +673,8 @@ def e2e_leg(args, gg, torch, device, world, dist):
             sec = float(t.item())
         out["graph"] = {"value": round(world * (1 << 30) * k / sec / 1e9, 3),
                         "h2d_bytes_per_step": N0 * 4, "d2h_bytes_per_step": (S + 1) * 8,
-                        "api": "capture_mode + torch.cuda.graph of the same step (host batch "
-                               "H2D + directory D2H + sync in every replay)"}
+                        "api": "GrowableArray.capture of the same step (host batch H2D + "
+                               "directory D2H + sync in every replay)"}
     except Exception as exc:
         out["graph"] = {"error": repr(exc)[:300]}
     return out

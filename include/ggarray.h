@@ -180,6 +180,11 @@ int gg_set(gg_array *a, uint32_t shard, uint64_t i, const void *h_val, void *str
  * state (e.g. reset + inserts) may be replayed; the host mirrors keep the
  * state after the captured sequence. */
 int gg_capture_mode(gg_array *a, int32_t on);
+/* on = 2: as 1, and the deferred metadata pass (gg_set_defer) stays enabled
+ * under capture -- the caller must gg_flush() before the capture ends (the
+ * Python GrowableArray.capture helper does). */
+/* launch a deferred metadata pass now, if one is pending (stream-ordered) */
+int gg_flush(gg_array *a);
 int gg_capture_release(gg_array *a);
 /* Tuning of the streaming kernels (sweeps): unroll U in {1,2,4,8} = 16 B
  * vectors per thread per tile (tile = 256 threads x U vectors); -1 = the

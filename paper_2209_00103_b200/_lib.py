@@ -75,6 +75,7 @@ _SIGS = {
     "gg_set": ([P, U32, U64, P, P], C.c_int),
     "gg_info": ([P, PU32], C.c_int),
     "gg_capture_mode": ([P, I32], C.c_int),
+    "gg_flush": ([P], C.c_int),
     "gg_set_tuning": ([I32, I32, U32, U32], C.c_int),
     "gg_set_pdl": ([C.c_int32], C.c_int),
     "gg_set_defer": ([C.c_int32], C.c_int),

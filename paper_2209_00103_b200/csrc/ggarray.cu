@@ -1494,6 +1494,7 @@ struct gg_array {
   bool pend = false;
   Fuse pend_fz{0, 0};
   cudaStream_t pend_st = nullptr;
+  bool defer_in_capture = false;                         // capture mode 2: caller flushes in-capture
   uint64_t alloc_calls = 0;
   uint64_t limit = 0;                                    // live-bytes cap (0 = none)
   gg_alloc_hook hook = nullptr;
@@ -1706,8 +1707,9 @@ int flush_pending(gg_array *a) {
 // that a following grow can run both in one launch
 int finish_planned(gg_array *a, Fuse fz, cudaStream_t st) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (g_defer && !a->up.capturing && cudaStreamIsCapturing(st, &cap) == cudaSuccess &&
-      cap == cudaStreamCaptureStatusNone) {
+  const bool capturing = a->up.capturing ||
+                         (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone);
+  if (g_defer && (!capturing || a->defer_in_capture)) {
     a->pend = true;
     a->pend_fz = fz;
     a->pend_st = st;
@@ -2635,9 +2637,16 @@ int gg_capture_mode(gg_array *a, int32_t on) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  a->defer_in_capture = on == 2;
   if (on && !a->up.capturing) return a->up.begin_capture();
   if (!on) a->up.capturing = false;
   return GG_OK;
+}
+
+int gg_flush(gg_array *a) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  return flush_pending(a);
 }
 
 int gg_capture_release(gg_array *a) {

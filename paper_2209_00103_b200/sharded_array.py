@@ -125,6 +125,28 @@ class GrowableArray:
         L.lib.gg_summary(self._h, L.ptr(self._summary))
         return self._summary
 
+    def flush(self) -> None:
+        """Launch the deferred metadata pass of the last append now (normally it
+        rides on the next device-touching call)."""
+        L.check(L.lib.gg_flush(self._h), "flush")
+
+    def capture(self, fn, graph=None, stream=None):
+        """Capture ``fn()`` (a sequence of operations on this array) into a CUDA
+        graph and return it: capture mode with the deferred metadata pass kept
+        on, flushed inside the capture before it ends, so the captured appends
+        fuse their metadata into the following grows like eager issue does."""
+        import torch
+        g = graph if graph is not None else torch.cuda.CUDAGraph()
+        L.check(L.lib.gg_capture_mode(self._h, 2), "capture_mode")
+        try:
+            kw = {} if stream is None else {"stream": stream}
+            with torch.cuda.graph(g, **kw):
+                fn()
+                self.flush()
+        finally:
+            L.lib.gg_capture_mode(self._h, 0)
+        return g
+
     @contextlib.contextmanager
     def capture_mode(self):
         """Make every operation inside the block legal under CUDA stream capture

@@ -237,3 +237,43 @@ def test_flatten_range_slices(gg, dtype):
         assert got.tobytes() == full[lo:hi].tobytes(), (lo, hi)
     with pytest.raises(IndexError):
         a.flatten_range(0, n + 1)
+
+
+@pytest.mark.parametrize("defer", [True, False])
+def test_captured_schedule_replays_match_eager(gg, defer):
+    """GrowableArray.capture (deferred metadata kept on and flushed in-capture)
+    and plain capture_mode: replays of reset + insert + doubling rounds end
+    in the eager state, device tables == host mirror, contents == closed form."""
+    import torch
+    S, fb, n0, rounds = 64, 32, 1 << 14, 5
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    src = torch.arange(n0, dtype=torch.int32, device="cuda")
+    off = np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(n0 // S), np.uint64(n0))
+
+    def step():
+        a.shrink(0, release=False)
+        a.insert_csr(src, off)
+        for _ in range(rounds):
+            a.grow(2 * a.committed_size)
+            a.insert_duplicate()
+
+    step()
+    torch.cuda.synchronize()
+    if defer:
+        g = a.capture(step)
+    else:
+        g = torch.cuda.CUDAGraph()
+        with a.capture_mode():
+            with torch.cuda.graph(g):
+                step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    dev, host = a.device_state(), a._host()     # device tables == host mirror (ops counts replays)
+    for k in ("sizes", "caps", "flags", "prefix"):
+        assert np.array_equal(dev[k], host[k]), k
+    assert int(dev["prefix"][-1]) == n0 << rounds
+    per = (n0 // S) << rounds
+    idx = torch.arange(n0 << rounds, device="cuda")
+    exp = ((idx // per) * (n0 // S) + idx % (n0 // S)).to(torch.int32)
+    assert torch.equal(a.flatten_device(), exp)
