@@ -265,6 +265,7 @@ def run_device(args, rank, world, local_rank):
         out.update(secondary(args, gg, torch, device, step, hbm))
         out["phased_config4"] = phased_leg(args, gg, torch, device)
         out["config5_per_gpu"] = config5_leg(args, gg, torch, device, hbm)
+        out["config1"] = config1_leg(args, gg, torch, device, rank == 0 and world == 1 and not args.no_cpu)
         out["e2e"] = e2e_leg(args, gg, torch, device, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args)
@@ -508,6 +509,63 @@ def phased_leg(args, gg, torch, device):
     del src
     torch.cuda.empty_cache()
     return out
+
+
+def config1_leg(args, gg, torch, device, with_cpu):
+    """Config 1 (BASELINE configs[0], the reference's CPU-runnable case): 512
+    LFVectors, one batch insert of 2^20 int32 split like split_batches, one +1
+    pass, flatten.  Latency-bound on a B200 (8 MiB); reported as time per
+    sequence through the reference-style API (numpy batches in, numpy out:
+    H2D + kernels + D2H, wall clock) and device-resident (CUDA events), next
+    to the oracle port on the CPU."""
+    vals = np.arange(1 << 20, dtype=np.int32)
+    batches = gg.split_batches(vals, S)
+    dvals = torch.from_numpy(vals).to(device)
+    offs = split_off(1 << 20)
+
+    def host_api():
+        a = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+        a.insert_parallel(batches)
+        a.rw_add(1)
+        return a.flatten()
+
+    ref = vals + 1
+    assert host_api().tobytes() == ref.tobytes()
+    ts = []
+    for _ in range(15):
+        t0 = time.perf_counter()
+        host_api()
+        ts.append(time.perf_counter() - t0)
+    a = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+    flat = torch.empty(1 << 20, dtype=torch.int32, device=device)
+
+    def dev_seq():
+        a.shrink(0, release=False)
+        a.insert_csr(dvals, offs)
+        a.rw_add(1)
+        a.flatten_device(out=flat)
+
+    dev_seq()
+    dev_ms = _time(torch, dev_seq, reps=20)
+    assert torch.equal(flat.cpu(), torch.from_numpy(ref))
+    res = {"elements": 1 << 20, "host_api_ms": round(1e3 * float(np.median(ts)), 3),
+           "device_resident_us": round(1e3 * dev_ms, 2),
+           "host_api": "GrowableArray(512) + insert_parallel(split_batches(numpy)) + rw_add(1) + "
+                       "flatten() -> numpy, median of 15 (includes array construction)",
+           "device_resident": "shrink(0) + insert_csr(device batch) + rw_add(1) + flatten_device, "
+                              "CUDA events, mean of 20"}
+    if with_cpu:
+        from oracle import ggoracle as O
+        tc = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            o = O.OracleGGArray(S, FB, dtype=np.int32)
+            o.insert_parallel(O.split_batches(vals, S))
+            o.rw_add(1)
+            o.flatten()
+            tc.append(time.perf_counter() - t0)
+        res["cpu_port_ms"] = round(1e3 * min(tc), 3)
+    return res
 
 
 def config5_leg(args, gg, torch, device, hbm):

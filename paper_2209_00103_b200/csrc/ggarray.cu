@@ -1404,23 +1404,47 @@ int sm_count(int dev) {
   return g_sms[dev];
 }
 
-// pinned upload ring: small per-op host arrays (offsets, ctl words) travel
-// through pinned slots; a slot is reused only after its copy completed.
-struct Uploader {
+// Pinned upload ring: small per-op host arrays (offsets, ctl words) travel
+// through pinned slots; a slot is reused only after its copy completed.  One
+// ring per device, shared by every array of the process (created on first
+// use), so constructing an array costs no pinned allocation; uploads larger
+// than a slot go through a per-array pinned buffer.
+struct Ring {
   static constexpr int kSlots = 64;
-  char *host[kSlots] = {nullptr};
+  static constexpr size_t kSlot = 64 << 10;
+  char *block = nullptr;
   cudaEvent_t ev[kSlots] = {nullptr};
   bool used[kSlots] = {false};
-  size_t cap = 0;
   int next = 0;
-  char *block = nullptr;
-  int init(size_t bytes) {
-    cap = (bytes + 255) & ~size_t(255);
-    CUDA_TRY(cudaMallocHost(&block, cap * kSlots));
-    for (int i = 0; i < kSlots; ++i) {
-      host[i] = block + cap * i;
-      CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-    }
+  std::mutex mu;
+  int init() {
+    CUDA_TRY(cudaMallocHost(&block, kSlot * kSlots));
+    for (int i = 0; i < kSlots; ++i) CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    return GG_OK;
+  }
+};
+
+Ring *ring_for(int dev) {
+  static std::mutex m;
+  static Ring *rings[64] = {nullptr};
+  if (dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> g(m);
+  if (!rings[dev]) {
+    Ring *r = new Ring();
+    if (r->init() != GG_OK) { delete r; return nullptr; }
+    rings[dev] = r;          // process lifetime (driver teardown frees it)
+  }
+  return rings[dev];
+}
+
+struct Uploader {
+  int dev = 0;
+  char *big = nullptr;           // per-array pinned buffer for uploads above a ring slot
+  size_t big_cap = 0;
+  cudaEvent_t big_ev = nullptr;
+  bool big_used = false;
+  int init(int device) {
+    dev = device;
     return GG_OK;
   }
   // copy `n` arrays (dst device ptr, src host ptr, bytes) in one slot
@@ -1439,6 +1463,16 @@ struct Uploader {
     capturing = true;
     return GG_OK;
   }
+  static int copy_in(char *h, cudaStream_t st, int n, void *const *dst, const void *const *src,
+                     const size_t *bytes) {
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      memcpy(h + off, src[i], bytes[i]);
+      CUDA_TRY(cudaMemcpyAsync(dst[i], h + off, bytes[i], cudaMemcpyHostToDevice, st));
+      off += (bytes[i] + 15) & ~size_t(15);
+    }
+    return GG_OK;
+  }
   int upload(cudaStream_t st, int n, void *const *dst, const void *const *src, const size_t *bytes) {
     if (capturing) {
       char *h = captured.back();
@@ -1450,18 +1484,34 @@ struct Uploader {
       }
       return GG_OK;
     }
-    int k = next;
-    next = (next + 1) % kSlots;
-    if (used[k]) CUDA_TRY(cudaEventSynchronize(ev[k]));
-    size_t off = 0;
-    for (int i = 0; i < n; ++i) {
-      if (off + bytes[i] > cap) return fail(GG_EVALUE, "upload slot overflow");
-      memcpy(host[k] + off, src[i], bytes[i]);
-      CUDA_TRY(cudaMemcpyAsync(dst[i], host[k] + off, bytes[i], cudaMemcpyHostToDevice, st));
-      off += (bytes[i] + 15) & ~size_t(15);
+    size_t total = 0;
+    for (int i = 0; i < n; ++i) total += (bytes[i] + 15) & ~size_t(15);
+    if (total <= Ring::kSlot) {
+      Ring *r = ring_for(dev);
+      if (!r) return fail(GG_ECUDA, "pinned upload ring unavailable");
+      std::lock_guard<std::mutex> g(r->mu);
+      const int k = r->next;
+      r->next = (r->next + 1) % Ring::kSlots;
+      if (r->used[k]) CUDA_TRY(cudaEventSynchronize(r->ev[k]));
+      int rc = copy_in(r->block + Ring::kSlot * k, st, n, dst, src, bytes);
+      if (rc) return rc;
+      CUDA_TRY(cudaEventRecord(r->ev[k], st));
+      r->used[k] = true;
+      return GG_OK;
     }
-    CUDA_TRY(cudaEventRecord(ev[k], st));
-    used[k] = true;
+    if (big_used) CUDA_TRY(cudaEventSynchronize(big_ev));
+    if (total > big_cap) {
+      if (big) cudaFreeHost(big);
+      big = nullptr;
+      big_cap = 0;
+      CUDA_TRY(cudaMallocHost(&big, total));
+      big_cap = total;
+      if (!big_ev) CUDA_TRY(cudaEventCreateWithFlags(&big_ev, cudaEventDisableTiming));
+    }
+    int rc = copy_in(big, st, n, dst, src, bytes);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(big_ev, st));
+    big_used = true;
     return GG_OK;
   }
   void release_captured() {
@@ -1469,11 +1519,11 @@ struct Uploader {
     captured.clear();
   }
   void destroy() {
-    for (int i = 0; i < kSlots; ++i)
-      if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
-    if (block) cudaFreeHost(block);
+    if (big_ev) cudaEventSynchronize(big_ev), cudaEventDestroy(big_ev);
+    if (big) cudaFreeHost(big);
     release_captured();
   }
+
 };
 
 }  // namespace gg
@@ -1946,9 +1996,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
   a->d_won = (int *)(base + o_won);
   a->d_scratch = base + o_scr;
-  if ((rc = a->up.init(std::max<size_t>(4 * (S + 1) * 8, 4096)))) { gg_destroy(a); return rc; }
-  e = cudaMallocHost(&a->h_scratch, 64);
-  if (e != cudaSuccess) { gg_destroy(a); return fail(GG_ECUDA, cudaGetErrorString(e)); }
+  if ((rc = a->up.init(device))) { gg_destroy(a); return rc; }
   if (a->slab.small.base) {           // the packed small-class region exists from the start
     std::vector<uint64_t> cb(max_buckets);
     for (uint32_t b = 0; b < max_buckets; ++b) cb[b] = a->slab.class_base(b);
@@ -2242,6 +2290,7 @@ int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *str
     { k_zero_buckets<<<1, kThreads, 0, st>>>(t, d_pairs, 1); g_launches.fetch_add(1, std::memory_order_relaxed); }
   }
   int won = 0;
+  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
   CUDA_TRY(cudaMemcpyAsync(a->h_scratch, a->d_won, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   memcpy(&won, a->h_scratch, sizeof(int));
@@ -2472,6 +2521,7 @@ int elem_addr(gg_array *a, uint32_t s, uint64_t i, char **out, cudaStream_t st) 
   if (b >= a->MB || !(a->flags[s] >> b & 1))
     return fail(GG_EUNPUBLISHED, "index is reserved but its bucket is unpublished");
   char *p = nullptr;
+  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
   CUDA_TRY(cudaMemcpyAsync(a->h_scratch, a->t.ptr + (size_t)s * a->MB + b, sizeof(char *),
                            cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -2489,6 +2539,7 @@ int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
   if (rc) return rc;
+  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
   CUDA_TRY(cudaMemcpyAsync(a->h_scratch, p, a->esz, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   memcpy(h_out, a->h_scratch, a->esz);
@@ -2503,6 +2554,7 @@ int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream)
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
   if (rc) return rc;
+  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
   memcpy(a->h_scratch, h_val, a->esz);
   CUDA_TRY(cudaMemcpyAsync(p, a->h_scratch, a->esz, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaStreamSynchronize(st));
