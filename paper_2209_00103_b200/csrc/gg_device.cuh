@@ -1,0 +1,920 @@
+// gg_device.cuh -- device side of the B200 GGArray library: bucket
+// publication, reservation, commit / shrink / metadata kernels, the streaming
+// primitives and the one-tile-per-CTA walker (insert, duplicate, flatten,
+// r/w), rw_g, gather/scatter and the static-array baseline kernels.
+#ifndef GG_DEVICE_CUH
+#define GG_DEVICE_CUH
+
+#include "gg_common.cuh"
+
+namespace gg {
+
+// ------------------------------------------------------------------ device side
+
+template <int ESZ> struct ElemT;
+template <> struct ElemT<1> { typedef uint8_t T; };
+template <> struct ElemT<2> { typedef uint16_t T; };
+template <> struct ElemT<4> { typedef uint32_t T; };
+template <> struct ElemT<8> { typedef unsigned long long T; };
+
+// Programmatic dependent launch: every library kernel lets its stream
+// successor launch as soon as all its CTAs are running, and waits for its
+// predecessor's completion before touching memory (griddepcontrol.wait is a
+// no-op when the launch was not programmatic).
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ void stage_cbase(const Tables &t, char **scb) {
+  for (uint32_t i = threadIdx.x; i < t.MB; i += blockDim.x) scb[i] = t.cbase[i];
+}
+
+// Host-planned allocation of class-b buckets for every lane with `need`
+// (each (shard, bucket) is requested by exactly one lane, so the once-flags
+// are uncontended and the slot is the shard's own: no address atomics at
+// all; one counter update per warp and class).
+__device__ __forceinline__ void warp_alloc_class(const Tables &t, bool need, uint32_t s,
+                                                 uint32_t b) {
+  const unsigned m = __ballot_sync(0xffffffffu, need);
+  if (!m) return;
+  if ((threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)__popc(m));
+  if (!need) return;
+  // plain stores: these launches only publish host-planned buckets and the
+  // kernel boundary orders them before any reader
+  t.ptr[(size_t)s * t.MB + b] = bucket_slot(t, s, b);
+  atomicAdd((unsigned long long *)&t.cap[s], 1ull << (t.log2fb + b));
+  t.flag[(size_t)s * t.MB + b] = kFlagPublished;
+  atomicOr(&t.pmask[s], 1ull << b);
+}
+
+// allocate buckets [lo, hi) of shard s that are not yet published, warp-wide
+// loop over classes (lanes without work pass lo = hi)
+__device__ __forceinline__ void warp_alloc_range(const Tables &t, uint32_t s, uint32_t lo,
+                                                 uint32_t hi) {
+  // classes this lane needs = [lo, hi) minus the published ones (one mask load)
+  unsigned long long want = 0;
+  if (hi > lo) {
+    want = (hi >= 64 ? ~0ull : ((1ull << hi) - 1ull)) & ~((1ull << lo) - 1ull);
+    want &= ~t.pmask[s];
+  }
+  unsigned long long any = want;
+#pragma unroll
+  for (int d = 16; d; d >>= 1) any |= __shfl_xor_sync(0xffffffffu, any, d);
+  while (any) {
+    const uint32_t b = __ffsll((long long)any) - 1;
+    any &= any - 1;
+    warp_alloc_class(t, (want >> b) & 1ull, s, b);
+  }
+}
+
+// Publish buckets `want` of shard s (host-planned, slots already backed) from
+// the one thread that owns s in this launch: slot pointer + once-flag per
+// bucket, the shard's pmask (pm = its value at kernel start) and capacity,
+// and one allocation-count update per warp.  Plain stores: the kernel
+// boundary orders them before any reader.  Call with the full warp.
+__device__ __forceinline__ void publish_buckets(const Tables &t, char *const *scb, uint32_t s,
+                                                unsigned long long pm, unsigned long long want,
+                                                uint32_t lg0) {
+  uint64_t add = 0;
+  for (unsigned long long m = want; m; m &= m - 1) {
+    const uint32_t b = __ffsll((long long)m) - 1;
+    t.ptr[(size_t)s * t.MB + b] = scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
+    t.flag[(size_t)s * t.MB + b] = kFlagPublished;
+    add += 1ull << (t.log2fb + b);
+  }
+  if (want) {
+    t.pmask[s] = pm | want;
+    atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)add);
+  }
+  const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(want));
+  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)tot);
+}
+
+// Reservation + bucket allocation, one thread per shard: one atomicAdd on the
+// shard's size per batch (bucket_vector.py:229 via insert_index.py:118-122),
+// then allocate every missing bucket of the reserved range
+// (bucket_vector.py:207-214, 234-238).  Count sources:
+//   mode 0: CSR offsets (insert); mode 1: committed lengths (duplicate);
+//   mode 2: explicit starts + counts already in t.start/t.count (fetch_add'ed)
+__device__ __forceinline__ void reserve_shards(const Tables &t, uint32_t s, bool live, int mode) {
+  uint64_t c = 0, start = 0;
+  uint32_t lo = 0, hi = 0;
+  if (live) {
+    if (mode == 0) c = t.offsets[s + 1] - t.offsets[s];
+    else if (mode == 1) c = t.prefix[s + 1] - t.prefix[s];
+    else c = t.count[s];
+    const uint32_t ctl = t.ctl ? t.ctl[s] : (kCtlWrite | t.MB);
+    if (mode != 2) {
+      t.count[s] = c;
+      if (c) {
+        start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+        t.ops[s] += 1;
+        t.start[s] = start;
+      }
+    } else {
+      start = t.start[s];
+    }
+    if (c) {
+      uint32_t b0, b1;
+      uint64_t o;
+      locate(start, t.log2fb, b0, o);
+      locate(start + c - 1, t.log2fb, b1, o);
+      lo = b0;
+      hi = min(ctl & kCtlLimitMask, b1 + 1);
+      if (hi < lo) hi = lo;
+    }
+  }
+  warp_alloc_range(t, live ? s : 0, lo, hi);
+}
+
+__global__ void k_reserve(Tables t, int mode) {
+  pdl_begin();
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  reserve_shards(t, s, s < t.S, mode);
+}
+
+// grow: thread per shard, allocate buckets [0, lim[s]); lim comes from the
+// ctl words, or (uniform_k != ~0u) is the same for every shard.  Latency
+// shaped: every global load (class bases, pmask, ctl) is issued up front, then
+// one round of stores (publish_buckets).
+__global__ void __launch_bounds__(256) k_grow(Tables t, uint32_t uniform_k) {
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  stage_cbase(t, scb);
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = s < t.S;
+  const unsigned long long pm = live ? t.pmask[s] : 0ull;
+  const uint32_t lim = !live ? 0u : (uniform_k != ~0u ? uniform_k : (t.ctl[s] & kCtlLimitMask));
+  __syncthreads();
+  const unsigned long long want = (lim >= 64 ? ~0ull : ((1ull << lim) - 1ull)) & ~pm;
+  publish_buckets(t, scb, live ? s : 0u, pm, live ? want : 0ull, t.log2fb + (31u - __clz(t.esz)));
+}
+
+__global__ void k_new_bucket(Tables t, uint32_t s, uint32_t b, int *won) {
+  *won = alloc_bucket(t, s, b);
+}
+
+__global__ void k_fetch_add(Tables t, uint32_t s, uint64_t c) {
+  atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+  t.ops[s] += 1;
+}
+
+// commit (sharded_array.py:213-222): one CTA, exclusive scan of S sizes.
+__global__ void __launch_bounds__(1024) k_commit(Tables t) {
+  pdl_begin();
+  __shared__ uint64_t warp_tot[32];
+  __shared__ uint64_t carry;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < t.S; base += 1024) {
+    uint32_t s = base + tid;
+    uint64_t v = s < t.S ? t.size[s] : 0;
+    uint64_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= (uint32_t)d) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint64_t w = warp_tot[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= (uint32_t)d) w += y;
+      }
+      warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    uint64_t incl = x + (wid ? warp_tot[wid - 1] : 0) + carry;
+    if (s < t.S) {
+      t.prefix[s + 1] = incl;
+      if (s == 0) t.prefix[0] = 0;
+    }
+    __syncthreads();
+    if (tid == 1023) carry = incl;
+    __syncthreads();
+  }
+}
+
+// block-wide exclusive scan of one u64 per thread (blockDim multiple of 32);
+// returns the exclusive prefix, *total gets the block sum.
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t *total,
+                                                         uint64_t *warp_sums /* smem[32] */) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t w = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= (uint32_t)d) w += y;
+    }
+    warp_sums[lane] = w;
+  }
+  __syncthreads();
+  uint64_t incl = x + (wid ? warp_sums[wid - 1] : 0);
+  *total = warp_sums[nw - 1];
+  __syncthreads();
+  return incl - v;
+}
+
+// Paper Alg. 1 with per-lane counts, pass 1: CTA per shard sums its lanes'
+// counts (so the host can map the arena exactly before pass 2).
+__global__ void __launch_bounds__(1024) k_lanes_count(Tables t, const uint32_t *counts) {
+  __shared__ uint64_t ws[32];
+  const uint32_t s = blockIdx.x;
+  const uint64_t lo = t.offsets[s], hi = t.offsets[s + 1];
+  uint64_t acc = 0;
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) acc += counts[j];
+  uint64_t tot;
+  block_exclusive_scan(acc, &tot, ws);
+  if (threadIdx.x == 0) t.count[s] = tot;
+}
+
+// Pass 2 (paper Alg. 1): the CTA of shard s reserves its whole batch with ONE
+// atomicAdd on the LFVector size, allocates the buckets the range touches
+// (Alg. 2), then block-scans the lane counts chunk by chunk and every lane
+// scatters its values to start + carry + exclusive_scan(lane).
+template <int ESZ>
+__global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *vals,
+                                                       const uint32_t *counts, uint32_t K) {
+  typedef typename ElemT<ESZ>::T E;
+  __shared__ uint64_t ws[32];
+  __shared__ char *bptr[64];
+  __shared__ uint64_t start_s;
+  __shared__ uint32_t ctl_s;
+  const uint32_t s = blockIdx.x, tid = threadIdx.x;
+  const uint64_t c = t.count[s];
+  if (c == 0) return;
+  if (tid == 0) {
+    const uint32_t ctl = t.ctl ? t.ctl[s] : (kCtlWrite | t.MB);
+    const uint64_t start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
+    t.ops[s] += 1;
+    uint32_t b0, b1; uint64_t o;
+    locate(start, t.log2fb, b0, o);
+    locate(start + c - 1, t.log2fb, b1, o);
+    uint32_t lim = min(ctl & kCtlLimitMask, b1 + 1);
+    for (uint32_t b = b0; b < lim; ++b)
+      if (alloc_bucket(t, s, b) < 0) atomicOr(&t.status[s], (uint32_t)GG_ENOMEM);
+    start_s = start;
+    ctl_s = ctl;
+  }
+  __syncthreads();
+  if (tid < t.MB) bptr[tid] = t.flag[(size_t)s * t.MB + tid] == kFlagPublished
+                                  ? t.ptr[(size_t)s * t.MB + tid] : nullptr;
+  __syncthreads();
+  const uint64_t start = start_s;
+  const uint32_t ctl = ctl_s;
+  if (!(ctl & (kCtlWrite | kCtlZero))) return;
+  const uint64_t lo = t.offsets[s], hi = t.offsets[s + 1];
+  uint64_t carry = 0;
+  for (uint64_t base = lo; base < hi; base += blockDim.x) {
+    const uint64_t j = base + tid;
+    const uint32_t cnt = j < hi ? counts[j] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan(cnt, &tot, ws);
+    const E *src = (const E *)vals + j * K;
+    for (uint32_t e = 0; e < cnt; ++e) {
+      uint32_t b; uint64_t o;
+      locate(start + carry + ex + e, t.log2fb, b, o);
+      if (bptr[b]) ((E *)bptr[b])[o] = (ctl & kCtlWrite) ? src[e] : E(0);
+    }
+    carry += tot;
+  }
+}
+
+// shrink (extension): one CTA; per shard size[s] = new size, buckets
+// b >= min_buckets_for(new size) unpublished (their slots stay reserved for
+// the shard; the host unmaps chunks that lost their last live bucket), then
+// the commit scan over the new sizes.  All loads issued up front.
+__global__ void __launch_bounds__(1024) k_shrink(Tables t, const uint64_t *new_sizes) {
+  __shared__ uint64_t ws[32];
+  pdl_begin();
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const bool live = s < t.S;
+    uint64_t ns = 0, cap = 0;
+    unsigned long long m = 0;
+    if (live) { ns = new_sizes[s]; m = t.pmask[s]; cap = t.cap[s]; }
+    if (live) {
+      const uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + (1ull << t.log2fb) - 1) >> t.log2fb))) : 0u;
+      const unsigned long long drop = keep < 64 ? (m & ~((1ull << keep) - 1ull)) : 0ull;
+      uint64_t freed = 0;
+      for (unsigned long long d = drop; d; d &= d - 1) {
+        const uint32_t b = __ffsll((long long)d) - 1;
+        t.ptr[(size_t)s * t.MB + b] = nullptr;
+        t.flag[(size_t)s * t.MB + b] = 0;
+        freed += 1ull << (t.log2fb + b);
+      }
+      if (drop) { t.pmask[s] = m & ~drop; t.cap[s] = cap - freed; }
+      t.size[s] = ns;
+    }
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_scan(ns, &tot, ws);
+    if (live) t.prefix[s + 1] = carry + ex + ns;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) t.prefix[0] = 0;
+}
+
+// ---- streaming primitives: a CTA moves one contiguous piece -------------
+
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_rw(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg(uint4 *p, const uint4 &v) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// Cache policy of the streaming loads/stores (selected by the tuning sweep):
+// 0 = L2-only (.cg), 1 = read-only path loads (.nc) + default stores,
+// 2 = default loads/stores, 3 = evict-first streaming (.cs).
+template <int LS> struct LdSt;
+template <> struct LdSt<0> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return __ldcg(p); }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { __stcg(p, v); }
+};
+template <> struct LdSt<1> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return __ldg(p); }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { *p = v; }
+};
+template <> struct LdSt<2> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return *p; }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { *p = v; }
+};
+template <> struct LdSt<3> {
+  template <class V> __device__ __forceinline__ static V ld(const V *p) { return __ldcs(p); }
+  template <class V> __device__ __forceinline__ static void st(V *p, const V &v) { __stcs(p, v); }
+};
+constexpr int kDefLS = 0;
+constexpr int kDefUnroll = 4;
+
+// dst[0..n) = src[0..n) (element granular, arbitrary relative alignment), or
+// zeros if src == nullptr.  Stores are 16 B aligned vectors; loads are 16 B
+// vectors when src shares dst's alignment, else element loads.
+template <int ESZ, int UNROLL, int LS = kDefLS>
+__device__ __forceinline__ void cta_copy(char *dst, const char *src, uint64_t n, uint32_t tid,
+                                         uint32_t nt) {
+  typedef LdSt<LS> M;
+  typedef typename ElemT<ESZ>::T E;
+  constexpr uint32_t VE = 16 / ESZ;
+  const uintptr_t d = (uintptr_t)dst;
+  uint64_t head = ((16 - (d & 15)) & 15) / ESZ;
+  if (head > n) head = n;
+  const uint64_t body = (n - head) / VE;
+  const uint64_t tail0 = head + body * VE;
+  E *de = (E *)dst;
+  const E *se = (const E *)src;
+  for (uint64_t e = tid; e < head; e += nt) de[e] = src ? se[e] : E(0);
+  for (uint64_t e = tail0 + tid; e < n; e += nt) de[e] = src ? se[e] : E(0);
+  uint4 *dv = (uint4 *)(dst + head * ESZ);
+  if (src == nullptr) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (uint64_t v = tid; v < body; v += nt) M::st(dv + v, z);
+    return;
+  }
+  const char *sb = src + head * ESZ;
+  if ((((uintptr_t)sb) & 15) == 0) {
+    // batches of UNROLL independent 16 B loads per thread, all issued before
+    // the stores; loads past the end are clamped (re-read the last vector) so
+    // they stay unconditional and the compiler cannot interleave them
+    const uint4 *sv = (const uint4 *)sb;
+    for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
+      uint4 r[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) r[u] = M::ld(sv + min(v0 + u * (uint64_t)nt, body - 1));
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (v0 + u * (uint64_t)nt < body) M::st(dv + v0 + u * nt, r[u]);
+    }
+  } else {
+    const E *s2 = (const E *)sb;
+    for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
+      union { uint4 q; E e[VE]; } u[UNROLL];
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k) {
+        const uint64_t v = min(v0 + k * (uint64_t)nt, body - 1);
+#pragma unroll
+        for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = M::ld(s2 + v * VE + j);
+      }
+#pragma unroll
+      for (int k = 0; k < UNROLL; ++k)
+        if (v0 + k * (uint64_t)nt < body) M::st(dv + v0 + k * nt, u[k].q);
+    }
+  }
+}
+
+// typed wrapping / IEEE add used by the r/w passes
+template <typename T> struct AddOp {
+  __device__ __forceinline__ static T apply(T x, T a) { return (T)(x + a); }
+};
+template <> struct AddOp<int8_t> {
+  __device__ __forceinline__ static int8_t apply(int8_t x, int8_t a) {
+    return (int8_t)(uint8_t)((uint8_t)x + (uint8_t)a);
+  }
+};
+template <> struct AddOp<int16_t> {
+  __device__ __forceinline__ static int16_t apply(int16_t x, int16_t a) {
+    return (int16_t)(uint16_t)((uint16_t)x + (uint16_t)a);
+  }
+};
+template <> struct AddOp<int32_t> {
+  __device__ __forceinline__ static int32_t apply(int32_t x, int32_t a) {
+    return (int32_t)((uint32_t)x + (uint32_t)a);
+  }
+};
+template <> struct AddOp<long long> {
+  __device__ __forceinline__ static long long apply(long long x, long long a) {
+    return (long long)((unsigned long long)x + (unsigned long long)a);
+  }
+};
+template <> struct AddOp<float> {
+  __device__ __forceinline__ static float apply(float x, float a) { return __fadd_rn(x, a); }
+};
+template <> struct AddOp<double> {
+  __device__ __forceinline__ static double apply(double x, double a) { return __dadd_rn(x, a); }
+};
+template <> struct AddOp<__half> {
+  // numpy float16 arithmetic: widen to float32, add, round back (exact RN)
+  __device__ __forceinline__ static __half apply(__half x, __half a) {
+    return __float2half_rn(__half2float(x) + __half2float(a));
+  }
+};
+
+// in-place p[0..n) = p + a (applied `reps` times in registers; reps = 1 for a
+// separate sweep per pass)
+template <typename T, int UNROLL, int LS = kDefLS>
+__device__ __forceinline__ void cta_add(char *p, uint64_t n, T a, uint32_t reps, uint32_t tid,
+                                        uint32_t nt) {
+  typedef LdSt<LS == 1 ? 2 : LS> M;   // no read-only path for in-place updates
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uintptr_t d = (uintptr_t)p;
+  uint64_t head = ((16 - (d & 15)) & 15) / sizeof(T);
+  if (head > n) head = n;
+  const uint64_t body = (n - head) / VE;
+  const uint64_t tail0 = head + body * VE;
+  T *pe = (T *)p;
+  for (uint64_t e = tid; e < head; e += nt) {
+    T x = pe[e];
+    for (uint32_t r = 0; r < reps; ++r) x = AddOp<T>::apply(x, a);
+    pe[e] = x;
+  }
+  for (uint64_t e = tail0 + tid; e < n; e += nt) {
+    T x = pe[e];
+    for (uint32_t r = 0; r < reps; ++r) x = AddOp<T>::apply(x, a);
+    pe[e] = x;
+  }
+  uint4 *pv = (uint4 *)(p + head * sizeof(T));
+  for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
+    union { uint4 q; T e[VE]; } u[UNROLL];
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) u[k].q = M::ld(pv + min(v0 + k * (uint64_t)nt, body - 1));
+#pragma unroll
+    for (int k = 0; k < UNROLL; ++k) {
+      if (v0 + k * (uint64_t)nt < body) {
+        for (uint32_t r = 0; r < reps; ++r)
+#pragma unroll
+          for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = AddOp<T>::apply(u[k].e[j], a);
+        M::st(pv + v0 + k * nt, u[k].q);
+      }
+    }
+  }
+}
+
+// ---- tile walker ------------------------------------------------------------
+// The work space is an index range [0, total) partitioned among shards by a
+// directory dir[S+1] (CSR offsets for inserts, the committed prefix for
+// duplicate / flatten / r/w).  A CTA takes one tile and walks it
+// in pieces over which shard, source bucket and destination bucket are all
+// constant; every thread computes the (uniform) piece bounds itself.
+enum { W_INSERT = 0, W_DUP = 1, W_FLATTEN = 2, W_RW = 3 };
+
+__device__ __forceinline__ uint32_t upper_shard(const uint64_t *dir, uint32_t S, uint64_t g) {
+  // largest s with dir[s] <= g (bisect_right - 1, sharded_array.py:136)
+  uint32_t lo = 0, hi = S;  // dir[0] = 0 <= g
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (dir[mid] <= g) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+
+// Bucket (s, b) sits at a fixed slot of class b's slab (gg_device_view), so
+// kernels compute bucket addresses instead of loading them: scb[] holds the
+// class bases staged in shared memory, lg0 = log2(fb * element bytes).
+__device__ __forceinline__ char *slot_addr(char *const *scb, uint32_t s, uint32_t b, uint32_t lg0) {
+  return scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
+}
+
+// shard of work index g: largest s with dir[s] <= g (bisect_right - 1,
+// sharded_array.py:136) by a 32-ary warp search -- 2 dependent loads for
+// S <= 1024, 3 up to 32768.  Called by a full warp; result in every lane.
+__device__ __forceinline__ uint32_t warp_find_shard(const uint64_t *dir, uint32_t S, uint64_t g) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = S;                 // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) >> 5;
+    const uint32_t p = lo + lane * step;
+    const bool ok = p < hi && dir[p] <= g;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);   // lane 0 (p = lo) always ok
+    lo = lo + (31u - __clz(m)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// One tile [g, gend) lying inside shard s with 16 B-congruent source and
+// destination: each thread moves U vectors, resolving every vector's bucket
+// on its own (clz locate + slot arithmetic) and issuing all U loads before
+// any store -- one memory round trip per tile however many buckets it
+// touches.  Returns false (tile not handled) when the tile crosses a shard
+// or the alignment does not hold.
+template <int ESZ, int W, typename T, int U, int LS>
+__device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, const uint64_t *dir,
+                                            uint32_t s, uint64_t dbase, uint64_t g, uint64_t gend,
+                                            const char *flat_src, char *flat_dst, T addend,
+                                            uint32_t reps) {
+  constexpr uint32_t VE = 16 / ESZ;
+  const uint64_t lo = dir[s];
+  if (gend > dir[s + 1] || ((g - lo) % VE) || ((gend - g) % VE) || (t.log2fb < 31 && ((1u << t.log2fb) % VE)))
+    return false;
+  if constexpr (W == W_INSERT || W == W_DUP) {
+    if (dbase % VE) return false;
+  }
+  if constexpr (W == W_INSERT) {
+    if (((uintptr_t)(flat_src + g * ESZ)) & 15) return false;
+  }
+  if constexpr (W == W_FLATTEN) {
+    if (((uintptr_t)(flat_dst + g * ESZ)) & 15) return false;
+  }
+  typedef LdSt<(W == W_RW && LS == 1) ? 2 : LS> M;
+  constexpr uint32_t LGE = ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3;
+  const uint32_t lg0 = t.log2fb + LGE;
+  const uint64_t nvec = (gend - g) / VE;
+  const uint64_t k0 = g - lo;              // work-space offset inside the shard
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  for (uint64_t v0 = tid; v0 < nvec; v0 += U * (uint64_t)nt) {
+    uint4 r[U];
+    char *sp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = min(v0 + u * (uint64_t)nt, nvec - 1);
+      if constexpr (W == W_INSERT) {
+        sp[u] = (char *)flat_src + (g + v * VE) * ESZ;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(k0 + v * VE, t.log2fb, b, o);
+        sp[u] = slot_addr(scb, s, b, lg0) + o * ESZ;
+      }
+      r[u] = M::ld((const uint4 *)sp[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = v0 + u * (uint64_t)nt;
+      if (v >= nvec) continue;
+      char *dp;
+      if constexpr (W == W_FLATTEN) {
+        dp = flat_dst + (g + v * VE) * ESZ;
+      } else if constexpr (W == W_RW) {
+        dp = sp[u];
+        union { uint4 q; T e[VE]; } x;
+        x.q = r[u];
+        for (uint32_t rr = 0; rr < reps; ++rr)
+#pragma unroll
+          for (uint32_t j = 0; j < VE; ++j) x.e[j] = AddOp<T>::apply(x.e[j], addend);
+        r[u] = x.q;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(dbase + k0 + v * VE, t.log2fb, b, o);
+        dp = slot_addr(scb, s, b, lg0) + o * ESZ;
+      }
+      M::st((uint4 *)dp, r[u]);
+    }
+  }
+  return true;
+}
+
+// Planned append (PLANNED): the host has already backed every destination
+// slot and knows each shard's count, so the copy needs no reservation phase:
+// destinations are slot arithmetic from the unchanged size[s]; k_planned_meta
+// applies the metadata right after.  (A last-CTA epilogue in the walk itself
+// costs more: the completion atomic lengthens every CTA's life.)
+struct Fuse { int rmode; int commit; uint64_t g0 = 0; };   // g0: first work index (ranges)
+
+// metadata of a planned append, run by one CTA after every tile is copied.
+// Latency shaped: all loads (directory pair, size, pmask) issued up front,
+// counters updated with fire-and-forget reductions, the commit scan runs on
+// the new sizes held in registers (no reload).
+__device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &fz) {
+  __shared__ uint64_t ws[32];
+  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+  const uint64_t *dir = fz.rmode == 0 ? t.offsets : t.prefix;
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const bool live = s < t.S;
+    uint64_t lo = 0, hi = 0, start = 0;
+    unsigned long long pm = 0;
+    if (live) { lo = dir[s]; hi = dir[s + 1]; start = t.size[s]; pm = t.pmask[s]; }
+    const uint64_t c = hi - lo, nsz = start + c;
+    unsigned long long want = 0;
+    if (c) {
+      t.size[s] = nsz;
+      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+      t.start[s] = start;
+      uint32_t b0, b1; uint64_t o;
+      locate(start, t.log2fb, b0, o);
+      locate(nsz - 1, t.log2fb, b1, o);
+      want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~pm;
+    }
+    if (live) t.count[s] = c;
+    publish_buckets(t, scb, live ? s : 0u, pm, want, lg0);
+    if (fz.commit) {
+      uint64_t tot;
+      const uint64_t ex = block_exclusive_scan(live ? nsz : 0, &tot, ws);
+      if (live) t.prefix[s + 1] = carry + ex + nsz;
+      carry += tot;
+    }
+  }
+  if (fz.commit && threadIdx.x == 0) t.prefix[0] = 0;
+}
+
+// The tile walker: ONE tile per CTA (a non-persistent grid streams ~15%
+// faster than a persistent grid-stride loop on B200, tools/probe), tile =
+// U vectors per thread.  The work space [0, total) is partitioned among
+// shards by dir[S+1] (CSR offsets for inserts, the committed prefix for
+// duplicate / flatten / r/w); a tile inside one shard with congruent
+// alignment takes vector_tile, anything else the piece walker (pieces over
+// which shard, source bucket and destination bucket are constant).
+template <int ESZ, int W, typename T, int U = 4, int LS = kDefLS, bool PLANNED = false>
+__global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, char *flat_dst,
+                                              uint64_t total, T addend, uint32_t reps,
+                                              uint32_t tile, Fuse fz) {
+  __shared__ char *scb[kMaxBuckets];
+  __shared__ uint32_t s_sh;
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  pdl_begin();
+  const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
+  uint64_t g = fz.g0 + (uint64_t)blockIdx.x * tile;
+  const uint64_t gend = min(total, g + tile);
+  if (tid < 32) {
+    const uint32_t s0 = warp_find_shard(dir, t.S, g);
+    if (tid == 0) s_sh = s0;
+  }
+  stage_cbase(t, scb);
+  __syncthreads();
+  constexpr uint32_t LGE = ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3;
+  const uint32_t lg0 = t.log2fb + LGE;
+  uint32_t s = s_sh;
+  bool fast = true;
+  uint64_t dbase = 0;                      // destination local index of shard s's work index 0
+  if constexpr (W == W_INSERT || W == W_DUP) {
+    if (!PLANNED && t.ctl && t.ctl[s] != (kCtlWrite | t.MB)) fast = false;   // planned failure
+    dbase = PLANNED ? t.size[s] : t.start[s];
+  }
+  if (!(fast && vector_tile<ESZ, W, T, U, LS>(t, scb, dir, s, dbase, g, gend, flat_src, flat_dst,
+                                              addend, reps))) {
+    while (g < gend) {
+      uint64_t shard_end = dir[s + 1];
+      while (shard_end <= g) { ++s; shard_end = dir[s + 1]; }
+      const uint64_t k = g - dir[s];
+      uint64_t len = min(gend, shard_end) - g;
+      const uint32_t ctl = (W == W_INSERT || W == W_DUP) && !PLANNED && t.ctl ? t.ctl[s] : kCtlWrite;
+      const char *sp = nullptr;
+      char *dp = nullptr;
+      bool dst_ok = true;
+      // source side
+      if constexpr (W == W_INSERT) {
+        sp = flat_src + g * ESZ;
+      } else {
+        uint32_t b; uint64_t o;
+        locate(k, t.log2fb, b, o);
+        len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
+        sp = slot_addr(scb, s, b, lg0) + o * ESZ;
+      }
+      // destination side
+      if constexpr (W == W_FLATTEN) {
+        dp = flat_dst + g * ESZ;
+      } else if constexpr (W == W_RW) {
+        dp = (char *)sp;
+      } else {
+        uint32_t b; uint64_t o;
+        locate((PLANNED ? t.size[s] : t.start[s]) + k, t.log2fb, b, o);
+        len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
+        if (!PLANNED) dst_ok = t.flag[(size_t)s * t.MB + b] == kFlagPublished;
+        dp = slot_addr(scb, s, b, lg0) + o * ESZ;
+      }
+      if constexpr (W == W_RW) {
+        cta_add<T, U, LS>(dp, len, addend, reps, tid, nt);
+      } else if (dst_ok && (ctl & (kCtlWrite | kCtlZero))) {
+        cta_copy<ESZ, U, LS>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
+      }
+      g += len;
+    }
+  }
+}
+
+// Metadata of a planned append (launched right behind its copy walk, PDL):
+// one size update per LFVector (the reference's single fetch_add per batch),
+// bucket publication (flag, ptr, pmask, cap) and, if asked, the commit scan.
+__global__ void __launch_bounds__(1024) k_planned_meta(Tables t, Fuse fz) {
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  stage_cbase(t, scb);
+  __syncthreads();
+  planned_metadata(t, scb, fz);
+}
+
+// A deferred planned-append metadata pass fused with the grow that follows it
+// (the doubling schedule's grow(2n) after every duplicate): one launch, the
+// metadata first, then buckets [0, uk) of every shard published.
+__global__ void __launch_bounds__(1024) k_meta_grow(Tables t, Fuse fz, uint32_t uk) {
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  stage_cbase(t, scb);
+  __syncthreads();
+  planned_metadata(t, scb, fz);
+  __syncthreads();
+  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+  const unsigned long long all = uk >= 64 ? ~0ull : ((1ull << uk) - 1ull);
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const bool live = s < t.S;
+    const unsigned long long pm = live ? t.pmask[s] : 0ull;
+    publish_buckets(t, scb, live ? s : 0u, pm, live ? (all & ~pm) : 0ull, lg0);
+  }
+}
+
+// rw_g (bench_cli.py:339-366, the paper's rw_g): every 16 B group of
+// consecutive GLOBAL indices is resolved through the directory on its own --
+// a warp-uniform bisect on the smem prefix for the chunk, a per-lane fix-up
+// and a clz locate -- and each thread keeps kDefUnroll such vectors in flight.
+// Groups that straddle a shard or are not 16 B-aligned inside their bucket
+// are updated element by element.
+template <typename T, int U = kDefUnroll>
+__global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total, T addend) {
+  pdl_begin();
+  __shared__ char *scb[kMaxBuckets];
+  stage_cbase(t, scb);
+  __syncthreads();
+  const uint64_t *pre = t.prefix;
+  constexpr uint32_t LGE = sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : sizeof(T) == 4 ? 2 : 3;
+  const uint32_t lg0 = t.log2fb + LGE;
+  constexpr uint32_t VE = 16 / sizeof(T);
+  
+  typedef LdSt<kDefLS == 1 ? 2 : kDefLS> M;
+  const uint64_t nvec = (total + VE - 1) / VE;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  for (uint64_t c0 = wid * 32 * U; c0 < nvec; c0 += nwarps * 32 * U) {
+    uint32_t s = warp_find_shard(pre, t.S, c0 * VE);  // warp-uniform 32-ary search
+    uint4 r[U];
+    T *p[U];
+    bool vec[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = c0 + lane + 32u * u;
+      const uint64_t g = v * VE;
+      vec[u] = false;
+      p[u] = nullptr;
+      if (v < nvec) {
+        while (pre[s + 1] <= g) ++s;
+        uint32_t b; uint64_t o;
+        locate(g - pre[s], t.log2fb, b, o);
+        p[u] = (T *)slot_addr(scb, s, b, lg0) + o;
+        vec[u] = g + VE <= pre[s + 1] && (o % VE) == 0 && o + VE <= (1ull << (t.log2fb + b));
+        if (vec[u]) r[u] = M::ld((const uint4 *)p[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t v = c0 + lane + 32u * u;
+      if (v >= nvec) continue;
+      if (vec[u]) {
+        union { uint4 q; T e[VE]; } x;
+        x.q = r[u];
+#pragma unroll
+        for (uint32_t j = 0; j < VE; ++j) x.e[j] = AddOp<T>::apply(x.e[j], addend);
+        M::st((uint4 *)p[u], x.q);
+      } else {
+        const uint64_t g = v * VE;
+        uint32_t sj = upper_shard(pre, t.S, g);
+        for (uint32_t j = 0; j < VE && g + j < total; ++j) {
+          const uint64_t gj = g + j;
+          while (pre[sj + 1] <= gj) ++sj;
+          uint32_t b; uint64_t o;
+          locate(gj - pre[sj], t.log2fb, b, o);
+          T *q = (T *)slot_addr(scb, sj, b, lg0) + o;
+          *q = AddOp<T>::apply(*q, addend);
+        }
+      }
+    }
+  }
+}
+
+template <int ESZ>
+__global__ void k_gather(Tables t, const int64_t *idx, uint64_t n, char *out, const char *vals,
+                         int scatter) {
+  typedef typename ElemT<ESZ>::T E;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t g = (uint64_t)idx[j];
+    uint32_t s = upper_shard(t.prefix, t.S, g);
+    uint32_t b; uint64_t o;
+    locate(g - t.prefix[s], t.log2fb, b, o);
+    E *p = (E *)(t.ptr[(size_t)s * t.MB + b]) + o;
+    if (scatter) *p = ((const E *)vals)[j];
+    else ((E *)out)[j] = *p;
+  }
+}
+
+// zero whole buckets listed as (shard, bucket) pairs (dirty shards only)
+__global__ void k_zero_buckets(Tables t, const uint32_t *pairs, uint32_t npairs) {
+  for (uint32_t k = blockIdx.x; k < npairs; k += gridDim.x) {
+    uint32_t s = pairs[2 * k], b = pairs[2 * k + 1];
+    char *p = t.ptr[(size_t)s * t.MB + b];
+    uint64_t n = (1ull << (t.log2fb + b)) * t.esz;
+    if (t.flag[(size_t)s * t.MB + b] != kFlagPublished) continue;
+    cta_copy<1, 4>(p, nullptr, n, threadIdx.x, blockDim.x);
+  }
+}
+
+// ---- static-array baselines ---------------------------------------------------
+template <int ESZ>
+__global__ void k_flat_insert(char *buf, uint64_t cap, unsigned long long *counter,
+                              const char *vals, uint64_t n, int algo, uint64_t opaque_zero) {
+  typedef typename ElemT<ESZ>::T E;
+  const E *v = (const E *)vals;
+  E *out = (E *)buf;
+  __shared__ unsigned long long base_s;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
+    uint64_t j = j0 + threadIdx.x;
+    bool have = j < n;
+    unsigned long long idx = 0;
+    if (algo == GG_ALGO_ATOMIC) {
+      // paper 3-B-1: one atomic per element.  The compiler warp-aggregates an
+      // atomicAdd on a provably uniform address by itself (ncu: 32x fewer L2
+      // atomic requests), which would turn this baseline into the warp one;
+      // the per-thread `j * opaque_zero` offset (0 at run time) keeps the
+      // address non-uniform to the compiler.
+      if (have) idx = atomicAdd(counter + j * opaque_zero, 1ull);
+    } else if (algo == GG_ALGO_WARP) {
+      // paper 3-B-2 (warp shuffle scan of 0/1 counts, one atomic per warp)
+      unsigned mask = __ballot_sync(0xffffffffu, have);
+      unsigned lane = threadIdx.x & 31;
+      unsigned long long wb = 0;
+      if (lane == 0 && mask) wb = atomicAdd(counter, (unsigned long long)__popc(mask));
+      wb = __shfl_sync(0xffffffffu, wb, 0);
+      idx = wb + __popc(mask & ((1u << lane) - 1u));
+    } else {  // GG_ALGO_BLOCK: block scan, one atomic per CTA
+      uint64_t cnt = min((uint64_t)blockDim.x, n - j0);
+      if (threadIdx.x == 0) base_s = atomicAdd(counter, (unsigned long long)cnt);
+      __syncthreads();
+      idx = base_s + threadIdx.x;
+      __syncthreads();
+    }
+    if (have && idx < cap) out[idx] = v[j];
+  }
+}
+
+template <typename T, int UNROLL = kDefUnroll, int LS = kDefLS>
+__global__ void __launch_bounds__(512) k_flat_add(char *buf, uint64_t n, T a, uint32_t reps) {
+  pdl_begin();
+  // one kFlatChunk chunk of the contiguous array per CTA (non-persistent grid)
+  constexpr uint64_t CH = kFlatChunk / sizeof(T);
+  const uint64_t nch = (n + CH - 1) / CH;
+  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    uint64_t lo = c * CH, len = min(n - lo, CH);
+    cta_add<T, UNROLL, LS>(buf + lo * sizeof(T), len, a, reps, threadIdx.x, blockDim.x);
+  }
+}
+
+}  // namespace gg
+
+#endif  // GG_DEVICE_CUH
