@@ -21,7 +21,7 @@
  * headroom no bucket took.
  *
  * The same structures and allocator back the library's own kernels
- * (paper_2209_00103_b200/csrc/ggarray.cu), so there is one implementation.
+ * (paper_2209_00103_b200/csrc/gg_device.cuh), so there is one implementation.
  */
 #ifndef GGARRAY_DEVICE_CUH
 #define GGARRAY_DEVICE_CUH
