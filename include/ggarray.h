@@ -227,6 +227,14 @@ int gg_mem_stats(gg_array *a, uint64_t *h_out6, void *stream);
  * [5]=ns in cuMemUnmap/Release, [6]=class regions reserved, [7]=VA bytes */
 int gg_slab_stats(gg_array *a, uint64_t *h_out8);
 
+/* Process-wide cache of physical slab chunks left by destroyed arrays
+ * (reused by new arrays instead of fresh driver allocations; bounded by
+ * GG_POOL_BYTES, default 4 GiB per device).  Shrink releases and trim() never
+ * go to the cache.  stats: [0]=cached bytes, [1]=chunks, [2]=hits,
+ * [3]=misses (process-wide), [4]=cap bytes. */
+int gg_pool_stats(int device, uint64_t *h_out5);
+int gg_pool_trim(int device);
+
 /* ---- baselines (baselines.py) on raw device buffers ---- */
 /* StaticArray/DoublingArray/ChunkTableArray.insert_batch (baselines.py:
  * 63-77, 143-157, 224-236): append d_vals[0..n) at *d_counter using `algo`

@@ -87,6 +87,8 @@ _SIGS = {
     "gg_mem_stats": ([P, PU64, P], C.c_int),
     "gg_prefix_copy": ([P, P, P], C.c_int),
     "gg_slab_stats": ([P, PU64], C.c_int),
+    "gg_pool_stats": ([C.c_int, PU64], C.c_int),
+    "gg_pool_trim": ([C.c_int], C.c_int),
     "gg_flat_insert": ([P, U64, P, P, U64, U32, I32, P], C.c_int),
     "gg_flat_add": ([P, U64, U32, P, U32, I32, P], C.c_int),
     "gg_ipc_alloc": ([U64, C.POINTER(C.c_void_p)], C.c_int),

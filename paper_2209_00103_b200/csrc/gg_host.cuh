@@ -86,6 +86,62 @@ struct Arena {
   }
 };
 
+// Process-wide cache of physical chunks released by DESTROYED arrays, per
+// device and chunk size: a new array maps a cached handle (cuMemMap +
+// cuMemSetAccess) instead of creating one, which avoids the driver's
+// allocate / scrub / free churn when arrays come and go (config 1 builds an
+// array per call).  Bounded (GG_POOL_BYTES, default 4 GiB per device) and
+// reported by gg_pool_stats / emptied by gg_pool_trim; a shrink's release
+// and trim() always return memory to the driver, so a live array's mapped
+// bytes are its whole footprint.
+struct ChunkPool {
+  std::mutex mu;
+  std::vector<std::pair<size_t, CUmemGenericAllocationHandle>> free[64];
+  uint64_t bytes[64] = {0};
+  uint64_t hits = 0, misses = 0;
+  uint64_t cap() {
+    static uint64_t c = [] {
+      const char *e = getenv("GG_POOL_BYTES");
+      return e ? strtoull(e, nullptr, 10) : (uint64_t(4) << 30);
+    }();
+    return c;
+  }
+  bool take(int dev, size_t size, CUmemGenericAllocationHandle *h) {
+    if (dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> g(mu);
+    auto &v = free[dev];
+    for (size_t i = v.size(); i-- > 0;)
+      if (v[i].first == size) {
+        *h = v[i].second;
+        v.erase(v.begin() + i);
+        bytes[dev] -= size;
+        ++hits;
+        return true;
+      }
+    ++misses;
+    return false;
+  }
+  bool give(int dev, size_t size, CUmemGenericAllocationHandle h) {
+    if (dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> g(mu);
+    if (bytes[dev] + size > cap()) return false;
+    free[dev].push_back({size, h});
+    bytes[dev] += size;
+    return true;
+  }
+  void trim(int dev) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto &e : free[dev]) drv().release(e.second);
+    free[dev].clear();
+    bytes[dev] = 0;
+  }
+};
+
+inline ChunkPool &chunk_pool() {
+  static ChunkPool p;
+  return p;
+}
+
 // Slab store of one GGArray: a VA region per bucket class, slot s of class b
 // = bucket (s, b).  Physical memory is mapped per chunk (a gran-multiple
 // piece of a region) and refcounted by the live buckets overlapping it, so
@@ -191,8 +247,10 @@ struct Slab {
     Chunk &k = r.chunks[c];
     if (k.mapped) { if (!k.refs) cached -= r.chunk; return GG_OK; }
     const uint64_t t0 = now_ns();
-    CUmemAllocationProp prop = props();
-    CU_TRY(drv().create(&k.h, r.chunk, &prop, 0));
+    if (!chunk_pool().take(dev, r.chunk, &k.h)) {
+      CUmemAllocationProp prop = props();
+      CU_TRY(drv().create(&k.h, r.chunk, &prop, 0));
+    }
     const CUdeviceptr at = r.base + c * r.chunk;
     if (drv().map(at, r.chunk, 0, k.h, 0) != CUDA_SUCCESS) {
       drv().release(k.h);
@@ -323,12 +381,14 @@ struct Slab {
     go(small);
     for (auto &r : big) go(r);
   }
+  // the array is going away: unmap everything, keep physical chunks in the
+  // process pool while it has room (the caller synchronised the device)
   void destroy() {
     auto go = [&](Region &r) {
       for (size_t c = 0; c < r.chunks.size(); ++c)
         if (r.chunks[c].mapped) {
           drv().unmap(r.base + c * r.chunk, r.chunk);
-          drv().release(r.chunks[c].h);
+          if (!chunk_pool().give(dev, r.chunk, r.chunks[c].h)) drv().release(r.chunks[c].h);
         }
       if (r.base) drv().addr_free(r.base, r.va);
       r = Region();

@@ -474,9 +474,9 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
          o_ctl = take(S * 4), o_flag = take(T * 4), o_status = take(S * 4), o_ptr = take(T * 8),
          o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_am = take(S * 8),
          o_cb = take(max_buckets * 8), o_pm = take(S * 8);
-  cudaError_t e = cudaMalloc(&a->dmem, bytes);
+  cudaError_t e = cudaMallocAsync(&a->dmem, bytes, 0);   // driver mempool: no device-wide sync
   if (e != cudaSuccess) { a->slab.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
-  cudaMemset(a->dmem, 0, bytes);
+  cudaMemsetAsync(a->dmem, 0, bytes, 0);
   char *base = (char *)a->dmem;
   Tables &t = a->t;
   t.size = (uint64_t *)(base + o_size); t.cap = (uint64_t *)(base + o_cap);
@@ -507,7 +507,7 @@ int gg_destroy(gg_array *a) {
   cudaDeviceSynchronize();
   a->up.destroy();
   if (a->h_scratch) cudaFreeHost(a->h_scratch);
-  if (a->dmem) cudaFree(a->dmem);
+  if (a->dmem) cudaFreeAsync(a->dmem, 0), cudaStreamSynchronize(0);
   a->slab.destroy();
   delete a;
   return GG_OK;
@@ -1276,6 +1276,20 @@ int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
   for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
   o[0] = cap * a->esz; o[1] = a->slab.mapped; o[2] = a->live; o[3] = need * a->esz;
   o[4] = a->alloc_calls; o[5] = a->slab.cached;
+  return GG_OK;
+}
+
+int gg_pool_stats(int device, uint64_t *o) {
+  ChunkPool &p = chunk_pool();
+  std::lock_guard<std::mutex> g(p.mu);
+  if (device < 0 || device >= 64) return fail(GG_EVALUE, "bad device");
+  o[0] = p.bytes[device]; o[1] = p.free[device].size(); o[2] = p.hits; o[3] = p.misses; o[4] = p.cap();
+  return GG_OK;
+}
+
+int gg_pool_trim(int device) {
+  if (device < 0 || device >= 64) return fail(GG_EVALUE, "bad device");
+  chunk_pool().trim(device);
   return GG_OK;
 }
 

@@ -192,7 +192,14 @@ class GrowableArray:
     def _to_numpy(self, t) -> np.ndarray:
         import torch
         ti = t.view(getattr(torch, self._int_np.name))
-        return ti.cpu().numpy().view(self.dtype)
+        if ti.numel() <= 65536:
+            return ti.cpu().numpy().view(self.dtype)
+        # large results land in pinned memory (torch's caching host allocator):
+        # one DMA at full PCIe speed instead of a pageable staging copy
+        host = torch.empty(ti.numel(), dtype=ti.dtype, pin_memory=True)
+        host.copy_(ti, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return host.numpy().view(self.dtype)
 
     def _failure(self, s: int, code: int) -> BaseException:
         if code == L.GG_ECAPACITY:
