@@ -725,3 +725,17 @@ class GrowableArray:
     def __repr__(self) -> str:
         return (f"GrowableArray(shards={self._S}, committed={self.committed_size}, "
                 f"capacity={self.total_capacity}, device={self.device})")
+
+
+def pool_stats(device: int = 0) -> dict:
+    """The process-wide cache of physical slab chunks left by destroyed arrays
+    (reused by new arrays instead of fresh driver allocations)."""
+    o = np.zeros(5, np.uint64)
+    L.check(L.lib.gg_pool_stats(int(device), L.ptr(o)), "pool_stats")
+    return {"cached_bytes": int(o[0]), "chunks": int(o[1]), "hits": int(o[2]), "misses": int(o[3]),
+            "cap_bytes": int(o[4])}
+
+
+def pool_trim(device: int = 0) -> None:
+    """Return every cached chunk to the driver."""
+    L.check(L.lib.gg_pool_trim(int(device)), "pool_trim")

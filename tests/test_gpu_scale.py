@@ -277,3 +277,27 @@ def test_captured_schedule_replays_match_eager(gg, defer):
     idx = torch.arange(n0 << rounds, device="cuda")
     exp = ((idx // per) * (n0 // S) + idx % (n0 // S)).to(torch.int32)
     assert torch.equal(a.flatten_device(), exp)
+
+
+def test_chunk_pool_reuse_and_trim(gg):
+    """Destroyed arrays leave their physical chunks in the process pool; the
+    next array maps them (hits), contents are fresh writes; trim empties it.
+    Shrink releases never feed the pool."""
+    import torch
+    gg.pool_trim(0)
+    s0 = gg.pool_stats(0)
+    a = gg.GrowableArray.from_flat(torch.arange(1 << 20, dtype=torch.int32, device="cuda"), 64, 32)
+    a.shrink(0, release=True)
+    assert gg.pool_stats(0)["cached_bytes"] == 0            # shrink release -> driver, not pool
+    a.insert_csr(torch.arange(1 << 20, dtype=torch.int32, device="cuda"),
+                 np.minimum(np.arange(65, dtype=np.uint64) * np.uint64((1 << 20) // 64), 1 << 20))
+    mapped = a.memory_stats()["mapped_bytes"]
+    a.close()
+    st = gg.pool_stats(0)
+    assert 0 < st["cached_bytes"] <= mapped
+    b = gg.GrowableArray.from_flat(torch.arange(1 << 20, dtype=torch.int32, device="cuda") * 3, 64, 32)
+    assert gg.pool_stats(0)["hits"] > st["hits"]
+    assert torch.equal(b.flatten_device(), torch.arange(1 << 20, dtype=torch.int32, device="cuda") * 3)
+    b.close()
+    gg.pool_trim(0)
+    assert gg.pool_stats(0)["cached_bytes"] == 0 and s0["cap_bytes"] > 0
