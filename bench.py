@@ -375,6 +375,13 @@ def secondary(args, gg, torch, device, step, hbm):
                                  "frac": round(8 * n / ms / 1e6 / hbm, 4), "passes": p}
     ms = _time(torch, lambda: a.rw_add(1, passes=passes, mode="fused"))
     rw["ggarray_fused_100_in_registers"] = {"ms": round(ms, 4)}
+    # every +1 above landed exactly once per element: sample against the closed form
+    adds = (1 + passes) + (1 + max(1, passes // 10)) + passes
+    idx = torch.randint(0, n, (1 << 16,), device=device, dtype=torch.int64)
+    per = (N0 // S) << ROUNDS
+    exp = (idx // per) * (N0 // S) + idx % (N0 // S) + adds
+    rw["contents_ok_after_passes"] = bool(torch.equal(a.get_many(idx).to(torch.int64), exp))
+    a.rw_add(-adds)                                  # back to the schedule's contents
     flat = a.flatten_device()
     fl_ms = _time(torch, lambda: a.flatten_device(out=flat), reps=5)
     res["flatten"] = {"ms": round(fl_ms, 4), "gbs": round(8 * n / fl_ms / 1e6, 1),
