@@ -633,14 +633,25 @@ __device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &
   __shared__ uint64_t ws[32];
   const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
   const uint64_t *dir = fz.rmode == 0 ? t.offsets : t.prefix;
+  // pass 1: every count is read before the commit below rewrites the prefix
+  // (the duplicate's directory); with more shards than threads a later chunk
+  // would otherwise read prefix entries an earlier chunk already replaced
+  if (t.S > blockDim.x) {
+    for (uint32_t s = threadIdx.x; s < t.S; s += blockDim.x) t.count[s] = dir[s + 1] - dir[s];
+    __syncthreads();
+  }
   uint64_t carry = 0;
   for (uint32_t base = 0; base < t.S; base += blockDim.x) {
     const uint32_t s = base + threadIdx.x;
     const bool live = s < t.S;
-    uint64_t lo = 0, hi = 0, start = 0;
+    uint64_t c = 0, start = 0;
     unsigned long long pm = 0;
-    if (live) { lo = dir[s]; hi = dir[s + 1]; start = t.size[s]; pm = t.pmask[s]; }
-    const uint64_t c = hi - lo, nsz = start + c;
+    if (live) {
+      c = t.S > blockDim.x ? t.count[s] : dir[s + 1] - dir[s];
+      start = t.size[s];
+      pm = t.pmask[s];
+    }
+    const uint64_t nsz = start + c;
     unsigned long long want = 0;
     if (c) {
       t.size[s] = nsz;

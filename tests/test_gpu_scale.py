@@ -301,3 +301,52 @@ def test_chunk_pool_reuse_and_trim(gg):
     b.close()
     gg.pool_trim(0)
     assert gg.pool_stats(0)["cached_bytes"] == 0 and s0["cap_bytes"] > 0
+
+
+@pytest.mark.parametrize("S", [1025, 5000, 70000])
+def test_many_shards_ragged(gg, S):
+    """Shard counts past one CTA of metadata threads and past two levels of
+    the 32-ary directory search: ragged insert, duplicate, +1 (per shard and
+    global), flatten and capacities against a direct numpy construction."""
+    import torch
+    rng = np.random.default_rng(S)
+    fb = 4
+    counts = rng.integers(0, 40, S)
+    counts[rng.random(S) < 0.3] = 0
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    vals = rng.integers(-1000, 1000, int(off[-1])).astype(np.int32)
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    a.insert_csr(torch.from_numpy(vals).cuda(), off)
+    a.insert_duplicate()
+    a.rw_add(1)
+    a.rw_add(2, mode="global")
+    want = np.concatenate([np.concatenate([vals[off[s]:off[s + 1]]] * 2) for s in range(S)]) + 3
+    assert a.flatten().tobytes() == want.astype(np.int32).tobytes()
+    st = a.device_state()
+    sizes = 2 * counts
+    assert np.array_equal(st["sizes"], sizes)
+    assert np.array_equal(st["caps"], [O.capacity_of(O.min_buckets_for(int(n), fb), fb) for n in sizes])
+    assert int(st["prefix"][-1]) == int(sizes.sum())
+    g = torch.from_numpy(rng.integers(0, int(sizes.sum()), 4096)).cuda()
+    assert torch.equal(a.get_many(g).cpu(), torch.from_numpy(want[g.cpu().numpy()]))
+
+
+@pytest.mark.parametrize("S", [3000, 40000])
+def test_many_shards_uniform_doubling(gg, S):
+    """The uniform fast paths (grow, duplicate, deferred metadata fused into
+    the next grow) with more shards than one metadata CTA has threads."""
+    import torch
+    fb, per0, rounds = 8, 12, 5
+    n0 = S * per0
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    a.insert_csr(torch.arange(n0, dtype=torch.int32, device="cuda"),
+                 np.arange(S + 1, dtype=np.uint64) * np.uint64(per0))
+    for _ in range(rounds):
+        a.grow(2 * a.committed_size)
+        a.insert_duplicate()
+    per = per0 << rounds
+    st = a.device_state()
+    assert np.all(st["sizes"] == per) and int(st["prefix"][-1]) == S * per
+    assert np.all(st["caps"] == O.capacity_of(O.min_buckets_for(per, fb), fb))
+    g = torch.arange(S * per, device="cuda")
+    assert torch.equal(a.flatten_device(), ((g // per) * per0 + g % per0).to(torch.int32))
