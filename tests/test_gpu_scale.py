@@ -350,3 +350,27 @@ def test_many_shards_uniform_doubling(gg, S):
     assert np.all(st["caps"] == O.capacity_of(O.min_buckets_for(per, fb), fb))
     g = torch.arange(S * per, device="cuda")
     assert torch.equal(a.flatten_device(), ((g // per) * per0 + g % per0).to(torch.int32))
+
+
+@pytest.mark.parametrize("dtype,fb,S", [("int8", 1, 3), ("int64", 1, 5), ("uint16", 2, 130), ("float64", 64, 7)])
+def test_large_ragged_dtypes(gg, dtype, fb, S):
+    """Large ragged shards with 1/2/8-byte elements and tiny first buckets
+    (up to ~25 buckets per shard): insert, duplicate, +1 passes, flatten and
+    capacities against direct numpy construction."""
+    import torch
+    rng = np.random.default_rng(fb * 100 + S)
+    counts = rng.integers(1 << 18, 1 << 21, S)
+    counts[0] = 1
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    vals = rng.integers(0, 100, int(off[-1])).astype(dtype)
+    a = gg.GrowableArray(S, fb, dtype=dtype)
+    a.insert_csr(torch.from_numpy(vals).cuda(), off)
+    a.insert_duplicate()
+    a.rw_add(1)
+    a.rw_add(1, mode="global")
+    one = np.asarray(2, dtype=dtype)
+    want = np.concatenate([np.concatenate([vals[off[s]:off[s + 1]]] * 2) for s in range(S)])
+    want = (want + one).astype(dtype)
+    assert a.flatten().tobytes() == want.tobytes()
+    st = a.device_state()
+    assert np.array_equal(st["caps"], [O.capacity_of(O.min_buckets_for(2 * int(c), fb), fb) for c in counts])
