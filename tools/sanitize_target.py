@@ -1,0 +1,44 @@
+"""Small run of every kernel for compute-sanitizer (memcheck / racecheck /
+synccheck): ragged CSR insert, duplicate, r/w both modes, flatten,
+flatten_range, grow, shrink, lanes insert, device push_back (warp / block),
+gather / scatter, static baselines, many-shard metadata."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2209_00103_b200 as gg
+
+rng = np.random.default_rng(0)
+for S, fb, dt in [(37, 4, np.int32), (5, 1, np.int8), (1100, 8, np.int64)]:
+    counts = rng.integers(0, 300, S)
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    vals = torch.from_numpy(rng.integers(0, 50, int(off[-1])).astype(dt)).cuda()
+    a = gg.GrowableArray(S, fb, dtype=dt)
+    a.insert_csr(vals, off)
+    a.grow(3 * a.committed_size)
+    a.insert_duplicate()
+    a.rw_add(1)
+    a.rw_add(1, mode="global")
+    f = a.flatten_device()
+    r = a.flatten_range(3, max(3, a.committed_size - 7))
+    idx = torch.from_numpy(rng.integers(0, a.committed_size, 1000)).cuda()
+    g = a.get_many(idx)
+    a.set_many(idx, g)
+    a.shrink(np.maximum(a._host()["sizes"].astype(np.int64) // 3, 0))
+    lanes = 64
+    cnt = torch.randint(0, 3, (S * lanes,), dtype=torch.int32, device="cuda")
+    lv = torch.arange(S * lanes * 2, device="cuda").to(torch.from_numpy(np.zeros(1, dt)).dtype)
+    a.insert_lanes(lv, cnt, np.arange(S + 1, dtype=np.uint64) * lanes, 2)
+    m = min(5000, lv.numel())
+    for mode in ("warp", "block"):
+        pred = (torch.arange(m, device="cuda") % 3 == 0).to(torch.uint8)
+        a.push_if(lv[:m], pred, mode=mode)
+    a.close()
+st = gg.StaticArray(1 << 16, dtype=np.int32)
+for algo in ("atomic", "warp", "block"):
+    st._count = 0
+    st._d_count.fill_(0)
+    st.insert_batch(torch.arange(1000, dtype=torch.int32, device="cuda"), algo=algo)
+torch.cuda.synchronize()
+print("sanitize target done")
