@@ -654,7 +654,10 @@ __device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &
     const uint64_t nsz = start + c;
     unsigned long long want = 0;
     if (c) {
-      t.size[s] = nsz;
+      // the batch's reservation: ONE atomicAdd on the LFVector size
+      // (insert_index.py:118-122), fire-and-forget -- the start was read above
+      // and this launch is the shard's only writer
+      atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
       atomicAdd((unsigned long long *)&t.ops[s], 1ull);
       t.start[s] = start;
       uint32_t b0, b1; uint64_t o;
