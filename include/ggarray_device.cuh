@@ -10,6 +10,7 @@
  *
  *   gg::gg_device_view v = ...;          // from gg_device_view_get() (host)
  *   gg::warp_push_back(v, shard, pred, value);        // one atomicAdd per warp
+ *   gg::warp_push_back_n<T, K>(v, shard, count, vals); // per-lane counts, one per warp
  *   gg::block_push_back<BLOCK>(v, shard, count, vals, scratch);  // one per block
  *
  * Device code cannot map memory, so the host backs the slots a launch may
@@ -185,6 +186,48 @@ __device__ inline uint64_t warp_push_back(const gg_device_view &t, uint32_t s, b
   char *base = bucket_acquire(t, s, b);
   if (base) store_cg(reinterpret_cast<T *>(base) + o, value);
   return start + rank;
+}
+
+// Paper Alg. 1, warp flavour with per-lane counts: lane j appends vals[0..
+// counts_j) (counts_j <= K); a warp shuffle scan gives every lane its offset,
+// lane 0 reserves the warp total with ONE atomicAdd and allocates the buckets,
+// values land in lane order.  Amortises the reservation over up to 32*K
+// values.  Must be called by all 32 lanes; s warp-uniform.
+template <typename T, int K>
+__device__ inline uint64_t warp_push_back_n(const gg_device_view &t, uint32_t s, uint32_t count,
+                                            const T (&vals)[K]) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t x = count;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, x, 31), excl = x - count;
+  if (!total) return ~0ull;
+  unsigned long long start = 0;
+  int ok = 1;
+  if (lane == 0) {
+    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)total);
+    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+    ok = ensure_buckets(t, s, start, total);
+  }
+  start = __shfl_sync(0xffffffffu, start, 0);
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (!ok) return ~0ull;
+  uint32_t cur_b = ~0u;
+  char *base = nullptr;
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    if ((uint32_t)e < count) {
+      uint32_t b;
+      uint64_t o;
+      locate(start + excl + e, t.log2fb, b, o);
+      if (b != cur_b) { base = bucket_acquire(t, s, b); cur_b = b; }
+      if (base) store_cg(reinterpret_cast<T *>(base) + o, vals[e]);
+    }
+  }
+  return start + excl;
 }
 
 // Paper Alg. 1, block flavour: thread j contributes vals[0..count_j); a

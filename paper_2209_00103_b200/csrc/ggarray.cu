@@ -416,18 +416,27 @@ namespace gg {
 // Example user kernel of the device API (paper Alg. 1): block b appends the
 // elements i of its slice with pred[i] != 0 to shard b % S, warp- or
 // block-aggregated.
-template <int ESZ, int BLOCK>
+// Each thread gathers the candidates of K consecutive rounds of its block's
+// slices (coalesced loads) and appends its kept values with one warp- or
+// block-aggregated push_back_n, so one reservation covers up to 32*K (warp)
+// or BLOCK*K (block) values.
+template <int ESZ, int BLOCK, int K>
 __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char *vals,
                                                    const uint8_t *pred, uint64_t n, int block_mode) {
   typedef typename ElemT<ESZ>::T E;
   __shared__ unsigned long long scratch[34];
   const uint32_t s = blockIdx.x % t.S;
-  for (uint64_t base = (uint64_t)blockIdx.x * BLOCK; base < n; base += (uint64_t)gridDim.x * BLOCK) {
-    const uint64_t i = base + threadIdx.x;
-    const bool p = i < n && pred[i];
-    const E v = p ? reinterpret_cast<const E *>(vals)[i] : E(0);
-    if (block_mode) block_push_back<BLOCK, E>(t, s, p ? 1u : 0u, &v, scratch);
-    else warp_push_back<E>(t, s, p, v);
+  const uint64_t round = (uint64_t)gridDim.x * BLOCK;
+  for (uint64_t r0 = 0; (uint64_t)blockIdx.x * BLOCK + r0 * round < n; r0 += K) {
+    E kept[K];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint64_t i = (uint64_t)blockIdx.x * BLOCK + (r0 + j) * round + threadIdx.x;
+      if (i < n && pred[i]) kept[cnt++] = reinterpret_cast<const E *>(vals)[i];
+    }
+    if (block_mode) block_push_back<BLOCK, E>(t, s, cnt, kept, scratch);
+    else warp_push_back_n<E, K>(t, s, cnt, kept);
   }
 }
 
@@ -1135,7 +1144,12 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   cudaStream_t st = S_(stream);
   if (n == 0) return GG_OK;
   const uint32_t B = 256;
-  if (!grid) grid = (uint32_t)std::min<uint64_t>((n + B - 1) / B, (uint64_t)a->S * 64);
+  // default grid: ~8 resident CTAs per SM (each CTA then loops over many
+  // rounds and its push_back_n calls reserve up to 8 rounds at once), at
+  // least one CTA per shard
+  if (!grid)
+    grid = (uint32_t)std::max<uint64_t>(
+        a->S, std::min<uint64_t>((n + B * 8 - 1) / (B * 8), (uint64_t)sm_count(a->dev) * 8));
   // worst case: every candidate of shard s appended
   std::vector<uint64_t> maxsz(a->S, 0);
   {
@@ -1152,10 +1166,10 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   int rc = gg_device_view_get(a, maxsz.data(), &v, sizeof v);
   if (rc) return rc;
   switch (a->esz) {
-    case 1: { k_push_if<1, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_push_if<2, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_push_if<4, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 8: { k_push_if<8, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 1: { k_push_if<1, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_push_if<2, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_push_if<4, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_push_if<8, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
   }
   CUDA_TRY(cudaGetLastError());
   return gg_device_view_sync(a, h_status, stream);
