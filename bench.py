@@ -165,7 +165,18 @@ def run_device(args, rank, world, local_rank):
     peaks, peaks_kind = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
 
+    gg.pool_trim(local_rank)
     step = Step(gg, torch, device)
+    # the very first step on a fresh array also maps its 8 GiB of slab chunks
+    # (driver work the steady-state steps reuse): reported, not in `value`
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    step.run(False)
+    torch.cuda.synchronize()
+    cold = {"ms": round((time.perf_counter() - c0) * 1e3, 3),
+            "map_ms": round(step.arr.slab_stats()["map_ns"] / 1e6, 3),
+            "chunks_mapped": step.arr.slab_stats()["chunks_mapped"],
+            "note": "first step of a fresh array, wall clock, incl. cuMemCreate/Map of its slab chunks"}
     for _ in range(args.warmup):
         step.run(False)
     torch.cuda.synchronize()
@@ -258,6 +269,7 @@ def run_device(args, rank, world, local_rank):
                   "eager: the same K steps issued op by op from Python",
         "eager": {"value": round(eager_value, 3), "ms_per_step": round(eager_ms / args.steps, 4),
                   "host_enqueue_ms_per_step": round(host_ms / args.steps, 4)},
+        "cold_first_step": cold,
     }
     if dist:
         out["gather_flatten"] = gather_leg(args, torch, device, step, dist, world)
