@@ -151,7 +151,7 @@ inline ChunkPool &chunk_pool() {
 struct Slab {
   struct Chunk { uint32_t refs = 0; bool mapped = false; CUmemGenericAllocationHandle h = 0; };
   struct Region { CUdeviceptr base = 0; size_t va = 0, chunk = 0; std::vector<Chunk> chunks; };
-  static constexpr size_t kChunk = size_t(64) << 20;   // mapping unit of large regions
+  static constexpr size_t kChunk = size_t(1) << 30;    // largest mapping unit of a region
   int dev = 0;
   size_t gran = 0;
   uint32_t S = 0, MB = 0;
@@ -206,13 +206,16 @@ struct Slab {
     return GG_OK;
   }
   // mapping unit of class b's region: a power of two >= one granule and >=
-  // one bucket, about 1/16 of the region (so a partly live top class -- an
-  // uneven split -- strands at most one chunk), at most kChunk otherwise
+  // one bucket, 1/8..1/16 of the region, at most kChunk.  Each cuMemCreate /
+  // Map / SetAccess call costs ~1.5-2 ms of driver time almost regardless of
+  // size (tools/vmm_fresh_probe.py: 8 GiB as 128 x 64 MiB 250-1450 ms, as
+  // 8 x 1 GiB 36 ms), so chunks are large; a partly live top class (an
+  // uneven split) strands at most one chunk, <= 1/8 of its region.
   uint64_t chunk_for(uint32_t b) const {
     if (bytes[b] >= kChunk) return bytes[b];
     const uint64_t R = S * bytes[b];
     uint64_t c = gran;
-    while (c < kChunk && c * 32 <= R) c <<= 1;
+    while (c < kChunk && c * 16 <= R) c <<= 1;
     return std::max<uint64_t>(c, bytes[b]);
   }
   Region &region(uint32_t b) { return small_off[b] != ~uint64_t(0) ? small : big[b]; }
