@@ -386,8 +386,13 @@ class GrowableArray:
 
     # ------------------------------------------------------------ traversal
     def for_each_shard(self, op: Callable, workers: int | None = 1) -> None:
-        """Apply ``op`` to writable device views (torch tensors) of every committed
-        segment, in ascending order within each shard; failures are aggregated."""
+        """Apply ``op`` to writable device views of every committed segment, in
+        ascending order within each shard; failures are aggregated.  The views
+        are :class:`~paper_2209_00103_b200.views.DeviceView` wrappers of torch
+        CUDA tensors aliasing the buckets: numpy ufuncs with ``out=`` (the
+        reference's ``np.add(v, 1, out=v)``) and torch methods (``v.add_(1)``)
+        both run on the device."""
+        from .views import DeviceView
         failures = {}
         for s, sh in enumerate(self.shards):
             n = self.committed_length(s)
@@ -395,7 +400,7 @@ class GrowableArray:
                 continue
             try:
                 for view in sh.iter_segments(n):
-                    op(view)
+                    op(DeviceView(view))
             except BaseException as exc:  # noqa: BLE001 -- reference aggregates per shard
                 failures[s] = exc
         if failures:

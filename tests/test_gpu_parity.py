@@ -207,3 +207,36 @@ def test_phased_insert_shrink_vs_oracle_model(gg):
         ms = a.memory_stats()
         assert ms["capacity_bytes"] <= 2 * ms["needed_bytes"] + S * fb * 4
     assert a.flatten().tobytes() == o.flatten().tobytes()
+
+
+def test_reference_quickstart_verbatim(gg):
+    """pkg/README.md's library quickstart with only the import swapped: numpy
+    ufunc ops in for_each_shard run on the device views."""
+    from paper_2209_00103_b200 import GrowableArray, split_batches
+
+    arr = GrowableArray(shards=32, first_bucket_size=32, dtype=np.int32)
+    arr.insert_parallel(split_batches(np.arange(10_000, dtype=np.int32), 32))
+
+    assert arr.get_global(1234) == 1234
+    arr.for_each_shard(lambda view: np.add(view, 1, out=view), workers=4)
+
+    flat = arr.flatten()
+    again = GrowableArray.from_flat(flat, shards=32)
+    assert np.array_equal(flat, np.arange(10_000, dtype=np.int32) + 1)
+    assert again.flatten().tobytes() == flat.tobytes()
+
+
+@pytest.mark.parametrize("dtype", ["int8", "int32", "float16", "float64"])
+def test_for_each_shard_numpy_ops_match_oracle(gg, dtype):
+    rng = np.random.default_rng(3)
+    S, fb = 9, 4
+    batches = [(rng.integers(0, 100, int(k))).astype(dtype) for k in rng.integers(0, 300, S)]
+    a = gg.GrowableArray(S, fb, dtype=dtype)
+    o = O.OracleGGArray(S, fb, dtype=dtype)
+    a.insert_parallel(batches); o.insert_parallel(batches)
+    c = np.asarray(3).astype(dtype)
+    a.for_each_shard(lambda v: np.add(v, c, out=v, casting="unsafe"))
+    a.for_each_shard(lambda v: np.multiply(v, 2, out=v, casting="unsafe"))
+    a.for_each_shard(lambda v: v.sub_(1))                 # torch methods still work
+    want = ((o.flatten() + c).astype(dtype) * np.asarray(2, dtype)).astype(dtype) - np.asarray(1, dtype)
+    assert a.flatten().tobytes() == want.astype(dtype).tobytes()
