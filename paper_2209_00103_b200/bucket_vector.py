@@ -115,7 +115,8 @@ class BucketTable:
         a, s = self._sh._arr, self._sh._s
         ptrs = a._bucket_ptrs()[s]
         fb = self.first_bucket_size
-        return [_view(a, int(p), fb << b) if p else None for b, p in enumerate(ptrs)]
+        from .views import DeviceView
+        return [DeviceView(_view(a, int(p), fb << b)) if p else None for b, p in enumerate(ptrs)]
 
 
 class ShardVector:
@@ -224,7 +225,15 @@ class ShardVector:
         self._arr._set(self._s, i, value)
 
     def iter_segments(self, stop=None, start: int = 0):
-        """Writable device views of local [start, stop), one per touched bucket."""
+        """Writable device views (:class:`~paper_2209_00103_b200.views.DeviceView`,
+        numpy-ufunc capable) of local [start, stop), one per touched bucket
+        (bucket_vector.py:279-295)."""
+        from .views import DeviceView
+        for t in self._segment_tensors(stop, start):
+            yield DeviceView(t)
+
+    def _segment_tensors(self, stop=None, start: int = 0):
+        """Raw torch CUDA tensors aliasing the buckets of local [start, stop)."""
         a = self._arr
         stop = self.size if stop is None else stop
         fb = self.first_bucket_size
@@ -241,7 +250,7 @@ class ShardVector:
 
     def to_numpy(self, stop=None) -> np.ndarray:
         import torch
-        segs = list(self.iter_segments(stop))
+        segs = list(self._segment_tensors(stop))
         if not segs:
             return np.empty(0, self.dtype)
         return self._arr._to_numpy(torch.cat(segs))

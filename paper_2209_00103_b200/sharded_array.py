@@ -399,7 +399,7 @@ class GrowableArray:
             if not n:
                 continue
             try:
-                for view in sh.iter_segments(n):
+                for view in sh._segment_tensors(n):
                     op(DeviceView(view))
             except BaseException as exc:  # noqa: BLE001 -- reference aggregates per shard
                 failures[s] = exc
