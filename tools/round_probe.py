@@ -35,12 +35,9 @@ st = torch.cuda.Stream()
 
 def graph_time(fn, reps=20):
     with torch.cuda.stream(st):
-        with a.capture_mode():
-            fn()
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=st):
-                fn()
+        fn()
+        torch.cuda.synchronize()
+        g = a.capture(fn, stream=st)
     g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
