@@ -56,7 +56,7 @@ typedef struct gg_array gg_array;
  * bucket an operation is about to allocate; nonzero = allocation failure.
  * Replaces the `allocator` callable of ShardVector (bucket_vector.py:130-134,
  * 194-201) for counting and failure injection; storage always comes from
- * the device arena. */
+ * the device slabs. */
 typedef int (*gg_alloc_hook)(void *ctx, uint32_t shard, uint32_t bucket, uint64_t elems);
 
 const char *gg_last_error(void);
@@ -105,7 +105,7 @@ int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream);
  * values d_values[j*values_per_lane ...] (values_per_lane = 1, counts in
  * {0,1} is the paper's predicated push_back).  Shard s's batch lands in lane
  * order.  Pass 1 sums the counts per shard (CTA per shard) so the host maps
- * the arena exactly; pass 2 reserves with ONE atomicAdd per shard, allocates
+ * the slabs exactly; pass 2 reserves with ONE atomicAdd per shard, allocates
  * the buckets, block-scans the counts and scatters. */
 int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
                     const uint64_t *h_lane_offsets, uint64_t values_per_lane,

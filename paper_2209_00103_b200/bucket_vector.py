@@ -1,10 +1,11 @@
 """LFVector (shard) layer of the drop-in API: layout arithmetic and the
 ``ShardVector`` / ``BucketTable`` views (bucket_vector.py:34-308 in the reference).
 
-Storage lives in the device arena of a ``gg_array`` handle; a ShardVector is a
+Storage lives in the device slabs of a ``gg_array`` handle; a ShardVector is a
 (handle, shard) pair.  A standalone ``ShardVector(...)`` owns a one-shard
 handle.  Bucket views handed out by ``iter_segments`` / ``table.buckets`` are
-torch CUDA tensors aliasing the arena (valid until the array is destroyed).
+device views aliasing the slabs (valid until the array is destroyed or the
+bucket is released by a shrink).
 """
 
 from __future__ import annotations
@@ -52,7 +53,7 @@ def min_buckets_for(n: int, first_bucket_size: int) -> int:
 
 
 class _CudaView:
-    """__cuda_array_interface__ shim so torch can alias arena memory."""
+    """__cuda_array_interface__ shim so torch can alias slab memory."""
 
     def __init__(self, addr: int, n: int, dtype: np.dtype):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": dtype.str,

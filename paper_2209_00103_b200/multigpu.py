@@ -1,5 +1,5 @@
 """GGArray across GPUs: one process per GPU, each owning a
-contiguous range of LFVectors in its own device arena.
+contiguous range of LFVectors in its own device slabs.
 
 Insert / grow / shrink / r/w are purely local (no communication).  The only
 exchange steps are

@@ -58,7 +58,7 @@ def _torch_dtype(dt: np.dtype):
 
 
 class GrowableArray:
-    """S LFVectors in one device arena plus the committed prefix directory."""
+    """S LFVectors in per-class device slabs plus the committed prefix directory."""
 
     def __init__(self, shards: int = DEFAULT_SHARDS,
                  first_bucket_size: int = DEFAULT_FIRST_BUCKET_SIZE, dtype=np.int64,
@@ -205,7 +205,7 @@ class GrowableArray:
         if code == L.GG_ECAPACITY:
             return CapacityError(f"shard {s}: range needs a bucket beyond the table of {self._mb}")
         if code == L.GG_ENOMEM:
-            return self._hook_exc.pop(s, None) or MemoryError(f"shard {s}: bucket arena exhausted")
+            return self._hook_exc.pop(s, None) or MemoryError(f"shard {s}: no device memory for a bucket")
         return RuntimeError(f"shard {s}: status {code}")
 
     def _insert_device(self, vals, offsets: np.ndarray, starts: np.ndarray | None = None,
@@ -516,7 +516,7 @@ class GrowableArray:
         rc = L.lib.gg_device_view_sync(self._h, L.ptr(status, C.c_int32), self._stream())
         self._dirty()
         if rc == L.GG_EPARTIAL:
-            failures = {int(s): MemoryError(f"shard {s}: bucket arena exhausted in a device append")
+            failures = {int(s): MemoryError(f"shard {s}: no backed bucket slot for a device append")
                         for s in np.flatnonzero(status)}
             raise ShardInsertError(failures, [])
         L.check(rc, "device_sync")
@@ -538,7 +538,7 @@ class GrowableArray:
                               self._stream())
         self._dirty()
         if rc == L.GG_EPARTIAL:
-            failures = {int(s): MemoryError(f"shard {s}: bucket arena exhausted in a device append")
+            failures = {int(s): MemoryError(f"shard {s}: no backed bucket slot for a device append")
                         for s in np.flatnonzero(status)}
             raise ShardInsertError(failures, [])
         L.check(rc, "push_if")
