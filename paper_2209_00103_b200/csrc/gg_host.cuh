@@ -259,20 +259,45 @@ struct Slab {
       drv().release(k.h);
       return fail(GG_ENOMEM, "cuMemMap failed");
     }
-    CUmemAccessDesc acc = {};
-    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    acc.location.id = dev;
-    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    if (drv().set_access(at, r.chunk, &acc, 1) != CUDA_SUCCESS) {
-      drv().unmap(at, r.chunk);
-      drv().release(k.h);
-      return fail(GG_ENOMEM, "cuMemSetAccess failed");
+    // access rights are granted in finalize_access(), one cuMemSetAccess per
+    // contiguous run of chunks mapped by the same operation (the call costs
+    // about as much as the mapping itself)
+    pending.push_back({&r, c});
+    static const bool batch = [] { const char *e = getenv("GG_BATCH_ACCESS"); return !e || e[0] != '0'; }();
+    if (!batch) {
+      int rc = finalize_access();
+      if (rc) return rc;
     }
     k.mapped = true;
     mapped += r.chunk;
     n_map += 1;
     ns_map += now_ns() - t0;
     return GG_OK;
+  }
+  std::vector<std::pair<Region *, size_t>> pending;   // mapped, access not granted yet
+  // grant read/write access to every chunk mapped since the last call; must
+  // run before a kernel can touch them (push_cbase calls it)
+  int finalize_access() {
+    if (pending.empty()) return GG_OK;
+    const uint64_t t0 = now_ns();
+    std::sort(pending.begin(), pending.end());
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    int rc = GG_OK;
+    for (size_t i = 0; i < pending.size();) {
+      Region *r = pending[i].first;
+      size_t j = i + 1;
+      while (j < pending.size() && pending[j].first == r && pending[j].second == pending[j - 1].second + 1) ++j;
+      const CUdeviceptr at = r->base + pending[i].second * r->chunk;
+      if (drv().set_access(at, (j - i) * r->chunk, &acc, 1) != CUDA_SUCCESS && !rc)
+        rc = fail(GG_ENOMEM, "cuMemSetAccess failed");
+      i = j;
+    }
+    pending.clear();
+    ns_map += now_ns() - t0;
+    return rc;
   }
   void unmap_chunk(Region &r, size_t c) {
     Chunk &k = r.chunks[c];
@@ -366,6 +391,7 @@ struct Slab {
   // unmap chunks without live buckets, largest class first, until at most
   // `keep` bytes stay mapped (caller synchronised the device)
   void trim_to(uint64_t keep) {
+    finalize_access();
     for (int b = (int)MB - 1; b >= 0 && mapped > keep && cached; --b) {
       if (small_off[b] != ~uint64_t(0)) continue;
       Region &r = big[b];
@@ -377,6 +403,7 @@ struct Slab {
   }
   // unmap every chunk without live buckets (caller synchronised the device)
   void trim() {
+    finalize_access();
     auto go = [&](Region &r) {
       for (size_t c = 0; c < r.chunks.size(); ++c)
         if (r.chunks[c].mapped && r.chunks[c].refs == 0) unmap_chunk(r, c);
@@ -387,6 +414,7 @@ struct Slab {
   // the array is going away: unmap everything, keep physical chunks in the
   // process pool while it has room (the caller synchronised the device)
   void destroy() {
+    pending.clear();
     auto go = [&](Region &r) {
       for (size_t c = 0; c < r.chunks.size(); ++c)
         if (r.chunks[c].mapped) {

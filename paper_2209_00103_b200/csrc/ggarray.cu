@@ -159,6 +159,8 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
 
 // class bases travel to the device when a new class region was reserved
 int push_cbase(gg_array *a, cudaStream_t st) {
+  int arc = a->slab.finalize_access();          // chunks mapped by this operation
+  if (arc) return arc;
   if (!a->cbase_dirty) return GG_OK;
   std::vector<uint64_t> cb(a->MB);
   for (uint32_t b = 0; b < a->MB; ++b) cb[b] = a->slab.class_base(b);

@@ -255,7 +255,9 @@ class GrowableArray:
             counts = [t.numel() for t in ts]
             vals = torch.cat(ts) if ts else torch.empty(0, dtype=self._torch_dtype, device=self.device)
         else:
-            arrs = [np.asarray(b.cpu() if isinstance(b, torch.Tensor) else b, dtype=self.dtype).reshape(-1)
+            dt = self.dtype
+            arrs = [b if (type(b) is np.ndarray and b.dtype == dt and b.ndim == 1) else
+                    np.asarray(b.cpu() if isinstance(b, torch.Tensor) else b, dtype=dt).reshape(-1)
                     for b in batches]
             counts = [len(a) for a in arrs]
             total = int(sum(counts))
