@@ -459,7 +459,54 @@ def secondary(args, gg, torch, device, step, hbm):
     res["baselines_last_doubling_2p29"] = base
     del src
     torch.cuda.empty_cache()
+    res["baselines_full_schedule"] = full_schedule_baselines(gg, torch, device, step, args)
     return res
+
+
+def full_schedule_baselines(gg, torch, device, step, args):
+    """The whole config-2 schedule (2^20 -> 2^30 by doubling: grow, then append
+    a copy of the current contents) on the static array (capacity 2^30
+    allocated up front), the host-resized doubling array and the memMap
+    array, block-scan insertion (the baselines' fastest), CUDA events over
+    the 10 rounds; next to the GGArray's eager step (same schedule + reset)."""
+    out = {}
+    n0, final = N0, N0 << ROUNDS
+
+    def schedule(arr, grow):
+        n = n0
+        e0, e1 = _events(torch)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(ROUNDS):
+            grow(arr, 2 * n)
+            arr.insert_batch(arr.view()[:n], algo="block")
+            n *= 2
+        e1.record()
+        torch.cuda.synchronize()
+        assert arr.size == final
+        return e0.elapsed_time(e1)
+
+    src = torch.arange(n0, dtype=torch.int32, device=device)
+    for name, make, grow in [
+            ("static_block", lambda: gg.StaticArray(final, dtype=np.int32, device=device), lambda a, m: None),
+            ("doubling_block", lambda: gg.DoublingArray(n0, dtype=np.int32, device=device), lambda a, m: a.resize(m)),
+            ("memmap_block", lambda: gg.ChunkTableArray(dtype=np.int32, device=device), lambda a, m: a.resize(m))]:
+        try:
+            ts = []
+            for _ in range(2):
+                a = make()
+                grow(a, n0)
+                a.insert_batch(src, algo="block")
+                ts.append(schedule(a, grow))
+                del a
+                torch.cuda.empty_cache()
+            out[name] = {"ms": round(min(ts), 3), "gelem_s": round((final - n0) / min(ts) / 1e6, 2)}
+        except Exception as exc:
+            out[name] = {"error": repr(exc)[:200]}
+    ins = (sum(step.dup_ms) + sum(step.grow_ms)) / args.steps
+    out["ggarray512_eager"] = {"ms": round(ins, 3), "gelem_s": round((final - n0) / ins / 1e6, 2),
+                               "note": "grow + duplicate-insert phases of the eager steps (events)"}
+    return out
 
 
 def phased_leg(args, gg, torch, device):
