@@ -137,6 +137,21 @@ class DistributedGrowableArray:
         r = int(np.searchsorted(np.asarray(p), g, side="right")) - 1
         return r, g - p[r]
 
+    def get_global(self, g: int, prefix=None):
+        """Element at global index g (collective: every rank gets the value;
+        the owner reads it with its local get_global)."""
+        r, loc = self.locate_global(g, prefix)
+        box = [self.local.get_global(loc) if self.rank == r else None]
+        self.dist.broadcast_object_list(box, src=r, group=self.group)
+        return box[0]
+
+    def set_global(self, g: int, value, prefix=None) -> None:
+        """Write the element at global index g (collective; only the owner writes)."""
+        r, loc = self.locate_global(g, prefix)
+        if self.rank == r:
+            self.local.set_global(loc, value)
+        self.dist.barrier(group=self.group)
+
     # ---- flatten / gather
     def _local_flat(self):
         import torch

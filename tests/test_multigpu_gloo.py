@@ -45,7 +45,12 @@ def _worker(rank, world, port, q):
         flat = d.flatten_global(root=0)
         allg = d.allgather_flat().numpy()
         loc = d.locate_global(pre[-1] - 1, pre)
-        q.put((rank, pre, None if flat is None else flat.numpy(), allg, loc))
+        probes = [0, pre[1], pre[-1] - 1] if pre[-1] else []
+        got = [int(d.get_global(g, pre)) for g in probes]
+        if probes:
+            d.set_global(probes[-1], -7, pre)
+            got.append(int(d.get_global(probes[-1], pre)))
+        q.put((rank, pre, None if flat is None else flat.numpy(), allg, loc, got))
     finally:
         dist.destroy_process_group()
 
@@ -79,8 +84,8 @@ def test_two_rank_directory_and_gather():
         p.start()
     res = {}
     for _ in range(2):
-        rank, pre, flat, allg, loc = q.get(timeout=120)
-        res[rank] = (pre, flat, allg, loc)
+        rank, pre, flat, allg, loc, got = q.get(timeout=120)
+        res[rank] = (pre, flat, allg, loc, got)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -90,3 +95,5 @@ def test_two_rank_directory_and_gather():
     assert res[1][1] is None
     assert np.array_equal(res[0][2], want) and np.array_equal(res[1][2], want)
     assert res[0][3] == (1, want_pre[2] - want_pre[1] - 1)
+    probes = [int(want[0]), int(want[want_pre[1]]), int(want[-1]), -7]      # distributed get/set_global
+    assert res[0][4] == res[1][4] == probes
