@@ -183,8 +183,16 @@ int gg_capture_mode(gg_array *a, int32_t on);
 /* on = 2: as 1, and the deferred metadata pass (gg_set_defer) stays enabled
  * under capture -- the caller must gg_flush() before the capture ends (the
  * Python GrowableArray.capture helper does). */
-/* launch a deferred metadata pass now, if one is pending (stream-ordered) */
+/* launch a deferred metadata pass / grow now, if one is pending (stream-ordered) */
 int gg_flush(gg_array *a);
+/* end of a capture-mode-2 sequence, called INSIDE the capture: flushes what
+ * is deferred and restores the size/prefix buffer parity the capture began
+ * with, so the graph can be replayed. */
+int gg_capture_end(gg_array *a, void *stream);
+/* Metadata pass inside the planned walk (default on): one launch per append,
+ * double-buffered size / prefix, and uniform grows deferred into the next
+ * append.  Process-wide; for A/B measurements. */
+int gg_set_fuse(int32_t on);
 int gg_capture_release(gg_array *a);
 /* Tuning of the streaming kernels (sweeps): unroll U in {1,2,4,8} = 16 B
  * vectors per thread per tile (tile = 256 threads x U vectors); -1 = the

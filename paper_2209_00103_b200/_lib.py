@@ -76,6 +76,8 @@ _SIGS = {
     "gg_info": ([P, PU32], C.c_int),
     "gg_capture_mode": ([P, I32], C.c_int),
     "gg_flush": ([P], C.c_int),
+    "gg_capture_end": ([P, P], C.c_int),
+    "gg_set_fuse": ([C.c_int32], C.c_int),
     "gg_set_tuning": ([I32, I32, U32, U32], C.c_int),
     "gg_set_pdl": ([C.c_int32], C.c_int),
     "gg_set_defer": ([C.c_int32], C.c_int),
@@ -155,3 +157,5 @@ if os.environ.get("GG_PDL") == "0":        # A/B switch for programmatic depende
     lib.gg_set_pdl(0)
 if os.environ.get("GG_DEFER") == "0":      # A/B switch for the deferred metadata pass
     lib.gg_set_defer(0)
+if os.environ.get("GG_FUSE_META") == "0":  # A/B switch for the metadata CTA inside the planned walk
+    lib.gg_set_fuse(0)

@@ -623,7 +623,17 @@ __device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, c
 // destinations are slot arithmetic from the unchanged size[s]; k_planned_meta
 // applies the metadata right after.  (A last-CTA epilogue in the walk itself
 // costs more: the completion atomic lengthens every CTA's life.)
-struct Fuse { int rmode; int commit; uint64_t g0 = 0; };   // g0: first work index (ranges)
+struct Fuse {
+  int rmode;
+  int commit;
+  uint64_t g0 = 0;                 // first work index (ranges)
+  // metadata CTA inside the planned walk (double-buffered size / prefix):
+  // the walk's copy CTAs read the current buffers, the last CTA writes the
+  // next ones (and publishes the buckets of a deferred uniform grow_k)
+  uint64_t *size_next = nullptr;
+  uint64_t *prefix_next = nullptr;
+  uint32_t grow_k = 0;
+};
 
 // metadata of a planned append, run by one CTA after every tile is copied.
 // Latency shaped: all loads (directory pair, size, pmask) issued up front,
@@ -677,6 +687,66 @@ __device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &
   if (fz.commit && threadIdx.x == 0) t.prefix[0] = 0;
 }
 
+// Metadata of a planned append run by the walk's extra CTA, concurrently with
+// the copy CTAs: everything the copy reads (size, directory) is read from the
+// current buffers and written to the next ones; nothing else it writes is
+// read by the copy (addresses are slot arithmetic).  Also publishes the
+// buckets of a deferred uniform grow (grow_k).
+__device__ void planned_metadata_db(const Tables &t, char *const *scb, const Fuse &fz) {
+  __shared__ uint64_t ws[32];
+  const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+  const uint64_t *dir = fz.rmode == 0 ? t.offsets : t.prefix;
+  const unsigned long long gmask = fz.grow_k >= 64 ? ~0ull : ((1ull << fz.grow_k) - 1ull);
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+    const uint32_t s = base + threadIdx.x;
+    const bool live = s < t.S;
+    uint64_t c = 0, start = 0, pre = 0;
+    unsigned long long pm = 0;
+    if (live) {
+      c = dir[s + 1] - dir[s];
+      start = t.size[s];
+      pm = t.pmask[s];
+      if (!fz.commit) pre = t.prefix[s + 1];
+    }
+    const uint64_t nsz = start + c;
+    unsigned long long want = gmask & ~pm;
+    if (c) {
+      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+      t.start[s] = start;
+      uint32_t b0, b1; uint64_t o;
+      locate(start, t.log2fb, b0, o);
+      locate(nsz - 1, t.log2fb, b1, o);
+      want |= (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~pm;
+    }
+    if (live) {
+      t.count[s] = c;
+      fz.size_next[s] = nsz;            // the batch's reservation: one update per LFVector
+    }
+    publish_buckets(t, scb, live ? s : 0u, pm, live ? want : 0ull, lg0);
+    if (fz.commit) {
+      uint64_t tot;
+      const uint64_t ex = block_exclusive_scan(live ? nsz : 0, &tot, ws);
+      if (live) fz.prefix_next[s + 1] = carry + ex + nsz;
+      carry += tot;
+    } else if (live) {
+      fz.prefix_next[s + 1] = pre;
+    }
+  }
+  if (threadIdx.x == 0) fz.prefix_next[0] = 0;
+}
+
+// copy the current size / prefix buffers into the other pair (restores the
+// buffer parity at the end of a captured sequence)
+__global__ void k_copy_db(uint64_t *size_dst, const uint64_t *size_src, uint64_t *pre_dst,
+                          const uint64_t *pre_src, uint32_t S) {
+  pdl_begin();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= S; i += gridDim.x * blockDim.x) {
+    if (i < S) size_dst[i] = size_src[i];
+    pre_dst[i] = pre_src[i];
+  }
+}
+
 // The tile walker: ONE tile per CTA (a non-persistent grid streams ~15%
 // faster than a persistent grid-stride loop on B200, tools/probe), tile =
 // U vectors per thread.  The work space [0, total) is partitioned among
@@ -692,6 +762,14 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
   __shared__ uint32_t s_sh;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   pdl_begin();
+  if constexpr (PLANNED) {
+    if (fz.size_next && blockIdx.x == gridDim.x - 1) {    // the metadata CTA
+      stage_cbase(t, scb);
+      __syncthreads();
+      planned_metadata_db(t, scb, fz);
+      return;
+    }
+  }
   const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
   uint64_t g = fz.g0 + (uint64_t)blockIdx.x * tile;
   const uint64_t gend = min(total, g + tile);

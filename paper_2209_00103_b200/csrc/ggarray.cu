@@ -39,6 +39,16 @@ struct gg_array {
   Fuse pend_fz{0, 0};
   cudaStream_t pend_st = nullptr;
   bool defer_in_capture = false;                         // capture mode 2: caller flushes in-capture
+  // double-buffered size / prefix (the planned walk's metadata CTA writes the
+  // next pair while its copy CTAs read the current one); t.size / t.prefix
+  // always point at the current pair
+  uint64_t *sz_buf[2] = {nullptr, nullptr}, *pf_buf[2] = {nullptr, nullptr};
+  int cur = 0;
+  int cap_parity = 0;                                    // buffer parity when capture mode 2 began
+  // a uniform grow not launched yet: published by the next planned walk's
+  // metadata CTA, or launched (k_grow) by any other device-touching call
+  uint32_t pend_grow = 0;
+  cudaStream_t pend_grow_st = nullptr;
   uint64_t alloc_calls = 0;
   uint64_t limit = 0;                                    // live-bytes cap (0 = none)
   gg_alloc_hook hook = nullptr;
@@ -200,7 +210,7 @@ template <int ESZ, int W, typename T, bool P, int U>
 cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
                    T add, uint32_t reps, Fuse fz, cudaStream_t st) {
   const uint32_t tile = (uint32_t)U * kThreads * (16 / ESZ);
-  const uint64_t grid = (total - fz.g0 + tile - 1) / tile;
+  const uint64_t grid = (total - fz.g0 + tile - 1) / tile + ((P && fz.size_next) ? 1 : 0);
   return launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src, dst,
                   total, add, reps, tile, fz);
 }
@@ -242,13 +252,48 @@ bool g_defer = true;            // defer + fuse planned metadata (GG_DEFER=0 dis
 
 uint32_t meta_threads(const gg_array *a) { return std::min<uint32_t>(1024, (a->S + 31) / 32 * 32); }
 
+bool g_fuse = true;             // metadata CTA inside the planned walk (GG_FUSE_META=0 disables)
+
 // launch a deferred metadata pass, if any (on the stream of its walk)
-int flush_pending(gg_array *a) {
+int flush_meta(gg_array *a) {
   if (!a->pend) return GG_OK;
   a->pend = false;
   Tables t = tables_for_launch(a, false);
   CUDA_TRY(launch_k(k_planned_meta, 1, meta_threads(a), 0, a->pend_st, t, a->pend_fz));
   return GG_OK;
+}
+
+// launch a deferred uniform grow, if any
+int flush_grow(gg_array *a) {
+  if (!a->pend_grow) return GG_OK;
+  const uint32_t k = a->pend_grow;
+  a->pend_grow = 0;
+  Tables t = tables_for_launch(a, true);
+  CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, a->pend_grow_st, t, k));
+  return GG_OK;
+}
+
+int flush_pending(gg_array *a) {
+  int rc = flush_meta(a);
+  return rc ? rc : flush_grow(a);
+}
+
+void flip_buffers(gg_array *a) {
+  a->cur ^= 1;
+  a->t.size = a->sz_buf[a->cur];
+  a->t.prefix = a->pf_buf[a->cur];
+}
+
+bool capturing_now(gg_array *a, cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  return a->up.capturing ||
+         (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone);
+}
+
+// the metadata pass may ride inside the planned walk (and take a deferred
+// grow with it): eager issue, or capture through GrowableArray.capture
+bool fuse_ok(gg_array *a, cudaStream_t st) {
+  return g_fuse && (!capturing_now(a, st) || a->defer_in_capture);
 }
 
 // after a planned walk: its metadata pass now, or deferred (eager issue) so
@@ -295,6 +340,22 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
   // copy kernels.
   if (!p.any_ctl && p.zero_pairs.empty() && reserve_mode != 2 && !(flags & GG_F_UNFUSED)) {
     const bool commit = (flags & GG_F_COMMIT) != 0;
+    if (total && fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
+      // ONE launch: copy CTAs + a metadata CTA writing the next size/prefix
+      // pair (and publishing a deferred grow)
+      Fuse fz{reserve_mode, commit ? 1 : 0};
+      fz.size_next = a->sz_buf[a->cur ^ 1];
+      fz.prefix_next = a->pf_buf[a->cur ^ 1];
+      fz.grow_k = a->pend_grow;
+      a->pend_grow = 0;
+      rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
+                          : walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fz, st);
+      if (rc) return rc;
+      flip_buffers(a);
+      if (commit) { host_commit(a); *committed = true; }
+      return GG_OK;
+    }
+    if ((rc = flush_grow(a))) return rc;
     if (total) {
       Fuse fz{reserve_mode, commit ? 1 : 0};
       rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
@@ -307,6 +368,7 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
     if (commit) { host_commit(a); *committed = true; }
     return GG_OK;
   }
+  if ((rc = flush_grow(a))) return rc;
   CUDA_TRY(launch_k(k_reserve, (a->S + 255) / 256, 256, 0, st, t, reserve_mode));
   CUDA_TRY(cudaGetLastError());
   if (!p.zero_pairs.empty()) {
@@ -486,7 +548,8 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
          o_count = take(S * 8), o_prefix = take((S + 1) * 8), o_off = take((S + 1) * 8),
          o_ctl = take(S * 4), o_flag = take(T * 4), o_status = take(S * 4), o_ptr = take(T * 8),
          o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_am = take(S * 8),
-         o_cb = take(max_buckets * 8), o_pm = take(S * 8);
+         o_cb = take(max_buckets * 8), o_pm = take(S * 8), o_size2 = take(S * 8),
+         o_prefix2 = take((S + 1) * 8);
   cudaError_t e = cudaMallocAsync(&a->dmem, bytes, 0);   // driver mempool: no device-wide sync
   if (e != cudaSuccess) { a->slab.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
   cudaMemsetAsync(a->dmem, 0, bytes, 0);
@@ -499,6 +562,8 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   t.flag = (uint32_t *)(base + o_flag); t.status = (uint32_t *)(base + o_status);
   t.ptr = (char **)(base + o_ptr); t.misc = (unsigned long long *)(base + o_misc);
   t.amask = (unsigned long long *)(base + o_am); t.cbase = (char **)(base + o_cb);
+  a->sz_buf[0] = t.size; a->sz_buf[1] = (uint64_t *)(base + o_size2);
+  a->pf_buf[0] = t.prefix; a->pf_buf[1] = (uint64_t *)(base + o_prefix2);
   t.pmask = (unsigned long long *)(base + o_pm);
   t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
   a->d_won = (int *)(base + o_won);
@@ -540,7 +605,7 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = flush_meta(a); if (frc_) return frc_; }   // a deferred grow may ride on this walk
   cudaStream_t st = S_(stream);
   if (h_offsets[0] != 0) return fail(GG_EVALUE, "offsets[0] must be 0");
   std::vector<uint64_t> counts(a->S);
@@ -579,7 +644,7 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
 int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = flush_meta(a); if (frc_) return frc_; }   // a deferred grow may ride on this walk
   cudaStream_t st = S_(stream);
   {
     // uniform fast path: every shard has the same committed length, size and
@@ -623,10 +688,21 @@ int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void 
           if ((rc = push_cbase(a, st))) return rc;
           const bool commit = (flags & GG_F_COMMIT) != 0;
           Tables t = tables_for_launch(a, false);
-          if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S],
-                                           Fuse{1, commit ? 1 : 0}, st)))
-            return rc;
-          if ((rc = finish_planned(a, Fuse{1, commit ? 1 : 0}, st))) return rc;
+          if (fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
+            Fuse fz{1, commit ? 1 : 0};
+            fz.size_next = a->sz_buf[a->cur ^ 1];
+            fz.prefix_next = a->pf_buf[a->cur ^ 1];
+            fz.grow_k = a->pend_grow;
+            a->pend_grow = 0;
+            if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S], fz, st))) return rc;
+            flip_buffers(a);
+          } else {
+            if ((rc = flush_grow(a))) return rc;
+            if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S],
+                                             Fuse{1, commit ? 1 : 0}, st)))
+              return rc;
+            if ((rc = finish_planned(a, Fuse{1, commit ? 1 : 0}, st))) return rc;
+          }
           if (commit) host_commit(a);
           if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
           return GG_OK;
@@ -676,7 +752,10 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_failed_shard) *h_failed_shard = -1;
-  if (a->pend && a->pend_st != st) { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  if ((a->pend && a->pend_st != st) || (a->pend_grow && a->pend_grow_st != st)) {
+    int frc_ = flush_pending(a);
+    if (frc_) return frc_;
+  }
   {
     // uniform fast path (every shard the same target and bucket set, no hook,
     // no cap, no failed shard): class-batched backing, no per-shard planning
@@ -705,6 +784,12 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
         a->live += bytes * a->S;
         a->alloc_calls += (uint64_t)__builtin_popcountll(want) * a->S;
         if ((rc = push_cbase(a, st))) return rc;
+        if (!a->pend && fuse_ok(a, st)) {     // published by the next planned walk's metadata CTA
+          a->pend_grow = std::max(a->pend_grow, k);
+          a->pend_grow_st = st;
+          return GG_OK;
+        }
+        if ((rc = flush_grow(a))) return rc;
         Tables t = tables_for_launch(a, true);
         if (a->pend) {                         // metadata of the last append + this grow: one launch
           a->pend = false;
@@ -1202,6 +1287,7 @@ int gg_capture_mode(gg_array *a, int32_t on) {
   use_dev(a->dev);
   { int frc_ = flush_pending(a); if (frc_) return frc_; }
   a->defer_in_capture = on == 2;
+  a->cap_parity = a->cur;
   if (on && !a->up.capturing) return a->up.begin_capture();
   if (!on) a->up.capturing = false;
   return GG_OK;
@@ -1211,6 +1297,26 @@ int gg_flush(gg_array *a) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   return flush_pending(a);
+}
+
+int gg_capture_end(gg_array *a, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  int rc = flush_pending(a);
+  if (rc) return rc;
+  if (a->cur != a->cap_parity) {     // an odd number of fused walks: copy back, restore the parity
+    const int o = a->cur ^ 1;
+    CUDA_TRY(launch_k(k_copy_db, (a->S + 256) / 256, 256, 0, S_(stream), a->sz_buf[o],
+                      (const uint64_t *)a->sz_buf[a->cur], a->pf_buf[o],
+                      (const uint64_t *)a->pf_buf[a->cur], a->S));
+    flip_buffers(a);
+  }
+  return GG_OK;
+}
+
+int gg_set_fuse(int32_t on) {
+  g_fuse = on != 0;
+  return GG_OK;
 }
 
 int gg_capture_release(gg_array *a) {

@@ -142,7 +142,7 @@ class GrowableArray:
             kw = {} if stream is None else {"stream": stream}
             with torch.cuda.graph(g, **kw):
                 fn()
-                self.flush()
+                L.check(L.lib.gg_capture_end(self._h, self._stream()), "capture_end")
         finally:
             L.lib.gg_capture_mode(self._h, 0)
         return g
