@@ -763,7 +763,9 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   pdl_begin();
   if constexpr (PLANNED) {
-    if (fz.size_next && blockIdx.x == gridDim.x - 1) {    // the metadata CTA
+    // block 0 is the metadata CTA (dispatched first, so it overlaps the copy
+    // instead of trailing it); the copy tiles are blocks 1..
+    if (fz.size_next && blockIdx.x == 0) {
       stage_cbase(t, scb);
       __syncthreads();
       planned_metadata_db(t, scb, fz);
@@ -771,7 +773,8 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
     }
   }
   const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
-  uint64_t g = fz.g0 + (uint64_t)blockIdx.x * tile;
+  const uint64_t tile_idx = (PLANNED && fz.size_next) ? blockIdx.x - 1 : blockIdx.x;
+  uint64_t g = fz.g0 + tile_idx * tile;
   const uint64_t gend = min(total, g + tile);
   if (tid < 32) {
     const uint32_t s0 = warp_find_shard(dir, t.S, g);

@@ -293,7 +293,9 @@ bool capturing_now(gg_array *a, cudaStream_t st) {
 // the metadata pass may ride inside the planned walk (and take a deferred
 // grow with it): eager issue, or capture through GrowableArray.capture
 bool fuse_ok(gg_array *a, cudaStream_t st) {
-  return g_fuse && (!capturing_now(a, st) || a->defer_in_capture);
+  // the metadata CTA has the walk's 256 threads: beyond 4096 shards its loop
+  // would outlast small copies -- take the separate 1024-thread kernel there
+  return g_fuse && a->S <= 4096 && (!capturing_now(a, st) || a->defer_in_capture);
 }
 
 // after a planned walk: its metadata pass now, or deferred (eager issue) so

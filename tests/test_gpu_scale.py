@@ -239,13 +239,13 @@ def test_flatten_range_slices(gg, dtype):
         a.flatten_range(0, n + 1)
 
 
-@pytest.mark.parametrize("defer", [True, False])
-def test_captured_schedule_replays_match_eager(gg, defer):
+@pytest.mark.parametrize("defer,rounds", [(True, 5), (True, 4), (False, 5)])
+def test_captured_schedule_replays_match_eager(gg, defer, rounds):
     """GrowableArray.capture (deferred metadata kept on and flushed in-capture)
     and plain capture_mode: replays of reset + insert + doubling rounds end
     in the eager state, device tables == host mirror, contents == closed form."""
     import torch
-    S, fb, n0, rounds = 64, 32, 1 << 14, 5
+    S, fb, n0 = 64, 32, 1 << 14                # rounds 4: an odd number of fused walks (parity restore)
     a = gg.GrowableArray(S, fb, dtype=np.int32)
     src = torch.arange(n0, dtype=torch.int32, device="cuda")
     off = np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(n0 // S), np.uint64(n0))
