@@ -530,6 +530,13 @@ __device__ __forceinline__ char *slot_addr(char *const *scb, uint32_t s, uint32_
   return scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
 }
 
+// directory accessor: loads dir[i], or i * ulen for a uniform directory
+struct DirV {
+  const uint64_t *p;
+  uint64_t u;
+  __device__ __forceinline__ uint64_t operator[](uint32_t i) const { return u ? (uint64_t)i * u : p[i]; }
+};
+
 // shard of work index g: largest s with dir[s] <= g (bisect_right - 1,
 // sharded_array.py:136) by a 32-ary warp search -- 2 dependent loads for
 // S <= 1024, 3 up to 32768.  Called by a full warp; result in every lane.
@@ -554,7 +561,7 @@ __device__ __forceinline__ uint32_t warp_find_shard(const uint64_t *dir, uint32_
 // touches.  Returns false (tile not handled) when the tile crosses a shard
 // or the alignment does not hold.
 template <int ESZ, int W, typename T, int U, int LS>
-__device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, const uint64_t *dir,
+__device__ __forceinline__ bool vector_tile(const Tables &t, char *const *scb, const DirV dir,
                                             uint32_t s, uint64_t dbase, uint64_t g, uint64_t gend,
                                             const char *flat_src, char *flat_dst, T addend,
                                             uint32_t reps) {
@@ -633,7 +640,13 @@ struct Fuse {
   uint64_t *size_next = nullptr;
   uint64_t *prefix_next = nullptr;
   uint32_t grow_k = 0;
+  // uniform directory (every shard's work length = ulen, known on the host):
+  // shard lookup is a division, no directory loads; planned walks also take
+  // the common destination start ustart instead of loading size[s]
+  uint64_t ulen = 0;
+  uint64_t ustart = 0;
 };
+
 
 // metadata of a planned append, run by one CTA after every tile is copied.
 // Latency shaped: all loads (directory pair, size, pmask) issued up front,
@@ -772,12 +785,14 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
       return;
     }
   }
-  const uint64_t *dir = (W == W_INSERT) ? t.offsets : t.prefix;
+  const DirV dir{(W == W_INSERT) ? t.offsets : t.prefix, fz.ulen};
   const uint64_t tile_idx = (PLANNED && fz.size_next) ? blockIdx.x - 1 : blockIdx.x;
   uint64_t g = fz.g0 + tile_idx * tile;
   const uint64_t gend = min(total, g + tile);
-  if (tid < 32) {
-    const uint32_t s0 = warp_find_shard(dir, t.S, g);
+  if (fz.ulen) {
+    if (tid == 0) s_sh = (uint32_t)(g / fz.ulen);
+  } else if (tid < 32) {
+    const uint32_t s0 = warp_find_shard(dir.p, t.S, g);
     if (tid == 0) s_sh = s0;
   }
   stage_cbase(t, scb);
@@ -789,7 +804,7 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
   uint64_t dbase = 0;                      // destination local index of shard s's work index 0
   if constexpr (W == W_INSERT || W == W_DUP) {
     if (!PLANNED && t.ctl && t.ctl[s] != (kCtlWrite | t.MB)) fast = false;   // planned failure
-    dbase = PLANNED ? t.size[s] : t.start[s];
+    dbase = PLANNED ? (fz.ulen ? fz.ustart : t.size[s]) : t.start[s];
   }
   if (!(fast && vector_tile<ESZ, W, T, U, LS>(t, scb, dir, s, dbase, g, gend, flat_src, flat_dst,
                                               addend, reps))) {
@@ -818,7 +833,7 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
         dp = (char *)sp;
       } else {
         uint32_t b; uint64_t o;
-        locate((PLANNED ? t.size[s] : t.start[s]) + k, t.log2fb, b, o);
+        locate((PLANNED ? (fz.ulen ? fz.ustart : t.size[s]) : t.start[s]) + k, t.log2fb, b, o);
         len = min(len, (uint64_t)((1ull << (t.log2fb + b)) - o));
         if (!PLANNED) dst_ok = t.flag[(size_t)s * t.MB + b] == kFlagPublished;
         dp = slot_addr(scb, s, b, lg0) + o * ESZ;

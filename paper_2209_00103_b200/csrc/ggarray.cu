@@ -242,10 +242,21 @@ int walk_copy(const gg_array *a, const Tables &t, const char *src, char *dst, ui
   }
 }
 
+// every shard's committed length when they are all equal (and nonzero), else
+// 0: a uniform directory lets the walks find shards by division
+uint64_t uniform_len(const gg_array *a) {
+  const uint64_t c = a->prefix[1] - a->prefix[0];
+  for (uint32_t s = 1; s < a->S; ++s)
+    if (a->prefix[s + 1] - a->prefix[s] != c) return 0;
+  return c;
+}
+
 template <int W>
 int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
                 cudaStream_t st) {
-  return walk_copy<W, false>(a, t, src, dst, total, Fuse{0, 0}, st);
+  Fuse fz{0, 0};
+  if (W == W_FLATTEN) fz.ulen = uniform_len(a);
+  return walk_copy<W, false>(a, t, src, dst, total, fz, st);
 }
 
 bool g_defer = true;            // defer + fuse planned metadata (GG_DEFER=0 disables)
@@ -424,7 +435,8 @@ int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode,
     }
     return GG_OK;
   }
-  const Fuse none{0, 0};
+  Fuse none{0, 0};
+  none.ulen = uniform_len(a);
   if (mode == GG_RW_FUSED)
     return walk<sizeof(T), W_RW, T>(a, t, nullptr, nullptr, total, addend, passes, none, st);
   for (uint32_t p = 0; p < passes; ++p) {
@@ -692,6 +704,8 @@ int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void 
           Tables t = tables_for_launch(a, false);
           if (fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
             Fuse fz{1, commit ? 1 : 0};
+            fz.ulen = c;                       // uniform directory and destination start
+            fz.ustart = start;
             fz.size_next = a->sz_buf[a->cur ^ 1];
             fz.prefix_next = a->pf_buf[a->cur ^ 1];
             fz.grow_k = a->pend_grow;
@@ -1066,6 +1080,7 @@ int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *s
   Tables t = tables_for_launch(a, false);
   Fuse fz{0, 0};
   fz.g0 = lo;
+  fz.ulen = uniform_len(a);
   // the walk stores element g at flat_dst + g * esz: shift the base so that
   // element lo lands at d_out (never dereferenced below lo)
   char *base = (char *)d_out - lo * a->esz;
