@@ -753,7 +753,20 @@ def e2e_leg(args, gg, torch, device, world, dist):
         t = torch.tensor([sec], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
+    # context for the host-side numbers: this box's pinned H2D bandwidth for the step's batch
+    dev_tmp = torch.empty(N0, dtype=torch.int32, device=device)
+    h2d = []
+    for _ in range(10):
+        e0, e1 = _events(torch)
+        e0.record()
+        dev_tmp.copy_(host, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        h2d.append(e0.elapsed_time(e1))
+    del dev_tmp
     out = {"value": round(world * (1 << 30) * k / sec / 1e9, 3), "unit": UNIT,
+           "h2d_gbs_of_4mib_batch": round(N0 * 4 / float(np.median(h2d)) / 1e6, 1),
+           "wall_ms_per_step": round(sec * 1e3 / k, 4),
            "h2d_bytes_per_step": N0 * 4, "d2h_bytes_per_step": (S + 1) * 8,
            "api": "GrowableArray.insert_csr(host batch) + grow + insert_duplicate + prefix_device "
                   "(committed directory D2H) + sync, op by op",
