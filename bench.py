@@ -251,8 +251,8 @@ def run_device(args, rank, world, local_rank):
                      "traffic_detail": traffic, "algorithmic_bytes_per_elem": 8,
                      "achieved_def": "sum of 8 B x elements duplicated / sum of CUDA-event times around "
                                      "the insert_duplicate calls of the K eager steps (the planned "
-                                     "copy walk k_walk<W_DUP>; its metadata pass is deferred into "
-                                     "the next grow, timed there)",
+                                     "copy walk k_walk<W_DUP> with its metadata CTA, which also "
+                                     "publishes the deferred grow)",
                      "last_round_2p29_gbs": round(float(last_gbs), 1),
                      "last_round_frac": round(float(last_gbs) / hbm, 4)},
         "phases": {"insert_ms_per_step": round(dup_ms / args.steps, 4),
