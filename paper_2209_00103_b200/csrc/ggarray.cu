@@ -199,11 +199,11 @@ int commit_plan(gg_array *a, Plan &p, cudaStream_t st) {
 uint32_t walk_unroll(const gg_array *a, uint64_t total, int w) {
   if (g_tune.unroll > 0) return (uint32_t)g_tune.unroll;
   static const uint32_t u_small = [] { const char *e = getenv("GG_U_SMALL"); return e ? (uint32_t)atoi(e) : 2u; }();
-  static const uint32_t u_mid = [] { const char *e = getenv("GG_U_MID"); return e ? (uint32_t)atoi(e) : 4u; }();
+  static const uint32_t u_mid = [] { const char *e = getenv("GG_U_MID"); return e ? (uint32_t)atoi(e) : 0u; }();
   const uint64_t bytes = total * a->esz;
   if (bytes < (uint64_t(32) << 20)) return u_small;
-  if (bytes < (uint64_t(256) << 20)) return u_mid;
-  return w == W_FLATTEN ? 4u : 8u;
+  if (bytes < (uint64_t(256) << 20) && u_mid) return u_mid;
+  return w == W_FLATTEN ? 4u : 8u;   // tools/ab_unroll.sh: U = 8 from 32 MiB on (1304 vs 1310 us/step)
 }
 
 template <int ESZ, int W, typename T, bool P, int U>
