@@ -192,10 +192,10 @@ int commit_plan(gg_array *a, Plan &p, cudaStream_t st) {
 }
 
 // Streaming launches: one tile per CTA of kThreads threads x U 16 B vectors.
-// Large work spaces use the U the sweep measured best per walk (tools/
-// sweep.py, B200: copies into / in place on the slabs U = 8 -- 32 KiB tiles,
-// flatten U = 4); smaller ones shrink U so small rounds still spread over
-// every SM.  gg_set_tuning can force U.
+// Work spaces from 32 MiB use the U the sweeps measured best per walk
+// (tools/sweep.py, tools/ab_unroll.sh, B200: copies into / in place on the
+// slabs U = 8 -- 32 KiB tiles, flatten U = 4); below, U = 2 so small rounds
+// still spread over every SM.  gg_set_tuning / GG_U_SMALL / GG_U_MID override.
 uint32_t walk_unroll(const gg_array *a, uint64_t total, int w) {
   if (g_tune.unroll > 0) return (uint32_t)g_tune.unroll;
   static const uint32_t u_small = [] { const char *e = getenv("GG_U_SMALL"); return e ? (uint32_t)atoi(e) : 2u; }();
