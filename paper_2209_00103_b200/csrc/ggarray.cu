@@ -1129,12 +1129,10 @@ int elem_addr(gg_array *a, uint32_t s, uint64_t i, char **out, cudaStream_t st) 
   host_locate(a, i, b, o);
   if (b >= a->MB || !(a->flags[s] >> b & 1))
     return fail(GG_EUNPUBLISHED, "index is reserved but its bucket is unpublished");
-  char *p = nullptr;
-  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
-  CUDA_TRY(cudaMemcpyAsync(a->h_scratch, a->t.ptr + (size_t)s * a->MB + b, sizeof(char *),
-                           cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  memcpy(&p, a->h_scratch, sizeof(char *));
+  (void)st;
+  // the bucket's slot is host-known (class base + s * bucket bytes): no
+  // device round trip for the address
+  char *p = (char *)a->slab.class_base(b) + (uint64_t)s * bucket_bytes(a, b);
   *out = p + o * a->esz;
   return GG_OK;
 }
