@@ -298,7 +298,9 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
 // b >= min_buckets_for(new size) unpublished (their slots stay reserved for
 // the shard; the host unmaps chunks that lost their last live bucket), then
 // the commit scan over the new sizes.  All loads issued up front.
-__global__ void __launch_bounds__(1024) k_shrink(Tables t, const uint64_t *new_sizes) {
+// new_sizes == nullptr: every shard shrinks to uniform_size (no upload)
+__global__ void __launch_bounds__(1024) k_shrink(Tables t, const uint64_t *new_sizes,
+                                                 uint64_t uniform_size) {
   __shared__ uint64_t ws[32];
   pdl_begin();
   uint64_t carry = 0;
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(1024) k_shrink(Tables t, const uint64_t *new_s
     const bool live = s < t.S;
     uint64_t ns = 0, cap = 0;
     unsigned long long m = 0;
-    if (live) { ns = new_sizes[s]; m = t.pmask[s]; cap = t.cap[s]; }
+    if (live) { ns = new_sizes ? new_sizes[s] : uniform_size; m = t.pmask[s]; cap = t.cap[s]; }
     if (live) {
       const uint32_t keep = ns ? (64u - (uint32_t)__clzll((long long)((ns + (1ull << t.log2fb) - 1) >> t.log2fb))) : 0u;
       const unsigned long long drop = keep < 64 ? (m & ~((1ull << keep) - 1ull)) : 0ull;
@@ -708,7 +710,7 @@ __device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &
 __device__ void planned_metadata_db(const Tables &t, char *const *scb, const Fuse &fz) {
   __shared__ uint64_t ws[32];
   const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
-  const uint64_t *dir = fz.rmode == 0 ? t.offsets : t.prefix;
+  const DirV dir{fz.rmode == 0 ? t.offsets : t.prefix, fz.ulen};
   const unsigned long long gmask = fz.grow_k >= 64 ? ~0ull : ((1ull << fz.grow_k) - 1ull);
   uint64_t carry = 0;
   for (uint32_t base = 0; base < t.S; base += blockDim.x) {

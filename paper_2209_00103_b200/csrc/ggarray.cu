@@ -336,7 +336,8 @@ void host_commit(gg_array *a) {
 // fused launch (reserve + allocate + copy [+ commit]) or the unfused
 // reserve / zero / copy sequence (failure paths that must zero buckets).
 int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
-               uint64_t total, cudaStream_t st, uint32_t flags, bool *committed) {
+               uint64_t total, cudaStream_t st, uint32_t flags, bool *committed,
+               const uint64_t *h_offsets = nullptr, uint64_t csr_ulen = 0, uint64_t csr_ustart = 0) {
   *committed = false;
   int rc = commit_plan(a, p, st);
   if (rc) return rc;
@@ -360,6 +361,8 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
       fz.size_next = a->sz_buf[a->cur ^ 1];
       fz.prefix_next = a->pf_buf[a->cur ^ 1];
       fz.grow_k = a->pend_grow;
+      fz.ulen = csr_ulen;                    // uniform CSR: no offsets on the device needed
+      fz.ustart = csr_ustart;
       a->pend_grow = 0;
       rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
                           : walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fz, st);
@@ -369,6 +372,12 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
       return GG_OK;
     }
     if ((rc = flush_grow(a))) return rc;
+    if (csr_ulen) {                          // the other paths read the offsets on the device
+      void *dst[1] = {a->t.offsets};
+      const void *srcs[1] = {h_offsets};
+      size_t bytes[1] = {(a->S + 1) * 8};
+      if ((rc = a->up.upload(st, 1, dst, srcs, bytes))) return rc;
+    }
     if (total) {
       Fuse fz{reserve_mode, commit ? 1 : 0};
       rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
@@ -382,6 +391,12 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
     return GG_OK;
   }
   if ((rc = flush_grow(a))) return rc;
+  if (csr_ulen) {
+    void *dst[1] = {a->t.offsets};
+    const void *srcs[1] = {h_offsets};
+    size_t bytes[1] = {(a->S + 1) * 8};
+    if ((rc = a->up.upload(st, 1, dst, srcs, bytes))) return rc;
+  }
   CUDA_TRY(launch_k(k_reserve, (a->S + 255) / 256, 256, 0, st, t, reserve_mode));
   CUDA_TRY(cudaGetLastError());
   if (!p.zero_pairs.empty()) {
@@ -640,7 +655,18 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
     const void *src[3] = {h_offsets, st0.data(), counts.data()};
     size_t bytes[3] = {(a->S + 1) * 8, a->S * 8, a->S * 8};
     if ((rc = a->up.upload(st, 3, dst, src, bytes))) return rc;
-  } else {
+  }
+  // uniform CSR over uniform shards (every batch c elements, every shard the
+  // same size): the fused walk derives the offsets and starts itself
+  uint64_t ulen = 0, ustart = 0;
+  if (!h_starts && h_offsets[1] > 0) {
+    bool u = true;
+    const uint64_t c = h_offsets[1];
+    for (uint32_t s = 0; s < a->S && u; ++s)
+      u = h_offsets[s + 1] - h_offsets[s] == c && a->size[s] == a->size[0];
+    if (u) { ulen = c; ustart = a->size[0]; }
+  }
+  if (!h_starts && !ulen) {
     void *dst[1] = {a->t.offsets};
     const void *src[1] = {h_offsets};
     size_t bytes[1] = {(a->S + 1) * 8};
@@ -648,7 +674,7 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
   }
   bool committed;
   if ((rc = run_append(a, p, h_starts ? 2 : 0, W_INSERT, (const char *)d_values, total, st, flags,
-                       &committed)))
+                       &committed, h_offsets, ulen, ustart)))
     return rc;
   if (!h_starts)
     for (uint32_t s = 0; s < a->S; ++s) if (counts[s]) a->ops[s] += 1;
@@ -959,14 +985,18 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
       a->size[s] = h_new_sizes[s];
     }
   }
-  void *dst[1] = {a->t.count};
-  const void *src[1] = {h_new_sizes};
-  size_t bytes[1] = {a->S * 8};
-  int rc = a->up.upload(st, 1, dst, src, bytes);
-  if (rc) return rc;
+  const uint64_t *d_sizes = nullptr;      // a uniform shrink passes its size as a scalar
+  if (!uni) {
+    void *dst[1] = {a->t.count};
+    const void *src[1] = {h_new_sizes};
+    size_t bytes[1] = {a->S * 8};
+    int rc = a->up.upload(st, 1, dst, src, bytes);
+    if (rc) return rc;
+    d_sizes = a->t.count;
+  }
   Tables t = tables_for_launch(a, false);
-  CUDA_TRY(launch_k(k_shrink, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t,
-                    (const uint64_t *)a->t.count));
+  CUDA_TRY(launch_k(k_shrink, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t, d_sizes,
+                    (uint64_t)h_new_sizes[0]));
   uint64_t acc = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
   // unmap emptied chunks down to keep_mapped_bytes (waits for the device:
