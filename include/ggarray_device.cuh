@@ -11,6 +11,8 @@
  *   gg::gg_device_view v = ...;          // from gg_device_view_get() (host)
  *   gg::warp_push_back(v, shard, pred, value);        // one atomicAdd per warp
  *   gg::warp_push_back_n<T, K>(v, shard, count, vals); // per-lane counts, one per warp
+ *   gg::warp_push_back_mask<T, K>(v, shard, mask, vals);        // K candidates, bitmask
+ *   gg::block_push_back_mask<BLOCK, T, K>(v, shard, mask, vals, scratch);
  *   gg::block_push_back<BLOCK>(v, shard, count, vals, scratch);  // one per block
  *
  * Device code cannot map memory, so the host backs the slots a launch may
@@ -228,6 +230,118 @@ __device__ inline uint64_t warp_push_back_n(const gg_device_view &t, uint32_t s,
     }
   }
   return start + excl;
+}
+
+// Paper Alg. 1 with up to K candidate values per lane selected by a bitmask:
+// value j of a lane lands at start + excl + popc(mask & ((1 << j) - 1)).  No
+// compaction into a dynamically indexed array (which would live in local
+// memory): all indexing is static, values stay in registers.  One atomicAdd
+// per warp; must be called by all 32 lanes, s warp-uniform.
+template <typename T, int K>
+__device__ inline uint64_t warp_push_back_mask(const gg_device_view &t, uint32_t s, uint32_t mask,
+                                               const T (&vals)[K]) {
+  const uint32_t lane = threadIdx.x & 31, count = __popc(mask);
+  uint32_t x = count;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, x, 31), excl = x - count;
+  if (!total) return ~0ull;
+  unsigned long long start = 0;
+  int ok = 1;
+  if (lane == 0) {
+    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)total);
+    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+    ok = ensure_buckets(t, s, start, total);
+  }
+  start = __shfl_sync(0xffffffffu, start, 0);
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  if (!ok) return ~0ull;
+  uint32_t cur_b = ~0u, r = 0;
+  char *base = nullptr;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    if ((mask >> j) & 1u) {
+      uint32_t b;
+      uint64_t o;
+      locate(start + excl + r, t.log2fb, b, o);
+      if (b != cur_b) { base = bucket_acquire(t, s, b); cur_b = b; }
+      if (base) store_cg(reinterpret_cast<T *>(base) + o, vals[j]);
+      ++r;
+    }
+  }
+  return start + excl;
+}
+
+// Block flavour of the mask variant: a shared-memory scan of the lanes'
+// popcounts, ONE atomicAdd per block, values in thread order.  scratch: 34 u64
+// of shared memory; all BLOCK threads must call it.
+template <int BLOCK, typename T, int K>
+__device__ inline uint64_t block_push_back_mask(const gg_device_view &t, uint32_t s, uint32_t mask,
+                                                const T (&vals)[K], unsigned long long *scratch) {
+  static_assert(BLOCK % 32 == 0 && BLOCK <= 1024, "BLOCK must be a multiple of 32, <= 1024");
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, count = __popc(mask);
+  unsigned long long x = count;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < BLOCK / 32 ? scratch[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= (uint32_t)d) w += y;
+    }
+    scratch[lane] = w;
+  }
+  __syncthreads();
+  const unsigned long long excl = x - count + (wid ? scratch[wid - 1] : 0);
+  const unsigned long long total = scratch[BLOCK / 32 - 1];
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long start = 0;
+    int ok = 1;
+    if (total) {
+      start = atomicAdd((unsigned long long *)&t.size[s], total);
+      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+      ok = ensure_buckets(t, s, start, total);
+    }
+    scratch[32] = start;
+    scratch[33] = ok;
+  }
+  __syncthreads();
+  const unsigned long long start = scratch[32];
+  const bool ok = scratch[33] != 0;
+  __shared__ char *bptr_m[64];
+  if (ok && total) {
+    uint32_t b0, b1;
+    uint64_t o;
+    locate(start, t.log2fb, b0, o);
+    locate(start + total - 1, t.log2fb, b1, o);
+    if (tid <= b1 - b0) bptr_m[b0 + tid] = bucket_acquire(t, s, b0 + tid);
+  }
+  __syncthreads();
+  if (ok) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if ((mask >> j) & 1u) {
+        uint32_t b;
+        uint64_t o;
+        locate(start + excl + r, t.log2fb, b, o);
+        if (bptr_m[b]) store_cg(reinterpret_cast<T *>(bptr_m[b]) + o, vals[j]);
+        ++r;
+      }
+    }
+  }
+  __syncthreads();
+  return start;
 }
 
 // Paper Alg. 1, block flavour: thread j contributes vals[0..count_j); a

@@ -15,6 +15,23 @@ template <int BLOCK>
 __global__ void user_emit(gg::gg_device_view v, const int32_t *in, uint64_t n, int block_mode) {
   __shared__ unsigned long long scratch[34];
   const uint32_t s = blockIdx.x % v.S;
+  if (block_mode >= 2) {            // mask variants: 4 rounds of candidates per thread
+    constexpr int K = 4;
+    const uint64_t round = (uint64_t)gridDim.x * BLOCK;
+    for (uint64_t r0 = 0; (uint64_t)blockIdx.x * BLOCK + r0 * round < n; r0 += K) {
+      int32_t cand[K];
+      uint32_t mask = 0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const uint64_t i = (uint64_t)blockIdx.x * BLOCK + (r0 + j) * round + threadIdx.x;
+        cand[j] = i < n ? in[i] : 0;
+        mask |= (uint32_t)(i < n && (cand[j] & 1)) << j;
+      }
+      if (block_mode == 3) gg::block_push_back_mask<BLOCK, int32_t, K>(v, s, mask, cand, scratch);
+      else gg::warp_push_back_mask<int32_t, K>(v, s, mask, cand);
+    }
+    return;
+  }
   for (uint64_t base = (uint64_t)blockIdx.x * BLOCK; base < n; base += (uint64_t)gridDim.x * BLOCK) {
     const uint64_t i = base + threadIdx.x;
     const int32_t x = i < n ? in[i] : 0;

@@ -30,12 +30,12 @@ def user_lib(tmp_path_factory):
     return lib
 
 
-@pytest.mark.parametrize("block_mode", [0, 1])
+@pytest.mark.parametrize("block_mode", [0, 1, 2, 3])   # warp, block, warp_mask, block_mask
 def test_user_kernel_appends(user_lib, block_mode):
     import torch
     import paper_2209_00103_b200 as gg
     S, fb, grid, n = 12, 8, 96, 300_000
-    rng = np.random.default_rng(block_mode)
+    rng = np.random.default_rng(block_mode % 2)
     x = rng.integers(0, 1 << 30, n).astype(np.int32)
     d = torch.from_numpy(x).cuda()
     a = gg.GrowableArray(S, fb, dtype=np.int32)
