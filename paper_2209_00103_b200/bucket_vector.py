@@ -96,6 +96,14 @@ class BucketTable:
         self._sh = shard
 
     @property
+    def flag_lock(self):
+        """The reference guards its once-flags with this lock
+        (bucket_vector.py:94, 189-199); here the flags live on the device and
+        are updated by CAS / planned kernels, so the lock only serialises host
+        callers of the shard's handle."""
+        return self._sh._arr._mu
+
+    @property
     def first_bucket_size(self) -> int:
         return self._sh.first_bucket_size
 
