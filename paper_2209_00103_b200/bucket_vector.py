@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import threading
+
 import numpy as np
 
 from . import _lib as L
@@ -90,10 +92,28 @@ class _SizeCounter:
 
 
 class BucketTable:
-    """Read view of one shard's bucket table (bucket_vector.py:82-101)."""
+    """A shard's bucket table (bucket_vector.py:82-101).
 
-    def __init__(self, shard: "ShardVector"):
-        self._sh = shard
+    ``BucketTable(first_bucket_size, max_buckets)`` builds an empty standalone
+    table like the reference's (no storage, all once-flags clear); the tables
+    of device arrays (``ShardVector.table``) are live views of the device
+    flags and bucket slots."""
+
+    def __init__(self, first_bucket_size: int, max_buckets: int = MAX_BUCKETS):
+        _check_fb(first_bucket_size)
+        if max_buckets < 1:
+            raise ValueError("max_buckets must be >= 1")
+        self._sh = None
+        self._fb = first_bucket_size
+        self._mb = max_buckets
+        self._flags = [False] * max_buckets
+        self._lock = threading.Lock()
+
+    @classmethod
+    def _bind(cls, shard: "ShardVector") -> "BucketTable":
+        t = cls.__new__(cls)
+        t._sh = shard
+        return t
 
     @property
     def flag_lock(self):
@@ -101,18 +121,20 @@ class BucketTable:
         (bucket_vector.py:94, 189-199); here the flags live on the device and
         are updated by CAS / planned kernels, so the lock only serialises host
         callers of the shard's handle."""
-        return self._sh._arr._mu
+        return self._lock if self._sh is None else self._sh._arr._mu
 
     @property
     def first_bucket_size(self) -> int:
-        return self._sh.first_bucket_size
+        return self._fb if self._sh is None else self._sh.first_bucket_size
 
     @property
     def max_buckets(self) -> int:
-        return self._sh.max_buckets
+        return self._mb if self._sh is None else self._sh.max_buckets
 
     @property
     def allocated_flags(self) -> list:
+        if self._sh is None:
+            return list(self._flags)
         m = int(self._sh._arr._host()["flags"][self._sh._s])
         return [bool(m >> b & 1) for b in range(self.max_buckets)]
 
@@ -121,6 +143,8 @@ class BucketTable:
 
     @property
     def buckets(self) -> list:
+        if self._sh is None:
+            return [None] * self._mb
         a, s = self._sh._arr, self._sh._s
         ptrs = a._bucket_ptrs()[s]
         fb = self.first_bucket_size
@@ -180,7 +204,7 @@ class ShardVector:
 
     @property
     def table(self) -> BucketTable:
-        return BucketTable(self)
+        return BucketTable._bind(self)
 
     def locate(self, i: int) -> tuple:
         return locate(i, self.first_bucket_size)
