@@ -100,7 +100,7 @@ class GrowableArray:
                     return 1
             self._hook_fn = L.HOOK(hook)
             L.lib.gg_set_alloc_hook(self._h, self._hook_fn, None)
-        self._cache = None
+        self._cache = self._tot = None
         self._ptrs = None
         self._summary = np.zeros(3, np.uint64)
         self._status = np.zeros(shards, np.int32)
@@ -118,12 +118,17 @@ class GrowableArray:
         return L.stream_handle(self._dev_index)
 
     def _dirty(self):
-        self._cache = None
+        self._cache = self._tot = None
         self._ptrs = None
 
     def _totals(self):
-        L.lib.gg_summary(self._h, L.ptr(self._summary))
-        return self._summary
+        # (committed, total size, total capacity) from the host mirrors; cached
+        # until the next mutating call (every one goes through _dirty / resets
+        # _cache), so per-round `committed_size` reads cost no ctypes call
+        if self._tot is None:
+            L.lib.gg_summary(self._h, L.ptr(self._summary))
+            self._tot = (int(self._summary[0]), int(self._summary[1]), int(self._summary[2]))
+        return self._tot
 
     def flush(self) -> None:
         """Launch the deferred metadata pass of the last append now (normally it
@@ -429,7 +434,7 @@ class GrowableArray:
             vals, offsets = self._pack(per_shard_batches)
             failures = self._insert_device(vals, offsets, commit=True)   # commit fused on success
             if not failures:
-                self._cache = None
+                self._cache = self._tot = None
                 return
             counts = np.diff(offsets.astype(np.int64))
             ok = [s for s in range(self._S) if counts[s] and s not in failures]
@@ -565,7 +570,7 @@ class GrowableArray:
 
     def commit(self) -> None:
         L.check(L.lib.gg_commit(self._h, self._stream()), "commit")
-        self._cache = None
+        self._cache = self._tot = None
 
     def grow(self, target_total_capacity: int, distribution: Sequence | None = None) -> None:
         if distribution is None:
