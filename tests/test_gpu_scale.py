@@ -374,3 +374,37 @@ def test_large_ragged_dtypes(gg, dtype, fb, S):
     assert a.flatten().tobytes() == want.tobytes()
     st = a.device_state()
     assert np.array_equal(st["caps"], [O.capacity_of(O.min_buckets_for(2 * int(c), fb), fb) for c in counts])
+
+
+def test_deferred_grow_is_flushed_by_every_device_reader(gg):
+    """A uniform grow is deferred into the next append's metadata CTA; any
+    other call that reads or writes device state must see it applied."""
+    import torch
+    S, fb = 16, 8
+    a = gg.GrowableArray.from_flat(np.arange(16 * 100, dtype=np.int32), S, fb)
+    o = O.OracleGGArray.from_flat(np.arange(16 * 100, dtype=np.int32), S, fb)
+    checks = [
+        lambda: a.device_state(),                                   # device tables read back
+        lambda: a.shards[3].table.buckets,                          # bucket pointers
+        lambda: a.get_global(5),                                    # single element
+        lambda: a.flatten(),                                        # walk
+        lambda: a.rw_add(0),                                        # walk in place
+        lambda: a.commit(),                                         # commit kernel
+    ]
+    for i, chk in enumerate(checks):
+        a.grow((3 + i) * a.committed_size)
+        o.grow((3 + i) * o.committed_size)
+        chk()
+        st = a.device_state()
+        assert [int(x) for x in st["caps"]] == [int(x) for x in o.capacity], i
+        assert [int(x) for x in st["flags"]] == [int(sum(1 << b for b in range(o.mb) if o.flags[s, b]))
+                                                 for s in range(S)], i
+    # a deferred grow followed by a non-uniform append (ragged) and a shrink
+    a.grow(2 * a.committed_size); o.grow(2 * o.committed_size)
+    batches = [np.arange(s * 7, dtype=np.int32) for s in range(S)]
+    a.insert_parallel(batches); o.insert_parallel(batches)
+    a.grow(4 * a.committed_size); o.grow(4 * o.committed_size)
+    a.shrink(np.full(S, 50)); o.shrink(np.full(S, 50))
+    st = a._parity_state()
+    assert st["sizes"] == [int(x) for x in o.size] and st["caps"] == [int(x) for x in o.capacity]
+    assert a.flatten().tobytes() == o.flatten().tobytes()
