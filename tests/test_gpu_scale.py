@@ -283,7 +283,17 @@ def test_chunk_pool_reuse_and_trim(gg):
     """Destroyed arrays leave their physical chunks in the process pool; the
     next array maps them (hits), contents are fresh writes; trim empties it.
     Shrink releases never feed the pool."""
+    import gc
     import torch
+    gc.collect()                       # earlier tests' arrays die now, not mid-test
+    gc.disable()
+    try:
+        _chunk_pool_body(gg, torch)
+    finally:
+        gc.enable()
+
+
+def _chunk_pool_body(gg, torch):
     gg.pool_trim(0)
     s0 = gg.pool_stats(0)
     a = gg.GrowableArray.from_flat(torch.arange(1 << 20, dtype=torch.int32, device="cuda"), 64, 32)
