@@ -407,6 +407,39 @@ def secondary(args, gg, torch, device, step, hbm):
     rw["flattened_contiguous"] = {"ms_per_pass": round(ms, 4), "gbs": round(8 * n / ms / 1e6, 1),
                                   "frac": round(8 * n / ms / 1e6 / hbm, 4)}
     res["rw_config3"] = rw
+    # --- two-phase usage (paper section 6): grow -> flatten -> static work -> rebuild.
+    # from_flat re-shards the flat array into a fresh GGArray (one planned CSR
+    # insert); the first build maps new slabs, the second reuses the chunk pool.
+    flat.sub_(passes)                                # flat_add put +passes on the copy: back to a's contents
+    tp = {"flatten_ms": res["flatten"]["ms"], "static_rw_ms_per_pass": rw["flattened_contiguous"]["ms_per_pass"]}
+    for tag in ("rebuild_cold", "rebuild_pooled"):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e0.record()
+        b = gg.GrowableArray.from_flat(flat, shards=S, first_bucket_size=FB, dtype=np.int32, device=device)
+        e1.record()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - w0) * 1e3
+        tp[tag] = {"wall_ms": round(wall, 3), "device_ms": round(e0.elapsed_time(e1), 3),
+                   "gelem_s": round(n / wall / 1e6, 2)}
+        if tag == "rebuild_pooled":
+            tp["roundtrip_ok"] = bool(torch.equal(b.flatten_device(), flat))
+            # steady two-phase loop: reuse the GGArray (reset keeps its buckets mapped)
+            from paper_2209_00103_b200.sharded_array import split_offsets
+            offs = split_offsets(n, S)
+
+            def reuse():
+                b.shrink(0, release=False)
+                b.insert_csr(flat, offs)
+            reuse()
+            ms = _time(torch, reuse, reps=5)
+            tp["rebuild_reuse"] = {"device_ms": round(ms, 4), "gelem_s": round(n / ms / 1e6, 2),
+                                   "gbs": round(8 * n / ms / 1e6, 1)}
+            tp["reuse_roundtrip_ok"] = bool(torch.equal(b.flatten_device(), flat))
+        b.close()
+        del b
+    res["two_phase"] = tp
     del flat
     # --- baselines: the last doubling step 2^29 -> 2^30 (paper Table II)
     half = 1 << 29
