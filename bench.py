@@ -119,10 +119,11 @@ def _events(torch):
 class Step:
     """One config-2 schedule on a persistent array; per-phase CUDA events."""
 
-    def __init__(self, gg, torch, device):
+    def __init__(self, gg, torch, device, dtype=np.int32):
         self.gg, self.torch = gg, torch
-        self.arr = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
-        self.vals = torch.arange(N0, dtype=torch.int32, device=device)
+        self.arr = gg.GrowableArray(S, FB, dtype=dtype, device=device)
+        tdt = {np.int32: torch.int32, np.float32: torch.float32, np.int64: torch.int64}[dtype]
+        self.vals = torch.arange(N0, dtype=tdt, device=device)
         self.offsets = np.minimum(np.arange(S + 1, dtype=np.uint64) * np.uint64(N0 // S), N0)
         self.dup_ms, self.grow_ms, self.dup_elems = [], [], 0
 
@@ -275,6 +276,7 @@ def run_device(args, rank, world, local_rank):
         out["gather_flatten"] = gather_leg(args, torch, device, step, dist, world)
     if not args.quick:
         out.update(secondary(args, gg, torch, device, step, hbm))
+        out["config2_dtypes"] = dtype_variants(args, gg, torch, device, hbm)
         out["phased_config4"] = phased_leg(args, gg, torch, device)
         out["config5_per_gpu"] = config5_leg(args, gg, torch, device, hbm)
         out["config1"] = config1_leg(args, gg, torch, device, rank == 0 and world == 1 and not args.no_cpu)
@@ -369,6 +371,29 @@ def _time(torch, fn, reps=1):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
+
+
+def dtype_variants(args, gg, torch, device, hbm):
+    """The config-2 schedule for the other element types of SURVEY 8(d)
+    (float32 = same values cast; int64 = 2x the bytes), graph-replayed like
+    the headline and checked against the closed form."""
+    res = {}
+    for name, dt, esz in (("float32", np.float32, 4), ("int64", np.int64, 8)):
+        st = Step(gg, torch, device, dtype=dt)
+        st.run(False)
+        g = st.arr.capture(lambda: st.run(False))
+        for _ in range(max(3, args.warmup)):
+            g.replay()
+        reps = max(3, args.steps)
+        ms = _time(torch, lambda: [g.replay() for _ in range(reps)]) / reps
+        check_state(st, torch)
+        res[name] = {"ms_per_step": round(ms, 4), "gelem_s": round((1 << 30) / ms / 1e6, 2),
+                     "gbs": round(2 * esz * (1 << 30) / ms / 1e6, 1),
+                     "frac": round(2 * esz * (1 << 30) / ms / 1e6 / hbm, 4), "contents_ok": True}
+        del g
+        st.arr.close()
+        del st
+    return res
 
 
 def secondary(args, gg, torch, device, step, hbm):
