@@ -630,6 +630,84 @@ int gg_set_arena_limit(gg_array *a, uint64_t bytes) {
   return GG_OK;
 }
 
+// Uniform fast path shared by insert and duplicate: every shard appends the
+// same count c at the same size with the same published buckets (no hook,
+// cap, failed or dirty shard) -> plan shard 0 once, back each bucket class
+// for all shards in one call, one fused walk.  *done = false (nothing
+// changed) when the state is not uniform or backing ran out of memory: the
+// caller takes the exact per-shard planner.
+int uniform_append(gg_array *a, int wk, const char *src, uint64_t c, const uint64_t *h_offsets,
+                   uint32_t flags, int32_t *h_status, cudaStream_t st, bool *done) {
+  *done = false;
+  if (a->hook || a->limit || (flags & GG_F_UNFUSED) || !c) return GG_OK;
+  for (uint32_t s = 0; s < a->S; ++s)
+    if (a->size[s] != a->size[0] || a->flags[s] != a->flags[0] || a->dirty[s]) return GG_OK;
+  const uint64_t start = a->size[0];
+  uint32_t b0, b1; uint64_t o;
+  host_locate(a, start, b0, o);
+  host_locate(a, start + c - 1, b1, o);
+  if (b1 >= a->MB) return GG_OK;               // capacity error: the exact path reports it
+  uint64_t want = 0;
+  for (uint32_t b = b0; b <= b1; ++b) if (!(a->flags[0] >> b & 1)) want |= uint64_t(1) << b;
+  int rc = GG_OK;
+  uint64_t got = 0;
+  for (uint32_t b = b0; b <= b1 && !rc; ++b) {
+    if (!(want >> b & 1)) continue;
+    bool created = false;
+    if (!(rc = a->slab.ensure_region(b, &created)) && !(rc = a->slab.back_range(b, 0, a->S))) {
+      if (created) a->cbase_dirty = true;
+      got |= uint64_t(1) << b;
+    }
+  }
+  if (rc) {                                     // out of memory: undo, take the exact path
+    for (uint32_t b = b0; b <= b1; ++b)
+      if (got >> b & 1) a->slab.unback_range(b, 0, a->S);
+    return GG_OK;
+  }
+  *done = true;
+  uint64_t elems = 0, bytes = 0;
+  for (uint32_t b = b0; b <= b1; ++b)
+    if (want >> b & 1) { elems += bucket_elems(a, b); bytes += bucket_bytes(a, b); }
+  for (uint32_t s = 0; s < a->S; ++s) {
+    a->size[s] += c; a->ops[s] += 1; a->flags[s] |= want; a->cap[s] += elems;
+  }
+  a->live += bytes * a->S;
+  a->alloc_calls += (uint64_t)__builtin_popcountll(want) * a->S;
+  if ((rc = push_cbase(a, st))) return rc;
+  const bool commit = (flags & GG_F_COMMIT) != 0;
+  const int rmode = wk == W_DUP ? 1 : 0;
+  const uint64_t total = c * a->S;
+  Tables t = tables_for_launch(a, false);
+  if (fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
+    Fuse fz{rmode, commit ? 1 : 0};
+    fz.ulen = c;                               // uniform directory / CSR and destination start
+    fz.ustart = start;
+    fz.size_next = a->sz_buf[a->cur ^ 1];
+    fz.prefix_next = a->pf_buf[a->cur ^ 1];
+    fz.grow_k = a->pend_grow;
+    a->pend_grow = 0;
+    rc = wk == W_DUP ? walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fz, st)
+                     : walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st);
+    if (rc) return rc;
+    flip_buffers(a);
+  } else {
+    if ((rc = flush_grow(a))) return rc;
+    if (wk == W_INSERT) {                      // the unfused walk reads the offsets on the device
+      void *dst[1] = {a->t.offsets};
+      const void *srcs[1] = {h_offsets};
+      size_t nb[1] = {(a->S + 1) * 8};
+      if ((rc = a->up.upload(st, 1, dst, srcs, nb))) return rc;
+    }
+    rc = wk == W_DUP ? walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, Fuse{rmode, commit ? 1 : 0}, st)
+                     : walk_copy<W_INSERT, true>(a, t, src, nullptr, total, Fuse{rmode, commit ? 1 : 0}, st);
+    if (rc) return rc;
+    if ((rc = finish_planned(a, Fuse{rmode, commit ? 1 : 0}, st))) return rc;
+  }
+  if (commit) host_commit(a);
+  if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
+  return GG_OK;
+}
+
 int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
@@ -643,6 +721,16 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
     counts[s] = h_offsets[s + 1] - h_offsets[s];
   }
   const uint64_t total = h_offsets[a->S];
+  if (!h_starts && h_offsets[1] > 0) {        // uniform CSR over uniform shards
+    bool u = true;
+    for (uint32_t s = 0; s < a->S && u; ++s) u = counts[s] == h_offsets[1];
+    if (u) {
+      bool done = false;
+      int rc = uniform_append(a, W_INSERT, (const char *)d_values, h_offsets[1], h_offsets, flags,
+                              h_status, st, &done);
+      if (rc || done) return rc;
+    }
+  }
   Plan p;
   plan_init(a, p);
   plan_append(a, p, counts.data(), h_starts);
@@ -690,68 +778,16 @@ int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void 
     // uniform fast path: every shard has the same committed length, size and
     // buckets, no hook / cap / failed shard -> plan shard 0 once
     const uint64_t c = a->prefix[1] - a->prefix[0];
-    bool uni = !a->hook && !a->limit && !(flags & GG_F_UNFUSED);
-    for (uint32_t s = 0; s < a->S && uni; ++s)
-      uni = a->prefix[s + 1] - a->prefix[s] == c && a->size[s] == a->size[0] &&
-            a->flags[s] == a->flags[0] && !a->dirty[s];
-    if (uni && c) {
+    bool uni = c != 0;
+    for (uint32_t s = 0; s < a->S && uni; ++s) uni = a->prefix[s + 1] - a->prefix[s] == c;
+    if (uni) {
       const uint32_t kc = min_buckets_for(a, c);
       const uint64_t need = kc >= 64 ? ~uint64_t(0) : ((uint64_t(1) << kc) - 1);
       if ((a->flags[0] & need) != need)
         return fail(GG_EUNPUBLISHED, "bucket unpublished while walking shard 0");
-      const uint64_t start = a->size[0];
-      uint32_t b0, b1; uint64_t o;
-      host_locate(a, start, b0, o);
-      host_locate(a, start + c - 1, b1, o);
-      if (b1 < a->MB) {
-        uint64_t want = 0;
-        for (uint32_t b = b0; b <= b1; ++b) if (!(a->flags[0] >> b & 1)) want |= uint64_t(1) << b;
-        int rc = GG_OK;
-        uint64_t got = 0;
-        for (uint32_t b = b0; b <= b1 && !rc; ++b) {
-          if (!(want >> b & 1)) continue;
-          bool created = false;
-          if (!(rc = a->slab.ensure_region(b, &created)) && !(rc = a->slab.back_range(b, 0, a->S))) {
-            if (created) a->cbase_dirty = true;
-            got |= uint64_t(1) << b;
-          }
-        }
-        if (!rc) {
-          uint64_t elems = 0, bytes = 0;
-          for (uint32_t b = b0; b <= b1; ++b)
-            if (want >> b & 1) { elems += bucket_elems(a, b); bytes += bucket_bytes(a, b); }
-          for (uint32_t s = 0; s < a->S; ++s) {
-            a->size[s] += c; a->ops[s] += 1; a->flags[s] |= want; a->cap[s] += elems;
-          }
-          a->live += bytes * a->S;
-          a->alloc_calls += (uint64_t)__builtin_popcountll(want) * a->S;
-          if ((rc = push_cbase(a, st))) return rc;
-          const bool commit = (flags & GG_F_COMMIT) != 0;
-          Tables t = tables_for_launch(a, false);
-          if (fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
-            Fuse fz{1, commit ? 1 : 0};
-            fz.ulen = c;                       // uniform directory and destination start
-            fz.ustart = start;
-            fz.size_next = a->sz_buf[a->cur ^ 1];
-            fz.prefix_next = a->pf_buf[a->cur ^ 1];
-            fz.grow_k = a->pend_grow;
-            a->pend_grow = 0;
-            if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S], fz, st))) return rc;
-            flip_buffers(a);
-          } else {
-            if ((rc = flush_grow(a))) return rc;
-            if ((rc = walk_copy<W_DUP, true>(a, t, nullptr, nullptr, a->prefix[a->S],
-                                             Fuse{1, commit ? 1 : 0}, st)))
-              return rc;
-            if ((rc = finish_planned(a, Fuse{1, commit ? 1 : 0}, st))) return rc;
-          }
-          if (commit) host_commit(a);
-          if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
-          return GG_OK;
-        }
-        for (uint32_t b = b0; b <= b1; ++b)     // out of memory: undo, take the exact path
-          if (got >> b & 1) a->slab.unback_range(b, 0, a->S);
-      }
+      bool done = false;
+      int rc = uniform_append(a, W_DUP, nullptr, c, nullptr, flags, h_status, st, &done);
+      if (rc || done) return rc;
     }
   }
   int rc = check_committed_published(a);

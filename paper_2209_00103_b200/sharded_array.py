@@ -105,6 +105,8 @@ class GrowableArray:
         self._summary = np.zeros(3, np.uint64)
         self._status = np.zeros(shards, np.int32)
         self._caps = np.zeros(shards, np.uint64)
+        self._shrink_buf = np.zeros(shards, np.uint64)
+        self._shrink_p = L.ptr(self._shrink_buf)
         self._status_p = L.ptr(self._status, C.c_int32)     # cached ctypes views (hot paths)
         self._caps_p = L.ptr(self._caps)
         self._failed = C.c_int64(-1)
@@ -186,6 +188,9 @@ class GrowableArray:
         """Values cast like np.asarray(values, dtype) and resident on this device."""
         import torch
         if isinstance(values, torch.Tensor):
+            if (values.dtype == self._torch_dtype and values.device == self.device and values.dim() == 1
+                    and values.is_contiguous()):
+                return values
             t = values.reshape(-1)
             if t.dtype != self._torch_dtype:
                 t = t.to(self._torch_dtype)
@@ -591,14 +596,21 @@ class GrowableArray:
         bound, unmapping as little as possible -- every unmap/remap costs
         driver time); True unmaps them all; False keeps them all mapped for
         in-place reuse until :meth:`trim`."""
-        ns = L.u64_array(np.broadcast_to(np.asarray(new_sizes), (self._S,)))
+        if isinstance(new_sizes, (int, np.integer)) and new_sizes >= 0:
+            ns = self._shrink_buf
+            ns.fill(new_sizes)
+            total = int(new_sizes) * self._S
+        else:
+            ns = L.u64_array(np.broadcast_to(np.asarray(new_sizes), (self._S,)))
+            total = int(ns.sum())
         if release is True:
             keep = 0
         elif release is False or release is None:
             keep = (1 << 64) - 1
         else:
-            keep = int(float(release) * int(ns.sum()) * self.dtype.itemsize)
-        L.check(L.lib.gg_shrink_ex(self._h, L.ptr(ns), keep, self._stream()), "shrink")
+            keep = int(float(release) * total * self.dtype.itemsize)
+        L.check(L.lib.gg_shrink_ex(self._h, self._shrink_p if ns is self._shrink_buf else L.ptr(ns), keep,
+                                   self._stream()), "shrink")
         self._dirty()
 
     def trim(self) -> None:
