@@ -418,3 +418,41 @@ def test_deferred_grow_is_flushed_by_every_device_reader(gg):
     st = a._parity_state()
     assert st["sizes"] == [int(x) for x in o.size] and st["caps"] == [int(x) for x in o.capacity]
     assert a.flatten().tobytes() == o.flatten().tobytes()
+
+
+@pytest.mark.parametrize("fuse", [1, 0])
+@pytest.mark.parametrize("S", [64, 4100])
+def test_uniform_insert_fast_path_vs_oracle(gg, fuse, S):
+    """Uniform CSR inserts over uniform shards take the plan-shard-0-once path
+    (fused metadata CTA, or the unfused walk + metadata kernel when the CTA is
+    off / S > 4096); interleaved with duplicates, grows and a shrink, the
+    state and contents equal the oracle's."""
+    import torch
+    from paper_2209_00103_b200 import _lib as L
+    fb = 8
+    L.lib.gg_set_fuse(fuse)
+    try:
+        a = gg.GrowableArray(S, fb, dtype=np.int32)
+        o = O.OracleGGArray(S, fb, dtype=np.int32)
+        base = 0
+        for step, c in enumerate([3, 8, 13, 40, 1, 100]):
+            vals = np.arange(base, base + c * S, dtype=np.int32)
+            base += c * S
+            offs = np.arange(S + 1, dtype=np.uint64) * np.uint64(c)
+            a.insert_csr(torch.from_numpy(vals).cuda(), offs)
+            o.insert_parallel([vals[s * c:(s + 1) * c] for s in range(S)])
+            if step % 2:
+                a.insert_duplicate(); o.insert_duplicate()
+            if step == 3:
+                a.grow(4 * a.committed_size); o.grow(4 * o.committed_size)
+            if step == 4:
+                a.shrink(17, release=False); o.shrink(np.full(S, 17))
+            st = a._parity_state()
+            assert st["sizes"] == [int(x) for x in o.size], step
+            assert st["caps"] == [int(x) for x in o.capacity], step
+            assert st["prefix"] == [int(x) for x in o.prefix], step
+        assert a.flatten().tobytes() == o.flatten().tobytes()
+        dev = a.device_state()
+        assert np.array_equal(dev["sizes"], a._host()["sizes"])
+    finally:
+        L.lib.gg_set_fuse(1)
