@@ -318,6 +318,33 @@ def gather_leg(args, torch, device, step, dist, world):
         g.close()
         del g
         torch.cuda.empty_cache()
+        nccl = None
+        if dist.get_backend() == "nccl":
+            # the library baseline for the same exchange: local K-flatten into
+            # a staging buffer, then NCCL gather to the root
+            local = step.arr.flatten_device()
+            glist = [torch.empty_like(local) for _ in range(world)] if dist.get_rank() == 0 else None
+
+            def nccl_gather():
+                step.arr.flatten_device(out=local)
+                dist.gather(local, glist, dst=0)
+            nccl_gather()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record()
+            for _ in range(k):
+                nccl_gather()
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / k], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nms = float(t.item())
+            nccl = {"ms": round(nms, 4), "nvlink_gbs_into_root": round(nvlink / (nms * 1e-3) / 1e9, 1),
+                    "method": "flatten_device + torch.distributed.gather (NCCL)"}
+            if dist.get_rank() == 0:
+                nccl["root_slice_ok"] = bool(torch.equal(glist[0], local))
+            del local, glist
+            torch.cuda.empty_cache()
         # even rebalance: every rank ends with N/G of the global flat array
         d.rebalance_flat_peer()
         dist.barrier()
@@ -334,7 +361,8 @@ def gather_leg(args, torch, device, step, dist, world):
                 "nvlink_gbs_into_root": round(nvlink / (ms * 1e-3) / 1e9, 1),
                 "root_slice_ok": ok, "method": "fused K-flatten into the root buffer (CUDA IPC)",
                 "rebalance_ms_incl_setup": round(rb_ms, 3),
-                "rebalance": "even slices N/G per rank, K-flatten ranges into the owners' buffers"}
+                "rebalance": "even slices N/G per rank, K-flatten ranges into the owners' buffers",
+                "nccl_baseline": nccl}
     except Exception as exc:                          # report, never lose the bench line
         return {"error": repr(exc)[:300]}
 
