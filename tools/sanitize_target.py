@@ -42,3 +42,17 @@ for algo in ("atomic", "warp", "block"):
     st.insert_batch(torch.arange(1000, dtype=torch.int32, device="cuda"), algo=algo)
 torch.cuda.synchronize()
 print("sanitize target done")
+# uniform CSR inserts over uniform shards (plan-shard-0-once path), fused and unfused metadata
+from paper_2209_00103_b200 import _lib as _L
+for fuse in (1, 0):
+    _L.lib.gg_set_fuse(fuse)
+    u = gg.GrowableArray(64, 8, dtype=np.int32)
+    for c in (3, 13, 40):
+        u.insert_csr(torch.arange(64 * c, dtype=torch.int32, device="cuda"),
+                     np.arange(65, dtype=np.uint64) * np.uint64(c))
+        u.insert_duplicate()
+    assert u.committed_size == ((3 * 2 + 13) * 2 + 40) * 2 * 64
+    u.flatten_device()
+_L.lib.gg_set_fuse(1)
+torch.cuda.synchronize()
+print("uniform insert ok")
