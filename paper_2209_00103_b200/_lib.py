@@ -14,7 +14,7 @@ import numpy as np
 from .errors import CapacityError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ggarray.so")
+LIB_PATH = os.environ.get("GG_LIB_PATH") or os.path.join(_HERE, "_ggarray.so")   # override: A/B builds (tools/)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
