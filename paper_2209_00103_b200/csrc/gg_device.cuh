@@ -905,6 +905,30 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
   const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   for (uint64_t c0 = wid * 32 * U; c0 < nvec; c0 += nwarps * 32 * U) {
     uint32_t s = warp_find_shard(pre, t.S, c0 * VE);  // warp-uniform 32-ary search
+    {
+      // warp-uniform fast path: the warp's 32*U vectors resolve (global index
+      // -> shard -> bucket) to one aligned run inside one bucket of shard s --
+      // one locate for the span instead of one per vector
+      const uint64_t g0 = c0 * VE, span = 32ull * U * VE;
+      const uint64_t lo = pre[s], hi = pre[s + 1];
+      uint32_t b0; uint64_t o0;
+      locate(g0 - lo, t.log2fb, b0, o0);
+      if (g0 + span <= hi && (o0 % VE) == 0 && o0 + span <= (1ull << (t.log2fb + b0))) {
+        T *base = (T *)slot_addr(scb, s, b0, lg0) + o0;
+        uint4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = M::ld((const uint4 *)(base + (size_t)(lane + 32u * u) * VE));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          union { uint4 q; T e[VE]; } x;
+          x.q = r[u];
+#pragma unroll
+          for (uint32_t j = 0; j < VE; ++j) x.e[j] = AddOp<T>::apply(x.e[j], addend);
+          M::st((uint4 *)(base + (size_t)(lane + 32u * u) * VE), x.q);
+        }
+        continue;
+      }
+    }
     uint4 r[U];
     T *p[U];
     bool vec[U];

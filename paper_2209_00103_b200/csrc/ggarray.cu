@@ -436,7 +436,8 @@ int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode,
     const uint64_t nvec = (total * sizeof(T) + 15) / 16;
     // sweep (tools/sweep.py): rw_g peaks at U = 4 (U = 8 spills the per-vector
     // pointers / masks into a lower occupancy)
-    const uint32_t U = std::min<uint32_t>(walk_unroll(a, total, W_RW), 4u);
+    static const uint32_t ucap = [] { const char *e = getenv("GG_RWG_U"); return e ? (uint32_t)atoi(e) : 4u; }();
+    const uint32_t U = std::min<uint32_t>(walk_unroll(a, total, W_RW), ucap);
     const uint64_t grid = (nvec + kThreads * U - 1) / (kThreads * U);
     for (uint32_t p = 0; p < passes; ++p) {
       cudaError_t e;
