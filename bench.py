@@ -60,10 +60,11 @@ def _peaks():
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """Polls NVML (SM clock + throttle reasons) every 5 ms on a thread while the
-    timed region runs; falls back to nothing if NVML is unavailable."""
+    """Polls NVML (SM clock + throttle reasons) every 1 ms on a thread while the
+    timed region runs (the headline region is ~13 ms); falls back to nothing
+    if NVML is unavailable."""
 
-    def __init__(self, index: int, period_s: float = 0.005):
+    def __init__(self, index: int, period_s: float = 0.001):
         self.index, self.period, self.rows, self._stop = index, period_s, [], None
 
     def __enter__(self):
@@ -108,7 +109,7 @@ class ClockSampler:
         sm = sorted(r[0] for r in self.rows)
         reasons = sorted({k for _, m in self.rows for k, bit in bits.items() if m & bit})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml (5 ms poll during the timed region)"}
+                "samples": len(self.rows), "source": "nvml (1 ms poll during the timed region)"}
 
 
 # --------------------------------------------------------------------------- device legs
