@@ -762,6 +762,60 @@ __global__ void k_copy_db(uint64_t *size_dst, const uint64_t *size_src, uint64_t
   }
 }
 
+// Tiles whose pieces are short (many LFVectors with a few elements each:
+// small per-shard batches, ragged directories) are walked element by
+// element: every thread resolves its own elements' shard (a bisect inside
+// the tile's shard range, or a division for a uniform directory) and bucket,
+// instead of the whole CTA stepping through the pieces one after another.
+template <int ESZ, int W, typename T, bool PLANNED>
+__device__ __forceinline__ void element_tile(const Tables &t, char *const *scb, const DirV &dir,
+                                             uint32_t s_lo, uint32_t s_hi, uint64_t g, uint64_t gend,
+                                             const char *flat_src, char *flat_dst, T addend,
+                                             uint32_t reps, const Fuse &fz, uint32_t lg0) {
+  typedef typename ElemT<ESZ>::T E;
+  for (uint64_t x = g + threadIdx.x; x < gend; x += blockDim.x) {
+    uint32_t s;
+    if (dir.u) {
+      s = (uint32_t)(x / dir.u);
+    } else {                                   // largest s in [s_lo, s_hi] with dir[s] <= x
+      uint32_t lo = s_lo, hi = s_hi + 1;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (dir.p[mid] <= x) lo = mid; else hi = mid;
+      }
+      s = lo;
+    }
+    const uint64_t k = x - dir[s];
+    const uint32_t ctl = (W == W_INSERT || W == W_DUP) && !PLANNED && t.ctl ? t.ctl[s] : kCtlWrite;
+    const char *sp;
+    if constexpr (W == W_INSERT) {
+      sp = flat_src + x * ESZ;
+    } else {
+      uint32_t b; uint64_t o;
+      locate(k, t.log2fb, b, o);
+      sp = slot_addr(scb, s, b, lg0) + o * ESZ;
+    }
+    if constexpr (W == W_RW) {
+      T v = *(const T *)sp;
+      for (uint32_t r = 0; r < reps; ++r) v = AddOp<T>::apply(v, addend);
+      *(T *)sp = v;
+    } else {
+      char *dp;
+      bool dst_ok = true;
+      if constexpr (W == W_FLATTEN) {
+        dp = flat_dst + x * ESZ;
+      } else {
+        uint32_t b; uint64_t o;
+        locate((PLANNED ? (fz.ulen ? fz.ustart : t.size[s]) : t.start[s]) + k, t.log2fb, b, o);
+        if (!PLANNED) dst_ok = t.flag[(size_t)s * t.MB + b] == kFlagPublished;
+        dp = slot_addr(scb, s, b, lg0) + o * ESZ;
+      }
+      if (dst_ok && (ctl & (kCtlWrite | kCtlZero)))
+        *(E *)dp = (ctl & kCtlWrite) ? *(const E *)sp : E(0);
+    }
+  }
+}
+
 // The tile walker: ONE tile per CTA (a non-persistent grid streams ~15%
 // faster than a persistent grid-stride loop on B200, tools/probe), tile =
 // U vectors per thread.  The work space [0, total) is partitioned among
@@ -774,7 +828,7 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
                                               uint64_t total, T addend, uint32_t reps,
                                               uint32_t tile, Fuse fz) {
   __shared__ char *scb[kMaxBuckets];
-  __shared__ uint32_t s_sh;
+  __shared__ uint32_t s_sh, s_last_sh;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   pdl_begin();
   if constexpr (PLANNED) {
@@ -810,6 +864,23 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
   }
   if (!(fast && vector_tile<ESZ, W, T, U, LS>(t, scb, dir, s, dbase, g, gend, flat_src, flat_dst,
                                               addend, reps))) {
+    // short pieces (average < 128 elements): element by element
+    uint32_t s_last;
+    if (fz.ulen) {
+      s_last = (uint32_t)((gend - 1) / fz.ulen);
+    } else {
+      if (tid < 32) {
+        const uint32_t sl = warp_find_shard(dir.p, t.S, gend - 1);
+        if (tid == 0) s_last_sh = sl;
+      }
+      __syncthreads();
+      s_last = s_last_sh;
+    }
+    if (gend - g < 128ull * (s_last - s + 1)) {
+      element_tile<ESZ, W, T, PLANNED>(t, scb, dir, s, s_last, g, gend, flat_src, flat_dst, addend, reps,
+                                       fz, lg0);
+      return;
+    }
     while (g < gend) {
       uint64_t shard_end = dir[s + 1];
       while (shard_end <= g) { ++s; shard_end = dir[s + 1]; }

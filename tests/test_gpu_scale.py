@@ -456,3 +456,53 @@ def test_uniform_insert_fast_path_vs_oracle(gg, fuse, S):
         assert np.array_equal(dev["sizes"], a._host()["sizes"])
     finally:
         L.lib.gg_set_fuse(1)
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.int32, np.float64])
+def test_short_piece_tiles_vs_oracle(gg, dtype):
+    """Tiles covering many LFVectors with a few elements each take the
+    element-by-element walk (insert, duplicate, r/w, flatten, flatten_range):
+    uniform 1 element per shard, then ragged 0..5 per shard, with a failing
+    allocator hook (the unplanned, per-shard-controlled walk) in between."""
+    import torch
+    from paper_2209_00103_b200 import ShardInsertError
+    S, fb = 1000, 2
+    rng = np.random.default_rng(7)
+    a = gg.GrowableArray(S, fb, dtype=dtype)
+    o = O.OracleGGArray(S, fb, dtype=dtype)
+    one = np.arange(S).astype(dtype)
+    a.insert_parallel([one[s:s + 1] for s in range(S)]); o.insert_parallel([one[s:s + 1] for s in range(S)])
+    for r in range(3):
+        cnt = rng.integers(0, 6, S)
+        vals = rng.integers(0, 100, int(cnt.sum())).astype(dtype)
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        batches = [vals[off[s]:off[s + 1]] for s in range(S)]
+        a.insert_parallel(batches); o.insert_parallel(batches)
+        a.insert_duplicate(); o.insert_duplicate()
+        a.rw_add(1); o.rw_add(1)
+        st = a._parity_state()
+        assert st["sizes"] == [int(x) for x in o.size], r
+        assert st["prefix"] == [int(x) for x in o.prefix], r
+        assert a.flatten().tobytes() == o.flatten().tobytes(), r
+    n = a.committed_size
+    lo, hi = 123, n - 77
+    assert np.array_equal(a.flatten_range(lo, hi).cpu().numpy(), o.flatten()[lo:hi])
+    # failing allocator on every 3rd shard's next bucket: unplanned walk with ctl words
+    calls = {"n": 0}
+
+    def alloc(nelem):
+        calls["n"] += 1
+        if calls["n"] % 3 == 0:
+            raise MemoryError("injected")
+        return np.zeros(nelem, dtype)
+    b = gg.GrowableArray(S, fb, dtype=dtype, allocator=alloc)
+    ob = O.OracleGGArray(S, fb, dtype=dtype, allocator=alloc)
+    batches = [np.full(3, s % 100, dtype) for s in range(S)]
+    calls["n"] = 0
+    with pytest.raises(ShardInsertError) as e1:
+        b.insert_parallel(batches)
+    calls["n"] = 0
+    with pytest.raises(O.ShardInsertError) as e2:
+        ob.insert_parallel(batches)
+    assert sorted(e1.value.failures) == sorted(e2.value.failures)
+    assert b._parity_state()["sizes"] == [int(x) for x in ob.size]

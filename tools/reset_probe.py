@@ -50,3 +50,22 @@ gr = a.capture(reset_only)
 print(json.dumps({"lib": os.environ.get("GG_LIB_PATH", "default"),
                   "step_us": round(1e3 * timed(gs, 50), 2),
                   "reset_plus_round_us": round(1e3 * timed(gr, 20) / 20, 2)}))
+# components: 20 x shrink(0) alone; 20 x (shrink(0) + 2^20 insert)
+
+
+def shrinks():
+    for _ in range(20):
+        a.shrink(0, release=False)
+
+
+def pairs():
+    for _ in range(20):
+        a.shrink(0, release=False)
+        a.insert_csr(vals, offs)
+
+
+step()
+g1 = a.capture(shrinks)
+g2 = a.capture(pairs)
+print(json.dumps({"shrink_us": round(1e3 * timed(g1, 20) / 20, 2),
+                  "shrink_plus_insert_us": round(1e3 * timed(g2, 20) / 20, 2)}))
