@@ -116,6 +116,7 @@ __device__ inline int alloc_bucket(const gg_device_view &t, uint32_t s, uint32_t
   atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
   __threadfence();
   st_release(f, kFlagPublished);
+  __threadfence();                 // the pmask bit never becomes visible before the flag
   atomicOr(&t.pmask[s], 1ull << b);
   return 1;
 }
@@ -130,8 +131,11 @@ __device__ inline bool ensure_buckets(const gg_device_view &t, uint32_t s, uint6
   locate(start, t.log2fb, b0, o);
   locate(start + n - 1, t.log2fb, b1, o);
   bool ok = b1 < t.MB;
+  // the once-flag (acquire) is the authority, not pmask: a bucket another warp
+  // is still allocating (flag 1) must be waited for, or this warp's lanes
+  // would find it unpublished and drop their stores
   for (uint32_t b = b0; ok && b <= b1; ++b)
-    if (!((t.pmask[s] >> b) & 1ull) && alloc_bucket(t, s, b) < 0) ok = false;
+    if (ld_acquire(t.flag + (size_t)s * t.MB + b) != kFlagPublished && alloc_bucket(t, s, b) < 0) ok = false;
   if (!ok) atomicOr(&t.status[s], kStatusNoMem);
   return ok;
 }

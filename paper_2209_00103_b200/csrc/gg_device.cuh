@@ -68,27 +68,52 @@ __device__ __forceinline__ void warp_alloc_range(const Tables &t, uint32_t s, ui
   }
 }
 
-// Publish buckets `want` of shard s (host-planned, slots already backed) from
-// the one thread that owns s in this launch: slot pointer + once-flag per
-// bucket, the shard's pmask (pm = its value at kernel start) and capacity,
-// and one allocation-count update per warp.  Plain stores: the kernel
-// boundary orders them before any reader.  Call with the full warp.
-__device__ __forceinline__ void publish_buckets(const Tables &t, char *const *scb, uint32_t s,
-                                                unsigned long long pm, unsigned long long want,
-                                                uint32_t lg0) {
+// Publish buckets (host-planned, slots already backed) for a whole CTA whose
+// thread i handles shard base + i with mask `want` (every thread calls it,
+// uniform control flow, blockDim <= NT): the shard's pmask (pm = its value at
+// kernel start) and capacity, one allocation-count update per warp, then the
+// bucket table rows (slot pointer + once-flag per bucket).  A row is t.MB
+// entries, so thread-per-shard stores land MB entries apart (one sector per
+// store, ~1.3 us per bucket and 512 shards from one SM); instead the CTA ORs
+// the masks and writes the [bmin, bmax] window of its rows with consecutive
+// threads on consecutive entries.  Plain stores: the kernel boundary orders
+// them before any reader.
+template <int NT>
+__device__ __forceinline__ void publish_buckets_cta(const Tables &t, char *const *scb, uint32_t base,
+                                                    unsigned long long pm, unsigned long long want,
+                                                    uint32_t lg0) {
+  __shared__ unsigned long long w_sh[NT];
+  __shared__ unsigned long long or_sh[NT / 32];
+  const uint32_t s = base + threadIdx.x, lane = threadIdx.x & 31;
   uint64_t add = 0;
-  for (unsigned long long m = want; m; m &= m - 1) {
-    const uint32_t b = __ffsll((long long)m) - 1;
-    t.ptr[(size_t)s * t.MB + b] = scb[b] + ((uint64_t)s << max(lg0 + b, 4u));
-    t.flag[(size_t)s * t.MB + b] = kFlagPublished;
-    add += 1ull << (t.log2fb + b);
-  }
+  for (unsigned long long m = want; m; m &= m - 1) add += 1ull << (t.log2fb + __ffsll((long long)m) - 1);
   if (want) {
     t.pmask[s] = pm | want;
     atomicAdd((unsigned long long *)&t.cap[s], (unsigned long long)add);
   }
   const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(want));
-  if ((threadIdx.x & 31) == 0 && tot) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)tot);
+  if (lane == 0 && tot) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)tot);
+  w_sh[threadIdx.x] = want;
+  const uint32_t olo = __reduce_or_sync(0xffffffffu, (uint32_t)want);
+  const uint32_t ohi = __reduce_or_sync(0xffffffffu, (uint32_t)(want >> 32));
+  if (lane == 0) or_sh[threadIdx.x >> 5] = ((unsigned long long)ohi << 32) | olo;
+  __syncthreads();
+  unsigned long long u = 0;
+  for (uint32_t i = 0; i < (blockDim.x >> 5); ++i) u |= or_sh[i];
+  if (u) {
+    const uint32_t bmin = __ffsll((long long)u) - 1, bmax = 63 - __clzll((long long)u);
+    const uint32_t W = bmax - bmin + 1;
+    const uint32_t rows = base < t.S ? min(blockDim.x, t.S - base) : 0u;
+    for (uint32_t e = threadIdx.x; e < rows * W; e += blockDim.x) {
+      const uint32_t r = e / W, b = bmin + e % W;
+      if (w_sh[r] >> b & 1) {
+        const uint32_t ss = base + r;
+        t.ptr[(size_t)ss * t.MB + b] = scb[b] + ((uint64_t)ss << max(lg0 + b, 4u));
+        t.flag[(size_t)ss * t.MB + b] = kFlagPublished;
+      }
+    }
+  }
+  __syncthreads();                       // w_sh / or_sh are reused by the next call
 }
 
 // Reservation + bucket allocation, one thread per shard: one atomicAdd on the
@@ -148,7 +173,8 @@ __global__ void __launch_bounds__(256) k_grow(Tables t, uint32_t uniform_k) {
   const uint32_t lim = !live ? 0u : (uniform_k != ~0u ? uniform_k : (t.ctl[s] & kCtlLimitMask));
   __syncthreads();
   const unsigned long long want = (lim >= 64 ? ~0ull : ((1ull << lim) - 1ull)) & ~pm;
-  publish_buckets(t, scb, live ? s : 0u, pm, live ? want : 0ull, t.log2fb + (31u - __clz(t.esz)));
+  publish_buckets_cta<256>(t, scb, blockIdx.x * blockDim.x, pm, live ? want : 0ull,
+                           t.log2fb + (31u - __clz(t.esz)));
 }
 
 __global__ void k_new_bucket(Tables t, uint32_t s, uint32_t b, int *won) {
@@ -691,7 +717,7 @@ __device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &
       want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~pm;
     }
     if (live) t.count[s] = c;
-    publish_buckets(t, scb, live ? s : 0u, pm, want, lg0);
+    publish_buckets_cta<1024>(t, scb, base, pm, live ? want : 0ull, lg0);
     if (fz.commit) {
       uint64_t tot;
       const uint64_t ex = block_exclusive_scan(live ? nsz : 0, &tot, ws);
@@ -738,7 +764,7 @@ __device__ void planned_metadata_db(const Tables &t, char *const *scb, const Fus
       t.count[s] = c;
       fz.size_next[s] = nsz;            // the batch's reservation: one update per LFVector
     }
-    publish_buckets(t, scb, live ? s : 0u, pm, live ? want : 0ull, lg0);
+    publish_buckets_cta<256>(t, scb, base, pm, live ? want : 0ull, lg0);
     if (fz.commit) {
       uint64_t tot;
       const uint64_t ex = block_exclusive_scan(live ? nsz : 0, &tot, ws);
@@ -948,7 +974,7 @@ __global__ void __launch_bounds__(1024) k_meta_grow(Tables t, Fuse fz, uint32_t 
     const uint32_t s = base + threadIdx.x;
     const bool live = s < t.S;
     const unsigned long long pm = live ? t.pmask[s] : 0ull;
-    publish_buckets(t, scb, live ? s : 0u, pm, live ? (all & ~pm) : 0ull, lg0);
+    publish_buckets_cta<1024>(t, scb, base, pm, live ? (all & ~pm) : 0ull, lg0);
   }
 }
 

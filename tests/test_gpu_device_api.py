@@ -71,3 +71,28 @@ def test_device_append_oom_keeps_reservation(gg):
     assert set(e.value.failures) <= {0, 1} and e.value.failures
     assert all(isinstance(x, MemoryError) for x in e.value.failures.values())
     assert a.total_size == 100_000                        # reservations kept
+
+
+def test_push_if_repeated_contention(gg):
+    """Many repetitions of the contended warp / block appends: a bucket another
+    warp is still allocating must be waited for (the once-flag is read with
+    acquire order), never written through a missing pointer.  Before the fix
+    about 1 run in 150 lost a run of appends."""
+    fails = []
+    for it in range(60):
+        for mode in ("warp", "block"):
+            S, fb, grid = (7, 4, 64) if it % 2 else (32, 32, 512)
+            rng = np.random.default_rng(10_000 + it)
+            n = 100_000
+            vals = rng.integers(-2**31, 2**31 - 1, n, dtype=np.int64).astype(np.int32)
+            pred = rng.random(n) < 0.37
+            a = gg.GrowableArray(S, fb, dtype=np.int32)
+            a.insert_parallel([np.arange(int(k), dtype=np.int32) for k in rng.integers(0, 100, S)])
+            pre = [a.shards[s].size for s in range(S)]
+            a.push_if(vals, pred, mode=mode, grid=grid)
+            exp = _expected(vals, pred, S, grid)
+            for s in range(S):
+                if not np.array_equal(np.sort(a.shards[s].to_numpy()[pre[s]:]), exp[s]):
+                    fails.append((it, mode, s))
+            a.close()
+    assert not fails, fails[:5]
