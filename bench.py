@@ -80,17 +80,25 @@ class ClockSampler:
         self._stop = threading.Event()
 
         def poll():
-            N, h = self._N, self._h
             while not self._stop.is_set():
-                try:
-                    self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
-                                      N.nvmlDeviceGetCurrentClocksEventReasons(h)))
-                except Exception:  # noqa: BLE001
-                    pass
+                self._sample()
                 self._stop.wait(self.period)
         self._t = threading.Thread(target=poll, daemon=True)
         self._t.start()
         return self
+
+    def _sample(self):
+        N, h = self._N, self._h
+        try:
+            self.rows.append((N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM),
+                              N.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def sample_now(self):
+        """One synchronous sample (call while the device is still busy)."""
+        if self._stop is not None:
+            self._sample()
 
     def __exit__(self, *exc):
         if self._stop is not None:
@@ -109,7 +117,7 @@ class ClockSampler:
         sm = sorted(r[0] for r in self.rows)
         reasons = sorted({k for _, m in self.rows for k, bit in bits.items() if m & bit})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml (1 ms poll during the timed region)"}
+                "samples": len(self.rows), "source": "nvml (1 ms poll thread + host polling while the queued replays run)"}
 
 
 # --------------------------------------------------------------------------- device legs
@@ -210,6 +218,9 @@ def run_device(args, rank, world, local_rank):
         for _ in range(args.steps):
             graph.replay()
         t1.record()
+        while not t1.query():            # the replays are queued: sample while they run
+            sampler.sample_now()
+            time.sleep(0.001)
         torch.cuda.synchronize()
     # graph replays do not pass through the launch counter: count the kernels
     # the captured step launches (same as one eager step) per replay
