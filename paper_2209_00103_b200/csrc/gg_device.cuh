@@ -733,25 +733,50 @@ __device__ void planned_metadata(const Tables &t, char *const *scb, const Fuse &
 // current buffers and written to the next ones; nothing else it writes is
 // read by the copy (addresses are slot arithmetic).  Also publishes the
 // buckets of a deferred uniform grow (grow_k).
-__device__ void planned_metadata_db(const Tables &t, char *const *scb, const Fuse &fz) {
+__device__ void planned_metadata_db(const Tables &t, char **scb, const Fuse &fz) {
   __shared__ uint64_t ws[32];
+  constexpr int K = 4;                    // shards per thread whose loads are hoisted
   const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
   const DirV dir{fz.rmode == 0 ? t.offsets : t.prefix, fz.ulen};
   const unsigned long long gmask = fz.grow_k >= 64 ? ~0ull : ((1ull << fz.grow_k) - 1ull);
+  // latency: every per-shard load of the first K slices is issued before the
+  // class bases are staged and before any dependent work (a uniform append
+  // knows its start, no size load)
+  uint64_t hc[K], hst[K], hpre[K];
+  unsigned long long hpm[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const uint32_t s = threadIdx.x + i * blockDim.x;
+    hc[i] = hst[i] = hpre[i] = 0;
+    hpm[i] = 0;
+    if (s < t.S) {
+      hc[i] = dir[s + 1] - dir[s];
+      hst[i] = fz.ulen ? fz.ustart : t.size[s];
+      hpm[i] = t.pmask[s];
+      if (!fz.commit) hpre[i] = t.prefix[s + 1];
+    }
+  }
+  stage_cbase(t, scb);
+  __syncthreads();
   uint64_t carry = 0;
-  for (uint32_t base = 0; base < t.S; base += blockDim.x) {
+  uint32_t it = 0;
+  for (uint32_t base = 0; base < t.S; base += blockDim.x, ++it) {
     const uint32_t s = base + threadIdx.x;
     const bool live = s < t.S;
     uint64_t c = 0, start = 0, pre = 0;
     unsigned long long pm = 0;
-    if (live) {
+    if (it < K) {
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+        if (i == (int)it) { c = hc[i]; start = hst[i]; pm = hpm[i]; pre = hpre[i]; }
+    } else if (live) {
       c = dir[s + 1] - dir[s];
-      start = t.size[s];
+      start = fz.ulen ? fz.ustart : t.size[s];
       pm = t.pmask[s];
       if (!fz.commit) pre = t.prefix[s + 1];
     }
     const uint64_t nsz = start + c;
-    unsigned long long want = gmask & ~pm;
+    unsigned long long want = live ? (gmask & ~pm) : 0ull;
     if (c) {
       atomicAdd((unsigned long long *)&t.ops[s], 1ull);
       t.start[s] = start;
@@ -764,7 +789,7 @@ __device__ void planned_metadata_db(const Tables &t, char *const *scb, const Fus
       t.count[s] = c;
       fz.size_next[s] = nsz;            // the batch's reservation: one update per LFVector
     }
-    publish_buckets_cta<256>(t, scb, base, pm, live ? want : 0ull, lg0);
+    publish_buckets_cta<256>(t, scb, base, pm, want, lg0);
     if (fz.commit) {
       uint64_t tot;
       const uint64_t ex = block_exclusive_scan(live ? nsz : 0, &tot, ws);
@@ -861,9 +886,7 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
     // block 0 is the metadata CTA (dispatched first, so it overlaps the copy
     // instead of trailing it); the copy tiles are blocks 1..
     if (fz.size_next && blockIdx.x == 0) {
-      stage_cbase(t, scb);
-      __syncthreads();
-      planned_metadata_db(t, scb, fz);
+      planned_metadata_db(t, scb, fz);   // stages the class bases itself
       return;
     }
   }
