@@ -193,8 +193,9 @@ int commit_plan(gg_array *a, Plan &p, cudaStream_t st) {
 
 // Streaming launches: one tile per CTA of kThreads threads x U 16 B vectors.
 // Work spaces from 32 MiB use the U the sweeps measured best per walk
-// (tools/sweep.py, tools/ab_unroll.sh, B200: copies into / in place on the
-// slabs U = 8 -- 32 KiB tiles, flatten U = 4); below, U = 2 so small rounds
+// (tools/sweep.py, tools/ab_unroll.sh, tools/rwb_probe.py, B200: copies into
+// the slabs U = 8 -- 32 KiB tiles; flatten and in-place r/w U = 4, 6.92 vs
+// 6.88 TB/s for r/w since the planned walks run 3 CTAs per SM); below, U = 2 so small rounds
 // still spread over every SM.  gg_set_tuning / GG_U_SMALL / GG_U_MID override.
 uint32_t walk_unroll(const gg_array *a, uint64_t total, int w) {
   if (g_tune.unroll > 0) return (uint32_t)g_tune.unroll;
@@ -203,7 +204,7 @@ uint32_t walk_unroll(const gg_array *a, uint64_t total, int w) {
   const uint64_t bytes = total * a->esz;
   if (bytes < (uint64_t(32) << 20)) return u_small;
   if (bytes < (uint64_t(256) << 20) && u_mid) return u_mid;
-  return w == W_FLATTEN ? 4u : 8u;   // tools/ab_unroll.sh: U = 8 from 32 MiB on (1304 vs 1310 us/step)
+  return (w == W_FLATTEN || w == W_RW) ? 4u : 8u;   // tools/ab_unroll.sh, tools/sweep.py
 }
 
 template <int ESZ, int W, typename T, bool P, int U>
