@@ -2,6 +2,8 @@
 drop-in and the oracle (itself pinned to the reference), identical recorded
 states (sizes, capacities, flags, prefix, counter ops, allocator calls,
 flattened bytes, get_global samples, exceptions) after every op."""
+import os
+
 import pytest
 from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
@@ -10,9 +12,10 @@ from hyp_scripts import op_scripts, run
 from oracle import ggoracle as O
 
 pytestmark = pytest.mark.gpu
+_SCALE = int(os.environ.get("GG_HYP_SCALE", "1"))     # stress runs: more examples
 
 
-@settings(max_examples=40, deadline=None, suppress_health_check=[HealthCheck.too_slow],
+@settings(max_examples=40 * _SCALE, deadline=None, suppress_health_check=[HealthCheck.too_slow],
           database=None)
 @given(ops=op_scripts())
 def test_gpu_equals_oracle_on_random_scripts(ops):
@@ -20,7 +23,7 @@ def test_gpu_equals_oracle_on_random_scripts(ops):
     assert run(gg, ops) == run(O, ops)
 
 
-@settings(max_examples=25, deadline=None, suppress_health_check=[HealthCheck.too_slow], database=None)
+@settings(max_examples=25 * _SCALE, deadline=None, suppress_health_check=[HealthCheck.too_slow], database=None)
 @given(S=st.sampled_from([1, 3, 8, 33]), fb=st.sampled_from([1, 2, 4, 32]), n=st.integers(1, 20000),
        grid=st.integers(1, 300), dens=st.floats(0.0, 1.0), mode=st.sampled_from(["warp", "block"]),
        seed=st.integers(0, 2**16))
