@@ -197,14 +197,15 @@ int commit_plan(gg_array *a, Plan &p, cudaStream_t st) {
 // the slabs U = 8 -- 32 KiB tiles; flatten and in-place r/w U = 4, 6.92 vs
 // 6.88 TB/s for r/w since the planned walks run 3 CTAs per SM); below, U = 2 so small rounds
 // still spread over every SM.  gg_set_tuning / GG_U_SMALL / GG_U_MID override.
-uint32_t walk_unroll(const gg_array *a, uint64_t total, int w) {
+uint32_t walk_unroll(const gg_array *a, uint64_t total, int w, uint32_t reps = 1) {
   if (g_tune.unroll > 0) return (uint32_t)g_tune.unroll;
   static const uint32_t u_small = [] { const char *e = getenv("GG_U_SMALL"); return e ? (uint32_t)atoi(e) : 2u; }();
   static const uint32_t u_mid = [] { const char *e = getenv("GG_U_MID"); return e ? (uint32_t)atoi(e) : 0u; }();
   const uint64_t bytes = total * a->esz;
   if (bytes < (uint64_t(32) << 20)) return u_small;
   if (bytes < (uint64_t(256) << 20) && u_mid) return u_mid;
-  return (w == W_FLATTEN || w == W_RW) ? 4u : 8u;   // tools/ab_unroll.sh, tools/sweep.py
+  // in-place passes fused in registers (reps > 1) are ALU-heavy: more vectors in flight
+  return (w == W_FLATTEN || (w == W_RW && reps <= 1)) ? 4u : 8u;   // tools/ab_unroll.sh, tools/sweep.py
 }
 
 template <int ESZ, int W, typename T, bool P, int U>
@@ -221,7 +222,7 @@ int walk(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_
          uint32_t reps, Fuse fz, cudaStream_t st) {
   if (total == 0) return GG_OK;
   cudaError_t e;
-  switch (walk_unroll(a, total, W)) {
+  switch (walk_unroll(a, total, W, reps)) {
     case 1: e = walk_u<ESZ, W, T, P, 1>(a, t, src, dst, total, add, reps, fz, st); break;
     case 2: e = walk_u<ESZ, W, T, P, 2>(a, t, src, dst, total, add, reps, fz, st); break;
     case 8: e = walk_u<ESZ, W, T, P, 8>(a, t, src, dst, total, add, reps, fz, st); break;
