@@ -480,6 +480,8 @@ def test_short_piece_tiles_vs_oracle(gg, dtype):
         a.insert_parallel(batches); o.insert_parallel(batches)
         a.insert_duplicate(); o.insert_duplicate()
         a.rw_add(1); o.rw_add(1)
+        mode = ("fused", "global", "per_shard")[r]
+        a.rw_add(3, passes=3, mode=mode); o.rw_add(3, passes=3)
         st = a._parity_state()
         assert st["sizes"] == [int(x) for x in o.size], r
         assert st["prefix"] == [int(x) for x in o.prefix], r
