@@ -325,6 +325,36 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
 // the shard; the host unmaps chunks that lost their last live bucket), then
 // the commit scan over the new sizes.  All loads issued up front.
 // new_sizes == nullptr: every shard shrinks to uniform_size (no upload)
+// Uniform shrink (every LFVector to the same size, same buckets): the host
+// knows the result, so the kernel only stores -- sizes, pmask, capacity and
+// the prefix (arithmetic, no scan) per LFVector, and the dropped buckets'
+// table entries as one coalesced window over all rows -- with as many CTAs
+// as the tables need (the one-CTA k_shrink strides MB entries apart per
+// thread and serialises over S).
+__global__ void __launch_bounds__(256) k_shrink_uniform(Tables t, uint64_t ns, unsigned long long drop,
+                                                        unsigned long long new_pm, uint64_t new_cap) {
+  pdl_begin();
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = tid; s < t.S; s += nt) {
+    t.size[s] = ns;
+    t.prefix[s + 1] = (s + 1) * ns;
+    if (drop) { t.pmask[s] = new_pm; t.cap[s] = new_cap; }
+  }
+  if (tid == 0) t.prefix[0] = 0;
+  if (drop) {
+    const uint32_t bmin = __ffsll((long long)drop) - 1, bmax = 63 - __clzll((long long)drop);
+    const uint32_t W = bmax - bmin + 1;
+    for (uint64_t e = tid; e < (uint64_t)t.S * W; e += nt) {
+      const uint32_t b = bmin + (uint32_t)(e % W);
+      if (drop >> b & 1) {
+        const size_t i = (size_t)(e / W) * t.MB + b;
+        t.ptr[i] = nullptr;
+        t.flag[i] = 0;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_shrink(Tables t, const uint64_t *new_sizes,
                                                  uint64_t uniform_size) {
   __shared__ uint64_t ws[32];

@@ -202,10 +202,18 @@ uint32_t walk_unroll(const gg_array *a, uint64_t total, int w, uint32_t reps = 1
   static const uint32_t u_small = [] { const char *e = getenv("GG_U_SMALL"); return e ? (uint32_t)atoi(e) : 2u; }();
   static const uint32_t u_mid = [] { const char *e = getenv("GG_U_MID"); return e ? (uint32_t)atoi(e) : 0u; }();
   const uint64_t bytes = total * a->esz;
-  if (bytes < (uint64_t(32) << 20)) return u_small;
-  if (bytes < (uint64_t(256) << 20) && u_mid) return u_mid;
+  uint32_t u;
+  if (bytes < (uint64_t(32) << 20)) u = u_small;
+  else if (bytes < (uint64_t(256) << 20) && u_mid) u = u_mid;
   // in-place passes fused in registers (reps > 1) are ALU-heavy: more vectors in flight
-  return (w == W_FLATTEN || (w == W_RW && reps <= 1)) ? 4u : 8u;   // tools/ab_unroll.sh, tools/sweep.py
+  else u = (w == W_FLATTEN || (w == W_RW && reps <= 1)) ? 4u : 8u;   // tools/ab_unroll.sh, tools/sweep.py
+  // many short LFVectors: a tile no longer than the average LFVector's work,
+  // so tiles stay inside one LFVector (the vector path) instead of stepping
+  // through several pieces one after another (S = 16384 x 2048 int32: 292 ->
+  // see tools/bigS_probe.py)
+  const uint64_t per = total / (a->S ? a->S : 1), unit = 256ull * (16u / a->esz);
+  while (u > 1 && (uint64_t)u * unit > per) u >>= 1;
+  return u;
 }
 
 template <int ESZ, int W, typename T, bool P, int U>
@@ -995,6 +1003,7 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
   bool uni = true;                             // same size and buckets everywhere: class-batched
   for (uint32_t s = 0; s < a->S && uni; ++s)
     uni = h_new_sizes[s] == h_new_sizes[0] && a->flags[s] == a->flags[0];
+  const uint64_t old_flags0 = a->flags[0];
   if (uni) {
     const uint32_t keep = min_buckets_for(a, h_new_sizes[0]);
     const uint64_t drop = keep >= 64 ? 0 : (a->flags[0] & ~((uint64_t(1) << keep) - 1));
@@ -1034,8 +1043,18 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
     d_sizes = a->t.count;
   }
   Tables t = tables_for_launch(a, false);
-  CUDA_TRY(launch_k(k_shrink, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t, d_sizes,
-                    (uint64_t)h_new_sizes[0]));
+  if (uni) {
+    const uint64_t keep_b = min_buckets_for(a, h_new_sizes[0]);
+    const uint64_t drop = keep_b >= 64 ? 0 : (old_flags0 & ~((uint64_t(1) << keep_b) - 1));
+    const uint64_t work = (uint64_t)a->S * (drop ? (64 - __builtin_clzll(drop)) - __builtin_ctzll(drop) : 1);
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((work + 255) / 256, (uint64_t)sm_count(a->dev) * 4);
+    CUDA_TRY(launch_k(k_shrink_uniform, std::max<uint32_t>(grid, 1), 256, 0, st, t,
+                      (uint64_t)h_new_sizes[0], (unsigned long long)drop,
+                      (unsigned long long)a->flags[0], (uint64_t)a->cap[0]));
+  } else {
+    CUDA_TRY(launch_k(k_shrink, 1, std::min<uint32_t>(1024, (a->S + 31) / 32 * 32), 0, st, t, d_sizes,
+                      (uint64_t)h_new_sizes[0]));
+  }
   uint64_t acc = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
   // unmap emptied chunks down to keep_mapped_bytes (waits for the device:
