@@ -1,3 +1,5 @@
+"""Reset + 2^25 insert + one doubling round at S = 16384 LFVectors x 2048
+int32 (run under ncu for the per-kernel launch list)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, paper_2209_00103_b200 as gg
