@@ -325,6 +325,45 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
 // the shard; the host unmaps chunks that lost their last live bucket), then
 // the commit scan over the new sizes.  All loads issued up front.
 // new_sizes == nullptr: every shard shrinks to uniform_size (no upload)
+// Metadata of a uniform planned append when the walk's metadata CTA is off
+// (S > 4096, plain capture, gg_set_fuse(0)): every LFVector appended c at the
+// same start with the same buckets, so the host knows every value and the
+// kernel only stores, with as many CTAs as the tables need (the one-CTA
+// k_planned_meta serialises over S).
+__global__ void __launch_bounds__(256) k_meta_uniform(Tables t, uint64_t start, uint64_t c, int commit,
+                                                      unsigned long long want, unsigned long long new_pm,
+                                                      uint64_t new_cap) {
+  pdl_begin();
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nsz = start + c;
+  for (uint64_t s = tid; s < t.S; s += nt) {
+    t.size[s] = nsz;
+    t.start[s] = start;
+    t.count[s] = c;
+    t.ops[s] += 1;
+    if (want) { t.pmask[s] = new_pm; t.cap[s] = new_cap; }
+    if (commit) t.prefix[s + 1] = (s + 1) * nsz;
+  }
+  if (tid == 0) {
+    if (commit) t.prefix[0] = 0;
+    if (want) atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)__popcll(want) * t.S);
+  }
+  if (want) {
+    char *const *cb = t.cbase;
+    const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+    const uint32_t bmin = __ffsll((long long)want) - 1, bmax = 63 - __clzll((long long)want);
+    const uint32_t W = bmax - bmin + 1;
+    for (uint64_t e = tid; e < (uint64_t)t.S * W; e += nt) {
+      const uint32_t b = bmin + (uint32_t)(e % W);
+      if (want >> b & 1) {
+        const uint64_t ss = e / W;
+        t.ptr[(size_t)ss * t.MB + b] = cb[b] + (ss << max(lg0 + b, 4u));
+        t.flag[(size_t)ss * t.MB + b] = kFlagPublished;
+      }
+    }
+  }
+}
+
 // Uniform shrink (every LFVector to the same size, same buckets): the host
 // knows the result, so the kernel only stores -- sizes, pmask, capacity and
 // the prefix (arithmetic, no scan) per LFVector, and the dropped buckets'

@@ -709,10 +709,21 @@ int uniform_append(gg_array *a, int wk, const char *src, uint64_t c, const uint6
       size_t nb[1] = {(a->S + 1) * 8};
       if ((rc = a->up.upload(st, 1, dst, srcs, nb))) return rc;
     }
-    rc = wk == W_DUP ? walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, Fuse{rmode, commit ? 1 : 0}, st)
-                     : walk_copy<W_INSERT, true>(a, t, src, nullptr, total, Fuse{rmode, commit ? 1 : 0}, st);
+    Fuse fu{rmode, commit ? 1 : 0};
+    fu.ulen = c;                               // uniform: no directory loads in the walk
+    fu.ustart = start;
+    rc = wk == W_DUP ? walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fu, st)
+                     : walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fu, st);
     if (rc) return rc;
-    if ((rc = finish_planned(a, Fuse{rmode, commit ? 1 : 0}, st))) return rc;
+    if (a->S > 4096) {
+      // store-only multi-CTA metadata: every value is known on the host
+      const uint64_t work = (uint64_t)a->S * (want ? (64 - __builtin_clzll(want)) - __builtin_ctzll(want) : 1);
+      const uint32_t grid = (uint32_t)std::min<uint64_t>((work + 255) / 256, (uint64_t)sm_count(a->dev) * 4);
+      CUDA_TRY(launch_k(k_meta_uniform, std::max<uint32_t>(grid, 1), 256, 0, st, t, start, c, commit ? 1 : 0,
+                        (unsigned long long)want, (unsigned long long)a->flags[0], (uint64_t)a->cap[0]));
+    } else if ((rc = finish_planned(a, Fuse{rmode, commit ? 1 : 0}, st))) {
+      return rc;
+    }
   }
   if (commit) host_commit(a);
   if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
