@@ -56,3 +56,16 @@ for fuse in (1, 0):
 _L.lib.gg_set_fuse(1)
 torch.cuda.synchronize()
 print("uniform insert ok")
+# S > 4096: uniform appends take the store-only multi-CTA metadata kernel;
+# uniform resets take the store-only shrink
+w = gg.GrowableArray(5000, 4, dtype=np.int32)
+for rnd in range(2):
+    w.shrink(0, release=False)
+    w.insert_csr(torch.arange(5000 * 7, dtype=torch.int32, device="cuda"),
+                 np.arange(5001, dtype=np.uint64) * np.uint64(7))
+    w.grow(2 * w.committed_size)
+    w.insert_duplicate()
+assert w.committed_size == 5000 * 14
+w.flatten_device()
+torch.cuda.synchronize()
+print("large-S uniform ok")
