@@ -221,8 +221,33 @@ cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *ds
                    T add, uint32_t reps, Fuse fz, cudaStream_t st) {
   const uint32_t tile = (uint32_t)U * kThreads * (16 / ESZ);
   const uint64_t grid = (total - fz.g0 + tile - 1) / tile + ((P && fz.size_next) ? 1 : 0);
-  return launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, 0, st, t, src, dst,
-                  total, add, reps, tile, fz);
+  // Residency: the large-tile copies into the slabs (planned insert /
+  // duplicate, U = 8) stream best at 3 CTAs of 256 threads per SM -- 4 are
+  // ~1% slower, 2 far slower (tools/reset_probe.py with GG_WALK_SMEM /
+  // GG_WALK_CARVEOUT).  Enforced with 16 KiB of dynamic shared memory under a
+  // 25% shared-memory carveout (57 KiB per SM fit 3 such CTAs, not 4), so it
+  // does not hinge on the kernel's register count.  The U = 4 flatten too;
+  // the U = 4 in-place r/w is best uncapped.  GG_WALK_SMEM / GG_WALK_CARVEOUT
+  // override both (tuning sweeps).
+  static const int env_smem = [] { const char *e = getenv("GG_WALK_SMEM"); return e ? atoi(e) : -1; }();
+  static const int env_carve = [] { const char *e = getenv("GG_WALK_CARVEOUT"); return e ? atoi(e) : -1; }();
+  int smem = -1, carve = -1;
+  if (U == 8 && P) { smem = 16 * 1024; carve = 25; }
+  if (U == 4 && W == W_FLATTEN) { smem = 12 * 1024; carve = 25; }   // flatten: 3 per SM too (+0.6%)
+  if (env_smem >= 0 && (U == 8 || U == 4)) smem = env_smem;
+  if (env_carve >= 0 && (U == 8 || U == 4)) carve = env_carve;
+  if (smem > 0 || carve >= 0) {
+    static bool attr = false;                 // once per kernel instantiation
+    if (!attr) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_walk<ESZ, W, T, U, kDefLS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (carve >= 0)
+        cudaFuncSetAttribute(k_walk<ESZ, W, T, U, kDefLS, P>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+      attr = true;
+    }
+  }
+  return launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, smem > 0 ? (size_t)smem : 0, st, t,
+                  src, dst, total, add, reps, tile, fz);
 }
 
 template <int ESZ, int W, typename T, bool P = false>
