@@ -33,6 +33,14 @@ UNIT = "Gelem/s"
 WORKLOAD = "config2: GGArray-512 doubling 2^20->2^30 int32 (grow + duplicate-insert per round)"
 
 
+def config_dict(world: int) -> dict:
+    """The workload both arms (GPU and --impl reference) run, per GPU."""
+    return {"workload": WORKLOAD, "shards_per_gpu": S, "first_bucket_size": FB,
+            "initial_elements": N0, "rounds": ROUNDS, "final_elements_per_gpu": 1 << 30,
+            "parallelism": f"lfvector-sharded x{world}",
+            "l2": "inputs larger than L2 (4 GiB live, 8 GiB capacity per GPU)"}
+
+
 def _ncu_traffic():
     """dram read+write bytes of the dominant kernel's largest launch, from the
     newest committed ncu summary (profiles/rNN_ncu_summary.json)."""
@@ -252,10 +260,7 @@ def run_device(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (np.arange tags, as bench_cli.py)",
-        "config": {"workload": WORKLOAD, "shards_per_gpu": S, "first_bucket_size": FB,
-                   "initial_elements": N0, "rounds": ROUNDS, "final_elements_per_gpu": 1 << 30,
-                   "parallelism": f"lfvector-sharded x{world}",
-                   "l2": "inputs larger than L2 (4 GiB live, 8 GiB capacity per GPU)"},
+        "config": config_dict(world),
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": "k_walk<4,W_DUP> (duplicate insert, all 10 rounds)",
                      "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -1002,50 +1007,136 @@ def e2e_leg(args, gg, torch, device, world, dist):
 
 
 # --------------------------------------------------------------------------- CPU legs
-def cpu_baseline(args):
-    """The oracle port (numpy restatement of growarray) on this host's cores: a
-    bounded sample of the same schedule (2^20 -> 2^(20+R) elements)."""
-    from oracle import ggoracle as O
-    cores = len(os.sched_getaffinity(0))
-    rounds = args.cpu_rounds
-    best = None
-    t_end = time.perf_counter() + 20
-    runs = 0
-    while runs < 1 or (time.perf_counter() < t_end and runs < 3):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The UNMODIFIED reference package ``growarray``, pip-installed into
+    baseline/_ref (git-ignored; it travels to the GPU box with the snapshot),
+    or None when it is absent."""
+    if not os.path.isfile(os.path.join(REF_DIR, "growarray", "__init__.py")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import growarray
+    assert os.path.dirname(os.path.abspath(growarray.__file__)) == os.path.join(REF_DIR, "growarray")
+    return growarray
+
+
+def reference_step(G, workers: int, rounds: int = ROUNDS):
+    """One config-2 step through growarray's own harness code path
+    (bench_cli.py:508-543 with structure=ggarray): from_flat(arange(2^20), 512,
+    32, int32) (_build_structure, :239-244), then per round _grow(2n) (:310-314)
+    and _insert_duplicate (:298-307: per-shard to_numpy + insert_parallel with
+    ``workers`` threads).  Returns the array (2^(20+rounds) elements)."""
+    from growarray import bench_cli as B
+    cfg = B.BenchConfig(structure="ggarray", shards=S, first_bucket=FB, workers=workers,
+                        initial_size=N0, iterations=rounds)
+    store = B._build_structure(cfg, np.arange(N0, dtype=B.BENCH_DTYPE), N0 << rounds)
+    for _ in range(rounds):
+        B._grow(store, 2 * B._committed_size(store))
+        B._insert_duplicate(store, cfg)
+    return store
+
+
+def _check_reference_state(store, rounds: int = ROUNDS) -> None:
+    """Sizes / capacity and sampled contents of the reference's end state
+    against the closed form of the schedule (element g = (g // per) * 2048 +
+    g % 2048)."""
+    n = N0 << rounds
+    assert store.committed_size == n and store.total_size == n
+    per, base = (N0 // S) << rounds, N0 // S
+    for g in (0, 1, base - 1, base, per - 1, per, n // 2 + 12345, n - 1):
+        assert int(store.get_global(g)) == (g // per) * base + g % base, g
+
+
+def _time_reference_steps(G, steps: int, workers: int, rounds: int = ROUNDS):
+    """Wall time of each step (array construction included); the previous
+    step's array is torn down outside the timed window."""
+    import gc
+    secs = []
+    for _ in range(steps):
+        gc.collect()
         t0 = time.perf_counter()
-        _, inserted, t_ins, t_grow = O.doubling_schedule_cpu(N0, rounds, S, FB, np.int32, cores)
-        wall = time.perf_counter() - t0
-        v = inserted / wall / 1e9
-        best = v if best is None else max(best, v)
-        runs += 1
-    return {"value": round(best, 5), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"oracle.ggoracle doubling_schedule_cpu: S=512 int32 2^20 -> 2^{20 + rounds} "
-                      f"({rounds} rounds, wall incl. grow), best of {runs}"}
+        store = reference_step(G, workers, rounds)
+        secs.append(time.perf_counter() - t0)
+        _check_reference_state(store, rounds)
+        del store
+    gc.collect()
+    return secs
+
+
+def _port_steps(steps: int, cores: int, rounds: int):
+    from oracle import ggoracle as O
+    secs = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.doubling_schedule_cpu(N0, rounds, S, FB, np.int32, cores)
+        secs.append(time.perf_counter() - t0)
+    return secs
+
+
+def cpu_baseline(args):
+    """The reference's own CPU path (growarray from baseline/_ref) on this
+    host's cores, on the full config-2 step (2^20 -> 2^30); a bounded sample
+    of 2 timed steps after one warm-up (~10-30 s).  Without baseline/_ref:
+    the oracle port (kind "port")."""
+    cores = len(os.sched_getaffinity(0))
+    G = load_reference()
+    if G is not None:
+        _time_reference_steps(G, 1, cores)
+        secs = _time_reference_steps(G, 2, cores)
+        v = 2 * (1 << 30) / sum(secs) / 1e9
+        return {"value": round(v, 5), "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"growarray (unmodified, baseline/_ref) bench_cli grow-insert-rw path, "
+                          f"structure=ggarray: from_flat(arange(2^20), 512, 32, int32) + 10 x "
+                          f"(grow(2n) + per-shard to_numpy + insert_parallel(workers={cores})) "
+                          f"-> 2^30, 2 steps after 1 warm-up, wall clock",
+                "step_s": [round(x, 3) for x in secs]}
+    rounds = args.cpu_rounds
+    secs = _port_steps(2, cores, rounds)
+    return {"value": round(2 * (1 << (20 + rounds)) / sum(secs) / 1e9, 5), "unit": UNIT, "cores": cores,
+            "kind": "port",
+            "sample": f"baseline/_ref absent: oracle.ggoracle doubling_schedule_cpu S=512 int32 "
+                      f"2^20 -> 2^{20 + rounds}, 2 steps"}
 
 
 def run_reference(args, rank, world):
+    """bench.py --impl reference: the reference's CPU implementation of the
+    path on this host's cores, same workload, metric and config as the GPU arm
+    (one config-2 step = 2^30 elements inserted).  Rank 0 alone runs."""
     if rank != 0:
         return None
-    from oracle import ggoracle as O
     cores = len(os.sched_getaffinity(0))
-    rounds = args.cpu_rounds
-    for _ in range(args.warmup):
-        O.doubling_schedule_cpu(N0, min(rounds, 2), S, FB, np.int32, cores)
-    t0 = time.perf_counter()
-    inserted = 0
-    for _ in range(args.steps):
-        _, ins, _, _ = O.doubling_schedule_cpu(N0, rounds, S, FB, np.int32, cores)
-        inserted += ins
-    sec = time.perf_counter() - t0
-    v = inserted / sec / 1e9
+    G = load_reference()
+    if G is not None:
+        rounds = args.ref_rounds                      # tests shorten the schedule; default = config 2
+        _time_reference_steps(G, args.warmup, cores, rounds)
+        secs = _time_reference_steps(G, args.steps, cores, rounds)
+        per_step = 1 << (20 + rounds)
+        kind = "reference"
+        sample = (f"growarray (unmodified, pip-installed into baseline/_ref) through its bench_cli "
+                  f"grow-insert-rw code path (structure=ggarray, workers={cores}): from_flat(arange(2^20), "
+                  f"512, 32, int32) + 10 x (grow(2n) + per-shard to_numpy + insert_parallel) -> 2^30 per "
+                  f"step, end state checked against the closed form")
+        cfg_extra = {} if rounds == ROUNDS else {"rounds": rounds, "final_elements_per_gpu": per_step}
+    else:
+        rounds = args.cpu_rounds
+        _port_steps(min(args.warmup, 1), cores, rounds)
+        secs = _port_steps(args.steps, cores, rounds)
+        per_step = 1 << (20 + rounds)
+        kind = "port"
+        sample = f"baseline/_ref absent: oracle port S=512 int32 2^20 -> 2^{20 + rounds} per step"
+        cfg_extra = {"cpu_sample_final_elements": per_step}
+    sec = sum(secs)
+    v = args.steps * per_step / sec / 1e9
     return {"metric": METRIC, "value": round(v, 5), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (np.arange tags)", "impl": "reference",
-            "config": {"workload": WORKLOAD, "shards_per_gpu": S, "first_bucket_size": FB,
-                       "cpu_sample_final_elements": 1 << (20 + rounds)},
-            "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"S=512 int32 2^20 -> 2^{20 + rounds} per step (bounded sample)"},
+            "data": "synthetic (np.arange tags, as bench_cli.py)", "impl": "reference",
+            "config": {**config_dict(world), **cfg_extra},
+            "cpu_baseline": {"value": round(v, 5), "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample, "workers": cores, "step_s": [round(x, 3) for x in secs]},
             "e2e": {"value": round(v, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -1056,7 +1147,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ggarray", choices=["ggarray", "reference"])
     ap.add_argument("--rw-passes", type=int, default=100)
-    ap.add_argument("--cpu-rounds", type=int, default=7)
+    ap.add_argument("--cpu-rounds", type=int, default=7, help="oracle-port fallback sample (no baseline/_ref)")
+    ap.add_argument("--ref-rounds", type=int, default=ROUNDS, help="reference arm schedule (tests only)")
     ap.add_argument("--quick", action="store_true", help="headline only")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

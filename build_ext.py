@@ -34,5 +34,32 @@ def build(verbose: bool = False) -> str:
     return out
 
 
+def install_reference(force: bool = False) -> str | None:
+    """pip-install the UNMODIFIED reference (/root/reference/pkg, pure Python,
+    numpy only) into baseline/_ref for bench.py --impl reference, from a /tmp
+    copy (the reference tree is read-only) with --no-deps (numpy is in the
+    image, the wheelhouse has no numpy wheel).  No-op when already installed
+    or when /root/reference is absent (GPU box)."""
+    import shutil
+    import tempfile
+    ref_src = "/root/reference/pkg"
+    target = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isfile(os.path.join(target, "growarray", "__init__.py")) and not force:
+        return target
+    if not os.path.isdir(ref_src):
+        return None
+    with tempfile.TemporaryDirectory() as tmp:
+        copy = os.path.join(tmp, "pkg")
+        shutil.copytree(ref_src, copy, ignore=shutil.ignore_patterns(".hypothesis", "__pycache__"))
+        shutil.rmtree(target, ignore_errors=True)
+        res = subprocess.run([sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation",
+                              "--no-deps", "--find-links", "/opt/wheelhouse", "--target", target, copy],
+                             capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout[-2000:] + res.stderr[-2000:])
+        return None
+    return target
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))
