@@ -191,10 +191,12 @@ def run_device(args, rank, world, local_rank):
     c0 = time.perf_counter()
     step.run(False)
     torch.cuda.synchronize()
+    sl = step.arr.slab_stats()
     cold = {"ms": round((time.perf_counter() - c0) * 1e3, 3),
-            "map_ms": round(step.arr.slab_stats()["map_ns"] / 1e6, 3),
-            "chunks_mapped": step.arr.slab_stats()["chunks_mapped"],
-            "note": "first step of a fresh array, wall clock, incl. cuMemCreate/Map of its slab chunks"}
+            "map_ms": round(sl["map_ns"] / 1e6, 3), "extents_mapped": sl["chunks_mapped"],
+            "driver_handles_created": sl["handles_created"],
+            "note": "first step of a fresh array in a fresh process (pool trimmed), wall clock, incl. "
+                    "cuMemCreate/Map/SetAccess of its 8 GiB of slab extents"}
     for _ in range(args.warmup):
         step.run(False)
     torch.cuda.synchronize()
@@ -287,16 +289,24 @@ def run_device(args, rank, world, local_rank):
                   "eager: the same K steps issued op by op from Python",
         "eager": {"value": round(eager_value, 3), "ms_per_step": round(eager_ms / args.steps, 4),
                   "host_enqueue_ms_per_step": round(host_ms / args.steps, 4)},
-        "cold_first_step": cold,
+        "cold_first_step": {**cold, "x_warm_step": round(cold["ms"] / (ms / args.steps), 2)},
     }
     if dist:
         out["gather_flatten"] = gather_leg(args, torch, device, step, dist, world)
     if not args.quick:
+        _between_legs(gg)
+        out["cold_steps"] = cold_leg(args, gg, torch, device, ms / args.steps)
+        _between_legs(gg)
         out.update(secondary(args, gg, torch, device, step, hbm))
+        _between_legs(gg)
         out["config2_dtypes"] = dtype_variants(args, gg, torch, device, hbm)
+        _between_legs(gg)
         out["phased_config4"] = phased_leg(args, gg, torch, device)
+        _between_legs(gg)
         out["config5_per_gpu"] = config5_leg(args, gg, torch, device, hbm)
+        _between_legs(gg)
         out["config1"] = config1_leg(args, gg, torch, device, rank == 0 and world == 1 and not args.no_cpu)
+        _between_legs(gg)
         out["e2e"] = e2e_leg(args, gg, torch, device, world, dist)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args)
@@ -382,6 +392,43 @@ def gather_leg(args, torch, device, step, dist, world):
                 "nccl_baseline": nccl}
     except Exception as exc:                          # report, never lose the bench line
         return {"error": repr(exc)[:300]}
+
+
+def _between_legs(gg):
+    """Outside every timed region: collect garbage (the collector is off
+    during the run, so no teardown lands inside a timed loop) and free what
+    dropped arrays left behind."""
+    import gc
+    gc.collect()
+    gg.reclaim(True)
+
+
+def cold_leg(args, gg, torch, device, warm_ms):
+    """The first config-2 step of a FRESH array, wall clock (host planning,
+    driver calls, kernels): (1) after pool_trim, every slab extent comes from
+    cuMemCreate; (2) after that array was destroyed, a new same-shape array
+    adopts its slab from the process slab cache (the two-phase / rebuild
+    pattern: no driver call)."""
+    out = {}
+    gg.pool_trim(device.index)
+    for tag in ("driver", "adopted_slab"):
+        st = Step(gg, torch, device)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st.run(False)
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t0) * 1e3
+        sl = st.arr.slab_stats()
+        check_state(st, torch)
+        out[tag] = {"ms": round(ms, 3), "x_warm_step": round(ms / warm_ms, 2),
+                    "map_ms": round(sl["map_ns"] / 1e6, 3), "extents_mapped": sl["chunks_mapped"],
+                    "driver_handles_created": sl["handles_created"],
+                    "handles_from_pool": sl["handles_from_pool"]}
+        st.arr.close()
+        del st
+        gg.reclaim(True)
+    out["note"] = "wall clock of one full step on a new GrowableArray, array construction excluded"
+    return out
 
 
 def launches_per_step(step) -> int:
@@ -483,6 +530,8 @@ def secondary(args, gg, torch, device, step, hbm):
     flat.sub_(passes)                                # flat_add put +passes on the copy: back to a's contents
     tp = {"flatten_ms": res["flatten"]["ms"], "static_rw_ms_per_pass": rw["flattened_contiguous"]["ms_per_pass"]}
     for tag in ("rebuild_cold", "rebuild_pooled"):
+        if tag == "rebuild_cold":
+            gg.pool_trim(device.index)               # fresh driver memory: no cached handles or slabs
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
@@ -491,8 +540,11 @@ def secondary(args, gg, torch, device, step, hbm):
         e1.record()
         torch.cuda.synchronize()
         wall = (time.perf_counter() - w0) * 1e3
+        sl = b.slab_stats()
         tp[tag] = {"wall_ms": round(wall, 3), "device_ms": round(e0.elapsed_time(e1), 3),
-                   "gelem_s": round(n / wall / 1e6, 2)}
+                   "gelem_s": round(n / wall / 1e6, 2), "driver_handles_created": sl["handles_created"],
+                   "handles_from_pool": sl["handles_from_pool"], "extents_mapped": sl["chunks_mapped"],
+                   "adopted_slab_bytes": int(b.memory_stats(settle=False)["mapped_bytes"]) if not sl["chunks_mapped"] else 0}
         if tag == "rebuild_pooled":
             tp["roundtrip_ok"] = bool(torch.equal(b.flatten_device(), flat))
             # steady two-phase loop: reuse the GGArray (reset keeps its buckets mapped)
@@ -509,6 +561,11 @@ def secondary(args, gg, torch, device, step, hbm):
             tp["reuse_roundtrip_ok"] = bool(torch.equal(b.flatten_device(), flat))
         b.close()
         del b
+        gg.reclaim(True)                             # b's slab -> the slab cache (same shape next)
+    tp["note"] = ("rebuild = GrowableArray.from_flat(flat) into a FRESH array: rebuild_cold after "
+                  "pool_trim (cuMemCreate/Map/SetAccess of 8 GiB), rebuild_pooled adopts the slab the "
+                  "destroyed cold array left (no driver call); rebuild_reuse = shrink(0) + insert_csr "
+                  "into the same array")
     res["two_phase"] = tp
     del flat
     # --- baselines: the last doubling step 2^29 -> 2^30 (paper Table II)
@@ -517,14 +574,19 @@ def secondary(args, gg, torch, device, step, hbm):
     base = {}
     st = gg.StaticArray(1 << 30, dtype=np.int32, device=device)
     st.insert_batch(src)
-    for algo in ("atomic", "warp", "block"):
+    for algo in ("atomic", "warp", "block", None):
         def ins(algo=algo):
             st._count = half
             st._d_count.fill_(half)
             st.insert_batch(src, algo=algo)
         ins()
         ms = _time(torch, ins, reps=3)
-        base[f"static_insert_{algo}"] = {"ms": round(ms, 4), "gelem_s": round(half / ms / 1e6, 2)}
+        base[f"static_insert_{algo or 'batch'}"] = {
+            "ms": round(ms, 4), "gelem_s": round(half / ms / 1e6, 2),
+            "gbs": round(8 * half / ms / 1e6, 1), "frac": round(8 * half / ms / 1e6 / hbm, 4)}
+    assert bool(torch.equal(st.view()[half:], src)), "static insert_batch contents"
+    base["static_insert_batch"]["kernel"] = "k_flat_append (one reservation, 16 B vector copy)"
+    base["static_insert_block"]["kernel"] = "k_flat_insert_block (one atomicAdd per 32 KiB tile, 16 B stores)"
     ms = _time(torch, lambda: st.rw_add(1, passes=passes)) / passes
     base["static_rw"] = {"ms_per_pass": round(ms, 4), "gbs": round(8 * (1 << 30) / ms / 1e6, 1)}
     del st
@@ -536,10 +598,12 @@ def secondary(args, gg, torch, device, step, hbm):
         d.insert_batch(src)
         torch.cuda.synchronize()
         g_ms.append(_time(torch, lambda: d.resize(1 << 30)))
-        i_ms.append(_time(torch, lambda: d.insert_batch(src, algo="block")))
+        i_ms.append(_time(torch, lambda: d.insert_batch(src)))
         del d
     base["doubling"] = {"grow_ms": round(min(g_ms), 4), "insert_ms": round(min(i_ms), 4),
-                        "insert_gelem_s": round(half / min(i_ms) / 1e6, 2)}
+                        "insert_gelem_s": round(half / min(i_ms) / 1e6, 2),
+                        "insert": "insert_batch (one reservation + k_flat_append)",
+                        "grow": "cudaMallocAsync(2^30) + zero + D2D copy of 2^29 + free (host-resized)"}
     # memMap (VMM append, no copy)
     g_ms, i_ms = [], []
     for _ in range(3):
@@ -547,12 +611,13 @@ def secondary(args, gg, torch, device, step, hbm):
         c.resize(half)
         c.insert_batch(src)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
         g_ms.append(_time(torch, lambda: c.resize(1 << 30)))
-        i_ms.append(_time(torch, lambda: c.insert_batch(src, algo="block")))
+        i_ms.append(_time(torch, lambda: c.insert_batch(src)))
         del c
     base["memmap"] = {"grow_ms": round(min(g_ms), 4), "insert_ms": round(min(i_ms), 4),
-                      "insert_gelem_s": round(half / min(i_ms) / 1e6, 2)}
+                      "insert_gelem_s": round(half / min(i_ms) / 1e6, 2),
+                      "insert": "insert_batch (one reservation + k_flat_append)",
+                      "grow": "cuMemCreate/Map/SetAccess of 2 GiB more (64 MiB pieces) + zero"}
     # ggarray, same last step
     last = step.dup_ms[ROUNDS - 1::ROUNDS]
     lastg = step.grow_ms[ROUNDS - 1::ROUNDS]
@@ -570,7 +635,8 @@ def full_schedule_baselines(gg, torch, device, step, args):
     """The whole config-2 schedule (2^20 -> 2^30 by doubling: grow, then append
     a copy of the current contents) on the static array (capacity 2^30
     allocated up front), the host-resized doubling array and the memMap
-    array, block-scan insertion (the baselines' fastest), CUDA events over
+    array, insert_batch (one reservation + vectorised copy, the reference's
+    semantics and the baselines' fastest), CUDA events over
     the 10 rounds; next to the GGArray's eager step (same schedule + reset)."""
     out = {}
     n0, final = N0, N0 << ROUNDS
@@ -582,7 +648,7 @@ def full_schedule_baselines(gg, torch, device, step, args):
         e0.record()
         for _ in range(ROUNDS):
             grow(arr, 2 * n)
-            arr.insert_batch(arr.view()[:n], algo="block")
+            arr.insert_batch(arr.view()[:n])
             n *= 2
         e1.record()
         torch.cuda.synchronize()
@@ -591,15 +657,15 @@ def full_schedule_baselines(gg, torch, device, step, args):
 
     src = torch.arange(n0, dtype=torch.int32, device=device)
     for name, make, grow in [
-            ("static_block", lambda: gg.StaticArray(final, dtype=np.int32, device=device), lambda a, m: None),
-            ("doubling_block", lambda: gg.DoublingArray(n0, dtype=np.int32, device=device), lambda a, m: a.resize(m)),
-            ("memmap_block", lambda: gg.ChunkTableArray(dtype=np.int32, device=device), lambda a, m: a.resize(m))]:
+            ("static_batch", lambda: gg.StaticArray(final, dtype=np.int32, device=device), lambda a, m: None),
+            ("doubling_batch", lambda: gg.DoublingArray(n0, dtype=np.int32, device=device), lambda a, m: a.resize(m)),
+            ("memmap_batch", lambda: gg.ChunkTableArray(dtype=np.int32, device=device), lambda a, m: a.resize(m))]:
         try:
             ts = []
             for _ in range(2):
                 a = make()
                 grow(a, n0)
-                a.insert_batch(src, algo="block")
+                a.insert_batch(src)
                 ts.append(schedule(a, grow))
                 del a
                 torch.cuda.empty_cache()
@@ -655,6 +721,7 @@ def phased_leg(args, gg, torch, device):
         torch.cuda.synchronize()
         ms_tot = e0.elapsed_time(e1)
         sl = a.slab_stats()
+        a.close()
         return {"ms": round(ms_tot, 3), "inserted_elements": moved,
                 "capacity_over_needed_max": round(max(cap_ratio), 4),
                 "capacity_over_needed_mean": round(float(np.mean(cap_ratio)), 4),
@@ -724,6 +791,21 @@ def config1_leg(args, gg, torch, device, with_cpu):
            "device_resident": "shrink(0) + insert_csr(device batch) + rw_add(1) + flatten_device, "
                               "CUDA events, mean of 20"}
     if with_cpu:
+        G = load_reference()
+        if G is not None:
+            # the reference itself (baseline/_ref): GrowableArray + insert_parallel +
+            # for_each_shard(v += 1) + flatten, one worker (its fastest at this size)
+            tr = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                r = G.GrowableArray(S, FB, dtype=np.int32)
+                r.insert_parallel(G.split_batches(vals, S), workers=1)
+                r.for_each_shard(lambda v: np.add(v, 1, out=v))
+                got = r.flatten()
+                tr.append(time.perf_counter() - t0)
+            assert got.tobytes() == ref.tobytes()
+            res["cpu_reference_ms"] = round(1e3 * min(tr), 3)
+            res["cpu_reference"] = "growarray (baseline/_ref), same sequence, workers=1, best of 5"
         from oracle import ggoracle as O
         tc = []
         for _ in range(5):
@@ -801,12 +883,17 @@ def config5_leg(args, gg, torch, device, hbm):
                         "capacity_over_needed": round(mem["capacity_over_needed"], 6),
                         "mapped_over_needed": round(mem["mapped_over_needed"], 6),
                         "mapped_gib": round(mem["mapped_bytes"] / 2**30, 2)})
+            a.close()
             del stage, a
+            gg.pool_trim(device.index)     # 128 GiB back to the driver before the next legs
             torch.cuda.empty_cache()
             return out
         except Exception as exc:                      # report, never lose the bench line
             out[f"error_2p{20 + rounds}"] = repr(exc)[:300]
+            if a is not None:
+                a.close()
             del a
+            gg.pool_trim(device.index)
             torch.cuda.empty_cache()
     return out
 
@@ -1156,6 +1243,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    import gc
+    gc.collect()
+    gc.disable()      # arrays hold no reference cycles; collections happen between legs only
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:

@@ -95,6 +95,13 @@ int gg_insert(gg_array *a, const void *d_values, const uint64_t *h_offsets,
 enum { GG_F_COMMIT = 1, GG_F_UNFUSED = 2 };
 int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream);
+/* gg_insert_ex that also returns each shard's reservation start in
+ * h_reserved[S] (may be NULL): the ReservedRange push_back_batch returns
+ * (bucket_vector.py:229-232), read under the handle's lock so concurrent
+ * callers on one shard get the ranges they actually reserved. */
+int gg_insert_ex2(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, uint64_t *h_reserved,
+                  void *stream);
 int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream);
 /* bench_cli.py:298-307 _insert_duplicate: every shard appends a copy of its
  * committed contents, read straight from its buckets (no snapshot). */
@@ -228,20 +235,38 @@ int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream);
  * size, the reference's capacity), [1]=mapped slab bytes (physical),
  * [2]=live bucket bytes (16 B rounded), [3]=needed bytes (sum of sizes),
  * [4]=device alloc calls, [5]=cached bytes (mapped chunks without a live
- * bucket) */
-int gg_mem_stats(gg_array *a, uint64_t *h_out6, void *stream);
+ * bucket), [6]=bytes a shrink released that are still mapped until the work
+ * queued before it completes (see gg_settle) */
+int gg_mem_stats(gg_array *a, uint64_t *h_out7, void *stream);
+/* unmap the chunks earlier shrinks released, waiting (event) for the work
+ * queued before them; after it mem_stats[1] is the settled footprint */
+int gg_settle(gg_array *a);
 /* slab mapping cost: [0]=mapped bytes, [1]=cached bytes, [2]=chunks mapped
  * (cumulative), [3]=chunks unmapped, [4]=ns in cuMemCreate/Map/SetAccess,
- * [5]=ns in cuMemUnmap/Release, [6]=class regions reserved, [7]=VA bytes */
-int gg_slab_stats(gg_array *a, uint64_t *h_out8);
+ * [5]=ns in cuMemUnmap/Release, [6]=class regions reserved, [7]=VA bytes,
+ * [8]=physical handles created by the driver, [9]=handles taken from the
+ * process pool, [10]=bytes pending an asynchronous unmap */
+int gg_slab_stats(gg_array *a, uint64_t *h_out11);
 
-/* Process-wide cache of physical slab chunks left by destroyed arrays
- * (reused by new arrays instead of fresh driver allocations; bounded by
- * GG_POOL_BYTES, default 4 GiB per device).  Shrink releases and trim() never
- * go to the cache.  stats: [0]=cached bytes, [1]=chunks, [2]=hits,
- * [3]=misses (process-wide), [4]=cap bytes. */
-int gg_pool_stats(int device, uint64_t *h_out5);
+/* Process-wide cache of physical slab chunks (per device and chunk size):
+ * chunks of destroyed arrays and chunks a shrink / trim unmaps, reused by any
+ * array before the driver is asked for new memory.  Bounded by GG_POOL_BYTES
+ * (default: a quarter of the device's memory); emptied on a cuMemCreate
+ * out-of-memory.  Besides loose handles it keeps whole slabs of destroyed
+ * arrays (VA regions with their extents still mapped) for the next array of
+ * the same shape, which adopts one with no driver call (GG_SLAB_CACHE=0
+ * disables).  stats: [0]=cached handle bytes, [1]=handles, [2]=hits,
+ * [3]=misses (process-wide), [4]=cap bytes (handles + slabs), [5]=destroyed
+ * arrays whose memory is not freed yet (their queued work is still
+ * running), [6]=handles the full pool refused (released to the driver),
+ * [7]=mapped bytes of cached slabs, [8]=cached slabs, [9]=slab adoptions
+ * (process-wide).  trim: wait for those, release everything to the driver. */
+int gg_pool_stats(int device, uint64_t *h_out10);
 int gg_pool_trim(int device);
+/* Free what destroyed arrays left behind once their queued work completed
+ * (gg_destroy records an event instead of synchronising the device);
+ * wait != 0 blocks until all of it is freed. */
+int gg_reclaim(int32_t wait);
 
 /* ---- baselines (baselines.py) on raw device buffers ---- */
 /* StaticArray/DoublingArray/ChunkTableArray.insert_batch (baselines.py:
@@ -251,6 +276,12 @@ int gg_pool_trim(int device);
  * landing at index >= capacity are dropped and counted in *d_counter. */
 int gg_flat_insert(void *d_buf, uint64_t capacity, uint64_t *d_counter, const void *d_vals,
                    uint64_t n, uint32_t elem_bytes, int32_t algo, void *stream);
+/* insert_batch with the reference's default semantics (one reservation,
+ * argument order; baselines.py:59-72): the caller reserved [start, start+n)
+ * on its host counter; the kernel copies d_vals there with 16 B vectors and
+ * adds n to *d_counter (may be NULL).  CapacityError past the capacity. */
+int gg_flat_append(void *d_buf, uint64_t capacity, uint64_t *d_counter, uint64_t start,
+                   const void *d_vals, uint64_t n, uint32_t elem_bytes, void *stream);
 /* contiguous +c passes over d_buf[0..n) (static r/w, flattened r/w) */
 int gg_flat_add(void *d_buf, uint64_t n, uint32_t dtype, const void *h_addend,
                 uint32_t passes, int32_t fused, void *stream);

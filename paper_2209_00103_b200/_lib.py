@@ -53,6 +53,7 @@ _SIGS = {
     "gg_insert": ([P, P, PU64, PU64, PI32, P], C.c_int),
     "gg_insert_duplicate": ([P, PI32, P], C.c_int),
     "gg_insert_ex": ([P, P, PU64, PU64, U32, PI32, P], C.c_int),
+    "gg_insert_ex2": ([P, P, PU64, PU64, U32, PI32, PU64, P], C.c_int),
     "gg_insert_duplicate_ex": ([P, U32, PI32, P], C.c_int),
     "gg_insert_lanes": ([P, P, P, PU64, U64, PI32, P], C.c_int),
     "gg_commit": ([P, P], C.c_int),
@@ -91,8 +92,11 @@ _SIGS = {
     "gg_slab_stats": ([P, PU64], C.c_int),
     "gg_pool_stats": ([C.c_int, PU64], C.c_int),
     "gg_pool_trim": ([C.c_int], C.c_int),
+    "gg_reclaim": ([I32], C.c_int),
+    "gg_settle": ([P], C.c_int),
     "gg_flat_insert": ([P, U64, P, P, U64, U32, I32, P], C.c_int),
     "gg_flat_add": ([P, U64, U32, P, U32, I32, P], C.c_int),
+    "gg_flat_append": ([P, U64, P, U64, P, U64, U32, P], C.c_int),
     "gg_ipc_alloc": ([U64, C.POINTER(C.c_void_p)], C.c_int),
     "gg_ipc_free": ([P], C.c_int),
     "gg_ipc_handle_bytes": ([], C.c_int),

@@ -118,8 +118,14 @@ class _FlatArray:
             self._tensor(rng.end)[rng.start:rng.end].copy_(v)
             return rng
         if algo is None:
-            self._tensor(start + n)[start:].copy_(v)
-            self.size_counter.fetch_add(n)
+            # one reservation of the whole batch (the reference's AtomicReserver:
+            # one counter op), then ONE vectorised copy kernel into [start, start+n)
+            self._count += n
+            self.size_counter.op_count += 1
+            L.check(L.lib.gg_flat_append(C.c_void_p(self._base), self.capacity,
+                                         C.c_void_p(self._d_count.data_ptr()), start,
+                                         C.c_void_p(v.data_ptr()), n, self.dtype.itemsize,
+                                         self._stream()), "flat_append")
             return ReservedRange(start, n)
         code = INSERT_ALGOS[algo]
         L.check(L.lib.gg_flat_insert(C.c_void_p(self._base), self.capacity,

@@ -11,8 +11,8 @@ bucket is released by a shrink).
 from __future__ import annotations
 
 import ctypes as C
-
 import threading
+import weakref
 
 import numpy as np
 
@@ -69,23 +69,34 @@ def _view(arr, addr: int, n: int):
 
 
 class _SizeCounter:
-    """The shard's size as the reference's AtomicCounter (value, op_count, fetch_add)."""
+    """The shard's size as the reference's AtomicCounter (value, op_count,
+    fetch_add).  One per (array, shard), cached by the array -- reservers
+    compare counters by identity -- and holding the array weakly, so the
+    cache forms no reference cycle (arrays are freed when dropped, not by
+    the cyclic collector at an arbitrary later point)."""
 
-    def __init__(self, shard: "ShardVector"):
-        self._sh = shard
+    def __init__(self, arr, s: int):
+        self._ref = weakref.ref(arr)
+        self._s = s
+
+    def _arr(self):
+        a = self._ref()
+        if a is None:
+            raise RuntimeError("the GrowableArray of this counter was destroyed")
+        return a
 
     @property
     def value(self) -> int:
-        return self._sh.size
+        return int(self._arr()._host()["sizes"][self._s])
 
     @property
     def op_count(self) -> int:
-        return int(self._sh._arr._host()["ops"][self._sh._s])
+        return int(self._arr()._host()["ops"][self._s])
 
     def fetch_add(self, amount: int) -> int:
-        a = self._sh._arr
+        a = self._arr()
         prev = C.c_uint64(0)
-        L.check(L.lib.gg_fetch_add(a._h, self._sh._s, int(amount), C.byref(prev), a._stream()),
+        L.check(L.lib.gg_fetch_add(a._h, self._s, int(amount), C.byref(prev), a._stream()),
                 "fetch_add")
         a._dirty()
         return int(prev.value)
@@ -196,11 +207,8 @@ class ShardVector:
 
     @property
     def size_counter(self) -> _SizeCounter:
-        # one counter object per shard: reservers compare counters by identity
-        c = self.__dict__.get("_counter")
-        if c is None:
-            c = self.__dict__["_counter"] = _SizeCounter(self)
-        return c
+        # one counter object per (array, shard): reservers compare counters by identity
+        return self._arr._counter(self._s)
 
     @property
     def table(self) -> BucketTable:
@@ -217,16 +225,19 @@ class ShardVector:
         """CAS-once allocation of bucket b on the device (paper Alg. 2)."""
         a = self._arr
         won = C.c_int32(0)
-        a._hook_exc.clear()
-        rc = L.lib.gg_new_bucket(a._h, self._s, int(b), C.byref(won), a._stream())
-        a._dirty()
-        if rc == L.GG_ENOMEM and self._s in a._hook_exc:
-            raise a._hook_exc.pop(self._s)
-        L.check(rc, "new_bucket")
+        with a._mu:
+            a._hook_exc = {}
+            rc = L.lib.gg_new_bucket(a._h, self._s, int(b), C.byref(won), a._stream())
+            a._dirty()
+            if rc == L.GG_ENOMEM and self._s in a._hook_exc:
+                raise a._hook_exc.pop(self._s)
+            L.check(rc, "new_bucket")
         return bool(won.value)
 
     def push_back_batch(self, values, reserver=None) -> ReservedRange:
-        """Append ``values`` at a freshly reserved contiguous range, argument order."""
+        """Append ``values`` at a freshly reserved contiguous range, argument
+        order; returns the range the library reserved (read under the
+        handle's lock, so concurrent callers on one shard get disjoint ranges)."""
         a = self._arr
         vals = a._device_values(values)
         n = int(vals.numel())
@@ -237,13 +248,12 @@ class ShardVector:
             return rng
         if n == 0:
             return ReservedRange(self.size_counter.fetch_add(0), 0)
-        start = self.size
         offsets = np.zeros(a.shard_count + 1, np.uint64)
         offsets[self._s + 1:] = n
-        failures = a._insert_device(vals, offsets)
+        failures, starts = a._insert_device(vals, offsets, want_starts=True)
         if failures:
             raise failures[self._s]
-        return ReservedRange(start, n)
+        return ReservedRange(int(starts[self._s]), n)
 
     def reserve(self, min_capacity: int) -> None:
         caps = np.zeros(self._arr.shard_count, np.uint64)

@@ -1190,6 +1190,44 @@ __global__ void k_zero_buckets(Tables t, const uint32_t *pairs, uint32_t npairs)
 }
 
 // ---- static-array baselines ---------------------------------------------------
+// Flat-array insert_batch with the reference's semantics (baselines.py:59-72,
+// 143-157, 224-236): ONE reservation of the whole batch, then an
+// argument-order copy to [start, start + n).  The reservation is the host's
+// (single host thread per array: `start` = the mirrored counter); CTA 0
+// publishes it on the device counter.  The copy is the walker's tile shape:
+// one tile of 256 threads x U 16 B vectors per CTA, all U loads issued
+// before the stores (cta_copy handles any relative alignment).
+template <int ESZ, int U>
+__global__ void __launch_bounds__(256) k_flat_append(char *buf, uint64_t start, unsigned long long *counter,
+                                                     const char *vals, uint64_t n, uint64_t tile) {
+  pdl_begin();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && counter) atomicAdd(counter, (unsigned long long)n);
+  const uint64_t lo = (uint64_t)blockIdx.x * tile;
+  if (lo >= n) return;
+  const uint64_t cnt = min(tile, n - lo);
+  cta_copy<ESZ, U>(buf + (start + lo) * ESZ, vals + lo * ESZ, cnt, threadIdx.x, blockDim.x);
+}
+
+// Paper 3-B-3 (block-level reservation), vectorised: each CTA reserves its
+// tile of 256 x U 16 B vectors with ONE atomicAdd on the shared counter and
+// copies it with 16 B stores (order between tiles is the atomics' order).
+// Elements past the capacity are dropped (counted in *counter).
+template <int ESZ, int U>
+__global__ void __launch_bounds__(256) k_flat_insert_block(char *buf, uint64_t cap,
+                                                           unsigned long long *counter,
+                                                           const char *vals, uint64_t n, uint64_t tile) {
+  __shared__ unsigned long long base_s;
+  pdl_begin();
+  const uint64_t lo = (uint64_t)blockIdx.x * tile;
+  if (lo >= n) return;
+  const uint64_t cnt = min(tile, n - lo);
+  if (threadIdx.x == 0) base_s = atomicAdd(counter, (unsigned long long)cnt);
+  __syncthreads();
+  const uint64_t base = base_s;
+  if (base >= cap) return;
+  cta_copy<ESZ, U>(buf + base * ESZ, vals + lo * ESZ, min(cnt, cap - base), threadIdx.x, blockDim.x);
+}
+
 template <int ESZ>
 __global__ void k_flat_insert(char *buf, uint64_t cap, unsigned long long *counter,
                               const char *vals, uint64_t n, int algo, uint64_t opaque_zero) {

@@ -86,25 +86,41 @@ struct Arena {
   }
 };
 
-// Process-wide cache of physical chunks released by DESTROYED arrays, per
-// device and chunk size: a new array maps a cached handle (cuMemMap +
-// cuMemSetAccess) instead of creating one, which avoids the driver's
-// allocate / scrub / free churn when arrays come and go (config 1 builds an
-// array per call).  Bounded (GG_POOL_BYTES, default 4 GiB per device) and
-// reported by gg_pool_stats / emptied by gg_pool_trim; a shrink's release
-// and trim() always return memory to the driver, so a live array's mapped
-// bytes are its whole footprint.
+// Process-wide cache of physical chunks, per device and chunk size (the
+// chunk size is a function of the bucket class and S, so the lists are
+// per-class free lists in effect): chunks of destroyed arrays and chunks a
+// shrink / trim unmaps go here, and a slab maps a cached handle (cuMemMap +
+// cuMemSetAccess) before asking the driver for a new one (cuMemCreate scrubs
+// pages; cuMemRelease frees them -- the expensive half of the VMM calls).
+// Bounded by GG_POOL_BYTES (default: a quarter of the device's memory, so an
+// array of up to that size is rebuilt entirely from cached chunks), reported
+// by gg_pool_stats, emptied by gg_pool_trim -- and emptied on demand when a
+// cuMemCreate runs out of memory.  A live array's mapped bytes are its
+// footprint; pooled chunks belong to no array.
 struct ChunkPool {
   std::mutex mu;
   std::vector<std::pair<size_t, CUmemGenericAllocationHandle>> free[64];
   uint64_t bytes[64] = {0};
-  uint64_t hits = 0, misses = 0;
-  uint64_t cap() {
-    static uint64_t c = [] {
+  uint64_t slab_bytes[64] = {0};           // mapped bytes of cached slabs (SlabCache), same cap
+  uint64_t caps[64] = {0};
+  uint64_t hits = 0, misses = 0, refused = 0;
+  uint64_t cap(int dev) {                  // caller holds mu
+    if (!caps[dev]) {
       const char *e = getenv("GG_POOL_BYTES");
-      return e ? strtoull(e, nullptr, 10) : (uint64_t(4) << 30);
-    }();
-    return c;
+      if (e) {
+        caps[dev] = strtoull(e, nullptr, 10);
+        if (!caps[dev]) caps[dev] = 1;     // 0 = no pooling
+      } else {
+        size_t fr = 0, tot = 0;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || !tot) tot = size_t(16) << 30;
+        if (cur != dev && cur >= 0) cudaSetDevice(cur);
+        caps[dev] = tot / 4;
+      }
+    }
+    return caps[dev];
   }
   bool take(int dev, size_t size, CUmemGenericAllocationHandle *h) {
     if (dev < 0 || dev >= 64) return false;
@@ -113,7 +129,8 @@ struct ChunkPool {
     for (size_t i = v.size(); i-- > 0;)
       if (v[i].first == size) {
         *h = v[i].second;
-        v.erase(v.begin() + i);
+        v[i] = v.back();
+        v.pop_back();
         bytes[dev] -= size;
         ++hits;
         return true;
@@ -124,16 +141,24 @@ struct ChunkPool {
   bool give(int dev, size_t size, CUmemGenericAllocationHandle h) {
     if (dev < 0 || dev >= 64) return false;
     std::lock_guard<std::mutex> g(mu);
-    if (bytes[dev] + size > cap()) return false;
+    if (bytes[dev] + slab_bytes[dev] + size > cap(dev)) { ++refused; return false; }
     free[dev].push_back({size, h});
     bytes[dev] += size;
     return true;
   }
-  void trim(int dev) {
+  // release cached handles to the driver (all of them, or until `want` bytes
+  // were freed)
+  uint64_t trim(int dev, uint64_t want = ~uint64_t(0)) {
     std::lock_guard<std::mutex> g(mu);
-    for (auto &e : free[dev]) drv().release(e.second);
-    free[dev].clear();
-    bytes[dev] = 0;
+    uint64_t got = 0;
+    auto &v = free[dev];
+    while (!v.empty() && got < want) {
+      drv().release(v.back().second);
+      got += v.back().first;
+      bytes[dev] -= v.back().first;
+      v.pop_back();
+    }
+    return got;
   }
 };
 
@@ -142,21 +167,41 @@ inline ChunkPool &chunk_pool() {
   return p;
 }
 
+// deferred teardown (defined below): free what destroyed arrays left once the
+// work queued on them completed; wait = block until all of it has
+inline void reclaim(bool wait);
+
 // Slab store of one GGArray: a VA region per bucket class, slot s of class b
-// = bucket (s, b).  Physical memory is mapped per chunk (a gran-multiple
-// piece of a region) and refcounted by the live buckets overlapping it, so
-// releasing buckets returns memory as soon as a chunk empties.  Classes whose
-// region is smaller than one granule share one packed region ("small"), so a
-// tiny array costs one granule, not one per class.
+// = bucket (s, b).  Physical memory is refcounted per grid chunk (a
+// gran-multiple piece of a region) by the live buckets overlapping it, and
+// mapped in EXTENTS -- runs of consecutive grid chunks backed by ONE
+// physical handle: a uniform operation that backs all S slots of a class
+// maps the whole region with one cuMemCreate + cuMemMap and one
+// cuMemSetAccess per operation (the driver charges ~0.5-1 ms per call almost
+// regardless of size: B200 probe, 8 GiB as one handle 1.0 ms, as 8 x 1 GiB
+// 4.8 ms, as 80 chunks ~21-111 ms), while per-shard backing (ragged plans)
+// maps single grid chunks, so an uneven split strands at most one grid
+// chunk (<= 1/8 of the region).  An extent is unmapped when none of its
+// chunks holds a live bucket.  Classes whose region is smaller than one
+// granule share one packed region ("small"), so a tiny array costs one
+// granule, not one per class.
 struct Slab {
-  struct Chunk { uint32_t refs = 0; bool mapped = false; CUmemGenericAllocationHandle h = 0; };
+  struct Chunk {
+    uint32_t refs = 0;
+    bool mapped = false, doomed = false;
+    uint32_t head = 0;                      // first grid chunk of its extent
+    uint32_t len = 0;                       // (head only) grid chunks in the extent
+    CUmemGenericAllocationHandle h = 0;     // (head only) the extent's handle
+  };
   struct Region { CUdeviceptr base = 0; size_t va = 0, chunk = 0; std::vector<Chunk> chunks; };
-  static constexpr size_t kChunk = size_t(1) << 30;    // largest mapping unit of a region
+  static constexpr size_t kChunk = size_t(1) << 30;    // largest grid chunk of a region
   int dev = 0;
   size_t gran = 0;
   uint32_t S = 0, MB = 0;
   uint64_t va_budget = 0, va_used = 0, mapped = 0, cached = 0;  // cached: mapped, 0 refs
   uint64_t n_map = 0, n_unmap = 0, ns_map = 0, ns_unmap = 0, n_regions = 0;  // cost counters
+  uint64_t n_create = 0, n_pool = 0;   // handles from the driver / from the process pool
+  uint64_t adopted = 0;                // bytes mapped when this slab was adopted (slab cache)
   static uint64_t now_ns() {
     return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
         std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -185,7 +230,7 @@ struct Slab {
       small.chunk = gran;
       small.chunks.assign(small.va / gran, Chunk());
       int rc = reserve_va(small);
-    if (rc) return rc;
+      if (rc) return rc;
     }
     return GG_OK;
   }
@@ -205,12 +250,10 @@ struct Slab {
     n_regions += 1;
     return GG_OK;
   }
-  // mapping unit of class b's region: a power of two >= one granule and >=
-  // one bucket, 1/8..1/16 of the region, at most kChunk.  Each cuMemCreate /
-  // Map / SetAccess call costs ~1.5-2 ms of driver time almost regardless of
-  // size (tools/vmm_fresh_probe.py: 8 GiB as 128 x 64 MiB 250-1450 ms, as
-  // 8 x 1 GiB 36 ms), so chunks are large; a partly live top class (an
-  // uneven split) strands at most one chunk, <= 1/8 of its region.
+  // refcount grid of class b's region: a power of two >= one granule and >=
+  // one bucket, 1/8..1/16 of the region, at most kChunk (uniform backing maps
+  // whole runs of grid chunks as one extent, so the grid only bounds what an
+  // uneven split strands)
   uint64_t chunk_for(uint32_t b) const {
     if (bytes[b] >= kChunk) return bytes[b];
     const uint64_t R = S * bytes[b];
@@ -246,36 +289,60 @@ struct Slab {
     c0 = off / r->chunk;
     c1 = (off + bytes[b] - 1) / r->chunk;
   }
-  int map_chunk(Region &r, size_t c) {
-    Chunk &k = r.chunks[c];
-    if (k.mapped) { if (!k.refs) cached -= r.chunk; return GG_OK; }
+  // a physical handle of `size` bytes: the process pool first (after freeing
+  // whatever destroyed arrays left behind), else the driver; on the driver's
+  // out-of-memory, wait for deferred teardown and empty the caches, then retry
+  int new_handle(size_t size, CUmemGenericAllocationHandle *h);
+  // map grid chunks [c0, c0 + n) of r (all unmapped) as one extent
+  int map_run(Region &r, size_t c0, size_t n) {
     const uint64_t t0 = now_ns();
-    if (!chunk_pool().take(dev, r.chunk, &k.h)) {
-      CUmemAllocationProp prop = props();
-      CU_TRY(drv().create(&k.h, r.chunk, &prop, 0));
-    }
-    const CUdeviceptr at = r.base + c * r.chunk;
-    if (drv().map(at, r.chunk, 0, k.h, 0) != CUDA_SUCCESS) {
-      drv().release(k.h);
+    const size_t bytes_ = n * r.chunk;
+    Chunk &hd = r.chunks[c0];
+    { int rc = new_handle(bytes_, &hd.h); if (rc) return rc; }
+    const CUdeviceptr at = r.base + c0 * r.chunk;
+    if (drv().map(at, bytes_, 0, hd.h, 0) != CUDA_SUCCESS) {
+      give_or_release(bytes_, hd.h);
+      hd.h = 0;
       return fail(GG_ENOMEM, "cuMemMap failed");
     }
     // access rights are granted in finalize_access(), one cuMemSetAccess per
-    // contiguous run of chunks mapped by the same operation (the call costs
+    // contiguous run of extents mapped by the same operation (the call costs
     // about as much as the mapping itself)
-    pending.push_back({&r, c});
-    static const bool batch = [] { const char *e = getenv("GG_BATCH_ACCESS"); return !e || e[0] != '0'; }();
-    if (!batch) {
-      int rc = finalize_access();
-      if (rc) return rc;
+    pending.push_back({&r, c0});
+    hd.len = (uint32_t)n;
+    for (size_t c = c0; c < c0 + n; ++c) {
+      r.chunks[c].mapped = true;
+      r.chunks[c].head = (uint32_t)c0;
+      cached += r.chunk;                      // refs are added by the caller
     }
-    k.mapped = true;
-    mapped += r.chunk;
+    mapped += bytes_;
     n_map += 1;
     ns_map += now_ns() - t0;
+    static const bool batch = [] { const char *e = getenv("GG_BATCH_ACCESS"); return !e || e[0] != '0'; }();
+    if (!batch) return finalize_access();
     return GG_OK;
   }
-  std::vector<std::pair<Region *, size_t>> pending;   // mapped, access not granted yet
-  // grant read/write access to every chunk mapped since the last call; must
+  void give_or_release(size_t size, CUmemGenericAllocationHandle h);
+  // a mapped chunk about to gain a reference: un-doom its extent
+  void revive(Region &r, size_t c) {
+    Chunk &k = r.chunks[c];
+    if (!k.doomed) return;
+    const Chunk &hd = r.chunks[k.head];
+    for (size_t i = k.head; i < k.head + hd.len; ++i) r.chunks[i].doomed = false;
+    doomed_bytes -= hd.len * r.chunk;
+  }
+  void add_ref(Region &r, size_t c, uint32_t n) {
+    Chunk &k = r.chunks[c];
+    revive(r, c);
+    if (!k.refs) cached -= r.chunk;
+    k.refs += n;
+  }
+  int map_chunk(Region &r, size_t c) {
+    if (r.chunks[c].mapped) return GG_OK;
+    return map_run(r, c, 1);
+  }
+  std::vector<std::pair<Region *, size_t>> pending;   // extents mapped, access not granted yet
+  // grant read/write access to every extent mapped since the last call; must
   // run before a kernel can touch them (push_cbase calls it)
   int finalize_access() {
     if (pending.empty()) return GG_OK;
@@ -288,10 +355,14 @@ struct Slab {
     int rc = GG_OK;
     for (size_t i = 0; i < pending.size();) {
       Region *r = pending[i].first;
+      size_t end = pending[i].second + r->chunks[pending[i].second].len;
       size_t j = i + 1;
-      while (j < pending.size() && pending[j].first == r && pending[j].second == pending[j - 1].second + 1) ++j;
+      while (j < pending.size() && pending[j].first == r && pending[j].second == end) {
+        end += r->chunks[pending[j].second].len;
+        ++j;
+      }
       const CUdeviceptr at = r->base + pending[i].second * r->chunk;
-      if (drv().set_access(at, (j - i) * r->chunk, &acc, 1) != CUDA_SUCCESS && !rc)
+      if (drv().set_access(at, (end - pending[i].second) * r->chunk, &acc, 1) != CUDA_SUCCESS && !rc)
         rc = fail(GG_ENOMEM, "cuMemSetAccess failed");
       i = j;
     }
@@ -299,17 +370,78 @@ struct Slab {
     ns_map += now_ns() - t0;
     return rc;
   }
-  void unmap_chunk(Region &r, size_t c) {
-    Chunk &k = r.chunks[c];
+  bool extent_free(const Region &r, size_t head) const {
+    const Chunk &hd = r.chunks[head];
+    for (size_t c = head; c < head + hd.len; ++c)
+      if (r.chunks[c].refs) return false;
+    return true;
+  }
+  // unmap an extent without live buckets; its physical handle goes to the
+  // process pool (released to the driver only when the pool is full)
+  void unmap_extent(Region &r, size_t head) {
+    Chunk &hd = r.chunks[head];
     const uint64_t t0 = now_ns();
-    drv().unmap(r.base + c * r.chunk, r.chunk);
-    drv().release(k.h);
-    k.mapped = false;
-    k.h = 0;
-    mapped -= r.chunk;
-    cached -= r.chunk;
+    const size_t n = hd.len, bytes_ = n * r.chunk;
+    drv().unmap(r.base + head * r.chunk, bytes_);
+    give_or_release(bytes_, hd.h);
+    if (hd.doomed) doomed_bytes -= bytes_;
+    for (size_t c = head; c < head + n; ++c) {
+      Chunk &k = r.chunks[c];
+      k.mapped = k.doomed = false;
+      k.len = 0;
+      k.h = 0;
+    }
+    mapped -= bytes_;
+    cached -= bytes_;
     n_unmap += 1;
     ns_unmap += now_ns() - t0;
+  }
+  // Asynchronous trim: extents that lose their last live bucket in a shrink
+  // stay mapped until the work queued before the shrink completed (an event
+  // on its stream, no device-wide synchronize); they are unmapped by the
+  // next reap_doomed -- or taken back in place for free if a later operation
+  // needs them first.
+  std::vector<std::pair<Region *, size_t>> doomed;
+  uint64_t doomed_bytes = 0;
+  cudaEvent_t doom_ev = nullptr;
+  template <typename F>
+  void for_free_extents(Region &r, F f) {      // highest first
+    for (size_t c = r.chunks.size(); c-- > 0;) {
+      Chunk &k = r.chunks[c];
+      if (k.mapped && k.head == c && extent_free(r, c) && !f(r, c)) return;
+    }
+  }
+  int doom_to(uint64_t keep, cudaStream_t st) {
+    finalize_access();
+    auto pick = [&](Region &r, size_t head) {
+      if (mapped - doomed_bytes <= keep) return false;
+      Chunk &hd = r.chunks[head];
+      if (hd.doomed) return true;
+      for (size_t c = head; c < head + hd.len; ++c) r.chunks[c].doomed = true;
+      doomed_bytes += hd.len * r.chunk;
+      doomed.push_back({&r, head});
+      return true;
+    };
+    for (int b = (int)MB - 1; b >= 0 && mapped - doomed_bytes > keep && cached; --b)
+      if (small_off[b] == ~uint64_t(0)) for_free_extents(big[b], pick);
+    if (mapped - doomed_bytes > keep) for_free_extents(small, pick);
+    if (doomed.empty()) return GG_OK;
+    if (!doom_ev) CUDA_TRY(cudaEventCreateWithFlags(&doom_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(doom_ev, st));    // everything queued so far (incl. the shrink)
+    return GG_OK;
+  }
+  // unmap the doomed extents once their event completed (wait = block on it)
+  void reap_doomed(bool wait) {
+    if (doomed.empty()) return;
+    if (wait) cudaEventSynchronize(doom_ev);
+    else if (cudaEventQuery(doom_ev) != cudaSuccess) return;
+    for (auto &d : doomed) {
+      Chunk &hd = d.first->chunks[d.second];
+      if (hd.doomed && hd.mapped && hd.head == d.second && extent_free(*d.first, d.second))
+        unmap_extent(*d.first, d.second);
+    }
+    doomed.clear();
+    doomed_bytes = 0;
   }
   // back bucket (s, b) with physical memory (region must exist)
   int back(uint32_t s, uint32_t b) {
@@ -321,13 +453,13 @@ struct Slab {
         for (size_t d = c0; d < c; ++d) drop(*r, d);
         return rc;
       }
-      r->chunks[c].refs += 1;
+      add_ref(*r, c, 1);
     }
     return GG_OK;
   }
   void drop(Region &r, size_t c) {
     Chunk &k = r.chunks[c];
-    if (--k.refs == 0) cached += r.chunk;      // stays mapped until trim()
+    if (--k.refs == 0) cached += r.chunk;      // stays mapped until trimmed
   }
   // bucket (s, b) is no longer live
   void unback(uint32_t s, uint32_t b) {
@@ -349,28 +481,23 @@ struct Slab {
       f(r, c, (uint32_t)(last - first + 1));
     }
   }
-  // back slots [s0, s1) of class b (region must exist); all-or-nothing
+  // back slots [s0, s1) of class b (region must exist); all-or-nothing.
+  // Maximal runs of unmapped grid chunks are mapped as one extent each.
   int back_range(uint32_t b, uint32_t s0, uint32_t s1) {
     if (s1 <= s0) return GG_OK;
-    int rc = GG_OK;
-    std::vector<std::pair<Region *, size_t>> done;
-    for_range(b, s0, s1, [&](Region &r, size_t c, uint32_t n) {
-      if (rc) return;
-      if ((rc = map_chunk(r, c))) return;
-      r.chunks[c].refs += n;
-      done.push_back({&r, c});
-    });
-    if (rc) {                                   // roll back this call's refs
-      size_t i = 0;
-      for_range(b, s0, s1, [&](Region &r, size_t c, uint32_t n) {
-        if (i < done.size() && done[i].first == &r && done[i].second == c) {
-          r.chunks[c].refs -= n;
-          if (!r.chunks[c].refs) cached += r.chunk;
-          ++i;
-        }
-      });
+    Region &r = region(b);
+    const uint64_t base = small_off[b] != ~uint64_t(0) ? small_off[b] : 0, bb = bytes[b];
+    const size_t lo = (base + (uint64_t)s0 * bb) / r.chunk, hi = (base + (uint64_t)s1 * bb - 1) / r.chunk;
+    for (size_t c = lo; c <= hi;) {
+      if (r.chunks[c].mapped) { ++c; continue; }
+      size_t e = c;
+      while (e + 1 <= hi && !r.chunks[e + 1].mapped) ++e;
+      int rc = map_run(r, c, e - c + 1);       // (a failure leaves earlier runs cached, refs 0)
+      if (rc) return rc;
+      c = e + 1;
     }
-    return rc;
+    for_range(b, s0, s1, [&](Region &rr, size_t c, uint32_t n) { add_ref(rr, c, n); });
+    return GG_OK;
   }
   void unback_range(uint32_t b, uint32_t s0, uint32_t s1) {
     if (s1 <= s0) return;
@@ -388,39 +515,37 @@ struct Slab {
     for (size_t c = c0; c <= c1; ++c) if (!r->chunks[c].mapped) n += r->chunk;
     return n;
   }
-  // unmap chunks without live buckets, largest class first, until at most
-  // `keep` bytes stay mapped (caller synchronised the device)
+  // unmap extents without live buckets, largest class first, until at most
+  // `keep` bytes stay mapped (caller synchronised the work that used them)
   void trim_to(uint64_t keep) {
     finalize_access();
-    for (int b = (int)MB - 1; b >= 0 && mapped > keep && cached; --b) {
-      if (small_off[b] != ~uint64_t(0)) continue;
-      Region &r = big[b];
-      for (size_t c = r.chunks.size(); c-- > 0 && mapped > keep;)
-        if (r.chunks[c].mapped && r.chunks[c].refs == 0) unmap_chunk(r, c);
-    }
-    for (size_t c = small.chunks.size(); c-- > 0 && mapped > keep;)
-      if (small.chunks[c].mapped && small.chunks[c].refs == 0) unmap_chunk(small, c);
-  }
-  // unmap every chunk without live buckets (caller synchronised the device)
-  void trim() {
-    finalize_access();
-    auto go = [&](Region &r) {
-      for (size_t c = 0; c < r.chunks.size(); ++c)
-        if (r.chunks[c].mapped && r.chunks[c].refs == 0) unmap_chunk(r, c);
+    reap_doomed(true);
+    auto go = [&](Region &r, size_t head) {
+      if (mapped <= keep) return false;
+      unmap_extent(r, head);
+      return true;
     };
-    go(small);
-    for (auto &r : big) go(r);
+    for (int b = (int)MB - 1; b >= 0 && mapped > keep && cached; --b)
+      if (small_off[b] == ~uint64_t(0)) for_free_extents(big[b], go);
+    if (mapped > keep) for_free_extents(small, go);
   }
-  // the array is going away: unmap everything, keep physical chunks in the
-  // process pool while it has room (the caller synchronised the device)
+  // unmap every extent without live buckets (caller synchronised)
+  void trim() { trim_to(0); }
+  // the array is going away: unmap everything, physical handles to the
+  // process pool while it has room (the caller synchronised the work)
   void destroy() {
     pending.clear();
+    doomed.clear();
+    doomed_bytes = 0;
+    if (doom_ev) cudaEventDestroy(doom_ev), doom_ev = nullptr;
     auto go = [&](Region &r) {
-      for (size_t c = 0; c < r.chunks.size(); ++c)
-        if (r.chunks[c].mapped) {
-          drv().unmap(r.base + c * r.chunk, r.chunk);
-          if (!chunk_pool().give(dev, r.chunk, r.chunks[c].h)) drv().release(r.chunks[c].h);
+      for (size_t c = 0; c < r.chunks.size(); ++c) {
+        Chunk &k = r.chunks[c];
+        if (k.mapped && k.head == c) {
+          drv().unmap(r.base + c * r.chunk, k.len * r.chunk);
+          give_or_release(k.len * r.chunk, k.h);
         }
+      }
       if (r.base) drv().addr_free(r.base, r.va);
       r = Region();
     };
@@ -428,7 +553,177 @@ struct Slab {
     for (auto &r : big) go(r);
     mapped = cached = va_used = 0;
   }
+  // the same slab for a new array (slab cache): no live buckets, every
+  // mapped chunk cached in place
+  void adopt_reset() {
+    pending.clear();
+    doomed.clear();
+    doomed_bytes = 0;
+    auto go = [&](Region &r) {
+      for (auto &k : r.chunks) { k.refs = 0; k.doomed = false; }
+    };
+    go(small);
+    for (auto &r : big) go(r);
+    cached = mapped;
+    adopted = mapped;
+    n_map = n_unmap = ns_map = ns_unmap = n_create = n_pool = 0;
+  }
+  // shape key of the slab cache: same S, classes, bucket bytes and budget
+  bool same_shape(const Slab &o) const {
+    return dev == o.dev && S == o.S && MB == o.MB && bytes == o.bytes && va_budget == o.va_budget &&
+           gran == o.gran;
+  }
 };
+
+// Slab cache: the slab of a destroyed array -- VA regions with their
+// extents still mapped -- kept whole for the next array of the same shape
+// (S, element size, first bucket size, max_buckets), which adopts it with
+// every chunk cached in place: rebuilding an array (from_flat into a fresh
+// GGArray, the paper's two-phase pattern) then costs no driver call at all.
+// Its mapped bytes count against the process pool's cap; least recently
+// cached slabs are evicted first (their handles go to the chunk pool).
+struct SlabCache {
+  std::mutex mu;
+  std::vector<Slab *> slabs;                 // oldest first
+  uint64_t hits = 0, offered = 0;
+};
+
+inline SlabCache &slab_cache() {
+  static SlabCache c;
+  return c;
+}
+
+inline void destroy_slabs(std::vector<Slab *> &v) {
+  for (Slab *x : v) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != x->dev) cudaSetDevice(x->dev);
+    x->destroy();
+    if (cur != x->dev && cur >= 0) cudaSetDevice(cur);
+    delete x;
+  }
+  v.clear();
+}
+
+// drop every cached slab of `dev` (-1: all devices)
+inline void slab_cache_evict(int dev) {
+  std::vector<Slab *> out;
+  {
+    SlabCache &C = slab_cache();
+    std::lock_guard<std::mutex> g(C.mu);
+    ChunkPool &P = chunk_pool();
+    std::lock_guard<std::mutex> g2(P.mu);
+    for (size_t i = 0; i < C.slabs.size();) {
+      if (dev < 0 || C.slabs[i]->dev == dev) {
+        P.slab_bytes[C.slabs[i]->dev] -= C.slabs[i]->mapped;
+        out.push_back(C.slabs[i]);
+        C.slabs.erase(C.slabs.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+  }
+  destroy_slabs(out);
+}
+
+// keep `sl` (moved in) for a later array of the same shape; false = not
+// kept (the caller destroys it)
+inline bool slab_offer(Slab &sl) {
+  if (!sl.mapped || sl.dev < 0 || sl.dev >= 64) return false;
+  static const bool on = [] { const char *e = getenv("GG_SLAB_CACHE"); return !e || e[0] != '0'; }();
+  if (!on) return false;
+  std::vector<Slab *> out;
+  bool kept = false;
+  {
+    SlabCache &C = slab_cache();
+    std::lock_guard<std::mutex> g(C.mu);
+    ChunkPool &P = chunk_pool();
+    std::lock_guard<std::mutex> g2(P.mu);
+    const int d = sl.dev;
+    const uint64_t cap = P.cap(d);
+    if (sl.mapped <= cap) {
+      // make room: oldest cached slabs of this device first, then pooled handles
+      for (size_t i = 0; i < C.slabs.size() && P.bytes[d] + P.slab_bytes[d] + sl.mapped > cap;) {
+        if (C.slabs[i]->dev == d) {
+          P.slab_bytes[d] -= C.slabs[i]->mapped;
+          out.push_back(C.slabs[i]);
+          C.slabs.erase(C.slabs.begin() + i);
+        } else {
+          ++i;
+        }
+      }
+      while (!P.free[d].empty() && P.bytes[d] + P.slab_bytes[d] + sl.mapped > cap) {
+        drv().release(P.free[d].back().second);
+        P.bytes[d] -= P.free[d].back().first;
+        P.free[d].pop_back();
+      }
+      if (P.bytes[d] + P.slab_bytes[d] + sl.mapped <= cap) {
+        Slab *x = new Slab(std::move(sl));
+        x->pending.clear();
+        x->doomed.clear();
+        x->doomed_bytes = 0;
+        if (x->doom_ev) cudaEventDestroy(x->doom_ev), x->doom_ev = nullptr;
+        C.slabs.push_back(x);
+        P.slab_bytes[d] += x->mapped;
+        ++C.offered;
+        kept = true;
+      }
+    }
+  }
+  destroy_slabs(out);                        // evicted slabs' handles -> the chunk pool
+  return kept;
+}
+
+// replace `sl` (freshly initialised, nothing mapped) by a cached slab of the
+// same shape, if any (most recent first)
+inline bool slab_adopt(Slab &sl) {
+  Slab *x = nullptr;
+  {
+    SlabCache &C = slab_cache();
+    std::lock_guard<std::mutex> g(C.mu);
+    for (size_t i = C.slabs.size(); i-- > 0;)
+      if (C.slabs[i]->same_shape(sl)) {
+        x = C.slabs[i];
+        C.slabs.erase(C.slabs.begin() + i);
+        ++C.hits;
+        break;
+      }
+    if (x) {
+      ChunkPool &P = chunk_pool();
+      std::lock_guard<std::mutex> g2(P.mu);
+      P.slab_bytes[x->dev] -= x->mapped;
+    }
+  }
+  if (!x) return false;
+  sl.destroy();                              // the fresh slab's (empty) regions
+  sl = std::move(*x);
+  delete x;
+  sl.adopt_reset();
+  return true;
+}
+
+inline void Slab::give_or_release(size_t size, CUmemGenericAllocationHandle h) {
+  if (!chunk_pool().give(dev, size, h)) drv().release(h);
+}
+
+inline int Slab::new_handle(size_t size, CUmemGenericAllocationHandle *h) {
+  if (chunk_pool().take(dev, size, h)) { ++n_pool; return GG_OK; }
+  reclaim(false);
+  if (chunk_pool().take(dev, size, h)) { ++n_pool; return GG_OK; }
+  CUmemAllocationProp prop = props();
+  CUresult r = drv().create(h, size, &prop, 0);
+  if (r == CUDA_ERROR_OUT_OF_MEMORY) {       // free what the process caches, then retry once
+    reclaim(true);
+    if (chunk_pool().take(dev, size, h)) { ++n_pool; return GG_OK; }
+    slab_cache_evict(dev);
+    if (chunk_pool().take(dev, size, h)) { ++n_pool; return GG_OK; }
+    chunk_pool().trim(dev);
+    r = drv().create(h, size, &prop, 0);
+  }
+  if (r != CUDA_SUCCESS) return fail(GG_ENOMEM, "cuMemCreate failed (device memory exhausted)");
+  ++n_create;
+  return GG_OK;
+}
 
 // Every library kernel is launched with programmatic stream serialization
 // (PDL): it may start while its predecessor drains and waits in
@@ -590,6 +885,81 @@ struct Uploader {
   }
 
 };
+
+// What a destroyed array leaves behind, freed once an event recorded behind
+// the array's last queued work completes (gg_destroy costs an event record,
+// not a device-wide synchronize).  Its slab chunks go to the process pool.
+struct Grave {
+  int dev = 0;
+  cudaEvent_t ev = nullptr;           // nullptr: nothing queued any more
+  Slab slab;
+  Uploader up;
+  void *dmem = nullptr;               // cudaMallocAsync'd metadata block
+  char *h_scratch = nullptr;          // pinned
+  cudaEvent_t ord_ev = nullptr;
+  void free_all() {
+    if (!slab_offer(slab)) slab.destroy();   // kept whole for the next same-shape array
+    up.destroy();
+    if (h_scratch) cudaFreeHost(h_scratch);
+    if (dmem) cudaFreeAsync(dmem, 0);
+    if (ord_ev) cudaEventDestroy(ord_ev);
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+
+struct Reclaimer {
+  std::mutex mu;
+  std::vector<Grave *> graves;
+  uint64_t buried = 0, freed = 0;
+};
+
+inline Reclaimer &reclaimer() {
+  static Reclaimer r;
+  return r;
+}
+
+inline void bury(Grave *g) {
+  Reclaimer &R = reclaimer();
+  std::lock_guard<std::mutex> l(R.mu);
+  R.graves.push_back(g);
+  ++R.buried;
+}
+
+inline void reclaim(bool wait) {
+  Reclaimer &R = reclaimer();
+  std::vector<Grave *> ready;
+  {
+    std::lock_guard<std::mutex> l(R.mu);
+    if (R.graves.empty()) return;
+    for (size_t i = 0; i < R.graves.size();) {
+      Grave *g = R.graves[i];
+      bool done = !g->ev;
+      if (!done) {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != g->dev) cudaSetDevice(g->dev);
+        done = wait ? cudaEventSynchronize(g->ev) == cudaSuccess : cudaEventQuery(g->ev) == cudaSuccess;
+        if (cur != g->dev && cur >= 0) cudaSetDevice(cur);
+      }
+      if (done) {
+        ready.push_back(g);
+        R.graves[i] = R.graves.back();
+        R.graves.pop_back();
+      } else {
+        ++i;
+      }
+    }
+    R.freed += ready.size();
+  }
+  for (Grave *g : ready) {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != g->dev) cudaSetDevice(g->dev);
+    g->free_all();
+    if (cur != g->dev && cur >= 0) cudaSetDevice(cur);
+    delete g;
+  }
+}
 
 }  // namespace gg
 

@@ -57,6 +57,14 @@ struct gg_array {
   Uploader up;
   Tables t;          // device pointers (kernel argument)
   void *dmem = nullptr;
+  // stream order between calls: every device-touching call on stream st waits
+  // for the previous call's stream when it differs (one event), so deferred
+  // passes and a later call on another stream never run concurrently
+  cudaStream_t last_st = nullptr;
+  bool have_last = false;
+  bool captured = false;                                 // ever issued under stream capture
+  cudaEvent_t ord_ev = nullptr;
+  bool view_out = false;                                 // gg_device_view_get without a sync yet
   int *d_won = nullptr;
   char *d_scratch = nullptr;   // 64 B element scratch for get/set
   char *h_scratch = nullptr;   // pinned
@@ -237,13 +245,16 @@ cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *ds
   if (env_smem >= 0 && (U == 8 || U == 4)) smem = env_smem;
   if (env_carve >= 0 && (U == 8 || U == 4)) carve = env_carve;
   if (smem > 0 || carve >= 0) {
-    static bool attr = false;                 // once per kernel instantiation
-    if (!attr) {
+    // function attributes live in each device's context: once per kernel
+    // instantiation and device (a->dev < 64)
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = uint64_t(1) << (a->dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_walk<ESZ, W, T, U, kDefLS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (carve >= 0)
         cudaFuncSetAttribute(k_walk<ESZ, W, T, U, kDefLS, P>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
-      attr = true;
+      attr_set.fetch_or(bit, std::memory_order_acq_rel);
     }
   }
   return launch_k(k_walk<ESZ, W, T, U, kDefLS, P>, (unsigned)grid, kThreads, smem > 0 ? (size_t)smem : 0, st, t,
@@ -300,28 +311,30 @@ uint32_t meta_threads(const gg_array *a) { return std::min<uint32_t>(1024, (a->S
 
 bool g_fuse = true;             // metadata CTA inside the planned walk (GG_FUSE_META=0 disables)
 
-// launch a deferred metadata pass, if any (on the stream of its walk)
-int flush_meta(gg_array *a) {
+// launch a deferred metadata pass, if any: on the calling stream `st`
+// (already ordered after the stream the pass was deferred on, order_stream),
+// or on the stream of its walk for calls without a stream
+int flush_meta(gg_array *a, cudaStream_t st = nullptr, bool on_st = false) {
   if (!a->pend) return GG_OK;
   a->pend = false;
   Tables t = tables_for_launch(a, false);
-  CUDA_TRY(launch_k(k_planned_meta, 1, meta_threads(a), 0, a->pend_st, t, a->pend_fz));
+  CUDA_TRY(launch_k(k_planned_meta, 1, meta_threads(a), 0, on_st ? st : a->pend_st, t, a->pend_fz));
   return GG_OK;
 }
 
-// launch a deferred uniform grow, if any
-int flush_grow(gg_array *a) {
+// launch a deferred uniform grow, if any (same stream rule)
+int flush_grow(gg_array *a, cudaStream_t st = nullptr, bool on_st = false) {
   if (!a->pend_grow) return GG_OK;
   const uint32_t k = a->pend_grow;
   a->pend_grow = 0;
   Tables t = tables_for_launch(a, true);
-  CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, a->pend_grow_st, t, k));
+  CUDA_TRY(launch_k(k_grow, (a->S + 255) / 256, 256, 0, on_st ? st : a->pend_grow_st, t, k));
   return GG_OK;
 }
 
-int flush_pending(gg_array *a) {
-  int rc = flush_meta(a);
-  return rc ? rc : flush_grow(a);
+int flush_pending(gg_array *a, cudaStream_t st = nullptr, bool on_st = false) {
+  int rc = flush_meta(a, st, on_st);
+  return rc ? rc : flush_grow(a, st, on_st);
 }
 
 void flip_buffers(gg_array *a) {
@@ -334,6 +347,48 @@ bool capturing_now(gg_array *a, cudaStream_t st) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   return a->up.capturing ||
          (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone);
+}
+
+// Stream order between calls on one handle (stream-ordered semantics across
+// streams): a call on stream st after a call on another stream makes st wait
+// for that stream's work so far (one event).  Deferred passes are then
+// launched on st.  Under stream capture the caller orders its streams (an
+// event recorded outside a capture cannot be waited on inside it).
+int order_stream(gg_array *a, cudaStream_t st) {
+  if (capturing_now(a, st)) { a->captured = true; return GG_OK; }
+  if (a->have_last && a->last_st != st) {
+    if (!a->ord_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->ord_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(a->ord_ev, a->last_st));
+    CUDA_TRY(cudaStreamWaitEvent(st, a->ord_ev, 0));
+  }
+  a->last_st = st;
+  a->have_last = true;
+  return GG_OK;
+}
+
+// entry of a device-touching call on stream st: order, then launch whatever
+// was deferred (on st)
+int enter(gg_array *a, cudaStream_t st) {
+  int rc = order_stream(a, st);
+  return rc ? rc : flush_pending(a, st, true);
+}
+
+// mutating calls are refused while a device view is out: a user kernel may
+// be appending through it, and the host mirrors the planner reads are stale
+// until gg_device_view_sync
+int check_no_view(const gg_array *a) {
+  return a->view_out ? fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync first)") : GG_OK;
+}
+
+// wait for the work queued on this handle so far: an event behind its last
+// call's stream (every earlier stream is ordered before it); a device
+// synchronize for handles that were captured into graphs
+int wait_last(gg_array *a) {
+  if (a->captured || !a->have_last) { CUDA_TRY(cudaDeviceSynchronize()); return GG_OK; }
+  if (!a->ord_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->ord_ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(a->ord_ev, a->last_st));
+  CUDA_TRY(cudaEventSynchronize(a->ord_ev));
+  return GG_OK;
 }
 
 // the metadata pass may ride inside the planned walk (and take a deferred
@@ -389,7 +444,7 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
   // copy kernels.
   if (!p.any_ctl && p.zero_pairs.empty() && reserve_mode != 2 && !(flags & GG_F_UNFUSED)) {
     const bool commit = (flags & GG_F_COMMIT) != 0;
-    if (total && fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
+    if (total && fuse_ok(a, st)) {
       // ONE launch: copy CTAs + a metadata CTA writing the next size/prefix
       // pair (and publishing a deferred grow)
       Fuse fz{reserve_mode, commit ? 1 : 0};
@@ -406,7 +461,7 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
       if (commit) { host_commit(a); *committed = true; }
       return GG_OK;
     }
-    if ((rc = flush_grow(a))) return rc;
+    if ((rc = flush_grow(a, st, true))) return rc;
     if (csr_ulen) {                          // the other paths read the offsets on the device
       void *dst[1] = {a->t.offsets};
       const void *srcs[1] = {h_offsets};
@@ -425,7 +480,7 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
     if (commit) { host_commit(a); *committed = true; }
     return GG_OK;
   }
-  if ((rc = flush_grow(a))) return rc;
+  if ((rc = flush_grow(a, st, true))) return rc;
   if (csr_ulen) {
     void *dst[1] = {a->t.offsets};
     const void *srcs[1] = {h_offsets};
@@ -595,6 +650,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   if (!esz) return fail(GG_EVALUE, "unsupported dtype");
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(cudaFree(0));
+  reclaim(false);                          // chunks of arrays destroyed earlier -> the pool
   gg_array *a = new gg_array();
   a->dev = device; a->S = shards; a->fb = fb; a->log2fb = ilog2(fb); a->dtype = dtype;
   a->esz = esz; a->MB = max_buckets;
@@ -605,6 +661,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   for (uint32_t b = 0; b < max_buckets; ++b) bb[b] = bucket_bytes(a, b);
   int rc = a->slab.init(device, shards, max_buckets, bb, arena_va_bytes);
   if (rc) { a->slab.destroy(); delete a; return rc; }
+  const bool adopted = slab_adopt(a->slab);   // a same-shape slab left by a destroyed array
   // metadata block
   const size_t S = shards, T = S * max_buckets;
   size_t bytes = 0;
@@ -633,26 +690,63 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
   a->d_won = (int *)(base + o_won);
   a->d_scratch = base + o_scr;
+  // creation work is queued on the legacy default stream (no device-wide
+  // synchronize); the first call on another stream waits for it (order_stream)
+  a->last_st = 0;
+  a->have_last = true;
   if ((rc = a->up.init(device))) { gg_destroy(a); return rc; }
-  if (a->slab.small.base) {           // the packed small-class region exists from the start
+  if (a->slab.small.base || adopted) {  // the packed small-class region (and adopted regions) exist
     std::vector<uint64_t> cb(max_buckets);
     for (uint32_t b = 0; b < max_buckets; ++b) cb[b] = a->slab.class_base(b);
-    CUDA_TRY(cudaMemcpy(t.cbase, cb.data(), max_buckets * 8, cudaMemcpyHostToDevice));
+    void *dst[1] = {t.cbase};
+    const void *src[1] = {cb.data()};
+    size_t nb[1] = {max_buckets * sizeof(uint64_t)};
+    if ((rc = a->up.upload(0, 1, dst, src, nb))) { gg_destroy(a); return rc; }
   }
-  CUDA_TRY(cudaDeviceSynchronize());
   *out = a;
   return GG_OK;
 }
 
+// Stream-ordered teardown: the handle's memory (slab chunks, metadata, pinned
+// buffers) is freed once an event recorded behind its last call's stream
+// completes -- every earlier call's stream is ordered before that one
+// (order_stream) -- so destroying an array never waits for the whole device
+// and costs no driver call here; the chunks then go to the process pool.
+// Arrays that were ever captured into a CUDA graph fall back to a device
+// synchronize (a graph may still replay their kernels on any stream).
 int gg_destroy(gg_array *a) {
   if (!a) return GG_OK;
+  std::unique_lock<std::mutex> lk(a->mu);
   use_dev(a->dev);
-  cudaDeviceSynchronize();
-  a->up.destroy();
-  if (a->h_scratch) cudaFreeHost(a->h_scratch);
-  if (a->dmem) cudaFreeAsync(a->dmem, 0), cudaStreamSynchronize(0);
-  a->slab.destroy();
+  Grave *g = new Grave();
+  g->dev = a->dev;
+  if (a->captured || a->up.capturing) {
+    cudaDeviceSynchronize();
+  } else if (a->have_last) {
+    if (cudaEventCreateWithFlags(&g->ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(g->ev, a->last_st) != cudaSuccess) {
+      if (g->ev) cudaEventDestroy(g->ev);
+      g->ev = nullptr;
+      cudaDeviceSynchronize();            // the last stream is gone: wait for the device
+    }
+  }
+  a->slab.pending.clear();                // (access of chunks never used needs no grant)
+  a->slab.doomed.clear();
+  a->slab.doomed_bytes = 0;
+  g->slab = std::move(a->slab);
+  g->up = std::move(a->up);
+  g->dmem = a->dmem;
+  g->h_scratch = a->h_scratch;
+  g->ord_ev = a->ord_ev;
+  lk.unlock();
   delete a;
+  bury(g);
+  reclaim(false);                         // frees this one at once if its work is done
+  return GG_OK;
+}
+
+int gg_reclaim(int32_t wait) {
+  reclaim(wait != 0);
   return GG_OK;
 }
 
@@ -714,7 +808,7 @@ int uniform_append(gg_array *a, int wk, const char *src, uint64_t c, const uint6
   const int rmode = wk == W_DUP ? 1 : 0;
   const uint64_t total = c * a->S;
   Tables t = tables_for_launch(a, false);
-  if (fuse_ok(a, st) && (!a->pend_grow || a->pend_grow_st == st)) {
+  if (fuse_ok(a, st)) {
     Fuse fz{rmode, commit ? 1 : 0};
     fz.ulen = c;                               // uniform directory / CSR and destination start
     fz.ustart = start;
@@ -727,7 +821,7 @@ int uniform_append(gg_array *a, int wk, const char *src, uint64_t c, const uint6
     if (rc) return rc;
     flip_buffers(a);
   } else {
-    if ((rc = flush_grow(a))) return rc;
+    if ((rc = flush_grow(a, st, true))) return rc;
     if (wk == W_INSERT) {                      // the unfused walk reads the offsets on the device
       void *dst[1] = {a->t.offsets};
       const void *srcs[1] = {h_offsets};
@@ -755,13 +849,30 @@ int uniform_append(gg_array *a, int wk, const char *src, uint64_t c, const uint6
   return GG_OK;
 }
 
+int gg_insert_ex2(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, uint64_t *h_reserved,
+                  void *stream);
+
 int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, void *stream) {
+  return gg_insert_ex2(a, d_values, h_offsets, h_starts, flags, h_status, nullptr, stream);
+}
+
+int gg_insert_ex2(gg_array *a, const void *d_values, const uint64_t *h_offsets,
+                  const uint64_t *h_starts, uint32_t flags, int32_t *h_status, uint64_t *h_reserved,
+                  void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_meta(a); if (frc_) return frc_; }   // a deferred grow may ride on this walk
   cudaStream_t st = S_(stream);
+  {   // a deferred grow may ride on this walk
+    int frc_ = check_no_view(a);
+    if (!frc_) frc_ = order_stream(a, st);
+    if (!frc_) frc_ = flush_meta(a, st, true);
+    if (frc_) return frc_;
+  }
   if (h_offsets[0] != 0) return fail(GG_EVALUE, "offsets[0] must be 0");
+  if (h_reserved)       // each shard's reservation start, read under the handle's lock
+    for (uint32_t s = 0; s < a->S; ++s) h_reserved[s] = h_starts ? h_starts[s] : a->size[s];
   std::vector<uint64_t> counts(a->S);
   for (uint32_t s = 0; s < a->S; ++s) {
     if (h_offsets[s + 1] < h_offsets[s]) return fail(GG_EVALUE, "offsets must be non-decreasing");
@@ -819,8 +930,13 @@ int gg_insert_ex(gg_array *a, const void *d_values, const uint64_t *h_offsets,
 int gg_insert_duplicate_ex(gg_array *a, uint32_t flags, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_meta(a); if (frc_) return frc_; }   // a deferred grow may ride on this walk
   cudaStream_t st = S_(stream);
+  {   // a deferred grow may ride on this walk
+    int frc_ = check_no_view(a);
+    if (!frc_) frc_ = order_stream(a, st);
+    if (!frc_) frc_ = flush_meta(a, st, true);
+    if (frc_) return frc_;
+  }
   {
     // uniform fast path: every shard has the same committed length, size and
     // buckets, no hook / cap / failed shard -> plan shard 0 once
@@ -863,7 +979,7 @@ int gg_insert_duplicate(gg_array *a, int32_t *h_status, void *stream) {
 int gg_commit(gg_array *a, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   uint64_t acc = 0;
   a->prefix[0] = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
@@ -877,8 +993,9 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
   use_dev(a->dev);
   cudaStream_t st = S_(stream);
   if (h_failed_shard) *h_failed_shard = -1;
-  if ((a->pend && a->pend_st != st) || (a->pend_grow && a->pend_grow_st != st)) {
-    int frc_ = flush_pending(a);
+  {   // a deferred metadata pass / grow is fused below (on this, ordered, stream)
+    int frc_ = check_no_view(a);
+    if (!frc_) frc_ = order_stream(a, st);
     if (frc_) return frc_;
   }
   {
@@ -914,7 +1031,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
           a->pend_grow_st = st;
           return GG_OK;
         }
-        if ((rc = flush_grow(a))) return rc;
+        if ((rc = flush_grow(a, st, true))) return rc;
         Tables t = tables_for_launch(a, true);
         if (a->pend) {                         // metadata of the last append + this grow: one launch
           a->pend = false;
@@ -928,7 +1045,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
         if (got >> b & 1) a->slab.unback_range(b, 0, a->S);
     }
   }
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = flush_pending(a, st, true); if (frc_) return frc_; }
   Plan p;
   plan_init(a, p);
   std::vector<uint32_t> lim(a->S, 0);
@@ -986,7 +1103,7 @@ int gg_reserve(gg_array *a, const uint64_t *h_min_capacity, int64_t *h_failed_sh
 int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   *h_won = 0;
   if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
@@ -1018,13 +1135,32 @@ int gg_new_bucket(gg_array *a, uint32_t s, uint32_t b, int32_t *h_won, void *str
 int gg_fetch_add(gg_array *a, uint32_t s, uint64_t c, uint64_t *h_prev, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (s >= a->S) return fail(GG_EVALUE, "shard out of range");
   *h_prev = a->size[s];
   a->size[s] += c;
   a->ops[s] += 1;
   { k_fetch_add<<<1, 1, 0, S_(stream)>>>(a->t, s, c); g_launches.fetch_add(1, std::memory_order_relaxed); }
   CUDA_TRY(cudaGetLastError());
+  if (c) {
+    // indices reserved here may never be written (a reserver that fails
+    // between reserve and write) and then read back after commit: they must
+    // read 0 like the reference's np.zeros buckets, but slab memory is
+    // recycled.  Zero the reserved range where its buckets already exist,
+    // and mark the shard so buckets it allocates later are zeroed.
+    a->dirty[s] = 1;
+    const uint64_t lo = *h_prev, hi = lo + c;
+    uint32_t b0, b1; uint64_t o;
+    host_locate(a, lo, b0, o);
+    host_locate(a, hi - 1, b1, o);
+    for (uint32_t b = b0; b <= b1 && b < a->MB; ++b) {
+      if (!(a->flags[s] >> b & 1)) continue;
+      const uint64_t bs = ((uint64_t(1) << b) - 1) << a->log2fb, be = bs + bucket_elems(a, b);
+      const uint64_t x0 = std::max(lo, bs), x1 = std::min(hi, be);
+      char *p = (char *)a->slab.class_base(b) + (uint64_t)s * bucket_bytes(a, b) + (x0 - bs) * a->esz;
+      CUDA_TRY(cudaMemsetAsync(p, 0, (x1 - x0) * a->esz, S_(stream)));
+    }
+  }
   return GG_OK;
 }
 
@@ -1032,7 +1168,7 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
                  void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_new_sizes[s] > a->size[s]) return fail(GG_EVALUE, "shrink cannot grow a shard");
@@ -1093,15 +1229,16 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
   }
   uint64_t acc = 0;
   for (uint32_t s = 0; s < a->S; ++s) { acc += a->size[s]; a->prefix[s + 1] = acc; }
-  // unmap emptied chunks down to keep_mapped_bytes (waits for the device:
-  // queued work may still read the released buckets).  Never under graph
-  // capture, where the chunks stay cached until gg_trim.
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(st, &cap);
-  if (cap == cudaStreamCaptureStatusNone && a->slab.cached && a->slab.mapped > keep_mapped_bytes) {
-    CUDA_TRY(cudaDeviceSynchronize());
-    a->slab.trim_to(keep_mapped_bytes);
+  // unmap emptied chunks down to keep_mapped_bytes -- asynchronously: queued
+  // work may still read the released buckets, so they are unmapped once an
+  // event behind this shrink completed (Slab::doom_to / reap_doomed), not
+  // after a device-wide synchronize.  Never under graph capture, where the
+  // chunks stay cached until gg_trim.
+  if (!capturing_now(a, st) && a->slab.cached && a->slab.mapped - a->slab.doomed_bytes > keep_mapped_bytes) {
+    int rc = a->slab.doom_to(keep_mapped_bytes, st);
+    if (rc) return rc;
   }
+  a->slab.reap_doomed(false);               // earlier shrinks' chunks whose work is done
   return GG_OK;
 }
 
@@ -1112,10 +1249,20 @@ int gg_shrink(gg_array *a, const uint64_t *h_new_sizes, void *stream) {
 int gg_trim(gg_array *a) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = flush_pending(a); if (frc_) return frc_; }
   if (!a->slab.cached) return GG_OK;
-  CUDA_TRY(cudaDeviceSynchronize());
+  int rc = wait_last(a);
+  if (rc) return rc;
   a->slab.trim();
+  return GG_OK;
+}
+
+// unmap what earlier shrinks released, waiting for the work queued before
+// them (the footprint a caller reads next is then settled)
+int gg_settle(gg_array *a) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  a->slab.reap_doomed(true);
   return GG_OK;
 }
 
@@ -1124,7 +1271,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
                     int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   if (h_lane_offsets[0] != 0) return fail(GG_EVALUE, "lane offsets must start at 0");
   for (uint32_t s = 0; s < a->S; ++s)
@@ -1170,7 +1317,7 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
 int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   int rc = check_committed_published(a);
   if (rc) return rc;
   const uint64_t total = a->prefix[a->S];
@@ -1186,7 +1333,7 @@ int gg_rw_add(gg_array *a, const void *h_addend, uint32_t passes, int32_t mode, 
 int gg_flatten(gg_array *a, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   int rc = check_committed_published(a);
   if (rc) return rc;
   Tables t = tables_for_launch(a, false);
@@ -1196,7 +1343,7 @@ int gg_flatten(gg_array *a, void *d_out, void *stream) {
 int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (lo > hi || hi > a->prefix[a->S]) return fail(GG_EINDEX, "flatten range outside the committed size");
   if (lo == hi) return GG_OK;
   int rc = check_committed_published(a);
@@ -1214,7 +1361,7 @@ int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *s
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
   Tables t = tables_for_launch(a, false);
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
@@ -1231,7 +1378,7 @@ int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
   Tables t = tables_for_launch(a, false);
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
@@ -1265,7 +1412,7 @@ int elem_addr(gg_array *a, uint32_t s, uint64_t i, char **out, cudaStream_t st) 
 int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
@@ -1280,7 +1427,7 @@ int gg_get(gg_array *a, uint32_t s, uint64_t i, void *h_out, void *stream) {
 int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   char *p;
   int rc = elem_addr(a, s, i, &p, st);
@@ -1299,7 +1446,7 @@ int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, u
   use_dev(a->dev);
   { int frc_ = flush_pending(a); if (frc_) return frc_; }
   if (view_bytes != sizeof(gg_device_view)) return fail(GG_EVALUE, "view size mismatch (ggarray_device.cuh)");
-  if (!a->headroom.empty()) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
+  if (a->view_out) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
   // back every slot the launch may take: buckets [0, min_buckets_for(max)) per
   // shard, in shard then bucket order, while the live-bytes cap allows
   std::vector<unsigned long long> am(a->S);
@@ -1326,6 +1473,7 @@ int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, u
   gg_device_view v = a->t;
   v.ctl = nullptr;                          // amask gates the device allocator
   memcpy(h_view, &v, sizeof v);
+  a->view_out = true;                       // mutating calls refused until gg_device_view_sync
   return GG_OK;
 }
 
@@ -1333,9 +1481,10 @@ int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, u
 int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   CUDA_TRY(cudaStreamSynchronize(st));
+  a->view_out = false;
   const size_t S = a->S;
   std::vector<uint32_t> f(S * a->MB), status(S);
   std::vector<unsigned long long> misc(MISC_N);
@@ -1441,7 +1590,7 @@ int gg_flush(gg_array *a) {
 int gg_capture_end(gg_array *a, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  int rc = flush_pending(a);
+  int rc = enter(a, S_(stream));
   if (rc) return rc;
   if (a->cur != a->cap_parity) {     // an odd number of fused walks: copy back, restore the parity
     const int o = a->cur ^ 1;
@@ -1494,7 +1643,7 @@ int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint6
                     uint64_t *ops, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
   CUDA_TRY(cudaStreamSynchronize(st));
   const size_t S = a->S;
@@ -1518,7 +1667,7 @@ int gg_device_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint6
 int gg_prefix_copy(gg_array *a, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   CUDA_TRY(cudaMemcpyAsync(d_out, a->t.prefix, (a->S + 1) * 8, cudaMemcpyDeviceToDevice, S_(stream)));
   return GG_OK;
 }
@@ -1526,7 +1675,7 @@ int gg_prefix_copy(gg_array *a, void *d_out, void *stream) {
 int gg_bucket_ptrs(gg_array *a, uint64_t *h_ptrs, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   CUDA_TRY(cudaStreamSynchronize(S_(stream)));
   CUDA_TRY(cudaMemcpy(h_ptrs, a->t.ptr, (size_t)a->S * a->MB * 8, cudaMemcpyDeviceToHost));
   return GG_OK;
@@ -1537,21 +1686,37 @@ int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   uint64_t cap = 0, need = 0;
   for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
+  a->slab.reap_doomed(false);
   o[0] = cap * a->esz; o[1] = a->slab.mapped; o[2] = a->live; o[3] = need * a->esz;
-  o[4] = a->alloc_calls; o[5] = a->slab.cached;
+  o[4] = a->alloc_calls; o[5] = a->slab.cached; o[6] = a->slab.doomed_bytes;
   return GG_OK;
 }
 
 int gg_pool_stats(int device, uint64_t *o) {
+  if (device < 0 || device >= 64) return fail(GG_EVALUE, "bad device");
+  reclaim(false);
+  size_t nslabs = 0;
+  uint64_t slab_hits = 0;
+  {
+    SlabCache &C = slab_cache();
+    std::lock_guard<std::mutex> g(C.mu);
+    for (Slab *x : C.slabs) nslabs += x->dev == device;
+    slab_hits = C.hits;
+  }
   ChunkPool &p = chunk_pool();
   std::lock_guard<std::mutex> g(p.mu);
-  if (device < 0 || device >= 64) return fail(GG_EVALUE, "bad device");
-  o[0] = p.bytes[device]; o[1] = p.free[device].size(); o[2] = p.hits; o[3] = p.misses; o[4] = p.cap();
+  o[0] = p.bytes[device]; o[1] = p.free[device].size(); o[2] = p.hits; o[3] = p.misses; o[4] = p.cap(device);
+  o[7] = p.slab_bytes[device]; o[8] = nslabs; o[9] = slab_hits;
+  Reclaimer &R = reclaimer();
+  std::lock_guard<std::mutex> l(R.mu);
+  o[5] = R.graves.size(); o[6] = p.refused;
   return GG_OK;
 }
 
 int gg_pool_trim(int device) {
   if (device < 0 || device >= 64) return fail(GG_EVALUE, "bad device");
+  reclaim(true);
+  slab_cache_evict(device);
   chunk_pool().trim(device);
   return GG_OK;
 }
@@ -1561,6 +1726,7 @@ int gg_slab_stats(gg_array *a, uint64_t *o) {
   const Slab &sl = a->slab;
   o[0] = sl.mapped; o[1] = sl.cached; o[2] = sl.n_map; o[3] = sl.n_unmap;
   o[4] = sl.ns_map; o[5] = sl.ns_unmap; o[6] = sl.n_regions; o[7] = sl.va_used;
+  o[8] = sl.n_create; o[9] = sl.n_pool; o[10] = sl.doomed_bytes;
   return GG_OK;
 }
 
@@ -1571,10 +1737,22 @@ int gg_flat_insert(void *d_buf, uint64_t capacity, uint64_t *d_counter, const vo
   int dev = 0;
   cudaGetDevice(&dev);
   cudaStream_t st = S_(stream);
-  if (algo == GG_ALGO_BATCH) {
-    // contiguous append at the host-known counter value is done by the caller
-    // with gg_buf_copy; here: device-side single reservation + copy
-    return fail(GG_EVALUE, "BATCH algo is host-side (reserve + gg_buf_copy)");
+  if (algo == GG_ALGO_BATCH)
+    return fail(GG_EVALUE, "BATCH: one host-side reservation, then gg_flat_append");
+  if (algo == GG_ALGO_BLOCK) {
+    // vectorised block reservation: tile = 256 threads x 8 x 16 B (tools/sweep.py U)
+    const uint64_t tile = 256ull * 8 * (16 / esz);
+    const unsigned grid_b = (unsigned)std::max<uint64_t>(1, (n + tile - 1) / tile);
+    cudaError_t e;
+    switch (esz) {
+      case 1: e = launch_k(k_flat_insert_block<1, 8>, grid_b, 256, 0, st, (char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+      case 2: e = launch_k(k_flat_insert_block<2, 8>, grid_b, 256, 0, st, (char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+      case 4: e = launch_k(k_flat_insert_block<4, 8>, grid_b, 256, 0, st, (char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+      case 8: e = launch_k(k_flat_insert_block<8, 8>, grid_b, 256, 0, st, (char *)d_buf, capacity, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+      default: return fail(GG_EVALUE, "bad element size");
+    }
+    CUDA_TRY(e);
+    return GG_OK;
   }
   int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(dev) * 16);
   switch (esz) {
@@ -1585,6 +1763,25 @@ int gg_flat_insert(void *d_buf, uint64_t capacity, uint64_t *d_counter, const vo
     default: return fail(GG_EVALUE, "bad element size");
   }
   CUDA_TRY(cudaGetLastError());
+  return GG_OK;
+}
+
+int gg_flat_append(void *d_buf, uint64_t capacity, uint64_t *d_counter, uint64_t start,
+                   const void *d_vals, uint64_t n, uint32_t esz, void *stream) {
+  if (n == 0) return GG_OK;
+  if (start > capacity || n > capacity - start) return fail(GG_ECAPACITY, "batch exceeds the capacity");
+  cudaStream_t st = S_(stream);
+  const uint64_t tile = 256ull * 8 * (16 / (esz ? esz : 1));
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, (n + tile - 1) / tile);
+  cudaError_t e;
+  switch (esz) {
+    case 1: e = launch_k(k_flat_append<1, 8>, grid, 256, 0, st, (char *)d_buf, start, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+    case 2: e = launch_k(k_flat_append<2, 8>, grid, 256, 0, st, (char *)d_buf, start, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+    case 4: e = launch_k(k_flat_append<4, 8>, grid, 256, 0, st, (char *)d_buf, start, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+    case 8: e = launch_k(k_flat_append<8, 8>, grid, 256, 0, st, (char *)d_buf, start, (unsigned long long *)d_counter, (const char *)d_vals, n, tile); break;
+    default: return fail(GG_EVALUE, "bad element size");
+  }
+  CUDA_TRY(e);
   return GG_OK;
 }
 

@@ -14,6 +14,7 @@ import contextlib
 import ctypes as C
 import os
 import threading
+import weakref
 from bisect import bisect_right
 from typing import Callable, Sequence
 
@@ -45,6 +46,32 @@ def split_batches(values, shards: int) -> list:
 def split_offsets(n: int, shards: int) -> np.ndarray:
     chunk = -(-n // shards) if n else 0
     return np.minimum(np.arange(shards + 1, dtype=np.uint64) * np.uint64(chunk), np.uint64(n))
+
+
+class _ShardList:
+    """``GrowableArray.shards``: a read-only sequence of per-shard views."""
+
+    __slots__ = ("_arr",)
+
+    def __init__(self, arr):
+        self._arr = arr
+
+    def __len__(self) -> int:
+        return self._arr._S
+
+    def __getitem__(self, s):
+        if isinstance(s, slice):
+            return [self[i] for i in range(*s.indices(len(self)))]
+        s = int(s)
+        n = len(self)
+        if s < 0:
+            s += n
+        if not 0 <= s < n:
+            raise IndexError(f"shard {s} outside [0, {n})")
+        return ShardVector._bind(self._arr, s)
+
+    def __iter__(self):
+        return (ShardVector._bind(self._arr, s) for s in range(len(self)))
 
 
 def _torch_dtype(dt: np.dtype):
@@ -91,12 +118,16 @@ class GrowableArray:
         self._hook_fn = None
         self._allocator = allocator
         if allocator is not None:
+            me = weakref.ref(self)          # no array <-> hook cycle
+
             def hook(_ctx, shard, _bucket, elems):
                 try:
                     allocator(int(elems))
                     return 0
                 except BaseException as exc:  # noqa: BLE001 -- becomes the shard's failure
-                    self._hook_exc[int(shard)] = exc
+                    arr = me()
+                    if arr is not None:
+                        arr._hook_exc[int(shard)] = exc
                     return 1
             self._hook_fn = L.HOOK(hook)
             L.lib.gg_set_alloc_hook(self._h, self._hook_fn, None)
@@ -112,14 +143,32 @@ class GrowableArray:
         self._failed = C.c_int64(-1)
         self._failed_p = C.byref(self._failed)
         self._dev_index = self.device.index
-        self._mu = threading.Lock()
-        self.shards = [ShardVector._bind(self, s) for s in range(shards)]
+        # host-side state of concurrent callers (status buffers, hook
+        # exceptions, mirror cache) is guarded by _mu; the C handle has its own
+        self._mu = threading.RLock()
+        self._gen = 0                     # bumped by every mutation (mirror cache validity)
+        self._counters: dict = {}
+
+    @property
+    def shards(self) -> "_ShardList":
+        """Per-shard views (``shards[s]`` -> ShardVector); built on access, so
+        the array holds no reference to them (no cycle: a dropped array is
+        freed at once, never later by the cyclic collector)."""
+        return _ShardList(self)
+
+    def _counter(self, s: int):
+        c = self._counters.get(s)
+        if c is None:
+            from .bucket_vector import _SizeCounter
+            c = self._counters.setdefault(s, _SizeCounter(self, s))
+        return c
 
     # ------------------------------------------------------------ plumbing
     def _stream(self):
         return L.stream_handle(self._dev_index)
 
     def _dirty(self):
+        self._gen += 1
         self._cache = self._tot = None
         self._ptrs = None
 
@@ -127,10 +176,15 @@ class GrowableArray:
         # (committed, total size, total capacity) from the host mirrors; cached
         # until the next mutating call (every one goes through _dirty / resets
         # _cache), so per-round `committed_size` reads cost no ctypes call
-        if self._tot is None:
-            L.lib.gg_summary(self._h, L.ptr(self._summary))
-            self._tot = (int(self._summary[0]), int(self._summary[1]), int(self._summary[2]))
-        return self._tot
+        tot = self._tot
+        if tot is None:
+            gen = self._gen
+            o = np.zeros(3, np.uint64)
+            L.lib.gg_summary(self._h, L.ptr(o))
+            tot = (int(o[0]), int(o[1]), int(o[2]))
+            if gen == self._gen:          # no mutation raced with the read
+                self._tot = tot
+        return tot
 
     def flush(self) -> None:
         """Launch the deferred metadata pass of the last append now (normally it
@@ -167,15 +221,18 @@ class GrowableArray:
             L.lib.gg_capture_mode(self._h, 0)
 
     def _host(self) -> dict:
-        if self._cache is None:
+        st = self._cache
+        if st is None:
+            gen = self._gen
             S = self._S
             st = {k: np.zeros(S + (k == "prefix"), np.uint64)
                   for k in ("sizes", "caps", "flags", "prefix", "ops")}
             L.check(L.lib.gg_host_state(self._h, *(L.ptr(st[k]) for k in
                                                    ("sizes", "caps", "flags", "prefix", "ops"))),
                     "host_state")
-            self._cache = st
-        return self._cache
+            if gen == self._gen:          # a mutation in between would make this stale
+                self._cache = st
+        return st
 
     def _bucket_ptrs(self) -> np.ndarray:
         if self._ptrs is None:
@@ -219,23 +276,28 @@ class GrowableArray:
         return RuntimeError(f"shard {s}: status {code}")
 
     def _insert_device(self, vals, offsets: np.ndarray, starts: np.ndarray | None = None,
-                       commit: bool = False) -> dict:
-        """gg_insert_ex; returns {shard: exception} for failed shards.  With
-        ``commit`` the prefix is rebuilt in the same launch iff nothing failed."""
+                       commit: bool = False, want_starts: bool = False):
+        """gg_insert_ex2; returns {shard: exception} for failed shards (and, with
+        ``want_starts``, each shard's reservation start).  With ``commit`` the
+        prefix is rebuilt in the same launch iff nothing failed.  Status and
+        hook exceptions are per call (concurrent callers do not share them)."""
         offsets = L.u64_array(offsets)
-        status = self._status
-        self._hook_exc.clear()
+        status = np.zeros(self._S, np.int32)
         starts = None if starts is None else L.u64_array(starts)
         st = None if starts is None else L.ptr(starts)
+        res = np.zeros(self._S, np.uint64) if want_starts else None
         flags = (L.GG_F_COMMIT if commit else 0) | _EXTRA_FLAGS
-        rc = L.lib.gg_insert_ex(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
-                                L.ptr(offsets), st, flags, L.ptr(status, C.c_int32), self._stream())
-        self._dirty()
-        if rc not in (L.GG_OK, L.GG_EPARTIAL):
-            L.check(rc, "insert")
-        if rc == L.GG_OK:
-            return {}
-        return {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
+        with self._mu:
+            self._hook_exc = {}
+            rc = L.lib.gg_insert_ex2(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
+                                     L.ptr(offsets), st, flags, L.ptr(status, C.c_int32),
+                                     None if res is None else L.ptr(res), self._stream())
+            self._dirty()
+            if rc not in (L.GG_OK, L.GG_EPARTIAL):
+                L.check(rc, "insert")
+            failures = {} if rc == L.GG_OK else {
+                int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
+        return (failures, res) if want_starts else failures
 
     def _write_ranges(self, ranges: dict) -> None:
         """Write values at ranges reserved earlier through size_counter.fetch_add."""
@@ -285,15 +347,16 @@ class GrowableArray:
         else:
             caps = L.u64_array(caps)
             cp = L.ptr(caps)
-        failed = self._failed
-        failed.value = -1
-        if self._hook_exc:
-            self._hook_exc.clear()
-        rc = L.lib.gg_reserve(self._h, cp, self._failed_p, self._stream())
-        self._dirty()
-        if rc == L.GG_ENOMEM and failed.value in self._hook_exc:
-            raise self._hook_exc.pop(failed.value)
-        L.check(rc, "grow")
+        with self._mu:
+            failed = self._failed
+            failed.value = -1
+            if self._hook_exc:
+                self._hook_exc = {}
+            rc = L.lib.gg_reserve(self._h, cp, self._failed_p, self._stream())
+            self._dirty()
+            if rc == L.GG_ENOMEM and failed.value in self._hook_exc:
+                raise self._hook_exc.pop(failed.value)
+            L.check(rc, "grow")
 
     def _get(self, s: int, i: int):
         if i < 0:
@@ -494,16 +557,17 @@ class GrowableArray:
         if vals.numel() < cnt.numel() * values_per_lane:
             raise ValueError("values must hold values_per_lane slots per lane")
         status = np.zeros(self._S, np.int32)
-        self._hook_exc.clear()
-        rc = L.lib.gg_insert_lanes(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
-                                   C.c_void_p(cnt.data_ptr() if cnt.numel() else 0), L.ptr(lo),
-                                   int(values_per_lane), L.ptr(status, C.c_int32), self._stream())
-        self._dirty()
-        if rc not in (L.GG_OK, L.GG_EPARTIAL):
-            L.check(rc, "insert_lanes")
-        if rc == L.GG_EPARTIAL:
-            failures = {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
-            raise ShardInsertError(failures, [])
+        with self._mu:
+            self._hook_exc = {}
+            rc = L.lib.gg_insert_lanes(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
+                                       C.c_void_p(cnt.data_ptr() if cnt.numel() else 0), L.ptr(lo),
+                                       int(values_per_lane), L.ptr(status, C.c_int32), self._stream())
+            self._dirty()
+            if rc not in (L.GG_OK, L.GG_EPARTIAL):
+                L.check(rc, "insert_lanes")
+            if rc == L.GG_EPARTIAL:
+                failures = {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
+                raise ShardInsertError(failures, [])
         if commit:
             self.commit()
 
@@ -524,9 +588,10 @@ class GrowableArray:
     def device_sync(self) -> None:
         """Refresh the host mirrors after device-side appends; ShardInsertError on
         shards whose appends failed (reservations kept, as in the reference)."""
-        status = self._status
-        rc = L.lib.gg_device_view_sync(self._h, L.ptr(status, C.c_int32), self._stream())
-        self._dirty()
+        status = np.zeros(self._S, np.int32)
+        with self._mu:
+            rc = L.lib.gg_device_view_sync(self._h, L.ptr(status, C.c_int32), self._stream())
+            self._dirty()
         if rc == L.GG_EPARTIAL:
             failures = {int(s): MemoryError(f"shard {s}: no backed bucket slot for a device append")
                         for s in np.flatnonzero(status)}
@@ -543,12 +608,13 @@ class GrowableArray:
         p = p.to(device=self.device, dtype=torch.uint8).contiguous()
         if p.numel() != vals.numel():
             raise ValueError("values and pred differ in length")
-        status = self._status
-        rc = L.lib.gg_push_if(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
-                              C.c_void_p(p.data_ptr() if p.numel() else 0), vals.numel(),
-                              1 if mode == "block" else 0, int(grid), L.ptr(status, C.c_int32),
-                              self._stream())
-        self._dirty()
+        status = np.zeros(self._S, np.int32)
+        with self._mu:
+            rc = L.lib.gg_push_if(self._h, C.c_void_p(vals.data_ptr() if vals.numel() else 0),
+                                  C.c_void_p(p.data_ptr() if p.numel() else 0), vals.numel(),
+                                  1 if mode == "block" else 0, int(grid), L.ptr(status, C.c_int32),
+                                  self._stream())
+            self._dirty()
         if rc == L.GG_EPARTIAL:
             failures = {int(s): MemoryError(f"shard {s}: no backed bucket slot for a device append")
                         for s in np.flatnonzero(status)}
@@ -560,16 +626,18 @@ class GrowableArray:
     def insert_duplicate(self, commit: bool = True) -> None:
         """Every shard appends a copy of its committed contents, read directly from
         its buckets (the bench's _insert_duplicate, bench_cli.py:298-307)."""
-        status = self._status
-        if self._hook_exc:
-            self._hook_exc.clear()
         flags = (L.GG_F_COMMIT if commit else 0) | _EXTRA_FLAGS
-        rc = L.lib.gg_insert_duplicate_ex(self._h, flags, self._status_p, self._stream())
-        self._dirty()
-        if rc not in (L.GG_OK, L.GG_EPARTIAL):
-            L.check(rc, "insert_duplicate")
+        with self._mu:
+            status = self._status
+            if self._hook_exc:
+                self._hook_exc = {}
+            rc = L.lib.gg_insert_duplicate_ex(self._h, flags, self._status_p, self._stream())
+            self._dirty()
+            if rc not in (L.GG_OK, L.GG_EPARTIAL):
+                L.check(rc, "insert_duplicate")
+            if rc == L.GG_EPARTIAL:
+                failures = {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
         if rc == L.GG_EPARTIAL:
-            failures = {int(s): self._failure(int(s), int(status[s])) for s in np.flatnonzero(status)}
             cl = np.diff(self._host()["prefix"].astype(np.int64))
             raise ShardInsertError(failures, [s for s in range(self._S) if cl[s] and s not in failures])
 
@@ -683,21 +751,30 @@ class GrowableArray:
         return arr
 
     # ------------------------------------------------------------ stats / parity
-    def memory_stats(self) -> dict:
-        o = np.zeros(6, np.uint64)
+    def memory_stats(self, settle: bool = True) -> dict:
+        """Footprint: capacity (the reference's), mapped (physical slab chunks),
+        needed bytes.  A shrink unmaps released chunks asynchronously (after
+        the work queued before it); ``settle`` waits for that first, so
+        ``mapped_bytes`` is the settled footprint (else they are counted in
+        ``mapped_bytes`` and reported as ``pending_unmap_bytes``)."""
+        if settle:
+            L.check(L.lib.gg_settle(self._h), "settle")
+        o = np.zeros(7, np.uint64)
         L.check(L.lib.gg_mem_stats(self._h, L.ptr(o), self._stream()), "mem_stats")
-        cap, mapped, live, need, allocs, cached = (int(x) for x in o)
+        cap, mapped, live, need, allocs, cached, pend = (int(x) for x in o)
         return {"capacity_bytes": cap, "mapped_bytes": mapped, "bucket_bytes": live,
                 "needed_bytes": need, "alloc_calls": allocs, "cached_bytes": cached,
+                "pending_unmap_bytes": pend,
                 "capacity_over_needed": cap / need if need else None,
                 "mapped_over_needed": mapped / need if need else None}
 
     def slab_stats(self) -> dict:
         """Cost of the slab's physical mapping (cumulative counters)."""
-        o = np.zeros(8, np.uint64)
+        o = np.zeros(11, np.uint64)
         L.check(L.lib.gg_slab_stats(self._h, L.ptr(o)), "slab_stats")
         keys = ("mapped_bytes", "cached_bytes", "chunks_mapped", "chunks_unmapped", "map_ns",
-                "unmap_ns", "regions", "va_bytes")
+                "unmap_ns", "regions", "va_bytes", "handles_created", "handles_from_pool",
+                "pending_unmap_bytes")
         return {k: int(v) for k, v in zip(keys, o)}
 
     def prefix_device(self, out=None):
@@ -752,14 +829,23 @@ class GrowableArray:
 
 
 def pool_stats(device: int = 0) -> dict:
-    """The process-wide cache of physical slab chunks left by destroyed arrays
-    (reused by new arrays instead of fresh driver allocations)."""
-    o = np.zeros(5, np.uint64)
+    """The process-wide cache of physical slab chunks (chunks of destroyed
+    arrays and chunks shrinks unmapped), reused by any array before the
+    driver is asked for new memory."""
+    o = np.zeros(10, np.uint64)
     L.check(L.lib.gg_pool_stats(int(device), L.ptr(o)), "pool_stats")
     return {"cached_bytes": int(o[0]), "chunks": int(o[1]), "hits": int(o[2]), "misses": int(o[3]),
-            "cap_bytes": int(o[4])}
+            "cap_bytes": int(o[4]), "graves": int(o[5]), "refused": int(o[6]),
+            "slab_cache_bytes": int(o[7]), "slabs_cached": int(o[8]), "slab_cache_hits": int(o[9])}
 
 
 def pool_trim(device: int = 0) -> None:
-    """Return every cached chunk to the driver."""
+    """Wait for destroyed arrays' queued work, then return every cached chunk
+    to the driver."""
     L.check(L.lib.gg_pool_trim(int(device)), "pool_trim")
+
+
+def reclaim(wait: bool = True) -> None:
+    """Free what destroyed arrays left behind (their chunks go to the pool);
+    destroy itself only records an event behind the array's last work."""
+    L.check(L.lib.gg_reclaim(1 if wait else 0), "reclaim")

@@ -279,10 +279,39 @@ def test_captured_schedule_replays_match_eager(gg, defer, rounds):
     assert torch.equal(a.flatten_device(), exp)
 
 
+def test_dropped_arrays_free_at_once(gg):
+    """No reference cycle keeps a GrowableArray alive: dropping it (gc off)
+    destroys the handle immediately -- shards views, size counters, the
+    allocator hook and device views included -- and its memory is reclaimed
+    stream-ordered, without a cyclic-GC pass landing in someone's timed loop."""
+    import gc
+    import weakref
+    import torch
+    gc.collect()
+    gc.disable()
+    try:
+        gg.pool_trim(0)
+        vals = torch.arange(1 << 16, dtype=torch.int32, device="cuda")
+        for i in range(4):
+            a = gg.GrowableArray.from_flat(vals, 64, 32, allocator=lambda n: None)
+            _ = [sh.size_counter for sh in a.shards]             # counters cached in the array
+            _ = a.shards[3].table.allocated_flags
+            a.rw_add(1)
+            r = weakref.ref(a)
+            del a, _
+            assert r() is None, "GrowableArray kept alive by a reference cycle"
+            gg.reclaim(True)
+            st = gg.pool_stats(0)
+            assert st["graves"] == 0 and st["slabs_cached"] == 1, st
+    finally:
+        gc.enable()
+        gg.pool_trim(0)
+
+
 def test_chunk_pool_reuse_and_trim(gg):
-    """Destroyed arrays leave their physical chunks in the process pool; the
-    next array maps them (hits), contents are fresh writes; trim empties it.
-    Shrink releases never feed the pool."""
+    """Shrink releases go to the process pool (asynchronously), growth maps
+    pooled handles, destroyed arrays leave their whole slab for a same-shape
+    successor, trim empties everything."""
     import gc
     import torch
     gc.collect()                       # earlier tests' arrays die now, not mid-test
@@ -294,23 +323,45 @@ def test_chunk_pool_reuse_and_trim(gg):
 
 
 def _chunk_pool_body(gg, torch):
+    """Physical-memory lifecycle: a shrink unmaps released extents
+    asynchronously into the process pool; the next growth maps pooled
+    handles (no cuMemCreate); a destroyed array's slab is kept whole and a
+    same-shape array adopts it with no driver call at all."""
     gg.pool_trim(0)
     s0 = gg.pool_stats(0)
-    a = gg.GrowableArray.from_flat(torch.arange(1 << 20, dtype=torch.int32, device="cuda"), 64, 32)
+    assert s0["cached_bytes"] == 0 and s0["slab_cache_bytes"] == 0 and s0["cap_bytes"] > 0
+    vals = torch.arange(1 << 20, dtype=torch.int32, device="cuda")
+    offs = np.minimum(np.arange(65, dtype=np.uint64) * np.uint64((1 << 20) // 64), 1 << 20)
+    a = gg.GrowableArray.from_flat(vals, 64, 32)
+    mapped0 = a.memory_stats()["mapped_bytes"]
+    created0 = a.slab_stats()["handles_created"]
+    assert mapped0 > 0 and created0 > 0
     a.shrink(0, release=True)
-    assert gg.pool_stats(0)["cached_bytes"] == 0            # shrink release -> driver, not pool
-    a.insert_csr(torch.arange(1 << 20, dtype=torch.int32, device="cuda"),
-                 np.minimum(np.arange(65, dtype=np.uint64) * np.uint64((1 << 20) // 64), 1 << 20))
-    mapped = a.memory_stats()["mapped_bytes"]
+    ms = a.memory_stats()                                    # settles the asynchronous unmap
+    assert ms["mapped_bytes"] == 0 and ms["pending_unmap_bytes"] == 0
+    assert gg.pool_stats(0)["cached_bytes"] == mapped0       # released handles -> the pool
+    a.insert_csr(vals, offs)
+    st = a.slab_stats()
+    assert st["handles_created"] == created0 and st["handles_from_pool"] > 0
+    assert a.memory_stats()["mapped_bytes"] == mapped0
     a.close()
-    st = gg.pool_stats(0)
-    assert 0 < st["cached_bytes"] <= mapped
-    b = gg.GrowableArray.from_flat(torch.arange(1 << 20, dtype=torch.int32, device="cuda") * 3, 64, 32)
-    assert gg.pool_stats(0)["hits"] > st["hits"]
-    assert torch.equal(b.flatten_device(), torch.arange(1 << 20, dtype=torch.int32, device="cuda") * 3)
+    gg.reclaim(True)
+    p1 = gg.pool_stats(0)
+    assert p1["slab_cache_bytes"] == mapped0 and p1["slabs_cached"] == 1
+    b = gg.GrowableArray.from_flat(vals * 3, 64, 32)          # same shape: adopts the slab
+    sb = b.slab_stats()
+    assert gg.pool_stats(0)["slab_cache_hits"] == p1["slab_cache_hits"] + 1
+    assert sb["handles_created"] == 0 and sb["handles_from_pool"] == 0 and sb["chunks_mapped"] == 0
+    assert torch.equal(b.flatten_device(), vals * 3)
+    assert b.memory_stats()["mapped_bytes"] == mapped0
+    c = gg.GrowableArray.from_flat(vals, 32, 32)              # another shape: no adoption
+    assert c.slab_stats()["handles_created"] + c.slab_stats()["handles_from_pool"] > 0
+    assert torch.equal(c.flatten_device(), vals)
     b.close()
+    c.close()
     gg.pool_trim(0)
-    assert gg.pool_stats(0)["cached_bytes"] == 0 and s0["cap_bytes"] > 0
+    p2 = gg.pool_stats(0)
+    assert p2["cached_bytes"] == 0 and p2["slab_cache_bytes"] == 0 and p2["graves"] == 0
 
 
 @pytest.mark.parametrize("S", [1025, 5000, 70000])
