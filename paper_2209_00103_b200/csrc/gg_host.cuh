@@ -202,6 +202,7 @@ struct Slab {
   uint64_t n_map = 0, n_unmap = 0, ns_map = 0, ns_unmap = 0, n_regions = 0;  // cost counters
   uint64_t n_create = 0, n_pool = 0;   // handles from the driver / from the process pool
   uint64_t adopted = 0;                // bytes mapped when this slab was adopted (slab cache)
+  bool adopt_guard = false;            // adopted chunks not yet settled against the footprint bound
   static uint64_t now_ns() {
     return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
         std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -566,6 +567,7 @@ struct Slab {
     for (auto &r : big) go(r);
     cached = mapped;
     adopted = mapped;
+    adopt_guard = mapped > 0;
     n_map = n_unmap = ns_map = ns_unmap = n_create = n_pool = 0;
   }
   // shape key of the slab cache: same S, classes, bucket bytes and budget

@@ -366,10 +366,28 @@ int order_stream(gg_array *a, cudaStream_t st) {
   return GG_OK;
 }
 
+// An array that adopted a cached slab (slab_adopt) starts with every chunk
+// of the destroyed array mapped.  Once its first allocating operation has
+// taken the chunks it needs (live > 0), the adopted chunks still without a
+// live bucket are doomed down to 2x the needed bytes -- unmapped
+// asynchronously behind an event, or taken back in place for free if a later
+// operation needs them before the reap -- so the adopted cache never leaves
+// the array above the footprint bound (the paper's <= 2x).
+int settle_adopted(gg_array *a, cudaStream_t st) {
+  if (!a->slab.adopt_guard || !a->live || capturing_now(a, st)) return GG_OK;
+  a->slab.adopt_guard = false;
+  uint64_t need = 0;
+  for (uint32_t s = 0; s < a->S; ++s) need += a->size[s];
+  const uint64_t keep = 2 * need * a->esz;
+  if (a->slab.cached && a->slab.mapped - a->slab.doomed_bytes > keep) return a->slab.doom_to(keep, st);
+  return GG_OK;
+}
+
 // entry of a device-touching call on stream st: order, then launch whatever
 // was deferred (on st)
 int enter(gg_array *a, cudaStream_t st) {
   int rc = order_stream(a, st);
+  if (!rc) rc = settle_adopted(a, st);
   return rc ? rc : flush_pending(a, st, true);
 }
 
@@ -1262,6 +1280,7 @@ int gg_trim(gg_array *a) {
 int gg_settle(gg_array *a) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int rc = settle_adopted(a, a->have_last ? a->last_st : nullptr); if (rc) return rc; }
   a->slab.reap_doomed(true);
   return GG_OK;
 }
@@ -1686,6 +1705,8 @@ int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   uint64_t cap = 0, need = 0;
   for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
+  use_dev(a->dev);
+  { int rc = settle_adopted(a, a->have_last ? a->last_st : nullptr); if (rc) return rc; }
   a->slab.reap_doomed(false);
   o[0] = cap * a->esz; o[1] = a->slab.mapped; o[2] = a->live; o[3] = need * a->esz;
   o[4] = a->alloc_calls; o[5] = a->slab.cached; o[6] = a->slab.doomed_bytes;
