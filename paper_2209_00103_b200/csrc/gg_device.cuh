@@ -257,12 +257,12 @@ __device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t *t
 
 // Paper Alg. 1 with per-lane counts, pass 1: CTA per shard sums its lanes'
 // counts (so the host can map the arena exactly before pass 2).
-__global__ void __launch_bounds__(1024) k_lanes_count(Tables t, const uint32_t *counts) {
+__global__ void __launch_bounds__(1024) k_lanes_count(Tables t, const uint32_t *counts, uint32_t K) {
   __shared__ uint64_t ws[32];
   const uint32_t s = blockIdx.x;
   const uint64_t lo = t.offsets[s], hi = t.offsets[s + 1];
   uint64_t acc = 0;
-  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) acc += counts[j];
+  for (uint64_t j = lo + threadIdx.x; j < hi; j += blockDim.x) acc += min(counts[j], K);   // clamped to K
   uint64_t tot;
   block_exclusive_scan(acc, &tot, ws);
   if (threadIdx.x == 0) t.count[s] = tot;
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(1024) k_lanes_insert(Tables t, const char *val
   uint64_t carry = 0;
   for (uint64_t base = lo; base < hi; base += blockDim.x) {
     const uint64_t j = base + tid;
-    const uint32_t cnt = j < hi ? counts[j] : 0;
+    const uint32_t cnt = j < hi ? min(counts[j], K) : 0;
     uint64_t tot;
     const uint64_t ex = block_exclusive_scan(cnt, &tot, ws);
     const E *src = (const E *)vals + j * K;
@@ -469,9 +469,21 @@ template <> struct LdSt<3> {
 constexpr int kDefLS = 0;
 constexpr int kDefUnroll = 4;
 
+// bytes [4q + r/8, 4q + r/8 + 16) of the 32-byte concatenation (a, b): the
+// 16 B vector starting m = 4q + r/8 bytes into a (q < 4, r in {0, 8, 16, 24})
+__device__ __forceinline__ uint4 realign16(const uint4 &a, const uint4 &b, uint32_t q, uint32_t r) {
+  const uint32_t w0 = q == 0 ? a.x : q == 1 ? a.y : q == 2 ? a.z : a.w;
+  const uint32_t w1 = q == 0 ? a.y : q == 1 ? a.z : q == 2 ? a.w : b.x;
+  const uint32_t w2 = q == 0 ? a.z : q == 1 ? a.w : q == 2 ? b.x : b.y;
+  const uint32_t w3 = q == 0 ? a.w : q == 1 ? b.x : q == 2 ? b.y : b.z;
+  const uint32_t w4 = q == 0 ? b.x : q == 1 ? b.y : q == 2 ? b.z : b.w;
+  return make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r), __funnelshift_r(w2, w3, r),
+                    __funnelshift_r(w3, w4, r));
+}
+
 // dst[0..n) = src[0..n) (element granular, arbitrary relative alignment), or
 // zeros if src == nullptr.  Stores are 16 B aligned vectors; loads are 16 B
-// vectors when src shares dst's alignment, else element loads.
+// vectors, realigned in registers when src and dst are not congruent.
 template <int ESZ, int UNROLL, int LS = kDefLS>
 __device__ __forceinline__ void cta_copy(char *dst, const char *src, uint64_t n, uint32_t tid,
                                          uint32_t nt) {
@@ -508,18 +520,35 @@ __device__ __forceinline__ void cta_copy(char *dst, const char *src, uint64_t n,
         if (v0 + u * (uint64_t)nt < body) M::st(dv + v0 + u * nt, r[u]);
     }
   } else {
-    const E *s2 = (const E *)sb;
-    for (uint64_t v0 = tid; v0 < body; v0 += UNROLL * (uint64_t)nt) {
-      union { uint4 q; E e[VE]; } u[UNROLL];
+    // source not congruent with the destination: aligned 16 B loads of the
+    // source; output vector v is assembled from aligned vectors v and v + 1
+    // shifted by the byte misalignment.  Each warp loads a window of 32
+    // consecutive aligned vectors and writes the 31 outputs it fully holds
+    // (lane l takes lane l + 1's vector by shuffle), so no lane loads twice
+    // and registers stay at U vectors.  Loop bounds are warp-uniform
+    // (shuffles); loads are clamped to vector `body` of the aligned source --
+    // an aligned 16 B vector holding at least one source byte, so it never
+    // leaves a mapped page.
+    const uint32_t m = (uint32_t)((uintptr_t)sb & 15), q = m >> 2, r = (m & 3) * 8;
+    const uint4 *sa = (const uint4 *)(sb - m);
+    // (at most 4 vectors in flight: the kernels' register budget is set by
+    // their congruent paths)
+    constexpr int UR = UNROLL > 4 ? 4 : UNROLL;
+    const uint32_t lane = tid & 31, nw = nt >> 5;
+    for (uint64_t w0 = tid >> 5; 31 * w0 < body; w0 += UR * (uint64_t)nw) {
+      uint4 a[UR];
 #pragma unroll
-      for (int k = 0; k < UNROLL; ++k) {
-        const uint64_t v = min(v0 + k * (uint64_t)nt, body - 1);
+      for (int k = 0; k < UR; ++k) a[k] = M::ld(sa + min(31 * (w0 + k * (uint64_t)nw) + lane, body));
 #pragma unroll
-        for (uint32_t j = 0; j < VE; ++j) u[k].e[j] = M::ld(s2 + v * VE + j);
+      for (int k = 0; k < UR; ++k) {
+        uint4 h;
+        h.x = __shfl_down_sync(0xffffffffu, a[k].x, 1);
+        h.y = __shfl_down_sync(0xffffffffu, a[k].y, 1);
+        h.z = __shfl_down_sync(0xffffffffu, a[k].z, 1);
+        h.w = __shfl_down_sync(0xffffffffu, a[k].w, 1);
+        const uint64_t v = 31 * (w0 + k * (uint64_t)nw) + lane;
+        if (lane < 31 && v < body) M::st(dv + v, realign16(a[k], h, q, r));
       }
-#pragma unroll
-      for (int k = 0; k < UNROLL; ++k)
-        if (v0 + k * (uint64_t)nt < body) M::st(dv + v0 + k * nt, u[k].q);
     }
   }
 }
@@ -1197,6 +1226,239 @@ __global__ void k_zero_buckets(Tables t, const uint32_t *pairs, uint32_t npairs)
 // publishes it on the device counter.  The copy is the walker's tile shape:
 // one tile of 256 threads x U 16 B vectors per CTA, all U loads issued
 // before the stores (cta_copy handles any relative alignment).
+// ---- paper Alg. 1 at throughput: the tiled lanes insert --------------------
+// The lanes of shard s ([offsets[s], offsets[s+1])) are cut into tiles of T
+// consecutive lanes that never cross a shard; tpre[s] = first tile of shard
+// s (tpre[S] = number of tiles).  Three launches, no host round trip (the
+// host backed the slots for the upper bound lanes x values_per_lane):
+//   k_lanes_sum:     a warp per tile sums its lanes' counts (coalesced) and
+//                    records the tile (shard, first lane, lanes, sum);
+//   k_lanes_reserve: a CTA per shard scans its tile sums (tile order = lane
+//                    order), reserves the whole batch with ONE atomicAdd on
+//                    the LFVector size (insert_index.py:118-143), publishes
+//                    the buckets the range covers (paper Alg. 2) and turns
+//                    the sums into absolute destination indices;
+//   k_lanes_scatter: a CTA per tile loads its [T x K] block of values with
+//                    coalesced 16 B loads and its counts, block-scans the
+//                    counts, compacts the valid values into shared memory
+//                    (lane order) and stores them as aligned 16 B vectors
+//                    through the bucket slots.
+struct LaneTile {
+  uint64_t base;      // sum of the tile's counts -> absolute destination index
+  uint64_t lane_lo;   // first lane of the tile
+  uint32_t shard, nl; // shard, lanes in the tile
+  uint32_t pad[2];
+};
+
+// largest s with tpre[s] <= x (tiles of empty shards skipped), 32-ary warp
+// search; called by a full warp, result in every lane
+__device__ __forceinline__ uint32_t warp_find_u32(const uint32_t *tpre, uint32_t S, uint32_t x) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t lo = 0, hi = S;
+  while (hi - lo > 1) {
+    const uint32_t step = (hi - lo + 31) >> 5;
+    const uint32_t p = lo + lane * step;
+    const bool ok = p < hi && tpre[p] <= x;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    lo = lo + (31u - __clz(m)) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_lanes_sum(Tables t, const uint32_t *counts, const uint32_t *tpre,
+                                                   LaneTile *tiles, uint32_t ntiles, uint32_t T, uint32_t K) {
+  pdl_begin();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (tile >= ntiles) return;
+  const uint32_t s = warp_find_u32(tpre, t.S, tile);
+  const uint64_t lo = t.offsets[s] + (uint64_t)(tile - tpre[s]) * T;
+  const uint32_t nl = (uint32_t)min((uint64_t)T, t.offsets[s + 1] - lo);
+  uint32_t acc = 0;
+#pragma unroll 8
+  for (uint32_t j = lane; j < nl; j += 32) acc += min(__ldcs(counts + lo + j), K);
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if (lane == 0) {
+    LaneTile lt;
+    lt.base = acc; lt.lane_lo = lo; lt.shard = s; lt.nl = nl; lt.pad[0] = lt.pad[1] = 0;
+    tiles[tile] = lt;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_lanes_reserve(Tables t, const uint32_t *tpre, LaneTile *tiles) {
+  __shared__ uint64_t ws[32];
+  __shared__ uint64_t start_sh;
+  pdl_begin();
+  const uint32_t s = blockIdx.x, tid = threadIdx.x;
+  const uint32_t first = tpre[s], nts = tpre[s + 1] - first;
+  if (!nts) return;
+  uint64_t carry = 0;
+  for (uint32_t j0 = 0; j0 < nts; j0 += blockDim.x) {
+    const uint32_t j = j0 + tid;
+    const uint64_t v = j < nts ? tiles[first + j].base : 0;
+    uint64_t ct;
+    const uint64_t ex = block_exclusive_scan(v, &ct, ws);
+    if (j < nts) tiles[first + j].base = carry + ex;
+    carry += ct;
+  }
+  if (tid == 0) {
+    uint64_t start = t.size[s];
+    if (carry) {
+      // the batch's reservation: ONE atomicAdd on the LFVector size
+      start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)carry);
+      t.ops[s] += 1;
+      uint32_t b0, b1; uint64_t o;
+      locate(start, t.log2fb, b0, o);
+      locate(start + carry - 1, t.log2fb, b1, o);
+      const unsigned long long pm = t.pmask[s];
+      const unsigned long long want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~pm;
+      uint64_t add = 0;
+      const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+      for (unsigned long long mm = want; mm; mm &= mm - 1) {
+        const uint32_t b = __ffsll((long long)mm) - 1;
+        t.ptr[(size_t)s * t.MB + b] = t.cbase[b] + ((uint64_t)s << max(lg0 + b, 4u));
+        t.flag[(size_t)s * t.MB + b] = kFlagPublished;
+        add += 1ull << (t.log2fb + b);
+      }
+      if (want) {
+        t.pmask[s] = pm | want;
+        t.cap[s] += add;
+        atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)__popcll(want));
+      }
+    }
+    t.start[s] = start;
+    t.count[s] = carry;
+    start_sh = start;
+  }
+  __syncthreads();
+  const uint64_t start = start_sh;
+  for (uint32_t j = tid; j < nts; j += blockDim.x) tiles[first + j].base += start;
+}
+
+// lane j's KB bytes of values (KB = K * ESZ, a power of two in [4, 64]) into
+// words w[r * KB / 4 ...] of the thread's register block
+template <int KB>
+__device__ __forceinline__ void lane_load(uint32_t *w, const char *p) {
+  if constexpr (KB >= 16) {
+#pragma unroll
+    for (int i = 0; i < KB / 16; ++i) {
+      const uint4 v = ldg_stream((const uint4 *)p + i);
+      w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+    }
+  } else if constexpr (KB == 8) {
+    const uint2 v = __ldcs((const uint2 *)p);
+    w[0] = v.x; w[1] = v.y;
+  } else {
+    w[0] = __ldcs((const uint32_t *)p);
+  }
+}
+
+// k_lanes_scatter: lane per thread.  A tile is 8 warps x R rows of 32 lanes
+// (R = 64 / KB, so every thread holds 64 B of values in registers); each
+// thread loads its lanes' counts and values (coalesced: consecutive lanes
+// are consecutive in memory).  Warp-scans of the counts (several rows packed
+// into one 32-bit scan, 8- or 16-bit fields) give every lane's offset in the
+// warp's run; the whole run is staged in the warp's shared buffer congruent
+// with its destination and leaves as aligned 16 B vector stores.  One
+// __syncthreads per tile (the warps' totals).
+template <int ESZ, int KB>
+__global__ void __launch_bounds__(256) k_lanes_scatter(Tables t, const char *vals, const uint32_t *counts,
+                                                       const LaneTile *tiles) {
+  typedef typename ElemT<ESZ>::T E;
+  constexpr uint32_t K = KB / ESZ, R = 64 / KB, VE = 16 / ESZ;
+  constexpr uint32_t FW = (32 * K < 256) ? 8 : 16, PF = 32 / FW, FM = (1u << FW) - 1;
+  __shared__ __align__(16) E stage_sm[8][32 * R * K + 2 * VE];
+  __shared__ uint32_t wsum[8];
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const LaneTile lt = tiles[blockIdx.x];
+  const uint32_t s = lt.shard, nl = lt.nl;
+  const uint64_t lo = lt.lane_lo;
+  const uint32_t wl0 = wid * R * 32;
+  uint32_t c[R];
+  uint32_t w[16];
+#pragma unroll
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint32_t j = wl0 + r * 32 + lane;
+    c[r] = 0;
+    if (j < nl) {
+      c[r] = min(__ldcs(counts + lo + j), K);
+      lane_load<KB>(w + r * (KB / 4), vals + (lo + j) * KB);
+    }
+  }
+  stage_cbase(t, scb);
+  // lane offsets in the warp's run: packed row scans
+  uint32_t ex[R];
+  uint32_t carry = 0;
+#pragma unroll
+  for (uint32_t r0 = 0; r0 < R; r0 += PF) {
+    uint32_t x = 0;
+#pragma unroll
+    for (uint32_t f = 0; f < PF; ++f)
+      if (r0 + f < R) x |= c[r0 + f] << (f * FW);
+    const uint32_t v = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= (uint32_t)d) x += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+    const uint32_t xe = x - v;
+#pragma unroll
+    for (uint32_t f = 0; f < PF; ++f) {
+      if (r0 + f < R) {
+        ex[r0 + f] = carry + ((xe >> (f * FW)) & FM);
+        carry += (tot >> (f * FW)) & FM;
+      }
+    }
+  }
+  if (lane == 0) wsum[wid] = carry;
+  __syncthreads();
+  uint32_t woff = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < (int)wid) woff += wsum[q];
+  const uint32_t run = carry;
+  if (!run) return;
+  const uint64_t rb = lt.base + woff;           // destination index of the warp's run
+  E *st = stage_sm[wid];
+  const uint32_t lg0 = t.log2fb + (ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3);
+  const bool vec = (1u << lg0) >= 16;           // 16 B vectors never straddle a bucket
+  const uint32_t shift = vec ? (uint32_t)(rb % VE) : 0u;
+#pragma unroll
+  for (uint32_t r = 0; r < R; ++r) {
+    const E *ev = (const E *)(w + r * (KB / 4));
+#pragma unroll
+    for (uint32_t k = 0; k < K; ++k)
+      if (k < c[r]) st[shift + ex[r] + k] = ev[k];
+  }
+  __syncwarp();
+  if (vec) {
+    const uint32_t nv = (shift + run + VE - 1) / VE;
+    for (uint32_t v = lane; v < nv; v += 32) {
+      uint32_t b; uint64_t o;
+      locate(rb - shift + (uint64_t)v * VE, t.log2fb, b, o);
+      E *dp = (E *)(slot_addr(scb, s, b, lg0) + o * ESZ);
+      const uint32_t k0 = v * VE;
+      if (k0 >= shift && k0 + VE <= shift + run) {
+        stg((uint4 *)dp, ((const uint4 *)st)[v]);
+      } else {
+#pragma unroll
+        for (uint32_t j = 0; j < VE; ++j)
+          if (k0 + j >= shift && k0 + j < shift + run) dp[j] = st[k0 + j];
+      }
+    }
+  } else {
+    for (uint32_t k = lane; k < run; k += 32) {
+      uint32_t b; uint64_t o;
+      locate(rb + k, t.log2fb, b, o);
+      ((E *)(slot_addr(scb, s, b, lg0)))[o] = st[k];
+    }
+  }
+}
+
 template <int ESZ, int U>
 __global__ void __launch_bounds__(256) k_flat_append(char *buf, uint64_t start, unsigned long long *counter,
                                                      const char *vals, uint64_t n, uint64_t tile) {

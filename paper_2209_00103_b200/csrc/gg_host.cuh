@@ -898,11 +898,17 @@ struct Grave {
   Uploader up;
   void *dmem = nullptr;               // cudaMallocAsync'd metadata block
   char *h_scratch = nullptr;          // pinned
+  uint64_t *h_lanes = nullptr;        // pinned
+  void *lanes_dmem = nullptr;         // cudaMallocAsync'd lanes scratch
+  cudaEvent_t lanes_ev = nullptr;
   cudaEvent_t ord_ev = nullptr;
   void free_all() {
     if (!slab_offer(slab)) slab.destroy();   // kept whole for the next same-shape array
     up.destroy();
     if (h_scratch) cudaFreeHost(h_scratch);
+    if (h_lanes) cudaFreeHost(h_lanes);
+    if (lanes_dmem) cudaFreeAsync(lanes_dmem, 0);
+    if (lanes_ev) cudaEventDestroy(lanes_ev);
     if (dmem) cudaFreeAsync(dmem, 0);
     if (ord_ev) cudaEventDestroy(ord_ev);
     if (ev) cudaEventDestroy(ev);

@@ -65,6 +65,21 @@ struct gg_array {
   bool captured = false;                                 // ever issued under stream capture
   cudaEvent_t ord_ev = nullptr;
   bool view_out = false;                                 // gg_device_view_get without a sync yet
+  // A tiled lanes insert (paper Alg. 1) is planned on the upper bound lanes x
+  // values_per_lane; the sizes it reached come back through a pinned buffer
+  // behind an event and are applied by resolve_lanes (at the next call that
+  // reads the host mirrors), which also unbacks the headroom no bucket took.
+  bool lanes_pend = false;
+  cudaEvent_t lanes_ev = nullptr;
+  uint64_t *h_lanes = nullptr;                           // pinned [S]
+  std::vector<uint32_t> lanes_head;                      // (s, b) backed for the upper bound
+  uint64_t lanes_keep = 0;                               // mapped bytes before that backing
+  uint64_t view_keep = 0;                                // mapped bytes before a device view's headroom
+  // the last shrink asked to keep released chunks cached (release=False):
+  // headroom returned by lanes inserts / device views stays cached too
+  bool keep_cached = false;
+  void *lanes_dmem = nullptr;                            // arrive[S] | tpre[S+1] | tiles[]
+  size_t lanes_tiles_cap = 0;
   int *d_won = nullptr;
   char *d_scratch = nullptr;   // 64 B element scratch for get/set
   char *h_scratch = nullptr;   // pinned
@@ -332,8 +347,12 @@ int flush_grow(gg_array *a, cudaStream_t st = nullptr, bool on_st = false) {
   return GG_OK;
 }
 
+int resolve_lanes(gg_array *a);
+
 int flush_pending(gg_array *a, cudaStream_t st = nullptr, bool on_st = false) {
-  int rc = flush_meta(a, st, on_st);
+  int rc = resolve_lanes(a);
+  if (rc) return rc;
+  rc = flush_meta(a, st, on_st);
   return rc ? rc : flush_grow(a, st, on_st);
 }
 
@@ -535,6 +554,47 @@ int finish_status(gg_array *a, const Plan &p, int32_t *h_status) {
     for (uint32_t s = 0; s < a->S; ++s) h_status[s] = p.status[s];
   if (!p.any_fail) return GG_OK;
   return fail(GG_EPARTIAL, "insert failed on some shards; commit withheld");
+}
+
+// Apply a tiled lanes insert to the host mirrors once its sizes are back
+// (the pinned copy behind lanes_ev): sizes, ops, the published buckets of
+// every reserved range (a deterministic function of the old and new sizes),
+// capacity and live bytes; the upper-bound headroom no bucket took is
+// unbacked, and chunks the backing newly mapped beyond max(2 x needed, the
+// mapped bytes before it) are released asynchronously (doomed behind an
+// event, taken back in place if an operation needs them first).
+int resolve_lanes(gg_array *a) {
+  if (!a->lanes_pend) return GG_OK;
+  CUDA_TRY(cudaEventSynchronize(a->lanes_ev));
+  a->lanes_pend = false;
+  uint64_t need = 0;
+  for (uint32_t s = 0; s < a->S; ++s) {
+    const uint64_t ns = a->h_lanes[s], os = a->size[s];
+    if (ns > os) {
+      a->ops[s] += 1;
+      uint32_t b0, b1; uint64_t o;
+      host_locate(a, os, b0, o);
+      host_locate(a, ns - 1, b1, o);
+      for (uint32_t b = b0; b <= b1 && b < a->MB; ++b) {
+        if (a->flags[s] >> b & 1) continue;
+        a->flags[s] |= uint64_t(1) << b;
+        a->cap[s] += bucket_elems(a, b);
+        a->live += bucket_bytes(a, b);
+        a->alloc_calls += 1;
+      }
+      a->size[s] = ns;
+    }
+    need += a->size[s];
+  }
+  for (size_t i = 0; i < a->lanes_head.size(); i += 2) {
+    const uint32_t s = a->lanes_head[i], b = a->lanes_head[i + 1];
+    if (!(a->flags[s] >> b & 1)) a->slab.unback(s, b);
+  }
+  a->lanes_head.clear();
+  const uint64_t keep = std::max<uint64_t>(2 * need * a->esz, a->lanes_keep);
+  if (!a->keep_cached && a->slab.cached && a->slab.mapped - a->slab.doomed_bytes > keep && a->have_last)
+    return a->slab.doom_to(keep, a->last_st);
+  return GG_OK;
 }
 
 template <typename T>
@@ -755,6 +815,9 @@ int gg_destroy(gg_array *a) {
   g->up = std::move(a->up);
   g->dmem = a->dmem;
   g->h_scratch = a->h_scratch;
+  g->h_lanes = a->h_lanes;
+  g->lanes_dmem = a->lanes_dmem;
+  g->lanes_ev = a->lanes_ev;
   g->ord_ev = a->ord_ev;
   lk.unlock();
   delete a;
@@ -1187,6 +1250,7 @@ int gg_shrink_ex(gg_array *a, const uint64_t *h_new_sizes, uint64_t keep_mapped_
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
+  a->keep_cached = keep_mapped_bytes == ~uint64_t(0);
   cudaStream_t st = S_(stream);
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_new_sizes[s] > a->size[s]) return fail(GG_EVALUE, "shrink cannot grow a shard");
@@ -1268,6 +1332,7 @@ int gg_trim(gg_array *a) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   { int frc_ = check_no_view(a); if (!frc_) frc_ = flush_pending(a); if (frc_) return frc_; }
+  a->keep_cached = false;
   if (!a->slab.cached) return GG_OK;
   int rc = wait_last(a);
   if (rc) return rc;
@@ -1280,10 +1345,106 @@ int gg_trim(gg_array *a) {
 int gg_settle(gg_array *a) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
+  { int rc = resolve_lanes(a); if (rc) return rc; }
   { int rc = settle_adopted(a, a->have_last ? a->last_st : nullptr); if (rc) return rc; }
   a->slab.reap_doomed(true);
   return GG_OK;
 }
+
+namespace {
+constexpr int GG_ENOTSUP = -1;      // internal: take the exact path
+
+// The tiled lanes insert (paper Alg. 1 at throughput): the host backs every
+// shard's slots for the upper bound lanes x values_per_lane (no device round
+// trip), the device reserves (one atomicAdd per LFVector), publishes and
+// scatters; the reached sizes come back asynchronously (resolve_lanes).
+int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, const uint64_t *off,
+                uint64_t K, cudaStream_t st) {
+  static const bool on = [] { const char *e = getenv("GG_LANES_TILED"); return !e || e[0] != '0'; }();
+  const uint64_t KB = K * a->esz;
+  // register-resident lanes: KB a power of two in [4, 64], 16 B-aligned values
+  if (!on || a->hook || a->limit || KB < 4 || KB > 64 || (KB & (KB - 1)) ||
+      ((uintptr_t)d_values % std::min<uint64_t>(KB, 16)) || capturing_now(a, st))
+    return GG_ENOTSUP;
+  const uint32_t S = a->S;
+  for (uint32_t s = 0; s < S; ++s)
+    if (off[s + 1] > off[s] && a->dirty[s]) return GG_ENOTSUP;
+  // back the upper bound (all or nothing)
+  const uint64_t mapped0 = a->slab.mapped;
+  std::vector<uint32_t> head;
+  bool ok = true;
+  for (uint32_t s = 0; s < S && ok; ++s) {
+    const uint64_t U = (off[s + 1] - off[s]) * K;
+    if (!U) continue;
+    uint32_t b0, b1; uint64_t o;
+    host_locate(a, a->size[s], b0, o);
+    host_locate(a, a->size[s] + U - 1, b1, o);
+    if (b1 >= a->MB) { ok = false; break; }
+    for (uint32_t b = b0; b <= b1; ++b) {
+      if (a->flags[s] >> b & 1) continue;
+      if (back_bucket(a, s, b) != GG_OK) { ok = false; break; }
+      head.push_back(s);
+      head.push_back(b);
+    }
+  }
+  if (!ok) {
+    for (size_t i = 0; i < head.size(); i += 2) a->slab.unback(head[i], head[i + 1]);
+    return GG_ENOTSUP;
+  }
+  int rc = push_cbase(a, st);
+  if (rc) return rc;
+  // tiles: 8 warps x (64 / KB) rows of 32 lanes (64 B of values per thread)
+  const uint32_t T = (uint32_t)(256 * (64 / KB));
+  std::vector<uint32_t> tpre(S + 1);
+  uint64_t nt = 0;
+  for (uint32_t s = 0; s < S; ++s) {
+    tpre[s] = (uint32_t)nt;
+    nt += (off[s + 1] - off[s] + T - 1) / T;
+  }
+  if (nt > 0x7fffffffu) return fail(GG_EVALUE, "too many lanes");
+  tpre[S] = (uint32_t)nt;
+  // scratch: tpre[S+1] | tiles[nt] (grown on demand, stream ordered)
+  const size_t o_tiles = ((size_t)(S + 1) * 4 + 31) & ~size_t(31);
+  if (!a->lanes_dmem || a->lanes_tiles_cap < nt) {
+    if (a->lanes_dmem) CUDA_TRY(cudaFreeAsync(a->lanes_dmem, st));
+    const size_t cap = std::max<uint64_t>(nt, 1024);
+    CUDA_TRY(cudaMallocAsync(&a->lanes_dmem, o_tiles + cap * sizeof(LaneTile), st));
+    a->lanes_tiles_cap = cap;
+  }
+  char *dm = (char *)a->lanes_dmem;
+  uint32_t *d_tpre = (uint32_t *)dm;
+  LaneTile *d_tiles = (LaneTile *)(dm + o_tiles);
+  void *dst[2] = {a->t.offsets, d_tpre};
+  const void *src[2] = {off, tpre.data()};
+  size_t bytes[2] = {(size_t)(S + 1) * 8, (size_t)(S + 1) * 4};
+  if ((rc = a->up.upload(st, 2, dst, src, bytes))) return rc;
+  if (!a->h_lanes) CUDA_TRY(cudaMallocHost(&a->h_lanes, S * 8));
+  if (!a->lanes_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->lanes_ev, cudaEventDisableTiming));
+  Tables t = tables_for_launch(a, false);
+  CUDA_TRY(launch_k(k_lanes_sum, (unsigned)((nt + 7) / 8), 256, 0, st, t, d_counts, (const uint32_t *)d_tpre,
+                    d_tiles, (uint32_t)nt, T, (uint32_t)K));
+  CUDA_TRY(launch_k(k_lanes_reserve, S, 256, 0, st, t, (const uint32_t *)d_tpre, d_tiles));
+  cudaError_t e = cudaSuccess;
+  const char *dv = (const char *)d_values;
+  const LaneTile *ct = d_tiles;
+#define GG_LANES_CASE(ESZ_, KB_) \
+  case KB_: e = launch_k(k_lanes_scatter<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, ct); break;
+  switch (a->esz) {
+    case 1: switch (KB) { GG_LANES_CASE(1, 4) GG_LANES_CASE(1, 8) GG_LANES_CASE(1, 16) GG_LANES_CASE(1, 32) GG_LANES_CASE(1, 64) } break;
+    case 2: switch (KB) { GG_LANES_CASE(2, 4) GG_LANES_CASE(2, 8) GG_LANES_CASE(2, 16) GG_LANES_CASE(2, 32) GG_LANES_CASE(2, 64) } break;
+    case 4: switch (KB) { GG_LANES_CASE(4, 4) GG_LANES_CASE(4, 8) GG_LANES_CASE(4, 16) GG_LANES_CASE(4, 32) GG_LANES_CASE(4, 64) } break;
+    default: switch (KB) { GG_LANES_CASE(8, 8) GG_LANES_CASE(8, 16) GG_LANES_CASE(8, 32) GG_LANES_CASE(8, 64) } break;
+  }
+#undef GG_LANES_CASE
+  CUDA_TRY(e);
+  CUDA_TRY(cudaMemcpyAsync(a->h_lanes, a->t.size, S * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(a->lanes_ev, st));
+  a->lanes_pend = true;
+  a->lanes_head.swap(head);
+  a->lanes_keep = mapped0;
+  return GG_OK;
+}
+}  // namespace
 
 int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
                     const uint64_t *h_lane_offsets, uint64_t values_per_lane,
@@ -1296,20 +1457,32 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_lane_offsets[s + 1] < h_lane_offsets[s]) return fail(GG_EVALUE, "lane offsets must be non-decreasing");
   if (values_per_lane == 0 || values_per_lane > 0xffffffffu) return fail(GG_EVALUE, "bad values_per_lane");
+  if (h_lane_offsets[a->S] == 0) {
+    if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
+    return GG_OK;
+  }
+  {
+    int frc = lanes_tiled(a, d_values, d_counts, h_lane_offsets, values_per_lane, st);
+    if (frc != GG_ENOTSUP) {
+      if (!frc && h_status) memset(h_status, 0, a->S * sizeof(int32_t));
+      return frc;
+    }
+  }
+  // exact two-pass path (allocator hook, live-bytes limit, shards with a
+  // failed reservation, capacity exhaustion possible within the upper bound,
+  // > 32 KiB of values per lane): counts summed on the device, brought back,
+  // planned exactly like an insert
   void *dst[1] = {a->t.offsets};
   const void *src[1] = {h_lane_offsets};
   size_t bytes[1] = {(a->S + 1) * 8};
   int rc = a->up.upload(st, 1, dst, src, bytes);
   if (rc) return rc;
   // pass 1: per-shard totals -> host (one sync per launch, not per insert)
-  { k_lanes_count<<<a->S, 1024, 0, st>>>(a->t, d_counts); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  { k_lanes_count<<<a->S, 1024, 0, st>>>(a->t, d_counts, (uint32_t)values_per_lane); g_launches.fetch_add(1, std::memory_order_relaxed); }
   CUDA_TRY(cudaGetLastError());
   std::vector<uint64_t> counts(a->S);
   CUDA_TRY(cudaMemcpyAsync(counts.data(), a->t.count, a->S * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  for (uint32_t s = 0; s < a->S; ++s)
-    if (counts[s] > (h_lane_offsets[s + 1] - h_lane_offsets[s]) * values_per_lane)
-      return fail(GG_EVALUE, "a lane count exceeds values_per_lane");
   Plan p;
   plan_init(a, p);
   plan_append(a, p, counts.data(), nullptr);
@@ -1470,6 +1643,7 @@ int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, u
   // shard, in shard then bucket order, while the live-bytes cap allows
   std::vector<unsigned long long> am(a->S);
   uint64_t live = a->live;
+  a->view_keep = a->slab.mapped;
   bool stop = false;
   for (uint32_t s = 0; s < a->S; ++s) {
     am[s] = a->flags[s];
@@ -1531,7 +1705,16 @@ int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
     else a->slab.unback(s, b);
   }
   a->headroom.clear();
-  if (a->slab.cached) a->slab.trim();
+  // headroom chunks no bucket took: released asynchronously down to
+  // max(2 x needed, the mapped bytes before the view), unless the array
+  // keeps its cache (release=False)
+  uint64_t need = 0;
+  for (size_t s = 0; s < S; ++s) need += a->size[s];
+  const uint64_t keep = std::max<uint64_t>(2 * need * a->esz, a->view_keep);
+  if (!a->keep_cached && a->slab.cached && a->slab.mapped - a->slab.doomed_bytes > keep) {
+    int drc = a->slab.doom_to(keep, st);
+    if (drc) return drc;
+  }
   return any ? fail(GG_EPARTIAL, "device-side appends failed on some shards") : GG_OK;
 }
 
@@ -1635,6 +1818,8 @@ int gg_capture_release(gg_array *a) {
 
 int gg_summary(gg_array *a, uint64_t *o) {
   std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int rc = resolve_lanes(a); if (rc) return rc; }
   uint64_t sz = 0, cp = 0;
   for (uint32_t s = 0; s < a->S; ++s) { sz += a->size[s]; cp += a->cap[s]; }
   o[0] = a->prefix[a->S]; o[1] = sz; o[2] = cp;
@@ -1649,6 +1834,8 @@ int gg_info(gg_array *a, uint32_t *o) {
 int gg_host_state(gg_array *a, uint64_t *sz, uint64_t *cp, uint64_t *fl, uint64_t *pre,
                   uint64_t *ops) {
   std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int rc = resolve_lanes(a); if (rc) return rc; }
   const size_t S = a->S;
   if (sz) memcpy(sz, a->size.data(), S * 8);
   if (cp) memcpy(cp, a->cap.data(), S * 8);
@@ -1706,6 +1893,7 @@ int gg_mem_stats(gg_array *a, uint64_t *o, void *stream) {
   uint64_t cap = 0, need = 0;
   for (uint32_t s = 0; s < a->S; ++s) { cap += a->cap[s]; need += a->size[s]; }
   use_dev(a->dev);
+  { int rc = resolve_lanes(a); if (rc) return rc; }
   { int rc = settle_adopted(a, a->have_last ? a->last_st : nullptr); if (rc) return rc; }
   a->slab.reap_doomed(false);
   o[0] = cap * a->esz; o[1] = a->slab.mapped; o[2] = a->live; o[3] = need * a->esz;
@@ -1744,6 +1932,8 @@ int gg_pool_trim(int device) {
 
 int gg_slab_stats(gg_array *a, uint64_t *o) {
   std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int rc = resolve_lanes(a); if (rc) return rc; }
   const Slab &sl = a->slab;
   o[0] = sl.mapped; o[1] = sl.cached; o[2] = sl.n_map; o[3] = sl.n_unmap;
   o[4] = sl.ns_map; o[5] = sl.ns_unmap; o[6] = sl.n_regions; o[7] = sl.va_used;

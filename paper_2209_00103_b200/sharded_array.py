@@ -544,9 +544,14 @@ class GrowableArray:
     def insert_lanes(self, values, counts, lane_offsets, values_per_lane: int = 1,
                      commit: bool = True) -> None:
         """Paper Alg. 1: lanes [lane_offsets[s], lane_offsets[s+1]) belong to shard s;
-        lane j appends its first counts[j] <= values_per_lane values
-        values[j*values_per_lane ...].  One CTA per shard block-scans the counts,
-        reserves with a single atomicAdd and scatters (lane order)."""
+        lane j appends its first counts[j] values values[j*values_per_lane ...]
+        (counts above values_per_lane are clamped to it), in lane order.  The
+        device reserves each shard's batch with a single atomicAdd on its size
+        (insert_index.py:125-143), publishes the buckets and scatters with
+        16 B vector stores; the host backs memory for the upper bound
+        lanes x values_per_lane and learns the sizes asynchronously (no host
+        round trip inside the call).  With an allocator hook, an arena limit
+        or a possible capacity overflow the exact two-pass path runs."""
         import torch
         vals = self._device_values(values)
         cnt = torch.as_tensor(np.asarray(counts) if not isinstance(counts, torch.Tensor) else counts)
