@@ -771,6 +771,9 @@ struct Fuse {
   // the common destination start ustart instead of loading size[s]
   uint64_t ulen = 0;
   uint64_t ustart = 0;
+  // (host only) longest shard work length of a non-uniform directory, 0 =
+  // unknown: enables the shard-grid walk (k_walk_shard)
+  uint64_t maxlen = 0;
 };
 
 
@@ -1064,6 +1067,147 @@ __global__ void __launch_bounds__(256) k_walk(Tables t, const char *flat_src, ch
         cta_copy<ESZ, U, LS>(dp, (ctl & kCtlWrite) ? sp : nullptr, len, tid, nt);
       }
       g += len;
+    }
+  }
+}
+
+// The shard-grid walker for non-uniform directories (ragged CSR inserts,
+// duplicates / flattens / r/w of ragged arrays): blockIdx.y = shard,
+// blockIdx.x = tile of that shard's work, so a tile never searches the
+// directory and never crosses a shard (CTAs past a shard's end exit at
+// once).  Tiles are aligned to the DESTINATION: tile 0 first stores the h
+// head elements up to the first 16 B boundary of the destination, every
+// tile then moves U x 256 full 16 B destination vectors.  When the source is
+// congruent with the destination the loads are plain 16 B vectors; when not
+// (a shard's CSR batch or committed range starting at another offset mod 16
+// B than its destination) each warp loads a window of 32 consecutive aligned
+// source vectors (every lane resolving its own bucket) and writes the 31
+// output vectors it fully holds, each assembled by a funnel shift from its
+// own load and the next lane's.  Source/destination positions: INSERT flat
+// src[dir[s] + k] -> bucket size[s] + k (planned); DUP bucket k -> bucket
+// size[s] + k (planned); FLATTEN bucket k -> flat dst[dir[s] + k]; RW bucket k
+// in place.
+template <int ESZ, int W, typename T, int U>
+__global__ void __launch_bounds__(256) k_walk_shard(Tables t, const char *flat_src, char *flat_dst, T addend,
+                                                    uint32_t reps) {
+  typedef typename ElemT<ESZ>::T E;
+  constexpr uint32_t VE = 16 / ESZ, TL = U * 256 * VE;
+  constexpr uint32_t LGE = ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3;
+  typedef LdSt<W == W_RW ? 2 : kDefLS> M;
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  const uint32_t s = blockIdx.y, i = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const uint64_t *dirp = W == W_INSERT ? t.offsets : t.prefix;
+  const uint64_t lo = dirp[s], hi = dirp[s + 1];
+  uint64_t dbase = 0;
+  if constexpr (W == W_INSERT || W == W_DUP) dbase = t.size[s];   // planned: the append starts at size[s]
+  const uint64_t len = hi - lo;
+  // head elements before the destination's first 16 B boundary (buckets are
+  // 16 B aligned and hold multiples of 16 B: fb * ESZ >= 16 is required)
+  uint32_t h;
+  if constexpr (W == W_FLATTEN) h = (uint32_t)(((16 - ((uintptr_t)(flat_dst + lo * ESZ) & 15)) & 15) / ESZ);
+  else h = (uint32_t)((VE - dbase % VE) % VE);
+  const uint64_t kb = h + (uint64_t)i * TL;                         // first body element of the tile
+  if (kb >= len && !(i == 0 && len)) return;
+  stage_cbase(t, scb);
+  __syncthreads();
+  const uint32_t lg0 = t.log2fb + LGE;
+  // element addresses
+  auto src_at = [&](uint64_t k) -> char * {
+    if constexpr (W == W_INSERT) {
+      return (char *)flat_src + (lo + k) * ESZ;
+    } else {
+      uint32_t b; uint64_t o;
+      locate(k, t.log2fb, b, o);
+      return slot_addr(scb, s, b, lg0) + o * ESZ;
+    }
+  };
+  auto dst_at = [&](uint64_t k) -> char * {
+    if constexpr (W == W_FLATTEN) {
+      return flat_dst + (lo + k) * ESZ;
+    } else if constexpr (W == W_RW) {
+      return src_at(k);
+    } else {
+      uint32_t b; uint64_t o;
+      locate(dbase + k, t.log2fb, b, o);
+      return slot_addr(scb, s, b, lg0) + o * ESZ;
+    }
+  };
+  auto elem = [&](uint64_t k) {
+    if constexpr (W == W_RW) {
+      T *p = (T *)src_at(k);
+      T x = *p;
+      for (uint32_t r = 0; r < reps; ++r) x = AddOp<T>::apply(x, addend);
+      *p = x;
+    } else {
+      *(E *)dst_at(k) = *(const E *)src_at(k);
+    }
+  };
+  // head (tile 0) and tail (last tile): element by element
+  if (i == 0)
+    for (uint64_t k = tid; k < min((uint64_t)h, len); k += 256) elem(k);
+  if (kb >= len) return;
+  const uint64_t ke = min(len, kb + TL);
+  const uint32_t nv = (uint32_t)((ke - kb) / VE);
+  for (uint64_t k = kb + (uint64_t)nv * VE + tid; k < ke; k += 256) elem(k);
+  if (!nv) return;
+  // source position (element index in the source's own space) of body element k
+  const uint32_t sig = W == W_INSERT ? (uint32_t)(((uintptr_t)(flat_src + (lo + kb) * ESZ) & 15) / ESZ)
+                                     : (uint32_t)(kb % VE);
+  if (sig == 0) {
+    for (uint32_t v0 = tid; v0 < nv; v0 += U * 256) {
+      uint4 r[U];
+      char *sp[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sp[u] = src_at(kb + (uint64_t)min(v0 + u * 256u, nv - 1) * VE);
+        r[u] = M::ld((const uint4 *)sp[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t v = v0 + u * 256u;
+        if (v >= nv) continue;
+        if constexpr (W == W_RW) {
+          union { uint4 q; T e[VE]; } x;
+          x.q = r[u];
+          for (uint32_t rr = 0; rr < reps; ++rr)
+#pragma unroll
+            for (uint32_t j = 0; j < VE; ++j) x.e[j] = AddOp<T>::apply(x.e[j], addend);
+          M::st((uint4 *)sp[u], x.q);
+        } else {
+          M::st((uint4 *)dst_at(kb + (uint64_t)v * VE), r[u]);
+        }
+      }
+    }
+    return;
+  }
+  if constexpr (W != W_RW) {
+    // non-congruent source: windows of 32 aligned source vectors -> 31 outputs
+    const uint64_t k0 = kb - sig;                    // body-relative: aligned source vector j holds k0 + j * VE ..
+    const uint32_t m = sig * ESZ, q = m >> 2, rsh = (m & 3) * 8;
+    const uint32_t nw = (uint32_t)(blockDim.x >> 5), wid = tid >> 5;
+    constexpr int UR = U > 4 ? 4 : U;       // (8 in flight: 76-80 registers, 3 CTAs per SM, slower)
+    for (uint32_t w0 = wid; 31 * w0 < nv; w0 += UR * nw) {
+      uint4 a[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const uint32_t j = min(31 * (w0 + u * nw) + lane, nv);        // aligned source vector (clamped)
+        if constexpr (W == W_INSERT) {
+          a[u] = M::ld((const uint4 *)(flat_src + (lo + k0) * ESZ) + j);
+        } else {
+          a[u] = M::ld((const uint4 *)src_at(k0 + (uint64_t)j * VE));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        uint4 hn;
+        hn.x = __shfl_down_sync(0xffffffffu, a[u].x, 1);
+        hn.y = __shfl_down_sync(0xffffffffu, a[u].y, 1);
+        hn.z = __shfl_down_sync(0xffffffffu, a[u].z, 1);
+        hn.w = __shfl_down_sync(0xffffffffu, a[u].w, 1);
+        const uint32_t v = 31 * (w0 + u * nw) + lane;
+        if (lane < 31 && v < nv) M::st((uint4 *)dst_at(kb + (uint64_t)v * VE), realign16(a[u], hn, q, rsh));
+      }
     }
   }
 }

@@ -276,10 +276,47 @@ cudaError_t walk_u(const gg_array *a, const Tables &t, const char *src, char *ds
                   src, dst, total, add, reps, tile, fz);
 }
 
+// the shard-grid walk (k_walk_shard) for a non-uniform directory: planned
+// appends, flatten and in-place r/w over whole shards, buckets of >= 16 B,
+// enough work per shard for full tiles
+bool shard_grid_ok(const gg_array *a, int w, bool planned, const Fuse &fz, uint64_t total) {
+  static const bool on = [] { const char *e = getenv("GG_SHARD_GRID"); return !e || e[0] != '0'; }();
+  return on && fz.maxlen && !fz.ulen && fz.g0 == 0 && !fz.size_next && a->S <= 65535 &&
+         ((uint64_t)a->fb * a->esz) >= 16 && total / a->S >= 2048 && (w == W_FLATTEN || w == W_RW || planned);
+}
+
+// longest shard of a directory dir[S+1]
+uint64_t dir_maxlen(const uint64_t *dir, uint32_t S) {
+  uint64_t m = 0;
+  for (uint32_t s = 0; s < S; ++s) m = std::max<uint64_t>(m, dir[s + 1] - dir[s]);
+  return m;
+}
+
+template <int ESZ, int W, typename T, int U>
+int walk_shard(const gg_array *a, const Tables &t, const char *src, char *dst, T add, uint32_t reps,
+               uint64_t maxlen, cudaStream_t st) {
+  constexpr uint64_t TL = (uint64_t)U * 256 * (16 / ESZ);
+  const dim3 grid((unsigned)((maxlen + 16 + TL - 1) / TL), a->S);
+  cudaError_t e = launch_k(k_walk_shard<ESZ, W, T, U>, grid, kThreads, 0, st, t, src, dst, add, reps);
+  if (e != cudaSuccess) return fail(GG_ECUDA, std::string("walk launch: ") + cudaGetErrorString(e));
+  return GG_OK;
+}
+
 template <int ESZ, int W, typename T, bool P = false>
 int walk(const gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total, T add,
          uint32_t reps, Fuse fz, cudaStream_t st) {
   if (total == 0) return GG_OK;
+  if (shard_grid_ok(a, W, P, fz, total)) {
+    // copies into the slabs move 32 KiB tiles, flatten / r/w 16 KiB (tools/sweep.py's split)
+    static const int u_sg = [] { const char *e = getenv("GG_SG_U"); return e ? atoi(e) : 0; }();
+    if constexpr (W == W_INSERT || W == W_DUP) {
+      if (u_sg == 4) return walk_shard<ESZ, W, T, 4>(a, t, src, dst, add, reps, fz.maxlen, st);
+      return walk_shard<ESZ, W, T, 8>(a, t, src, dst, add, reps, fz.maxlen, st);
+    } else {
+      if (u_sg == 8) return walk_shard<ESZ, W, T, 8>(a, t, src, dst, add, reps, fz.maxlen, st);
+      return walk_shard<ESZ, W, T, 4>(a, t, src, dst, add, reps, fz.maxlen, st);
+    }
+  }
   cudaError_t e;
   switch (walk_unroll(a, total, W, reps)) {
     case 1: e = walk_u<ESZ, W, T, P, 1>(a, t, src, dst, total, add, reps, fz, st); break;
@@ -316,7 +353,10 @@ template <int W>
 int launch_walk(gg_array *a, const Tables &t, const char *src, char *dst, uint64_t total,
                 cudaStream_t st) {
   Fuse fz{0, 0};
-  if (W == W_FLATTEN) fz.ulen = uniform_len(a);
+  if (W == W_FLATTEN) {
+    fz.ulen = uniform_len(a);
+    if (!fz.ulen) fz.maxlen = dir_maxlen(a->prefix.data(), a->S);
+  }
   return walk_copy<W, false>(a, t, src, dst, total, fz, st);
 }
 
@@ -481,7 +521,15 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
   // copy kernels.
   if (!p.any_ctl && p.zero_pairs.empty() && reserve_mode != 2 && !(flags & GG_F_UNFUSED)) {
     const bool commit = (flags & GG_F_COMMIT) != 0;
-    if (total && fuse_ok(a, st)) {
+    // a non-uniform directory with whole tiles per shard takes the shard-grid
+    // walk (its metadata pass is deferred, like the unfused planned walk)
+    Fuse gz{reserve_mode, commit ? 1 : 0};
+    if (!csr_ulen && total) {
+      if (wk == W_INSERT && h_offsets) gz.maxlen = dir_maxlen(h_offsets, a->S);
+      else if (wk == W_DUP && !uniform_len(a)) gz.maxlen = dir_maxlen(a->prefix.data(), a->S);
+    }
+    const bool grid2d = shard_grid_ok(a, wk, true, gz, total);
+    if (total && fuse_ok(a, st) && !grid2d) {
       // ONE launch: copy CTAs + a metadata CTA writing the next size/prefix
       // pair (and publishing a deferred grow)
       Fuse fz{reserve_mode, commit ? 1 : 0};
@@ -506,7 +554,7 @@ int run_append(gg_array *a, Plan &p, int reserve_mode, int wk, const char *src,
       if ((rc = a->up.upload(st, 1, dst, srcs, bytes))) return rc;
     }
     if (total) {
-      Fuse fz{reserve_mode, commit ? 1 : 0};
+      Fuse fz = gz;
       rc = wk == W_INSERT ? walk_copy<W_INSERT, true>(a, t, src, nullptr, total, fz, st)
                             : walk_copy<W_DUP, true>(a, t, nullptr, nullptr, total, fz, st);
       if (rc) return rc;
@@ -621,6 +669,7 @@ int launch_rw(gg_array *a, const Tables &t, T addend, uint32_t passes, int mode,
   }
   Fuse none{0, 0};
   none.ulen = uniform_len(a);
+  if (!none.ulen) none.maxlen = dir_maxlen(a->prefix.data(), a->S);
   if (mode == GG_RW_FUSED)
     return walk<sizeof(T), W_RW, T>(a, t, nullptr, nullptr, total, addend, passes, none, st);
   for (uint32_t p = 0; p < passes; ++p) {

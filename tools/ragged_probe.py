@@ -54,16 +54,43 @@ a.insert_csr(src, off)
 a.insert_duplicate()
 a.shrink(0, release=False)
 torch.cuda.synchronize()
-rec("ragged_insert_csr", timed(lambda: a.insert_csr(src, off), lambda: a.shrink(0, release=False)), 8 * N, N)
+rec("ragged_insert_csr", timed(lambda: (a.insert_csr(src, off), a.flush()), lambda: a.shrink(0, release=False)),
+    8 * N, N)                                 # flush(): the deferred metadata pass is inside the timing
+
+
+def graph_ms(fn, reps=10):
+    """device time per replay of fn captured once (host planning excluded)"""
+    g = a.capture(fn)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+rec("ragged_insert_csr_graph", graph_ms(lambda: (a.shrink(0, release=False), a.insert_csr(src, off))), 8 * N, N)
+out["ragged_insert_csr_graph"]["note"] = "reset + insert replayed as a CUDA graph (device time)"
+rec("ragged_insert_dup_graph", graph_ms(lambda: (a.shrink(0, release=False), a.insert_csr(src, off),
+                                                  a.insert_duplicate())), 16 * N, 2 * N)
+out["ragged_insert_dup_graph"]["note"] = "reset + insert + duplicate replayed as a CUDA graph (device time)"
 # duplicate of the ragged array (source and destination misaligned per shard)
 def reset_dup():
     a.shrink(0, release=False)
     a.insert_csr(src, off)
-rec("ragged_duplicate", timed(lambda: a.insert_duplicate(), reset_dup), 8 * N, N)
+rec("ragged_duplicate", timed(lambda: (a.insert_duplicate(), a.flush()), reset_dup), 8 * N, N)
 exp = torch.cat([torch.cat([src[int(off[s]):int(off[s + 1])]] * 2) for s in range(S)])
 out["ragged_contents_ok"] = bool(torch.equal(a.flatten_device(), exp))
 del exp
 rec("ragged_flatten", timed(lambda: a.flatten_device(), lambda: None), 8 * 2 * N, 2 * N)
+rec("ragged_rw_per_shard", timed(lambda: a.rw_add(1), lambda: None), 8 * 2 * N, 2 * N)
+exp = torch.cat([torch.cat([src[int(off[s]):int(off[s + 1])]] * 2) for s in range(S)]) + 5
+out["ragged_rw_contents_ok"] = bool(torch.equal(a.flatten_device(), exp))
+del exp
 
 # lanes insert (paper Alg. 1 with per-lane counts)
 for K in (8, 1):
