@@ -899,6 +899,7 @@ struct Grave {
   void *dmem = nullptr;               // cudaMallocAsync'd metadata block
   char *h_scratch = nullptr;          // pinned
   uint64_t *h_lanes = nullptr;        // pinned
+  char *h_view = nullptr;             // pinned
   void *lanes_dmem = nullptr;         // cudaMallocAsync'd lanes scratch
   cudaEvent_t lanes_ev = nullptr;
   cudaEvent_t ord_ev = nullptr;
@@ -907,6 +908,7 @@ struct Grave {
     up.destroy();
     if (h_scratch) cudaFreeHost(h_scratch);
     if (h_lanes) cudaFreeHost(h_lanes);
+    if (h_view) cudaFreeHost(h_view);
     if (lanes_dmem) cudaFreeAsync(lanes_dmem, 0);
     if (lanes_ev) cudaEventDestroy(lanes_ev);
     if (dmem) cudaFreeAsync(dmem, 0);

@@ -75,6 +75,8 @@ struct gg_array {
   std::vector<uint32_t> lanes_head;                      // (s, b) backed for the upper bound
   uint64_t lanes_keep = 0;                               // mapped bytes before that backing
   uint64_t view_keep = 0;                                // mapped bytes before a device view's headroom
+  char *h_view = nullptr;                                // pinned staging of view_finish
+  size_t h_view_cap = 0;
   // the last shrink asked to keep released chunks cached (release=False):
   // headroom returned by lanes inserts / device views stays cached too
   bool keep_cached = false;
@@ -730,9 +732,11 @@ namespace gg {
 // elements i of its slice with pred[i] != 0 to shard b % S, warp- or
 // block-aggregated.
 // Each thread gathers the candidates of K consecutive rounds of its block's
-// slices (coalesced loads) and appends its kept values with one warp- or
-// block-aggregated push_back_n, so one reservation covers up to 32*K (warp)
-// or BLOCK*K (block) values.
+// slices (coalesced loads; the value is loaded whatever the predicate, its
+// sector is read anyway at any useful density) into registers with a
+// K-bit keep mask, and appends them with one warp- or block-aggregated
+// push_back_mask: one reservation covers up to 32*K (warp) or BLOCK*K
+// (block) values, all indexing static (no local memory).
 template <int ESZ, int BLOCK, int K>
 __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char *vals,
                                                    const uint8_t *pred, uint64_t n, int block_mode) {
@@ -741,15 +745,19 @@ __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char 
   const uint32_t s = blockIdx.x % t.S;
   const uint64_t round = (uint64_t)gridDim.x * BLOCK;
   for (uint64_t r0 = 0; (uint64_t)blockIdx.x * BLOCK + r0 * round < n; r0 += K) {
-    E kept[K];
-    uint32_t cnt = 0;
+    E v[K];
+    uint32_t mask = 0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const uint64_t i = (uint64_t)blockIdx.x * BLOCK + (r0 + j) * round + threadIdx.x;
-      if (i < n && pred[i]) kept[cnt++] = reinterpret_cast<const E *>(vals)[i];
+      v[j] = E(0);
+      if (i < n) {
+        v[j] = __ldcs(reinterpret_cast<const E *>(vals) + i);
+        mask |= (__ldcs(pred + i) ? 1u : 0u) << j;
+      }
     }
-    if (block_mode) block_push_back<BLOCK, E>(t, s, cnt, kept, scratch);
-    else warp_push_back_n<E, K>(t, s, cnt, kept);
+    if (block_mode) block_push_back_mask<BLOCK, E, K>(t, s, mask, v, scratch);
+    else warp_push_back_mask<E, K>(t, s, mask, v);
   }
 }
 
@@ -865,6 +873,7 @@ int gg_destroy(gg_array *a) {
   g->dmem = a->dmem;
   g->h_scratch = a->h_scratch;
   g->h_lanes = a->h_lanes;
+  g->h_view = a->h_view;
   g->lanes_dmem = a->lanes_dmem;
   g->lanes_ev = a->lanes_ev;
   g->ord_ev = a->ord_ev;
@@ -1682,14 +1691,14 @@ int gg_set(gg_array *a, uint32_t s, uint64_t i, const void *h_val, void *stream)
 
 uint64_t gg_device_view_bytes(void) { return sizeof(gg_device_view); }
 
-int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, uint64_t view_bytes) {
-  std::lock_guard<std::mutex> g(a->mu);
-  use_dev(a->dev);
-  { int frc_ = flush_pending(a); if (frc_) return frc_; }
-  if (view_bytes != sizeof(gg_device_view)) return fail(GG_EVALUE, "view size mismatch (ggarray_device.cuh)");
+namespace {
+// Back every slot a device-side append may take (buckets [0,
+// min_buckets_for(max)) per shard, in shard then bucket order, while the
+// live-bytes cap allows) and publish the backed-slot masks on stream st.
+// sync: wait for the device (the public entry point, whose user kernel may
+// run on any stream); the library's own push_if stays stream-ordered.
+int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool sync, gg_device_view *out) {
   if (a->view_out) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
-  // back every slot the launch may take: buckets [0, min_buckets_for(max)) per
-  // shard, in shard then bucket order, while the live-bytes cap allows
   std::vector<unsigned long long> am(a->S);
   uint64_t live = a->live;
   a->view_keep = a->slab.mapped;
@@ -1708,46 +1717,58 @@ int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, u
       a->headroom.push_back(b);
     }
   }
-  int rc = push_cbase(a, 0);
+  int rc = push_cbase(a, st);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpy(a->t.amask, am.data(), a->S * 8, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaDeviceSynchronize());
+  void *dst[1] = {a->t.amask};
+  const void *src[1] = {am.data()};
+  size_t bytes[1] = {a->S * 8};
+  if ((rc = a->up.upload(st, 1, dst, src, bytes))) return rc;
+  if (sync) CUDA_TRY(cudaDeviceSynchronize());
   gg_device_view v = a->t;
   v.ctl = nullptr;                          // amask gates the device allocator
-  memcpy(h_view, &v, sizeof v);
-  a->view_out = true;                       // mutating calls refused until gg_device_view_sync
+  *out = v;
+  a->view_out = true;                       // mutating calls refused until the view is synced
   return GG_OK;
 }
 
-// refresh the host mirrors from the device after user kernels appended
-int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
-  std::lock_guard<std::mutex> g(a->mu);
-  use_dev(a->dev);
-  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
-  cudaStream_t st = S_(stream);
+// refresh the host mirrors from the device after device-side appends: one
+// asynchronous copy of sizes / capacities / ops / published masks / status /
+// counters into a pinned buffer and ONE stream synchronize
+int view_finish(gg_array *a, int32_t *h_status, cudaStream_t st) {
+  const size_t S = a->S;
+  const size_t nb = S * 8 * 4 + ((S * 4 + 7) & ~size_t(7)) + MISC_N * 8;
+  if (!a->h_view || a->h_view_cap < nb) {
+    if (a->h_view) CUDA_TRY(cudaFreeHost(a->h_view));
+    a->h_view = nullptr;
+    CUDA_TRY(cudaMallocHost(&a->h_view, nb));
+    a->h_view_cap = nb;
+  }
+  char *hb = a->h_view;
+  uint64_t *hs = (uint64_t *)hb, *hc = hs + S, *ho = hc + S, *hp = ho + S;
+  uint32_t *hst = (uint32_t *)(hp + S);
+  unsigned long long *hm = (unsigned long long *)(hb + S * 32 + ((S * 4 + 7) & ~size_t(7)));
+  CUDA_TRY(cudaMemcpyAsync(hs, a->t.size, S * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hc, a->t.cap, S * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(ho, a->t.ops, S * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hp, a->t.pmask, S * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hst, a->t.status, S * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hm, a->t.misc, MISC_N * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemsetAsync(a->t.status, 0, S * 4, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   a->view_out = false;
-  const size_t S = a->S;
-  std::vector<uint32_t> f(S * a->MB), status(S);
-  std::vector<unsigned long long> misc(MISC_N);
-  CUDA_TRY(cudaMemcpy(a->size.data(), a->t.size, S * 8, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(a->cap.data(), a->t.cap, S * 8, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(a->ops.data(), a->t.ops, S * 8, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(f.data(), a->t.flag, f.size() * 4, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(status.data(), a->t.status, S * 4, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(misc.data(), a->t.misc, MISC_N * 8, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemset(a->t.status, 0, S * 4));
   bool any = false;
   for (size_t s = 0; s < S; ++s) {
-    uint64_t m = 0;
-    for (uint32_t b = 0; b < a->MB; ++b)
-      if (f[s * a->MB + b] == kFlagPublished) m |= uint64_t(1) << b;
-    a->flags[s] = m;
-    if (h_status) h_status[s] = (int32_t)status[s];
-    if (status[s]) { any = true; a->dirty[s] = 1; }
+    a->size[s] = hs[s];
+    a->cap[s] = hc[s];
+    a->ops[s] = ho[s];
+    // pmask bits are set after the once-flag is published (and never for a
+    // rolled-back allocation): at kernel completion they are the published set
+    a->flags[s] = hp[s];
+    if (h_status) h_status[s] = (int32_t)hst[s];
+    if (hst[s]) { any = true; a->dirty[s] = 1; }
   }
-  a->alloc_calls = misc[MISC_ALLOCS];
-  // headroom the kernel took becomes live; the rest is unmapped again
+  a->alloc_calls = hm[MISC_ALLOCS];
+  // headroom the kernel took becomes live; the rest is unbacked
   for (size_t i = 0; i < a->headroom.size(); i += 2) {
     const uint32_t s = a->headroom[i], b = a->headroom[i + 1];
     if (a->flags[s] >> b & 1) a->live += bucket_bytes(a, b);
@@ -1766,6 +1787,29 @@ int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
   }
   return any ? fail(GG_EPARTIAL, "device-side appends failed on some shards") : GG_OK;
 }
+}  // namespace
+
+int gg_device_view_get(gg_array *a, const uint64_t *h_max_sizes, void *h_view, uint64_t view_bytes) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int frc_ = flush_pending(a); if (frc_) return frc_; }
+  if (view_bytes != sizeof(gg_device_view)) return fail(GG_EVALUE, "view size mismatch (ggarray_device.cuh)");
+  gg_device_view v;
+  // the view's user kernel may run on any stream: prepared on the legacy
+  // stream and waited for
+  int rc = view_prepare(a, h_max_sizes, 0, true, &v);
+  if (rc) return rc;
+  memcpy(h_view, &v, sizeof v);
+  return GG_OK;
+}
+
+// refresh the host mirrors from the device after user kernels appended
+int gg_device_view_sync(gg_array *a, int32_t *h_status, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
+  return view_finish(a, h_status, S_(stream));
+}
 
 int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t n, int32_t mode,
                uint32_t grid, int32_t *h_status, void *stream) {
@@ -1778,20 +1822,20 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   if (!grid)
     grid = (uint32_t)std::max<uint64_t>(
         a->S, std::min<uint64_t>((n + B * 8 - 1) / (B * 8), (uint64_t)sm_count(a->dev) * 8));
-  // worst case: every candidate of shard s appended
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, st); if (frc_) return frc_; }
+  // worst case: every candidate of shard s appended (block blk takes slice
+  // blk of every round of grid * B candidates)
   std::vector<uint64_t> maxsz(a->S, 0);
-  {
-    std::lock_guard<std::mutex> g(a->mu);
-    const uint64_t per_round = (uint64_t)grid * B;
-    for (uint32_t blk = 0; blk < grid; ++blk) {
-      uint64_t lo = (uint64_t)blk * B, c = 0;
-      for (uint64_t base = lo; base < n; base += per_round) c += std::min<uint64_t>(B, n - base);
-      maxsz[blk % a->S] += c;
-    }
-    for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += a->size[s];
+  const uint64_t per_round = (uint64_t)grid * B, full = n / per_round, rem = n % per_round;
+  for (uint32_t blk = 0; blk < grid; ++blk) {
+    const uint64_t lo = (uint64_t)blk * B;
+    maxsz[blk % a->S] += full * B + (rem > lo ? std::min<uint64_t>(B, rem - lo) : 0);
   }
+  for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += a->size[s];
   gg_device_view v;
-  int rc = gg_device_view_get(a, maxsz.data(), &v, sizeof v);
+  int rc = view_prepare(a, maxsz.data(), st, false, &v);
   if (rc) return rc;
   switch (a->esz) {
     case 1: { k_push_if<1, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
@@ -1800,7 +1844,7 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
     case 8: { k_push_if<8, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
   }
   CUDA_TRY(cudaGetLastError());
-  return gg_device_view_sync(a, h_status, stream);
+  return view_finish(a, h_status, st);
 }
 
 int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads) {
