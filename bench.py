@@ -303,6 +303,8 @@ def run_device(args, rank, world, local_rank):
         _between_legs(gg)
         out["phased_config4"] = phased_leg(args, gg, torch, device)
         _between_legs(gg)
+        out["insert_paths"] = insert_paths_leg(args, gg, torch, device, hbm)
+        _between_legs(gg)
         out["config5_per_gpu"] = config5_leg(args, gg, torch, device, hbm)
         _between_legs(gg)
         out["config1"] = config1_leg(args, gg, torch, device, rank == 0 and world == 1 and not args.no_cpu)
@@ -618,6 +620,25 @@ def secondary(args, gg, torch, device, step, hbm):
                       "insert_gelem_s": round(half / min(i_ms) / 1e6, 2),
                       "insert": "insert_batch (one reservation + k_flat_append)",
                       "grow": "cuMemCreate/Map/SetAccess of 2 GiB more (64 MiB pieces) + zero"}
+    # GGArray's grow of the same step from FRESH driver memory, like memMap's
+    # (the steady-state step below grows into chunks its reset kept mapped)
+    from paper_2209_00103_b200.sharded_array import split_offsets
+    g_ms, mapped = [], 0
+    for _ in range(3):
+        gg.pool_trim(device.index)
+        e = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+        e.insert_csr(src, split_offsets(half, S))
+        e.flush()
+        torch.cuda.synchronize()
+        m0 = e.memory_stats(settle=False)["mapped_bytes"]
+        g_ms.append(_time(torch, lambda: (e.grow(1 << 30), e.flush())))
+        mapped = e.memory_stats(settle=False)["mapped_bytes"] - m0
+        e.close()
+        del e
+        gg.reclaim(True)
+    base["ggarray512_cold_grow"] = {"grow_ms": round(min(g_ms), 4), "mapped_bytes": int(mapped),
+                                    "grow": "grow(2^30) on a fresh array after pool_trim: cuMemCreate/Map/"
+                                            "SetAccess of the new bucket class (one extent) + k_grow"}
     # ggarray, same last step
     last = step.dup_ms[ROUNDS - 1::ROUNDS]
     lastg = step.grow_ms[ROUNDS - 1::ROUNDS]
@@ -629,6 +650,132 @@ def secondary(args, gg, torch, device, step, hbm):
     torch.cuda.empty_cache()
     res["baselines_full_schedule"] = full_schedule_baselines(gg, torch, device, step, args)
     return res
+
+
+def insert_paths_leg(args, gg, torch, device, hbm):
+    """The insert paths beside config 2's uniform doubling, at 2^28 int32 over
+    512 LFVectors (inputs and arrays far larger than L2):
+      * ragged CSR insert: per-LFVector batch sizes uniform in [0, 2 x mean]
+        (BASELINE config 4's distribution), then the duplicate of that ragged
+        array (every LFVector's source and destination start at another
+        offset mod 16 B), its flatten and a +1 r/w pass -- the shard-grid walk
+        (k_walk_shard); 8 B algorithmic per element;
+      * paper Alg. 1 with per-lane counts (insert_lanes): lanes of K values,
+        counts uniform in [0, K]; algorithmic bytes = counts (4 B / lane) +
+        the [lanes x K] value block the counts select from + the compacted
+        output (the layout the API takes), the useful bytes (counts + kept
+        values read + written) beside it;
+      * push_if (the device push_back API from a kernel): 2^28 candidates,
+        predicate density 1/2; bytes = values + predicates read + kept written.
+    Eager timings are CUDA events around the public call (host planning and
+    the deferred metadata pass, flushed, inside); graph timings replay the
+    reset + insert captured once (device time)."""
+    from paper_2209_00103_b200.sharded_array import split_offsets  # noqa: F401
+    N = 1 << 28
+    rng = np.random.default_rng(0)
+    out = {"elements": N, "shards": S}
+
+    def rec(name, ms, nbytes, elems, extra=None):
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 4), "gbs": round(gbs, 1), "frac": round(gbs / hbm, 4),
+                     "gelem_s": round(elems / (ms * 1e-3) / 1e9, 2), **(extra or {})}
+
+    def best(fn, reset, reps=5):
+        ms = 1e9
+        for _ in range(reps):
+            reset()
+            torch.cuda.synchronize()
+            e0, e1 = _events(torch)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = min(ms, e0.elapsed_time(e1))
+        return ms
+
+    counts = rng.integers(0, 2 * (N // S) + 1, S).astype(np.int64)
+    counts = (counts * (N / counts.sum())).astype(np.int64)
+    counts[-1] += N - counts.sum()
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64)
+    src = torch.arange(N, dtype=torch.int32, device=device)
+    a = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+    a.insert_csr(src, off)
+    a.insert_duplicate()
+    reset = lambda: a.shrink(0, release=False)
+    rec("ragged_insert_csr", best(lambda: (a.insert_csr(src, off), a.flush()), reset), 8 * N, N)
+
+    def graph_ms(fn, reps=10):
+        g = a.capture(fn)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = _events(torch)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    rec("ragged_insert_csr_graph", graph_ms(lambda: (a.shrink(0, release=False), a.insert_csr(src, off))),
+        8 * N, N, {"note": "reset + insert captured once, replayed (device time)"})
+
+    def reset_dup():
+        a.shrink(0, release=False)
+        a.insert_csr(src, off)
+    rec("ragged_duplicate", best(lambda: (a.insert_duplicate(), a.flush()), reset_dup), 8 * N, N)
+    exp = torch.cat([torch.cat([src[int(off[s]):int(off[s + 1])]] * 2) for s in range(S)])
+    got = a.flatten_device()
+    out["ragged_contents_ok"] = bool(torch.equal(got, exp))
+    rec("ragged_flatten", best(lambda: a.flatten_device(out=got), lambda: None), 16 * N, 2 * N)
+    rec("ragged_rw_per_shard", best(lambda: a.rw_add(1), lambda: None), 16 * N, 2 * N)
+    out["ragged_rw_contents_ok"] = bool(torch.equal(a.flatten_device(out=got), exp + 5))
+    a.close()
+    del a, exp, got, src
+    torch.cuda.empty_cache()
+    _between_legs(gg)
+    # paper Alg. 1 with per-lane counts
+    for K in (8, 1):
+        L = N // max(1, K // 2)                      # expected appended elements ~ N (K = 8) / N / 2 (K = 1)
+        lo = np.arange(S + 1, dtype=np.uint64) * np.uint64(L // S)
+        g = torch.Generator(device=device).manual_seed(K)
+        cnt = torch.randint(0, K + 1, (L,), dtype=torch.int32, device=device, generator=g)
+        vals = torch.arange(L * K, dtype=torch.int32, device=device)
+        tot = int(cnt.sum())
+        b = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+        b.insert_lanes(vals, cnt, lo, K, commit=False)
+        ms = best(lambda: b.insert_lanes(vals, cnt, lo, K, commit=False), lambda: b.shrink(0, release=False))
+        layout = 4 * L + 4 * L * K + 4 * tot
+        useful = 4 * L + 8 * tot
+        rec(f"lanes_K{K}", ms, layout, tot,
+            {"lanes": L, "appended": tot, "algorithmic_bytes": layout, "useful_bytes": useful,
+             "useful_frac": round(useful / (ms * 1e-3) / 1e9 / hbm, 4),
+             "kernels": "k_lanes_sum + k_lanes_reserve + k_lanes_scatter"})
+        b.commit()
+        mask = torch.arange(K, device=device)[None, :] < cnt[:, None]
+        out[f"lanes_K{K}"]["contents_ok"] = bool(torch.equal(b.flatten_device(), vals.view(-1, K)[mask]))
+        b.close()
+        del b, vals, cnt, mask
+        torch.cuda.empty_cache()
+        _between_legs(gg)
+    # push_if (device push_back API)
+    vals = torch.arange(N, dtype=torch.int32, device=device)
+    g = torch.Generator(device=device).manual_seed(7)
+    pred = (torch.rand(N, device=device, generator=g) < 0.5).to(torch.uint8)
+    tot = int(pred.sum())
+    for mode in ("block", "warp"):
+        c = gg.GrowableArray(S, FB, dtype=np.int32, device=device)
+        c.push_if(vals, pred, mode=mode, commit=False)
+        ms = best(lambda: c.push_if(vals, pred, mode=mode, commit=False), lambda: c.shrink(0, release=False))
+        rec(f"push_if_{mode}", ms, 5 * N + 4 * tot, tot,
+            {"candidates": N, "appended": tot, "kernel": f"k_push_if ({mode}_push_back_mask, 8 rounds per thread)"})
+        c.commit()
+        out[f"push_if_{mode}"]["multiset_ok"] = bool(torch.equal(torch.sort(c.flatten_device())[0],
+                                                                 vals[pred.bool()]))
+        c.close()
+        del c
+    del vals, pred
+    torch.cuda.empty_cache()
+    return out
 
 
 def full_schedule_baselines(gg, torch, device, step, args):
