@@ -320,7 +320,7 @@ def bench_grow_insert_rw(config) -> list:
 
 def _two_phase_run(config, kind: str, start: int, k: int, final: int):
     import torch
-    import paper_2209_00103_b200 as gg
+    from paper_2209_00103_b200.sharded_array import split_offsets
     store = _build(replace(config, structure=kind), torch.arange(start, dtype=torch.int32, device="cuda"), final)
     oracle = torch.arange(start, dtype=torch.int64, device="cuda")
     tag, total, phases = start, 0, []
@@ -351,7 +351,11 @@ def _two_phase_run(config, kind: str, start: int, k: int, final: int):
                 _flat_rw(flat, config.work_passes)
             w_ns = t.ns
             with _Timer() as t:
-                store = gg.GrowableArray.from_flat(flat, config.shards, config.first_bucket)
+                # rebuild (from_flat's re-sharding, sharded_array.py:259-282) into
+                # the same handle: the reset keeps its buckets mapped, so the
+                # rebuild is one planned insert, no VMM driver call
+                store.shrink(0, release=False)
+                store.insert_csr(flat, split_offsets(int(flat.numel()), store.shard_count))
             f_ns += t.ns
             total += f_ns + w_ns
             phases.append(dict(iteration=it, phase="flatten", elapsed_ns=f_ns, size_after=after))
