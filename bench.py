@@ -323,6 +323,12 @@ def gather_leg(args, torch, device, step, dist, world):
     try:
         from paper_2209_00103_b200.multigpu import DistributedGrowableArray, PeerGather
         d = DistributedGrowableArray(step.arr, device=device)
+        ok_peer, why = d.peer_topology()
+        pre = d.global_prefix()
+        # bytes each rank moves into the root's buffer (the root's own slice stays local)
+        per_rank = [0 if r == 0 else (pre[r + 1] - pre[r]) * 4 for r in range(world)]
+        if not ok_peer:
+            return fallback_gather_leg(torch, device, d, dist, pre, per_rank, why)
         g = PeerGather(d, 0)
         g.run(); g.wait()
         k = 3
@@ -387,6 +393,7 @@ def gather_leg(args, torch, device, step, dist, world):
         del part
         torch.cuda.empty_cache()
         return {"ms": round(ms, 4), "bytes_total": total, "bytes_over_nvlink": nvlink,
+                "bytes_over_nvlink_per_rank": per_rank, "peer_topology": "ok",
                 "nvlink_gbs_into_root": round(nvlink / (ms * 1e-3) / 1e9, 1),
                 "root_slice_ok": ok, "method": "fused K-flatten into the root buffer (CUDA IPC)",
                 "rebalance_ms_incl_setup": round(rb_ms, 3),
@@ -394,6 +401,34 @@ def gather_leg(args, torch, device, step, dist, world):
                 "nccl_baseline": nccl}
     except Exception as exc:                          # report, never lose the bench line
         return {"error": repr(exc)[:300]}
+
+
+def fallback_gather_leg(torch, device, d, dist, pre, per_rank, why):
+    """No peer access between the ranks' GPUs (multigpu.peer_topology): the
+    same gather through DistributedGrowableArray.flatten_global's NCCL path
+    (local K-flatten + point-to-point into the root), with the reason."""
+    e0, e1 = _events(torch)
+    d.flatten_global(0, method="nccl")
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    out = d.flatten_global(0, method="nccl")
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ok = True
+    if dist.get_rank() == 0:
+        n0 = pre[1] - pre[0]
+        ok = bool(torch.equal(out[:n0].to(device), d.local.flatten_device()))
+    del out
+    torch.cuda.empty_cache()
+    moved = sum(per_rank)
+    return {"ms": round(ms, 4), "bytes_total": pre[-1] * 4, "bytes_over_nvlink": moved,
+            "bytes_over_nvlink_per_rank": per_rank, "gbs_into_root": round(moved / (ms * 1e-3) / 1e9, 1),
+            "root_slice_ok": ok, "method": f"fallback: {d.last_method} (local K-flatten + point-to-point)",
+            "peer_topology": "unavailable", "fallback_reason": why}
 
 
 def _between_legs(gg):

@@ -25,8 +25,13 @@ with the gloo backend and the oracle array (tests/test_multigpu_gloo.py).
 from __future__ import annotations
 
 import ctypes as C
+import logging
+import os
+import socket
 
 import numpy as np
+
+log = logging.getLogger(__name__)
 
 _TORCH_DT = None
 
@@ -111,6 +116,71 @@ class DistributedGrowableArray:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = device
+        self._topo = None
+        self.last_method = None          # method the last gather / rebalance used
+        self.fallback_reason = None      # why it did not use peer stores (None = it did)
+
+    # ---- peer reachability (checked once, agreed by every rank)
+    def peer_topology(self) -> tuple:
+        """(ok, reason): can this group's kernels store straight into every other
+        rank's device memory (CUDA IPC + peer access)?  Every rank contributes
+        its host name, GPU UUID and which peer GPUs it can address
+        (``cudaDeviceCanAccessPeer``); the answer is the same on every rank.
+        ``GG_PEER=0`` forces the NCCL path (tests, A/B)."""
+        if self._topo is not None:
+            return self._topo
+        import torch
+        reason = None
+        if os.environ.get("GG_PEER", "1") == "0":
+            reason = "GG_PEER=0"
+        elif not self._peer_ok():
+            reason = "local array has no device flatten_to (host / oracle array)"
+        dev = None
+        uuid = None
+        vis = {}
+        if reason is None:
+            dev = self.device.index if self.device is not None and self.device.index is not None \
+                else torch.cuda.current_device()
+            for i in range(torch.cuda.device_count()):
+                vis[str(torch.cuda.get_device_properties(i).uuid)] = i
+            uuid = str(torch.cuda.get_device_properties(dev).uuid)
+        mine = (socket.gethostname(), uuid, reason)
+        every = [None] * self.world
+        self.dist.all_gather_object(every, mine, group=self.group)
+        if reason is None:
+            for r, (host, peer_uuid, peer_reason) in enumerate(every):
+                if peer_reason is not None:
+                    reason = f"rank {r}: {peer_reason}"
+                elif host != mine[0]:
+                    reason = f"rank {r} on another host ({host}): CUDA IPC is intra-node"
+                elif peer_uuid != uuid:
+                    j = vis.get(peer_uuid)
+                    if j is None:
+                        reason = f"rank {r}'s GPU {peer_uuid} is not visible to rank {self.rank}"
+                    elif not torch.cuda.can_device_access_peer(dev, j):
+                        reason = f"cudaDeviceCanAccessPeer({dev}, {j}) = 0"
+                if reason is not None:
+                    break
+        verdicts = [None] * self.world
+        self.dist.all_gather_object(verdicts, reason, group=self.group)
+        bad = [v for v in verdicts if v is not None]
+        self._topo = (not bad, bad[0] if bad else None)
+        return self._topo
+
+    def _choose(self, method: str) -> str:
+        """Resolve "auto" / "peer" against the topology; a peer request that
+        cannot be honoured falls back to NCCL with a logged reason."""
+        if method in ("auto", "peer"):
+            ok, why = self.peer_topology()
+            if ok:
+                self.last_method, self.fallback_reason = "peer", None
+                return "peer"
+            if method == "peer" or self._peer_ok():
+                log.warning("GGArray peer-store gather unavailable (%s); using NCCL", why)
+            self.last_method, self.fallback_reason = "nccl", why
+            return "nccl"
+        self.last_method, self.fallback_reason = method, None
+        return method
 
     # ---- directory (the one collective on the data path)
     def global_prefix(self) -> list:
@@ -172,9 +242,7 @@ class DistributedGrowableArray:
         ``method``: "peer" (fused flatten into the root's buffer over CUDA
         IPC), "nccl" (local flatten + point-to-point), "auto" = peer for
         device arrays."""
-        if method == "auto":
-            method = "peer" if self._peer_ok() else "nccl"
-        if method == "peer":
+        if self._choose(method) == "peer":
             return self._flatten_global_peer(root)
         return self._flatten_global_p2p(root)
 
@@ -189,7 +257,9 @@ class DistributedGrowableArray:
     def all_gather_flat_peer(self):
         """Every rank receives the whole flattened array: each rank's K-flatten
         stores its slice into EVERY rank's buffer (one fused flatten per
-        destination, over CUDA IPC)."""
+        destination, over CUDA IPC).  Without peer access: allgather_flat."""
+        if self._choose("peer") != "peer":
+            return self.allgather_flat()
         p = self.global_prefix()
         esz = np.dtype(self.local.dtype).itemsize
         buf = PeerBuffer(p[-1], self.local.dtype)
@@ -212,9 +282,14 @@ class DistributedGrowableArray:
         [r*q, min((r+1)*q, N)), q = ceil(N / G).  Each rank flattens the pieces
         of its committed range straight into the owning ranks' buffers
         (gg_flatten_range into CUDA-IPC mapped peer memory): the rebalance is
-        the flatten, with no staging copy and no collective on the data path."""
+        the flatten, with no staging copy and no collective on the data path.
+        Without peer access: allgather_flat, then this rank's slice."""
         p = self.global_prefix()
         n, G, me = p[-1], self.world, self.rank
+        if self._choose("peer") != "peer":
+            q = -(-n // G) if n else 0
+            lo, hi = min(me * q, n), min((me + 1) * q, n)
+            return self.allgather_flat()[lo:hi].clone(), (lo, hi)
         q = -(-n // G) if n else 0
         lo = [min(r * q, n) for r in range(G)]
         hi = [min((r + 1) * q, n) for r in range(G)]
@@ -235,10 +310,21 @@ class DistributedGrowableArray:
                 m.close()
         return buf.tensor(self.device), (lo[me], hi[me])
 
+    def _host_staged(self) -> bool:
+        return self.dist.get_backend(self.group) == "gloo"
+
     def _flatten_global_p2p(self, root: int):
         import torch
         p = self.global_prefix()
         mine = self._local_flat()
+        if self._host_staged() and mine.is_cuda:
+            dev = mine.device
+            out = self._flatten_global_p2p_tensor(root, p, mine.cpu())
+            return None if out is None else out.to(dev)
+        return self._flatten_global_p2p_tensor(root, p, mine)
+
+    def _flatten_global_p2p_tensor(self, root: int, p: list, mine):
+        import torch
         if self.rank == root:
             out = torch.empty(p[-1], dtype=mine.dtype, device=mine.device)
             out[p[self.rank]:p[self.rank + 1]] = mine
@@ -258,12 +344,15 @@ class DistributedGrowableArray:
         import torch
         p = self.global_prefix()
         mine = self._local_flat()
+        dev = mine.device
+        if self._host_staged() and mine.is_cuda:
+            mine = mine.cpu()
         n_max = max(p[r + 1] - p[r] for r in range(self.world))
         buf = torch.zeros(n_max, dtype=mine.dtype, device=mine.device)
         buf[:mine.numel()] = mine
         parts = [torch.empty_like(buf) for _ in range(self.world)]
         self.dist.all_gather(parts, buf, group=self.group)
-        return torch.cat([parts[r][:p[r + 1] - p[r]] for r in range(self.world)])
+        return torch.cat([parts[r][:p[r + 1] - p[r]] for r in range(self.world)]).to(dev)
 
 
 class PeerGather:

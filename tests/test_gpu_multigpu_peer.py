@@ -52,6 +52,7 @@ def _worker(rank, world, port, q):
         a.rw_add(rank + 1)
         d = DistributedGrowableArray(a, device=torch.device("cuda", 0))
         flat = d.flatten_global(root=0, method="peer")
+        assert d.peer_topology() == (True, None) and d.last_method == "peer"   # same GPU: reachable
         allg = d.all_gather_flat_peer()
         reb, rng_ = d.rebalance_flat_peer()
         part = a.flatten_range(3, max(3, a.committed_size - 5)).cpu().numpy()

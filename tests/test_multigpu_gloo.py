@@ -50,9 +50,39 @@ def _worker(rank, world, port, q):
         if probes:
             d.set_global(probes[-1], -7, pre)
             got.append(int(d.get_global(probes[-1], pre)))
-        q.put((rank, pre, None if flat is None else flat.numpy(), allg, loc, got))
+        # a device-capable local whose peer stores are unavailable: the "peer"
+        # request must fall back to NCCL-style point-to-point with the reason
+        os.environ["GG_PEER"] = "0"
+        fake = _PeerlessLocal(local)
+        d2 = DistributedGrowableArray(fake)
+        flat2 = d2.flatten_global(root=0, method="peer")
+        reb, (rlo, rhi) = d2.rebalance_flat_peer()
+        fb = (d2.last_method, d2.fallback_reason, d2.peer_topology(),
+              None if flat2 is None else flat2.numpy(), reb.numpy(), rlo, rhi)
+        q.put((rank, pre, None if flat is None else flat.numpy(), allg, loc, got, fb))
     finally:
         dist.destroy_process_group()
+
+
+class _PeerlessLocal:
+    """An array that offers device flatten_to (so "auto" would pick peer
+    stores) on a group whose topology says no: flatten_to must never run."""
+
+    def __init__(self, inner):
+        self.inner = inner
+        self.dtype = inner.dtype
+
+    @property
+    def committed_size(self):
+        return self.inner.committed_size
+
+    def flatten(self):
+        return self.inner.flatten()
+
+    def flatten_to(self, ptr):
+        raise AssertionError("peer store attempted without peer access")
+
+    flatten_range_to = flatten_to
 
 
 def _single_array_reference():
@@ -84,8 +114,8 @@ def test_two_rank_directory_and_gather():
         p.start()
     res = {}
     for _ in range(2):
-        rank, pre, flat, allg, loc, got = q.get(timeout=120)
-        res[rank] = (pre, flat, allg, loc, got)
+        rank, pre, flat, allg, loc, got, fb = q.get(timeout=120)
+        res[rank] = (pre, flat, allg, loc, got, fb)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -97,3 +127,10 @@ def test_two_rank_directory_and_gather():
     assert res[0][3] == (1, want_pre[2] - want_pre[1] - 1)
     probes = [int(want[0]), int(want[want_pre[1]]), int(want[-1]), -7]      # distributed get/set_global
     assert res[0][4] == res[1][4] == probes
+    want2 = want.copy()
+    want2[-1] = -7                                     # the set_global above
+    for r in (0, 1):                                   # peer request fell back, with the reason
+        method, why, topo, flat2, reb, lo, hi = res[r][5]
+        assert method == "nccl" and why == "GG_PEER=0" and topo == (False, "GG_PEER=0")
+        assert reb.tobytes() == want2[lo:hi].tobytes()
+    assert np.array_equal(res[0][5][3], want2) and res[1][5][3] is None
