@@ -172,8 +172,9 @@ leg("static insert, one atomicAdd per element, 2^24 (paper 3-B)", 8 * NI, NI, "k
 st.insert_batch(st_src[:NI], algo="atomic")
 leg("static insert, one atomicAdd per warp, 2^26", 8 * (1 << 26), 1 << 26, "k_flat_insert")
 st.insert_batch(st_src[:1 << 26], algo="warp")
-leg("static insert, one atomicAdd per 32 KiB tile, 2^29", 8 * (1 << 29), 1 << 29, "k_flat_insert_block")
-st.insert_batch(st_src[:(1 << 29) - NI - (1 << 26)], algo="block")
+NB = (1 << 29) - NI - (1 << 26)
+leg(f"static insert, one atomicAdd per 32 KiB tile, {NB} elements", 8 * NB, NB, "k_flat_insert_block")
+st.insert_batch(st_src[:NB], algo="block")
 st2 = gg.StaticArray(1 << 30, dtype=np.int32)
 leg("static insert_batch (one reservation, k_flat_append), 2^29", 8 * (1 << 29), 1 << 29, "k_flat_append")
 st2.insert_batch(st_src)
@@ -185,6 +186,7 @@ leg("memMap insert_batch 2^29 (k_flat_append)", 8 * (1 << 29), 1 << 29, "k_flat_
 ct.insert_batch(st_src)
 leg("capture with an odd number of fused walks (k_copy_db restores the buffer parity)", 0, 0, "k_copy_db")
 g = b.capture(lambda: b.insert_duplicate())
+g.replay()
 leg("end", 0, 0, "")
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()

@@ -119,3 +119,30 @@ with open(os.path.join(P, f"{tag}_all_kernels.md"), "w") as fh:
                      f"{l['us']} | {l['dram_bytes']} | {l['dram_pct_peak']} | {l['l2_atomic_requests']} | "
                      f"{l['l2_red_requests']} |\n")
 print(json.dumps({"kernels_seen": kernels, "legs": len(rows)}, indent=1))
+
+# --set full captures of the non-uniform paths (prof_paths_raw.csv), if present
+fp = os.path.join(src, "prof_paths_raw.csv")
+if os.path.exists(fp):
+    raw = list(csv.reader(open(fp)))
+    h, units = raw[0], dict(zip(raw[0], raw[1]))
+    want = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM read"),
+            ("dram__bytes_write.sum", "DRAM write"),
+            ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+            ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+            ("launch__registers_per_thread", "regs"),
+            ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "long-scoreboard warps per issue"),
+            ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "barrier warps per issue"),
+            ("lts__t_sector_hit_rate.pct", "L2 hit %"), ("launch__grid_size", "grid")]
+    full = []
+    for row in raw[2:]:
+        d = dict(zip(h, row))
+        full.append({"kernel": short(d["Kernel Name"]),
+                     **{lab: f"{d.get(k, '')} {units.get(k, '')}".strip() for k, lab in want}})
+    out["paths_full_capture"] = full
+    json.dump(out, open(os.path.join(P, f"{tag}_all_kernels.json"), "w"), indent=1)
+    with open(os.path.join(P, f"{tag}_all_kernels.md"), "a") as fh:
+        fh.write("\n## `ncu --set full` of the non-uniform paths (tools/prof_all.py, "
+                 "kernels k_walk_shard / k_lanes_scatter / k_push_if / k_flat_insert_block / k_flat_append / k_gather)\n\n")
+        fh.write("| kernel | " + " | ".join(l for _, l in want) + " |\n|" + "---|" * (len(want) + 1) + "\n")
+        for e in full:
+            fh.write(f"| `{e['kernel'][:60]}` | " + " | ".join(e[l] for _, l in want) + " |\n")
