@@ -13,6 +13,7 @@
  *   gg::warp_push_back_n<T, K>(v, shard, count, vals); // per-lane counts, one per warp
  *   gg::warp_push_back_mask<T, K>(v, shard, mask, vals);        // K candidates, bitmask
  *   gg::block_push_back_mask<BLOCK, T, K>(v, shard, mask, vals, scratch);
+ *   gg::block_push_back_staged<BLOCK, T, K>(v, shard, mask, vals, scratch, stage); // 16 B stores
  *   gg::block_push_back<BLOCK>(v, shard, count, vals, scratch);  // one per block
  *
  * Device code cannot map memory, so the host backs the slots a launch may
@@ -341,6 +342,101 @@ __device__ inline uint64_t block_push_back_mask(const gg_device_view &t, uint32_
         locate(start + excl + r, t.log2fb, b, o);
         if (bptr_m[b]) store_cg(reinterpret_cast<T *>(bptr_m[b]) + o, vals[j]);
         ++r;
+      }
+    }
+  }
+  __syncthreads();
+  return start;
+}
+
+// Block flavour of the mask variant with the appends leaving as whole
+// vectors: after the block scan and the ONE atomicAdd, every thread writes
+// its kept values into the shared `stage` (thread order, shifted so that the
+// run is congruent with its destination mod 16 B), then the block stores the
+// run [start, start + total) with aligned 16 B vector stores through the
+// bucket slots (element stores at the run's ends, or everywhere when a
+// bucket holds less than 16 B).  stage: BLOCK*K + 32/sizeof(T) elements of
+// shared memory, scratch: 34 u64; all BLOCK threads must call it.
+template <int BLOCK, typename T, int K>
+__device__ inline uint64_t block_push_back_staged(const gg_device_view &t, uint32_t s, uint32_t mask,
+                                                  const T (&vals)[K], unsigned long long *scratch, T *stage) {
+  static_assert(BLOCK % 32 == 0 && BLOCK <= 1024, "BLOCK must be a multiple of 32, <= 1024");
+  static_assert(16 % sizeof(T) == 0, "element size must divide 16 B");
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, count = __popc(mask);
+  uint32_t x = count;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long w = lane < BLOCK / 32 ? scratch[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= (uint32_t)d) w += y;
+    }
+    const unsigned long long total = __shfl_sync(0xffffffffu, w, 31);
+    scratch[lane] = w;
+    unsigned long long start = 0;
+    int ok = 1;
+    if (lane == 0 && total) {
+      start = atomicAdd((unsigned long long *)&t.size[s], total);
+      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+      ok = ensure_buckets(t, s, start, total);
+    }
+    if (lane == 0) { scratch[32] = start; scratch[33] = ok; }
+  }
+  __syncthreads();
+  const unsigned long long total = scratch[BLOCK / 32 - 1];
+  const unsigned long long start = scratch[32];
+  const bool ok = scratch[33] != 0;
+  const uint32_t excl = x - count + (wid ? (uint32_t)scratch[wid - 1] : 0u);
+  __shared__ char *bptr_s[64];
+  const uint32_t esz_log = sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : sizeof(T) == 4 ? 2 : 3;
+  const bool vec = t.log2fb + esz_log >= 4;               // every bucket is whole 16 B vectors
+  const uint32_t shift = vec ? (uint32_t)(start % VE) : 0u;
+  if (ok && total) {
+    uint32_t b0, b1;
+    uint64_t o;
+    locate(start, t.log2fb, b0, o);
+    locate(start + total - 1, t.log2fb, b1, o);
+    if (tid <= b1 - b0) bptr_s[b0 + tid] = bucket_acquire(t, s, b0 + tid);
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if ((mask >> j) & 1u) stage[shift + excl + r++] = vals[j];
+  }
+  __syncthreads();
+  if (ok && total) {
+    if (vec) {
+      const uint32_t nv = (uint32_t)((shift + total + VE - 1) / VE);
+      for (uint32_t v = tid; v < nv; v += BLOCK) {
+        uint32_t b;
+        uint64_t o;
+        locate(start - shift + (uint64_t)v * VE, t.log2fb, b, o);
+        char *base = bptr_s[b];
+        if (!base) continue;
+        T *dp = reinterpret_cast<T *>(base) + o;
+        const uint32_t k0 = v * VE;
+        if (k0 >= shift && k0 + VE <= shift + total) {
+          const uint4 q = reinterpret_cast<const uint4 *>(stage)[v];
+          asm volatile("st.global.cg.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dp), "r"(q.x), "r"(q.y), "r"(q.z),
+                       "r"(q.w) : "memory");
+        } else {
+          for (uint32_t j = 0; j < VE; ++j)
+            if (k0 + j >= shift && k0 + j < shift + total) store_cg(dp + j, stage[k0 + j]);
+        }
+      }
+    } else {
+      for (uint32_t k = tid; k < total; k += BLOCK) {
+        uint32_t b;
+        uint64_t o;
+        locate(start + k, t.log2fb, b, o);
+        if (bptr_s[b]) store_cg(reinterpret_cast<T *>(bptr_s[b]) + o, stage[k]);
       }
     }
   }

@@ -1480,8 +1480,35 @@ __global__ void __launch_bounds__(256) k_lanes_reserve(Tables t, const uint32_t 
   for (uint32_t j = tid; j < nts; j += blockDim.x) tiles[first + j].base += start;
 }
 
-// lane j's KB bytes of values (KB = K * ESZ, a power of two in [4, 64]) into
-// words w[r * KB / 4 ...] of the thread's register block
+// One tile of the lanes insert.  Every thread holds 64 B of values in
+// registers: R rows of GL consecutive lanes (GL = 16 / KB lanes share one
+// 16 B vector when a lane's values are narrower than 16 B, else GL = 1 and
+// a lane is KB / 16 vectors), so counts and values move as 16 B (or 8 B)
+// loads; consecutive threads hold consecutive groups (coalesced).  Warp
+// scans of the per-row group totals (several rows packed into one 32-bit
+// scan, 8- or 16-bit fields) give every group's offset in its warp's run;
+// the whole run is staged in the warp's shared buffer congruent with its
+// destination and leaves as aligned 16 B vector stores.  Lanes outside the
+// valid range [vlo, vhi) count 0 (tiles start at a GL-aligned lane so the
+// groups are aligned; only the edge groups take per-lane loads).  One
+// __syncthreads per tile (the warps' totals, double-buffered by `par`).
+template <int ESZ, int KB, bool VEC = true>
+struct LaneShape {
+  static constexpr uint32_t K = KB / ESZ, GL = (VEC && KB < 16) ? 16 / KB : 1, R = 64 / (KB * GL),
+                            T = 256 * GL * R, VE = 16 / ESZ, WPR = GL * KB / 4;   // words per row
+};
+
+template <int ESZ, int KB, bool VEC = true>
+struct LaneSmem {
+  typedef typename ElemT<ESZ>::T E;
+  typedef LaneShape<ESZ, KB, VEC> L;
+  __align__(16) E stage[8][32 * L::R * L::GL * L::K + 2 * L::VE];
+  uint32_t wsum[2][8];
+  char *scb[kMaxBuckets];
+  unsigned long long base;
+};
+
+// lane j's KB bytes of values into w[0 .. KB/4) (KB a power of two in [4, 64])
 template <int KB>
 __device__ __forceinline__ void lane_load(uint32_t *w, const char *p) {
   if constexpr (KB >= 16) {
@@ -1498,42 +1525,51 @@ __device__ __forceinline__ void lane_load(uint32_t *w, const char *p) {
   }
 }
 
-// k_lanes_scatter: lane per thread.  A tile is 8 warps x R rows of 32 lanes
-// (R = 64 / KB, so every thread holds 64 B of values in registers); each
-// thread loads its lanes' counts and values (coalesced: consecutive lanes
-// are consecutive in memory).  Warp-scans of the counts (several rows packed
-// into one 32-bit scan, 8- or 16-bit fields) give every lane's offset in the
-// warp's run; the whole run is staged in the warp's shared buffer congruent
-// with its destination and leaves as aligned 16 B vector stores.  One
-// __syncthreads per tile (the warps' totals).
-template <int ESZ, int KB>
-__global__ void __launch_bounds__(256) k_lanes_scatter(Tables t, const char *vals, const uint32_t *counts,
-                                                       const LaneTile *tiles) {
-  typedef typename ElemT<ESZ>::T E;
-  constexpr uint32_t K = KB / ESZ, R = 64 / KB, VE = 16 / ESZ;
-  constexpr uint32_t FW = (32 * K < 256) ? 8 : 16, PF = 32 / FW, FM = (1u << FW) - 1;
-  __shared__ __align__(16) E stage_sm[8][32 * R * K + 2 * VE];
-  __shared__ uint32_t wsum[8];
-  __shared__ char *scb[kMaxBuckets];
-  pdl_begin();
-  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const LaneTile lt = tiles[blockIdx.x];
-  const uint32_t s = lt.shard, nl = lt.nl;
-  const uint64_t lo = lt.lane_lo;
-  const uint32_t wl0 = wid * R * 32;
-  uint32_t c[R];
-  uint32_t w[16];
+template <int ESZ, int KB, bool VEC = true>
+__device__ __forceinline__ void lanes_load(const char *vals, const uint32_t *counts, uint64_t wlo, uint64_t vlo,
+                                           uint64_t vhi,
+                                           uint32_t (&c)[LaneShape<ESZ, KB, VEC>::R][LaneShape<ESZ, KB, VEC>::GL],
+                                           uint32_t (&w)[16]) {
+  typedef LaneShape<ESZ, KB, VEC> L;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
-  for (uint32_t r = 0; r < R; ++r) {
-    const uint32_t j = wl0 + r * 32 + lane;
-    c[r] = 0;
-    if (j < nl) {
-      c[r] = min(__ldcs(counts + lo + j), K);
-      lane_load<KB>(w + r * (KB / 4), vals + (lo + j) * KB);
+  for (uint32_t r = 0; r < L::R; ++r) {
+    const uint64_t g0 = wlo + ((uint64_t)(wid * L::R + r) * 32 + lane) * L::GL;
+    uint32_t *wr = w + r * L::WPR;
+    if (g0 >= vlo && g0 + L::GL <= vhi && (L::GL == 1 || g0 % L::GL == 0)) {
+      if constexpr (L::GL == 4) {
+        const uint4 x = __ldcs((const uint4 *)(counts + g0));
+        c[r][0] = min(x.x, L::K); c[r][1] = min(x.y, L::K); c[r][2] = min(x.z, L::K); c[r][3] = min(x.w, L::K);
+      } else if constexpr (L::GL == 2) {
+        const uint2 x = __ldcs((const uint2 *)(counts + g0));
+        c[r][0] = min(x.x, L::K); c[r][1] = min(x.y, L::K);
+      } else {
+        c[r][0] = min(__ldcs(counts + g0), L::K);
+      }
+      lane_load<L::GL * KB>(wr, vals + g0 * KB);
+    } else {
+#pragma unroll
+      for (uint32_t g = 0; g < L::GL; ++g) {
+        c[r][g] = 0;
+        if (g0 + g >= vlo && g0 + g < vhi) {
+          c[r][g] = min(__ldcs(counts + g0 + g), L::K);
+          lane_load<KB>(wr + g * (KB / 4), vals + (g0 + g) * KB);
+        }
+      }
     }
   }
-  stage_cbase(t, scb);
-  // lane offsets in the warp's run: packed row scans
+}
+
+// scans + staging + stores of a loaded tile; returns the tile total
+template <int ESZ, int KB, bool VEC = true>
+__device__ __forceinline__ uint32_t lanes_store(const Tables &t, LaneSmem<ESZ, KB, VEC> &sm, uint32_t s,
+                                                const uint32_t (&c)[LaneShape<ESZ, KB, VEC>::R][LaneShape<ESZ, KB, VEC>::GL],
+                                                const uint32_t (&w)[16], uint64_t base, int par) {
+  typedef typename ElemT<ESZ>::T E;
+  typedef LaneShape<ESZ, KB, VEC> L;
+  constexpr uint32_t R = L::R, GL = L::GL, K = L::K, VE = L::VE;
+  constexpr uint32_t FW = (32 * GL * K < 256) ? 8 : 16, PF = 32 / FW, FM = (1u << FW) - 1;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t ex[R];
   uint32_t carry = 0;
 #pragma unroll
@@ -1541,7 +1577,12 @@ __global__ void __launch_bounds__(256) k_lanes_scatter(Tables t, const char *val
     uint32_t x = 0;
 #pragma unroll
     for (uint32_t f = 0; f < PF; ++f)
-      if (r0 + f < R) x |= c[r0 + f] << (f * FW);
+      if (r0 + f < R) {
+        uint32_t cr = 0;
+#pragma unroll
+        for (uint32_t g = 0; g < GL; ++g) cr += c[r0 + f][g];
+        x |= cr << (f * FW);
+      }
     const uint32_t v = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1558,48 +1599,226 @@ __global__ void __launch_bounds__(256) k_lanes_scatter(Tables t, const char *val
       }
     }
   }
-  if (lane == 0) wsum[wid] = carry;
+  if (lane == 0) sm.wsum[par][wid] = carry;
   __syncthreads();
-  uint32_t woff = 0;
+  uint32_t woff = 0, total = 0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
-    if (q < (int)wid) woff += wsum[q];
-  const uint32_t run = carry;
-  if (!run) return;
-  const uint64_t rb = lt.base + woff;           // destination index of the warp's run
-  E *st = stage_sm[wid];
-  const uint32_t lg0 = t.log2fb + (ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3);
-  const bool vec = (1u << lg0) >= 16;           // 16 B vectors never straddle a bucket
-  const uint32_t shift = vec ? (uint32_t)(rb % VE) : 0u;
-#pragma unroll
-  for (uint32_t r = 0; r < R; ++r) {
-    const E *ev = (const E *)(w + r * (KB / 4));
-#pragma unroll
-    for (uint32_t k = 0; k < K; ++k)
-      if (k < c[r]) st[shift + ex[r] + k] = ev[k];
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t x = sm.wsum[par][q];
+    if (q < (int)wid) woff += x;
+    total += x;
   }
-  __syncwarp();
-  if (vec) {
-    const uint32_t nv = (shift + run + VE - 1) / VE;
-    for (uint32_t v = lane; v < nv; v += 32) {
-      uint32_t b; uint64_t o;
-      locate(rb - shift + (uint64_t)v * VE, t.log2fb, b, o);
-      E *dp = (E *)(slot_addr(scb, s, b, lg0) + o * ESZ);
-      const uint32_t k0 = v * VE;
-      if (k0 >= shift && k0 + VE <= shift + run) {
-        stg((uint4 *)dp, ((const uint4 *)st)[v]);
-      } else {
+  const uint32_t run = carry;
+  if (run) {
+    const uint64_t rb = base + woff;              // destination index of the warp's run
+    E *st = sm.stage[wid];
+    const uint32_t lg0 = t.log2fb + (ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3);
+    const bool vec = (1u << lg0) >= 16;           // 16 B vectors never straddle a bucket
+    const uint32_t shift = vec ? (uint32_t)(rb % VE) : 0u;
 #pragma unroll
-        for (uint32_t j = 0; j < VE; ++j)
-          if (k0 + j >= shift && k0 + j < shift + run) dp[j] = st[k0 + j];
+    for (uint32_t r = 0; r < R; ++r) {
+      const E *ev = (const E *)(w + r * L::WPR);
+      uint32_t o = shift + ex[r];
+#pragma unroll
+      for (uint32_t g = 0; g < GL; ++g) {
+#pragma unroll
+        for (uint32_t k = 0; k < K; ++k)
+          if (k < c[r][g]) st[o + k] = ev[g * K + k];
+        o += c[r][g];
       }
     }
-  } else {
-    for (uint32_t k = lane; k < run; k += 32) {
-      uint32_t b; uint64_t o;
-      locate(rb + k, t.log2fb, b, o);
-      ((E *)(slot_addr(scb, s, b, lg0)))[o] = st[k];
+    __syncwarp();
+    if (vec) {
+      const uint32_t nv = (shift + run + VE - 1) / VE;
+      for (uint32_t v = lane; v < nv; v += 32) {
+        uint32_t b; uint64_t o;
+        locate(rb - shift + (uint64_t)v * VE, t.log2fb, b, o);
+        E *dp = (E *)(slot_addr(sm.scb, s, b, lg0) + o * ESZ);
+        const uint32_t k0 = v * VE;
+        if (k0 >= shift && k0 + VE <= shift + run) {
+          stg((uint4 *)dp, ((const uint4 *)st)[v]);
+        } else {
+#pragma unroll
+          for (uint32_t j = 0; j < VE; ++j)
+            if (k0 + j >= shift && k0 + j < shift + run) dp[j] = st[k0 + j];
+        }
+      }
+    } else {
+      for (uint32_t k = lane; k < run; k += 32) {
+        uint32_t b; uint64_t o;
+        locate(rb + k, t.log2fb, b, o);
+        ((E *)(slot_addr(sm.scb, s, b, lg0)))[o] = st[k];
+      }
     }
+    __syncwarp();                                 // the stage buffer is reused by the next tile
+  }
+  return total;
+}
+
+// the batch's reservation (ONE atomicAdd on the LFVector size,
+// insert_index.py:118-143) and the publication of the buckets [start, end)
+// covers (paper Alg. 2; the host backed the slots for the upper bound)
+__device__ __forceinline__ void lanes_reserve_publish(const Tables &t, uint32_t s, uint64_t start,
+                                                      uint64_t total) {
+  if (total) {
+    atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)total);
+    t.ops[s] += 1;
+    uint32_t b0, b1; uint64_t o;
+    locate(start, t.log2fb, b0, o);
+    locate(start + total - 1, t.log2fb, b1, o);
+    const unsigned long long pm = t.pmask[s];
+    const unsigned long long want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull) & ~pm;
+    uint64_t add = 0;
+    const uint32_t lg0 = t.log2fb + (31u - __clz(t.esz));
+    for (unsigned long long mm = want; mm; mm &= mm - 1) {
+      const uint32_t b = __ffsll((long long)mm) - 1;
+      t.ptr[(size_t)s * t.MB + b] = t.cbase[b] + ((uint64_t)s << max(lg0 + b, 4u));
+      t.flag[(size_t)s * t.MB + b] = kFlagPublished;
+      add += 1ull << (t.log2fb + b);
+    }
+    if (want) {
+      t.pmask[s] = pm | want;
+      t.cap[s] += add;
+      atomicAdd(&t.misc[MISC_ALLOCS], (unsigned long long)__popcll(want));
+    }
+  }
+  t.start[s] = start;
+  t.count[s] = total;
+}
+
+// k_lanes_scatter: the 3-pass path's last pass, one tile per CTA at the
+// destination k_lanes_reserve computed (GG_LANES_CHAIN=0, A/B)
+template <int ESZ, int KB>
+__global__ void __launch_bounds__(256) k_lanes_scatter(Tables t, const char *vals, const uint32_t *counts,
+                                                       const LaneTile *tiles) {
+  __shared__ LaneSmem<ESZ, KB> sm;
+  pdl_begin();
+  const LaneTile lt = tiles[blockIdx.x];
+  uint32_t c[LaneShape<ESZ, KB>::R][LaneShape<ESZ, KB>::GL], w[16];
+  lanes_load<ESZ, KB>(vals, counts, lt.lane_lo, lt.lane_lo, lt.lane_lo + lt.nl, c, w);
+  stage_cbase(t, sm.scb);
+  lanes_store<ESZ, KB>(t, sm, lt.shard, c, w, lt.base, 0);
+}
+
+// ---- paper Alg. 1 in ONE pass over HBM: the chunked lanes insert ----------
+// The lanes of shard s are cut into chunks of C lanes (a multiple of the
+// tile) that never cross a shard; cpre[s] = first chunk of shard s.  A CTA
+// per chunk:
+//   1. sums the chunk's counts (16 B loads, many in flight; the chunk's
+//      counts -- 64 KiB -- stay in L2 for step 3, so HBM sees them once);
+//   2. chains the chunk sums of its shard with a decoupled look-back: the
+//      first chunk reads the LFVector size (the batch's start) and publishes
+//      start + its sum as an INCLUSIVE prefix, every other chunk publishes
+//      its sum as an AGGREGATE at once and warp 0 looks back over its
+//      shard's predecessors (32 status words per step) to an inclusive
+//      prefix, then publishes its own; chunks are CTA indices, dispatched in
+//      order, so every chunk waited on is already running;
+//   3. walks its tiles in order (register-resident values, warp runs staged
+//      in shared memory, 16 B vector stores) from that destination;
+//   4. the last chunk of the shard holds start + total: it makes the
+//      batch's reservation -- ONE atomicAdd on the LFVector size -- and
+//      publishes the buckets (tiles write through slot arithmetic, which
+//      does not depend on the publication).
+// Status word: flag in bits 62-63 (1 = aggregate, 2 = inclusive), value below.
+constexpr uint32_t kLanesChunk = 16384;     // lanes per chunk: 64 KiB of counts (L2-resident between steps 1 and 3)
+constexpr unsigned long long kChainA = 1ull << 62, kChainP = 2ull << 62, kChainV = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_chain(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_chain(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// sum of min(counts[lo + j], K) over j < n, by the whole CTA (result in every thread)
+__device__ __forceinline__ uint32_t chunk_count_sum(const uint32_t *counts, uint64_t lo, uint32_t n, uint32_t K,
+                                                    uint32_t *red) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t acc = 0;
+  const uint32_t head = (uint32_t)min((uint64_t)n, (uint64_t)((4 - (lo & 3)) & 3));
+  if (tid < head) acc += min(__ldcs(counts + lo + tid), K);
+  const uint32_t nv = (n - head) >> 2;
+  const uint4 *cv = (const uint4 *)(counts + lo + head);
+#pragma unroll 4
+  for (uint32_t v = tid; v < nv; v += 256) {
+    const uint4 x = __ldcg(cv + v);               // kept in L2 for the tile walk
+    acc += min(x.x, K) + min(x.y, K) + min(x.z, K) + min(x.w, K);
+  }
+  for (uint32_t j = head + 4 * nv + tid; j < n; j += 256) acc += min(__ldcs(counts + lo + j), K);
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  uint32_t tot = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tot += red[q];
+  return tot;
+}
+
+template <int ESZ, int KB, bool VEC = true>
+__global__ void __launch_bounds__(256) k_lanes_chunk(Tables t, const char *vals, const uint32_t *counts,
+                                                     const uint32_t *cpre, unsigned long long *chain,
+                                                     uint32_t C) {
+  typedef LaneShape<ESZ, KB, VEC> L;
+  constexpr uint32_t K = L::K, T = L::T;
+  __shared__ LaneSmem<ESZ, KB, VEC> sm;
+  __shared__ uint32_t red[8];
+  pdl_begin();
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t chunk = blockIdx.x;
+  const uint32_t s = warp_find_u32(cpre, t.S, chunk);
+  const uint32_t first = cpre[s], last = cpre[s + 1] - 1;
+  const uint64_t lo = t.offsets[s] + (uint64_t)(chunk - first) * C;
+  const uint32_t nl = (uint32_t)min((uint64_t)C, t.offsets[s + 1] - lo);
+  stage_cbase(t, sm.scb);
+  const uint32_t agg = chunk_count_sum(counts, lo, nl, K, red);
+  if (wid == 0) {
+    unsigned long long excl = 0;
+    if (chunk == first) {
+      if (lane == 0) {
+        excl = t.size[s];                            // the batch's start (before any reservation)
+        st_chain(chain + chunk, kChainP | (excl + agg));
+      }
+      excl = __shfl_sync(0xffffffffu, excl, 0);
+    } else {
+      if (lane == 0) st_chain(chain + chunk, kChainA | agg);
+      int64_t j = (int64_t)chunk - 1;
+      for (;;) {
+        const int64_t idx = j - lane;
+        unsigned long long v;
+        do {                                         // wait until the window is published
+          v = idx >= (int64_t)first ? ld_chain(chain + idx) : kChainP;
+        } while (__any_sync(0xffffffffu, (v >> 62) == 0));
+        const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const uint32_t stop = pm ? (uint32_t)(__ffs(pm) - 1) : 31u;
+        unsigned long long x = lane <= stop ? (v & kChainV) : 0ull;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+        excl += x;
+        if (pm) break;
+        j -= 32;
+      }
+      if (lane == 0) st_chain(chain + chunk, kChainP | (excl + agg));
+    }
+    if (lane == 0) {
+      sm.base = excl;
+      if (chunk == last) {                           // the size the first chunk read: no other writer yet
+        const unsigned long long start = t.size[s];
+        lanes_reserve_publish(t, s, start, excl + agg - start);
+      }
+    }
+  }
+  __syncthreads();
+  uint64_t base = sm.base;
+  int par = 0;
+  // tiles from a GL-aligned lane: whole groups take the vector loads
+  const uint64_t wlo = lo - lo % L::GL;
+  for (uint64_t t0 = wlo; t0 < lo + nl; t0 += T) {
+    uint32_t c[L::R][L::GL], w[16];
+    lanes_load<ESZ, KB, VEC>(vals, counts, t0, lo, lo + nl, c, w);
+    base += lanes_store<ESZ, KB, VEC>(t, sm, s, c, w, base, par);
+    par ^= 1;
   }
 }
 

@@ -729,34 +729,64 @@ int check_committed_published(const gg_array *a) {
 
 namespace gg {
 // Example user kernel of the device API (paper Alg. 1): block b appends the
-// elements i of its slice with pred[i] != 0 to shard b % S, warp- or
-// block-aggregated.
-// Each thread gathers the candidates of K consecutive rounds of its block's
-// slices (coalesced loads; the value is loaded whatever the predicate, its
-// sector is read anyway at any useful density) into registers with a
-// K-bit keep mask, and appends them with one warp- or block-aggregated
-// push_back_mask: one reservation covers up to 32*K (warp) or BLOCK*K
-// (block) values, all indexing static (no local memory).
-template <int ESZ, int BLOCK, int K>
+// candidates i of its slices with pred[i] != 0 to shard b % S, warp- or
+// block-aggregated.  Slice = kPushSlice consecutive candidates: block b
+// takes slice b of every round of grid x kPushSlice candidates.  Each thread
+// loads G = 4 consecutive candidates per round (one 16 B / 8 B / 4 B vector
+// of values + 4 predicate bytes) for R rounds into registers with a
+// (G x R)-bit keep mask and appends them with ONE warp- or block-aggregated
+// reservation per call (block mode: the run is staged in shared memory and
+// leaves as 16 B vector stores); all indexing static (no local memory).
+constexpr uint32_t kPushG = 4, kPushSlice = 256 * kPushG;
+
+template <int ESZ, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char *vals,
-                                                   const uint8_t *pred, uint64_t n, int block_mode) {
+                                                   const uint8_t *pred, uint64_t n, int block_mode,
+                                                   int aligned) {
   typedef typename ElemT<ESZ>::T E;
+  constexpr uint32_t kPushR = ESZ == 8 ? 4 : 8;         // rounds per append call
+  constexpr int K = kPushG * kPushR;
   __shared__ unsigned long long scratch[34];
+  __shared__ __align__(16) E stage[BLOCK * K + 32 / ESZ];
   const uint32_t s = blockIdx.x % t.S;
-  const uint64_t round = (uint64_t)gridDim.x * BLOCK;
-  for (uint64_t r0 = 0; (uint64_t)blockIdx.x * BLOCK + r0 * round < n; r0 += K) {
+  const uint64_t round = (uint64_t)gridDim.x * kPushSlice;
+  for (uint64_t r0 = 0; (uint64_t)blockIdx.x * kPushSlice + r0 * round < n; r0 += kPushR) {
     E v[K];
     uint32_t mask = 0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const uint64_t i = (uint64_t)blockIdx.x * BLOCK + (r0 + j) * round + threadIdx.x;
-      v[j] = E(0);
-      if (i < n) {
-        v[j] = __ldcs(reinterpret_cast<const E *>(vals) + i);
-        mask |= (__ldcs(pred + i) ? 1u : 0u) << j;
+    for (int j = 0; j < (int)kPushR; ++j) {
+      const uint64_t i = (uint64_t)blockIdx.x * kPushSlice + (r0 + j) * round + threadIdx.x * kPushG;
+      if (aligned && i + kPushG <= n) {
+        const uint32_t p4 = __ldcs(reinterpret_cast<const uint32_t *>(pred + i));
+        if constexpr (ESZ * kPushG == 16) {
+          const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ));
+          memcpy(&v[j * kPushG], &q, 16);
+        } else if constexpr (ESZ * kPushG == 8) {
+          const uint2 q = __ldcs(reinterpret_cast<const uint2 *>(vals + i * ESZ));
+          memcpy(&v[j * kPushG], &q, 8);
+        } else if constexpr (ESZ * kPushG == 4) {
+          const uint32_t q = __ldcs(reinterpret_cast<const uint32_t *>(vals + i * ESZ));
+          memcpy(&v[j * kPushG], &q, 4);
+        } else {
+          const uint4 q0 = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ));
+          const uint4 q1 = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ) + 1);
+          memcpy(&v[j * kPushG], &q0, 16);
+          memcpy(&v[j * kPushG + 2], &q1, 16);
+        }
+#pragma unroll
+        for (int g = 0; g < (int)kPushG; ++g) mask |= ((p4 >> (8 * g)) & 0xffu ? 1u : 0u) << (j * kPushG + g);
+      } else {
+#pragma unroll
+        for (int g = 0; g < (int)kPushG; ++g) {
+          v[j * kPushG + g] = E(0);
+          if (i + g < n) {
+            v[j * kPushG + g] = __ldcs(reinterpret_cast<const E *>(vals) + i + g);
+            mask |= (__ldcs(pred + i + g) ? 1u : 0u) << (j * kPushG + g);
+          }
+        }
       }
     }
-    if (block_mode) block_push_back_mask<BLOCK, E, K>(t, s, mask, v, scratch);
+    if (block_mode) block_push_back_staged<BLOCK, E, K>(t, s, mask, v, scratch, stage);
     else warp_push_back_mask<E, K>(t, s, mask, v);
   }
 }
@@ -1452,16 +1482,21 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   int rc = push_cbase(a, st);
   if (rc) return rc;
   // tiles: 8 warps x (64 / KB) rows of 32 lanes (64 B of values per thread)
+  // one pass (default): chunks of C lanes, a CTA each; 3-pass A/B
+  // (GG_LANES_CHAIN=0): tiles of T lanes for k_lanes_sum / k_lanes_scatter
+  static const bool chain = [] { const char *e = getenv("GG_LANES_CHAIN"); return !e || e[0] != '0'; }();
   const uint32_t T = (uint32_t)(256 * (64 / KB));
+  const uint32_t unit = chain ? kLanesChunk : T;
   std::vector<uint32_t> tpre(S + 1);
   uint64_t nt = 0;
   for (uint32_t s = 0; s < S; ++s) {
     tpre[s] = (uint32_t)nt;
-    nt += (off[s + 1] - off[s] + T - 1) / T;
+    nt += (off[s + 1] - off[s] + unit - 1) / unit;
   }
   if (nt > 0x7fffffffu) return fail(GG_EVALUE, "too many lanes");
   tpre[S] = (uint32_t)nt;
-  // scratch: tpre[S+1] | tiles[nt] (grown on demand, stream ordered)
+  // scratch: tpre[S+1] | tiles[nt] (3-pass) or chain[nt] status words (one
+  // pass) (grown on demand, stream ordered)
   const size_t o_tiles = ((size_t)(S + 1) * 4 + 31) & ~size_t(31);
   if (!a->lanes_dmem || a->lanes_tiles_cap < nt) {
     if (a->lanes_dmem) CUDA_TRY(cudaFreeAsync(a->lanes_dmem, st));
@@ -1479,6 +1514,23 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   if (!a->h_lanes) CUDA_TRY(cudaMallocHost(&a->h_lanes, S * 8));
   if (!a->lanes_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->lanes_ev, cudaEventDisableTiming));
   Tables t = tables_for_launch(a, false);
+  if (chain) {
+    unsigned long long *d_chain = (unsigned long long *)(dm + o_tiles);
+    CUDA_TRY(cudaMemsetAsync(d_chain, 0, nt * sizeof(unsigned long long), st));
+    cudaError_t e = cudaSuccess;
+    const char *dv = (const char *)d_values;
+    const uint32_t *tp = (const uint32_t *)d_tpre;
+#define GG_CHAIN_CASE(ESZ_, KB_) \
+  case KB_: e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, kLanesChunk); break;
+    switch (a->esz) {
+      case 1: switch (KB) { GG_CHAIN_CASE(1, 4) GG_CHAIN_CASE(1, 8) GG_CHAIN_CASE(1, 16) GG_CHAIN_CASE(1, 32) GG_CHAIN_CASE(1, 64) } break;
+      case 2: switch (KB) { GG_CHAIN_CASE(2, 4) GG_CHAIN_CASE(2, 8) GG_CHAIN_CASE(2, 16) GG_CHAIN_CASE(2, 32) GG_CHAIN_CASE(2, 64) } break;
+      case 4: switch (KB) { GG_CHAIN_CASE(4, 4) GG_CHAIN_CASE(4, 8) GG_CHAIN_CASE(4, 16) GG_CHAIN_CASE(4, 32) GG_CHAIN_CASE(4, 64) } break;
+      default: switch (KB) { GG_CHAIN_CASE(8, 8) GG_CHAIN_CASE(8, 16) GG_CHAIN_CASE(8, 32) GG_CHAIN_CASE(8, 64) } break;
+    }
+#undef GG_CHAIN_CASE
+    CUDA_TRY(e);
+  } else {
   CUDA_TRY(launch_k(k_lanes_sum, (unsigned)((nt + 7) / 8), 256, 0, st, t, d_counts, (const uint32_t *)d_tpre,
                     d_tiles, (uint32_t)nt, T, (uint32_t)K));
   CUDA_TRY(launch_k(k_lanes_reserve, S, 256, 0, st, t, (const uint32_t *)d_tpre, d_tiles));
@@ -1495,6 +1547,7 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   }
 #undef GG_LANES_CASE
   CUDA_TRY(e);
+  }
   CUDA_TRY(cudaMemcpyAsync(a->h_lanes, a->t.size, S * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(a->lanes_ev, st));
   a->lanes_pend = true;
@@ -1816,32 +1869,34 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   cudaStream_t st = S_(stream);
   if (n == 0) return GG_OK;
   const uint32_t B = 256;
-  // default grid: ~8 resident CTAs per SM (each CTA then loops over many
-  // rounds and its push_back_n calls reserve up to 8 rounds at once), at
-  // least one CTA per shard
+  // default grid: ~6 resident CTAs per SM (each CTA then loops over many
+  // rounds and each append call reserves up to R rounds at once), at least
+  // one CTA per shard
   if (!grid)
     grid = (uint32_t)std::max<uint64_t>(
-        a->S, std::min<uint64_t>((n + B * 8 - 1) / (B * 8), (uint64_t)sm_count(a->dev) * 8));
+        a->S, std::min<uint64_t>((n + kPushSlice * 8 - 1) / (kPushSlice * 8),
+                                 (uint64_t)sm_count(a->dev) * 6));
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, st); if (frc_) return frc_; }
   // worst case: every candidate of shard s appended (block blk takes slice
-  // blk of every round of grid * B candidates)
+  // blk of every round of grid * kPushSlice candidates)
   std::vector<uint64_t> maxsz(a->S, 0);
-  const uint64_t per_round = (uint64_t)grid * B, full = n / per_round, rem = n % per_round;
+  const uint64_t per_round = (uint64_t)grid * kPushSlice, full = n / per_round, rem = n % per_round;
   for (uint32_t blk = 0; blk < grid; ++blk) {
-    const uint64_t lo = (uint64_t)blk * B;
-    maxsz[blk % a->S] += full * B + (rem > lo ? std::min<uint64_t>(B, rem - lo) : 0);
+    const uint64_t lo = (uint64_t)blk * kPushSlice;
+    maxsz[blk % a->S] += full * kPushSlice + (rem > lo ? std::min<uint64_t>(kPushSlice, rem - lo) : 0);
   }
   for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += a->size[s];
   gg_device_view v;
   int rc = view_prepare(a, maxsz.data(), st, false, &v);
   if (rc) return rc;
+  const int al = ((uintptr_t)d_vals % (kPushG * a->esz) == 0 && (uintptr_t)d_pred % kPushG == 0) ? 1 : 0;
   switch (a->esz) {
-    case 1: { k_push_if<1, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_push_if<2, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_push_if<4, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 8: { k_push_if<8, 256, 8><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 1: { k_push_if<1, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 2: { k_push_if<2, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 4: { k_push_if<4, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+    case 8: { k_push_if<8, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
   }
   CUDA_TRY(cudaGetLastError());
   return view_finish(a, h_status, st);

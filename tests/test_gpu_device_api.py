@@ -15,7 +15,7 @@ def gg():
     return gg
 
 
-def _expected(vals, pred, S, grid, B=256):
+def _expected(vals, pred, S, grid, B=1024):   # slice = 1024 candidates (kPushSlice)
     blk = (np.arange(len(vals)) // B) % grid
     shard = blk % S
     return [np.sort(vals[(shard == s) & pred]) for s in range(S)]
@@ -51,13 +51,13 @@ def test_push_if_multiset_and_layout(gg, mode, S, fb, grid):
 
 def test_block_order_within_a_block(gg):
     # with one block per shard and one round, block_push_back keeps thread order
-    S, n = 4, 4 * 256
+    S, n = 4, 4 * 1024
     vals = np.arange(n, dtype=np.int32)
     pred = (vals % 3) != 0
     a = gg.GrowableArray(S, 32, dtype=np.int32)
     a.push_if(vals, pred, mode="block", grid=4)
     for s in range(S):
-        sl = vals[s * 256:(s + 1) * 256]
+        sl = vals[s * 1024:(s + 1) * 1024]
         assert np.array_equal(a.shards[s].to_numpy(), sl[(sl % 3) != 0])
 
 

@@ -40,7 +40,7 @@ def test_device_push_back_random(S, fb, n, grid, dens, mode, seed):
     a.insert_parallel(pre)
     grid = max(grid, S)
     a.push_if(vals, pred, mode=mode, grid=grid)
-    blk = (np.arange(n) // 256) % grid
+    blk = (np.arange(n) // 1024) % grid           # slice = 1024 candidates (kPushSlice)
     st_ = a._parity_state()
     for s in range(S):
         got = a.shards[s].to_numpy()

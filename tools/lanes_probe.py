@@ -1,0 +1,74 @@
+"""insert_lanes (paper Alg. 1, per-lane counts) throughput and contents across
+K and element sizes at ~2^28 appended elements over 512 LFVectors; A/B of the
+one-pass chained kernel against the 3-pass path with GG_LANES_CHAIN=0.
+Algorithmic bytes = counts (4 B / lane) + the [lanes x K] value block + the
+compacted output.  Also a repetition check of the look-back (contents of
+every run compared) with PROBE_REPS."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2209_00103_b200 as gg
+
+S, FB = 512, 32
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6548.5) \
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6548.5
+dev = torch.device("cuda", 0)
+out = {"chain": os.environ.get("GG_LANES_CHAIN", "1"), "peak": PEAK}
+TD = {1: torch.int8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
+ND = {1: np.int8, 2: np.int16, 4: np.int32, 8: np.int64}
+
+
+def run(K, esz, target=1 << 28, reps=5, ragged=False):
+    L = max(S, (2 * target // K) // S * S) if K > 1 else target
+    g = torch.Generator(device=dev).manual_seed(K * 10 + esz)
+    cnt = torch.randint(0, K + 1, (L,), dtype=torch.int32, device=dev, generator=g)
+    vals = (torch.arange(L * K, device=dev) % 100003).to(TD[esz])
+    if ragged:
+        w = np.random.default_rng(K).integers(0, 3, S).astype(np.float64) + 0.01
+        per = np.floor(w / w.sum() * L).astype(np.int64)
+        per[-1] += L - per.sum()
+        lo = np.concatenate([[0], np.cumsum(per)]).astype(np.uint64)
+    else:
+        lo = np.arange(S + 1, dtype=np.uint64) * np.uint64(L // S)
+    tot = int(cnt.sum())
+    a = gg.GrowableArray(S, FB, dtype=ND[esz])
+    a.insert_lanes(vals, cnt, lo, K, commit=False)
+    best = 1e9
+    for _ in range(reps):
+        a.shrink(0, release=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        a.insert_lanes(vals, cnt, lo, K, commit=False)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    a.commit()
+    mask = torch.arange(K, device=dev)[None, :] < cnt[:, None]
+    ok = bool(torch.equal(a.flatten_device(), vals.view(-1, K)[mask]))
+    nbytes = 4 * L + esz * L * K + esz * tot
+    a.close()
+    return {"lanes": L, "appended": tot, "ms": round(best, 4),
+            "gbs": round(nbytes / (best * 1e-3) / 1e9, 1),
+            "frac": round(nbytes / (best * 1e-3) / 1e9 / PEAK, 4), "contents_ok": ok}
+
+
+for K, esz in ((1, 4), (2, 4), (4, 4), (8, 4), (16, 4), (4, 8), (16, 1), (1, 8)):
+    out[f"K{K}_e{esz}"] = run(K, esz)
+    torch.cuda.empty_cache()
+out["K8_e4_ragged"] = run(8, 4, ragged=True)
+out["K1_e4_ragged"] = run(1, 4, ragged=True)
+reps = int(os.environ.get("PROBE_REPS", "0"))
+if reps:
+    bad = 0
+    for i in range(reps):
+        r = run(1 + (i % 8), 4, target=1 << 22, reps=1, ragged=bool(i & 1))
+        bad += not r["contents_ok"]
+    out["stress"] = {"runs": reps, "bad": bad}
+print(json.dumps(out))

@@ -145,7 +145,7 @@ for K in (8, 1):
     Ln = cnt.numel()
     dst = lanes_arr if K == 8 else gg.GrowableArray(S, FB, dtype=np.int32)
     leg(f"insert_lanes K={K} ({Ln} lanes, paper Alg. 1)", 4 * Ln + 4 * Ln * K + 4 * tot, tot,
-        "k_lanes_scatter", "counts + the [lanes x K] value block + compacted output")
+        "k_lanes_chunk", "counts + the [lanes x K] value block + compacted output")
     dst.insert_lanes(v, cnt, lo, K, commit=False)
 for mode in ("block", "warp"):
     dst = pa if mode == "block" else gg.GrowableArray(S, FB, dtype=np.int32)

@@ -1,7 +1,7 @@
 """One launch of each non-uniform insert path at 2^28 int32 over 512
 LFVectors, for ncu --set full: ragged CSR insert, duplicate and flatten of
-the ragged array, lanes insert (K = 8 and K = 1: k_lanes_reserve +
-k_lanes_scatter), push_if (block mode)."""
+the ragged array, lanes insert (K = 8 and K = 1: k_lanes_chunk),
+push_if (block mode)."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

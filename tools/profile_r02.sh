@@ -23,7 +23,7 @@ timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvt
     -k regex:"k_walk|k_rw_global" -o $REP/prof_full -f python tools/prof_target.py > $OUT/prof.log 2>&1
 ncu -i $REP/prof_full.ncu-rep --page raw --csv > $OUT/prof_raw.csv 2>/dev/null
 timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "profiled/" \
-    -k regex:"^(k_walk_shard|k_lanes_scatter|k_push_if|k_flat_insert_block|k_flat_append|k_gather)" \
+    -k regex:"^(k_walk_shard|k_lanes_chunk|k_push_if|k_flat_insert_block|k_flat_append|k_gather)" \
     -o $REP/prof_paths_full -f python tools/prof_all.py > $OUT/prof_paths.log 2>&1
 ncu -i $REP/prof_paths_full.ncu-rep --page raw --csv > $OUT/prof_paths_raw.csv 2>/dev/null
 ncu -i $REP/prof_full.ncu-rep --page details --csv > $OUT/prof_details.csv 2>/dev/null

@@ -20,7 +20,7 @@ for it in range(iters):
             pre = [np.arange(int(k), dtype=np.int32) for k in rng.integers(0, 100, S)]
             a.insert_parallel(pre)
             a.push_if(vals, pred, mode=mode, grid=grid)
-            blk = (np.arange(n) // 256) % grid
+            blk = (np.arange(n) // 1024) % grid           # kPushSlice
             shard = blk % S
             st = a._parity_state()
             for s in range(S):

@@ -142,7 +142,7 @@ if os.path.exists(fp):
     json.dump(out, open(os.path.join(P, f"{tag}_all_kernels.json"), "w"), indent=1)
     with open(os.path.join(P, f"{tag}_all_kernels.md"), "a") as fh:
         fh.write("\n## `ncu --set full` of the non-uniform paths (tools/prof_all.py, "
-                 "kernels k_walk_shard / k_lanes_scatter / k_push_if / k_flat_insert_block / k_flat_append / k_gather)\n\n")
+                 "kernels k_walk_shard / k_lanes_chunk / k_push_if / k_flat_insert_block / k_flat_append / k_gather)\n\n")
         fh.write("| kernel | " + " | ".join(l for _, l in want) + " |\n|" + "---|" * (len(want) + 1) + "\n")
         for e in full:
             fh.write(f"| `{e['kernel'][:60]}` | " + " | ".join(e[l] for _, l in want) + " |\n")
