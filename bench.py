@@ -183,8 +183,15 @@ def run_device(args, rank, world, local_rank):
     peaks, peaks_kind = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
 
+    # once per process and device: CUDA context + the library's kernel image
+    # (gg_create would do it at the first construction); reported, not in any step
+    i0 = time.perf_counter()
+    _lib.check(_lib.lib.gg_init(local_rank), "init")
+    init_ms = (time.perf_counter() - i0) * 1e3
     gg.pool_trim(local_rank)
+    c0 = time.perf_counter()
     step = Step(gg, torch, device)
+    construct_ms = (time.perf_counter() - c0) * 1e3
     # the very first step on a fresh array also maps its 8 GiB of slab chunks
     # (driver work the steady-state steps reuse): reported, not in `value`
     torch.cuda.synchronize()
@@ -195,8 +202,11 @@ def run_device(args, rank, world, local_rank):
     cold = {"ms": round((time.perf_counter() - c0) * 1e3, 3),
             "map_ms": round(sl["map_ns"] / 1e6, 3), "extents_mapped": sl["chunks_mapped"],
             "driver_handles_created": sl["handles_created"],
+            "library_init_ms": round(init_ms, 3), "array_construct_ms": round(construct_ms, 3),
             "note": "first step of a fresh array in a fresh process (pool trimmed), wall clock, incl. "
-                    "cuMemCreate/Map/SetAccess of its 8 GiB of slab extents"}
+                    "cuMemCreate/Map/SetAccess of its 8 GiB of slab extents; the once-per-process "
+                    "library init (CUDA context + kernel image load, gg_init) and the array "
+                    "construction are reported beside it"}
     for _ in range(args.warmup):
         step.run(False)
     torch.cuda.synchronize()

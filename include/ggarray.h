@@ -61,6 +61,11 @@ typedef int (*gg_alloc_hook)(void *ctx, uint32_t shard, uint32_t bucket, uint64_
 
 const char *gg_last_error(void);
 int gg_version(void);
+
+/* Per-device library initialisation (CUDA context + the library's kernel
+ * image), once per process; gg_create calls it.  Exposed so a host can pay
+ * it up front.  No reference counterpart (the reference has no device). */
+int gg_init(int device);
 /* number of kernels this library has launched (process-wide counter) */
 uint64_t gg_kernel_launches(void);
 

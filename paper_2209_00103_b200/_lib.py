@@ -44,6 +44,7 @@ PU64, PI32, PI64, PU32 = C.POINTER(U64), C.POINTER(I32), C.POINTER(I64), C.POINT
 _SIGS = {
     "gg_last_error": ([], C.c_char_p),
     "gg_version": ([], C.c_int),
+    "gg_init": ([C.c_int], C.c_int),
     "gg_kernel_launches": ([], U64),
     "gg_device_sms": ([C.c_int, PI32], C.c_int),
     "gg_create": ([C.c_int, U32, U32, U32, U32, U64, C.POINTER(P)], C.c_int),

@@ -805,6 +805,24 @@ int gg_device_sms(int device, int32_t *h_sms) {
   return GG_OK;
 }
 
+// Per-device library initialisation, once per process: the CUDA context and
+// the library's kernel image (lazy module loading would otherwise load it
+// at the first launch, ~30 ms inside the first operation).  Called by
+// gg_create; callable up front.
+int gg_init(int device) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  if (device < 0 || device >= 64) return fail(GG_EVALUE, "device out of range");
+  std::lock_guard<std::mutex> g(mu);
+  if (done >> device & 1) return GG_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaFree(0));
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, k_shrink_uniform));
+  done |= 1ull << device;
+  return GG_OK;
+}
+
 int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t max_buckets,
               uint64_t arena_va_bytes, gg_array **out) {
   *out = nullptr;
@@ -813,8 +831,8 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   if (max_buckets < 1 || max_buckets > kMaxBuckets) return fail(GG_EVALUE, "max_buckets must be in [1, 64]");
   uint32_t esz = elem_bytes_of(dtype);
   if (!esz) return fail(GG_EVALUE, "unsupported dtype");
+  { int rc = gg_init(device); if (rc) return rc; }
   CUDA_TRY(cudaSetDevice(device));
-  CUDA_TRY(cudaFree(0));
   reclaim(false);                          // chunks of arrays destroyed earlier -> the pool
   gg_array *a = new gg_array();
   a->dev = device; a->S = shards; a->fb = fb; a->log2fb = ilog2(fb); a->dtype = dtype;

@@ -2,7 +2,7 @@
 # The growarray-bench experiments on one B200 -> profiles/<round>_bench_cli/
 # (then: python tools/summarize_cli.py profiles/<round>_bench_cli)
 set -e
-OUT=${1:-profiles/r01_bench_cli}
+OUT=${1:-profiles/r02_bench_cli}
 mkdir -p $OUT
 CLI="python -m paper_2209_00103_b200.bench_cli"
 for s in ggarray static doubling chunktable; do
