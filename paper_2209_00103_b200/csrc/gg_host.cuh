@@ -500,6 +500,24 @@ struct Slab {
     for_range(b, s0, s1, [&](Region &rr, size_t c, uint32_t n) { add_ref(rr, c, n); });
     return GG_OK;
   }
+  // map (without references) the unmapped grid chunks slots [s0, s1) of
+  // class b overlap, maximal runs as one extent each but at most `cap` grid
+  // chunks per extent (release granularity); best effort: a failure leaves
+  // the rest to per-slot backing, which fails exactly the shard concerned
+  void premap_range(uint32_t b, uint32_t s0, uint32_t s1, size_t cap) {
+    if (s1 <= s0) return;
+    Region &r = region(b);
+    const uint64_t base = small_off[b] != ~uint64_t(0) ? small_off[b] : 0, bb = bytes[b];
+    const size_t lo = (base + (uint64_t)s0 * bb) / r.chunk, hi = (base + (uint64_t)s1 * bb - 1) / r.chunk;
+    for (size_t c = lo; c <= hi;) {
+      if (r.chunks[c].mapped) { ++c; continue; }
+      size_t e = c;
+      while (e + 1 <= hi && e + 1 - c < cap && !r.chunks[e + 1].mapped) ++e;
+      if (e == c) { ++c; continue; }              // a single chunk: per-slot backing maps it
+      if (map_run(r, c, e - c + 1)) return;
+      c = e + 1;
+    }
+  }
   void unback_range(uint32_t b, uint32_t s0, uint32_t s1) {
     if (s1 <= s0) return;
     for_range(b, s0, s1, [&](Region &r, size_t c, uint32_t n) {

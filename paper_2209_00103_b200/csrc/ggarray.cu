@@ -164,8 +164,46 @@ bool plan_alloc(gg_array *a, Plan &p, uint32_t s, uint32_t b) {
   return true;
 }
 
+// Runs of consecutive shards that will allocate the same bucket class are
+// mapped as extents up front (ragged plans otherwise map one grid chunk per
+// driver call); the per-shard backing below then only takes references.
+// Skipped with an allocator hook or an arena limit (exact per-shard failure
+// semantics first).  GG_PREMAP_CHUNKS caps an extent (default 8 grid chunks
+// = 1/2..1 class region; 0 = off).
+void plan_premap(gg_array *a, const Plan &p, const uint64_t *counts, const uint64_t *starts) {
+  static const size_t cap = [] { const char *e = getenv("GG_PREMAP_CHUNKS"); return e ? (size_t)atol(e) : (size_t)8; }();
+  if (!cap || a->hook || a->limit) return;
+  std::vector<uint64_t> need(a->S, 0);          // bitmask of classes shard s will allocate
+  uint64_t any = 0;
+  for (uint32_t s = 0; s < a->S; ++s) {
+    if (!counts[s]) continue;
+    const uint64_t start = starts ? starts[s] : p.size[s];
+    uint32_t b0, b1; uint64_t o;
+    host_locate(a, start, b0, o);
+    host_locate(a, start + counts[s] - 1, b1, o);
+    if (b1 >= a->MB) continue;
+    const uint64_t m = ((b1 >= 63 ? ~0ull : ((2ull << b1) - 1)) & ~((1ull << b0) - 1)) & ~p.flags[s];
+    need[s] = m;
+    any |= m;
+  }
+  for (uint64_t mm = any; mm; mm &= mm - 1) {
+    const uint32_t b = (uint32_t)__builtin_ctzll(mm);
+    bool created = false;
+    if (a->slab.ensure_region(b, &created)) continue;
+    if (created) a->cbase_dirty = true;
+    for (uint32_t s = 0; s < a->S;) {
+      if (!(need[s] >> b & 1)) { ++s; continue; }
+      uint32_t e = s;
+      while (e + 1 < a->S && (need[e + 1] >> b & 1)) ++e;
+      a->slab.premap_range(b, s, e + 1, cap);
+      s = e + 1;
+    }
+  }
+}
+
 // Plan an append of counts[s] at starts (explicit) or at size[s] (reserve).
 void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *starts) {
+  plan_premap(a, p, counts, starts);
   for (uint32_t s = 0; s < a->S; ++s) {
     uint64_t c = counts[s];
     if (c == 0) continue;
