@@ -92,6 +92,12 @@ __device__ __forceinline__ uint64_t bucket_bytes(const gg_device_view &t, uint32
 __device__ __forceinline__ char *bucket_slot(const gg_device_view &t, uint32_t s, uint32_t b) {
   return t.cbase[b] + (uint64_t)s * bucket_bytes(t, b);
 }
+// the same address for a bucket the caller knows is published (ensure_buckets
+// succeeded for its range): slots never move, so no pointer load is needed --
+// only the class base, a read-only (L1-cached) load
+__device__ __forceinline__ char *bucket_known(const gg_device_view &t, uint32_t s, uint32_t b) {
+  return (char *)__ldg(reinterpret_cast<const unsigned long long *>(t.cbase) + b) + (uint64_t)s * bucket_bytes(t, b);
+}
 
 // Paper Alg. 2 (new_bucket): CAS the once-flag; the winner takes the shard's
 // slot of class b (if the host backed it) and publishes it with release
@@ -115,10 +121,9 @@ __device__ inline int alloc_bucket(const gg_device_view &t, uint32_t s, uint32_t
   t.ptr[(size_t)s * t.MB + b] = bucket_slot(t, s, b);
   atomicAdd((unsigned long long *)&t.cap[s], 1ull << (t.log2fb + b));
   atomicAdd(&t.misc[MISC_ALLOCS], 1ull);
-  __threadfence();
-  st_release(f, kFlagPublished);
-  __threadfence();                 // the pmask bit never becomes visible before the flag
-  atomicOr(&t.pmask[s], 1ull << b);
+  st_release(f, kFlagPublished);   // orders the pointer (and counters) before the flag
+  // release RMW: the pmask bit never becomes visible before the flag
+  asm volatile("red.release.gpu.global.or.b64 [%0], %1;" ::"l"(t.pmask + s), "l"(1ull << b) : "memory");
   return 1;
 }
 
@@ -135,10 +140,87 @@ __device__ inline bool ensure_buckets(const gg_device_view &t, uint32_t s, uint6
   // the once-flag (acquire) is the authority, not pmask: a bucket another warp
   // is still allocating (flag 1) must be waited for, or this warp's lanes
   // would find it unpublished and drop their stores
+  // fast path: one acquire load of the shard's published-bucket mask (a pmask
+  // bit is set only after its flag was released as published)
+  if (ok) {
+    const unsigned long long want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull);
+    if ((ld_acquire64(reinterpret_cast<const uint64_t *>(t.pmask + s)) & want) == want) return true;
+  }
   for (uint32_t b = b0; ok && b <= b1; ++b)
     if (ld_acquire(t.flag + (size_t)s * t.MB + b) != kFlagPublished && alloc_bucket(t, s, b) < 0) ok = false;
   if (!ok) atomicOr(&t.status[s], kStatusNoMem);
   return ok;
+}
+
+// The reservation of one append (insert_index.py:118-143): ONE atomicAdd of
+// n on the LFVector size, then the buckets of [start, start + n).  The
+// shard's published-bucket mask is loaded BEFORE the atomic so both round
+// trips overlap; when it already covers the range (the common case: a bucket
+// is published once per doubling) no further load is needed -- a set pmask
+// bit can only mean a published bucket, however stale the read.
+__device__ inline bool reserve_ensure(const gg_device_view &t, uint32_t s, uint64_t n,
+                                      unsigned long long &start) {
+  unsigned long long pm;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(pm) : "l"(t.pmask + s) : "memory");
+  start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)n);
+  atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+  if (!n) return true;
+  uint32_t b0, b1;
+  uint64_t o;
+  locate(start, t.log2fb, b0, o);
+  locate(start + n - 1, t.log2fb, b1, o);
+  if (b1 < t.MB) {
+    const unsigned long long want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull);
+    if ((pm & want) == want) return true;
+  }
+  return ensure_buckets(t, s, start, n);
+}
+
+// Warp-cooperative ensure_buckets: lane k takes buckets b0 + k, b0 + k + 32,
+// ... so the (rare) appends that open several buckets allocate them in
+// parallel instead of one CAS / publish chain after another.  Called by all 32
+// lanes with the same arguments; the result is in every lane.
+__device__ inline bool warp_ensure_buckets(const gg_device_view &t, uint32_t s, uint64_t start,
+                                           uint64_t n) {
+  if (!n) return true;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t b0, b1;
+  uint64_t o;
+  locate(start, t.log2fb, b0, o);
+  locate(start + n - 1, t.log2fb, b1, o);
+  bool ok = b1 < t.MB;
+  if (ok)
+    for (uint32_t b = b0 + lane; b <= b1; b += 32)
+      if (ld_acquire(t.flag + (size_t)s * t.MB + b) != kFlagPublished && alloc_bucket(t, s, b) < 0) ok = false;
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok && lane == 0) atomicOr(&t.status[s], kStatusNoMem);
+  return ok;
+}
+
+// reserve_ensure by a whole warp (same arguments in every lane): lane 0 makes
+// the reservation, the warp allocates what the published mask does not cover.
+// start and the result are returned in every lane.
+__device__ inline bool warp_reserve_ensure(const gg_device_view &t, uint32_t s, uint64_t n,
+                                           unsigned long long &start) {
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long pm = 0, st = 0;
+  if (lane == 0) {
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(pm) : "l"(t.pmask + s) : "memory");
+    st = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)n);
+    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
+  }
+  start = __shfl_sync(0xffffffffu, st, 0);
+  pm = __shfl_sync(0xffffffffu, pm, 0);
+  if (!n) return true;
+  uint32_t b0, b1;
+  uint64_t o;
+  locate(start, t.log2fb, b0, o);
+  locate(start + n - 1, t.log2fb, b1, o);
+  if (b1 < t.MB) {
+    const unsigned long long want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull);
+    if ((pm & want) == want) return true;
+  }
+  return warp_ensure_buckets(t, s, start, n);
 }
 
 // Bucket base of (s, b) read with acquire order: the flag load synchronises
@@ -174,24 +256,16 @@ __device__ inline uint64_t warp_push_back(const gg_device_view &t, uint32_t s, b
   if (!m) return ~0ull;
   const uint32_t lane = threadIdx.x & 31, cnt = __popc(m), rank = __popc(m & ((1u << lane) - 1u));
   unsigned long long start = 0;
-  int ok = 1;
-  if (lane == 0) {
-    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)cnt);
-    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
-    ok = ensure_buckets(t, s, start, cnt);
-  }
-  start = __shfl_sync(0xffffffffu, start, 0);
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (!ok) return ~0ull;
+  if (!warp_reserve_ensure(t, s, cnt, start)) return ~0ull;
   if (!pred) return ~0ull;
-  // each lane resolves its own bucket with an acquire load (no shuffle: a
+  // every bucket of [start, start + cnt) is published (ensure_buckets), so
+  // each lane computes its slot address (no pointer load, no shuffle: a
   // full-mask shuffle next to the predicated return can be sunk into a
   // divergent branch by the compiler)
   uint32_t b;
   uint64_t o;
   locate(start + rank, t.log2fb, b, o);
-  char *base = bucket_acquire(t, s, b);
-  if (base) store_cg(reinterpret_cast<T *>(base) + o, value);
+  store_cg(reinterpret_cast<T *>(bucket_known(t, s, b)) + o, value);
   return start + rank;
 }
 
@@ -213,15 +287,7 @@ __device__ inline uint64_t warp_push_back_n(const gg_device_view &t, uint32_t s,
   const uint32_t total = __shfl_sync(0xffffffffu, x, 31), excl = x - count;
   if (!total) return ~0ull;
   unsigned long long start = 0;
-  int ok = 1;
-  if (lane == 0) {
-    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)total);
-    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
-    ok = ensure_buckets(t, s, start, total);
-  }
-  start = __shfl_sync(0xffffffffu, start, 0);
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (!ok) return ~0ull;
+  if (!warp_reserve_ensure(t, s, total, start)) return ~0ull;
   uint32_t cur_b = ~0u;
   char *base = nullptr;
 #pragma unroll
@@ -230,8 +296,8 @@ __device__ inline uint64_t warp_push_back_n(const gg_device_view &t, uint32_t s,
       uint32_t b;
       uint64_t o;
       locate(start + excl + e, t.log2fb, b, o);
-      if (b != cur_b) { base = bucket_acquire(t, s, b); cur_b = b; }
-      if (base) store_cg(reinterpret_cast<T *>(base) + o, vals[e]);
+      if (b != cur_b) { base = bucket_known(t, s, b); cur_b = b; }
+      store_cg(reinterpret_cast<T *>(base) + o, vals[e]);
     }
   }
   return start + excl;
@@ -255,15 +321,7 @@ __device__ inline uint64_t warp_push_back_mask(const gg_device_view &t, uint32_t
   const uint32_t total = __shfl_sync(0xffffffffu, x, 31), excl = x - count;
   if (!total) return ~0ull;
   unsigned long long start = 0;
-  int ok = 1;
-  if (lane == 0) {
-    start = atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)total);
-    atomicAdd((unsigned long long *)&t.ops[s], 1ull);
-    ok = ensure_buckets(t, s, start, total);
-  }
-  start = __shfl_sync(0xffffffffu, start, 0);
-  ok = __shfl_sync(0xffffffffu, ok, 0);
-  if (!ok) return ~0ull;
+  if (!warp_reserve_ensure(t, s, total, start)) return ~0ull;
   uint32_t cur_b = ~0u, r = 0;
   char *base = nullptr;
 #pragma unroll
@@ -272,8 +330,8 @@ __device__ inline uint64_t warp_push_back_mask(const gg_device_view &t, uint32_t
       uint32_t b;
       uint64_t o;
       locate(start + excl + r, t.log2fb, b, o);
-      if (b != cur_b) { base = bucket_acquire(t, s, b); cur_b = b; }
-      if (base) store_cg(reinterpret_cast<T *>(base) + o, vals[j]);
+      if (b != cur_b) { base = bucket_known(t, s, b); cur_b = b; }
+      store_cg(reinterpret_cast<T *>(base) + o, vals[j]);
       ++r;
     }
   }
@@ -309,16 +367,13 @@ __device__ inline uint64_t block_push_back_mask(const gg_device_view &t, uint32_
   const unsigned long long excl = x - count + (wid ? scratch[wid - 1] : 0);
   const unsigned long long total = scratch[BLOCK / 32 - 1];
   __syncthreads();
-  if (tid == 0) {
+  if (wid == 0 && total) {                 // warp 0 reserves (and allocates in parallel)
     unsigned long long start = 0;
-    int ok = 1;
-    if (total) {
-      start = atomicAdd((unsigned long long *)&t.size[s], total);
-      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
-      ok = ensure_buckets(t, s, start, total);
-    }
-    scratch[32] = start;
-    scratch[33] = ok;
+    const bool ok = warp_reserve_ensure(t, s, total, start);
+    if (lane == 0) { scratch[32] = start; scratch[33] = ok; }
+  } else if (tid == 0) {
+    scratch[32] = 0;
+    scratch[33] = 1;
   }
   __syncthreads();
   const unsigned long long start = scratch[32];
@@ -329,7 +384,7 @@ __device__ inline uint64_t block_push_back_mask(const gg_device_view &t, uint32_
     uint64_t o;
     locate(start, t.log2fb, b0, o);
     locate(start + total - 1, t.log2fb, b1, o);
-    if (tid <= b1 - b0) bptr_m[b0 + tid] = bucket_acquire(t, s, b0 + tid);
+    if (tid <= b1 - b0) bptr_m[b0 + tid] = bucket_known(t, s, b0 + tid);
   }
   __syncthreads();
   if (ok) {
@@ -382,12 +437,8 @@ __device__ inline uint64_t block_push_back_staged(const gg_device_view &t, uint3
     const unsigned long long total = __shfl_sync(0xffffffffu, w, 31);
     scratch[lane] = w;
     unsigned long long start = 0;
-    int ok = 1;
-    if (lane == 0 && total) {
-      start = atomicAdd((unsigned long long *)&t.size[s], total);
-      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
-      ok = ensure_buckets(t, s, start, total);
-    }
+    bool ok = true;
+    if (total) ok = warp_reserve_ensure(t, s, total, start);
     if (lane == 0) { scratch[32] = start; scratch[33] = ok; }
   }
   __syncthreads();
@@ -404,7 +455,7 @@ __device__ inline uint64_t block_push_back_staged(const gg_device_view &t, uint3
     uint64_t o;
     locate(start, t.log2fb, b0, o);
     locate(start + total - 1, t.log2fb, b1, o);
-    if (tid <= b1 - b0) bptr_s[b0 + tid] = bucket_acquire(t, s, b0 + tid);
+    if (tid <= b1 - b0) bptr_s[b0 + tid] = bucket_known(t, s, b0 + tid);
     uint32_t r = 0;
 #pragma unroll
     for (int j = 0; j < K; ++j)
@@ -475,16 +526,13 @@ __device__ inline uint64_t block_push_back(const gg_device_view &t, uint32_t s, 
   const unsigned long long excl = x - count + (wid ? scratch[wid - 1] : 0);
   const unsigned long long total = scratch[BLOCK / 32 - 1];
   __syncthreads();
-  if (tid == 0) {
+  if (wid == 0 && total) {                 // warp 0 reserves (and allocates in parallel)
     unsigned long long start = 0;
-    int ok = 1;
-    if (total) {
-      start = atomicAdd((unsigned long long *)&t.size[s], total);
-      atomicAdd((unsigned long long *)&t.ops[s], 1ull);
-      ok = ensure_buckets(t, s, start, total);
-    }
-    scratch[32] = start;
-    scratch[33] = ok;
+    const bool ok = warp_reserve_ensure(t, s, total, start);
+    if (lane == 0) { scratch[32] = start; scratch[33] = ok; }
+  } else if (tid == 0) {
+    scratch[32] = 0;
+    scratch[33] = 1;
   }
   __syncthreads();
   const unsigned long long start = scratch[32];
@@ -495,7 +543,7 @@ __device__ inline uint64_t block_push_back(const gg_device_view &t, uint32_t s, 
     uint64_t o;
     locate(start, t.log2fb, b0, o);
     locate(start + total - 1, t.log2fb, b1, o);
-    if (tid <= b1 - b0) bptr[b0 + tid] = bucket_acquire(t, s, b0 + tid);
+    if (tid <= b1 - b0) bptr[b0 + tid] = bucket_known(t, s, b0 + tid);
   }
   __syncthreads();
   if (ok)

@@ -1532,6 +1532,35 @@ __device__ __forceinline__ void lanes_load(const char *vals, const uint32_t *cou
                                            uint32_t (&w)[16]) {
   typedef LaneShape<ESZ, KB, VEC> L;
   const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  {
+    // interior thread (every row's group inside [vlo, vhi), GL-aligned since
+    // wlo is): all rows' loads issue before any is consumed -- a per-row
+    // bounds branch around load + use would serialise them
+    const uint64_t ga = wlo + ((uint64_t)(wid * L::R) * 32 + lane) * L::GL;
+    const uint64_t gz = wlo + ((uint64_t)(wid * L::R + L::R - 1) * 32 + lane) * L::GL;
+    if (ga >= vlo && gz + L::GL <= vhi && (L::GL == 1 || ga % L::GL == 0)) {
+      uint32_t cr[L::R][L::GL];
+#pragma unroll
+      for (uint32_t r = 0; r < L::R; ++r) {
+        const uint64_t g0 = ga + (uint64_t)r * 32 * L::GL;
+        if constexpr (L::GL == 4) {
+          const uint4 x = __ldcs((const uint4 *)(counts + g0));
+          cr[r][0] = x.x; cr[r][1] = x.y; cr[r][2] = x.z; cr[r][3] = x.w;
+        } else if constexpr (L::GL == 2) {
+          const uint2 x = __ldcs((const uint2 *)(counts + g0));
+          cr[r][0] = x.x; cr[r][1] = x.y;
+        } else {
+          cr[r][0] = __ldcs(counts + g0);
+        }
+        lane_load<L::GL * KB>(w + r * L::WPR, vals + g0 * KB);
+      }
+#pragma unroll
+      for (uint32_t r = 0; r < L::R; ++r)
+#pragma unroll
+        for (uint32_t g = 0; g < L::GL; ++g) c[r][g] = min(cr[r][g], L::K);
+      return;
+    }
+  }
 #pragma unroll
   for (uint32_t r = 0; r < L::R; ++r) {
     const uint64_t g0 = wlo + ((uint64_t)(wid * L::R + r) * 32 + lane) * L::GL;

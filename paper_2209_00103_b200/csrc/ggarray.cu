@@ -791,11 +791,16 @@ __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char 
   for (uint64_t r0 = 0; (uint64_t)blockIdx.x * kPushSlice + r0 * round < n; r0 += kPushR) {
     E v[K];
     uint32_t mask = 0;
+    const uint64_t i0 = (uint64_t)blockIdx.x * kPushSlice + r0 * round + threadIdx.x * kPushG;
+    if (aligned && i0 + (kPushR - 1) * round + kPushG <= n) {
+      // interior: every round in bounds -- all R rounds' loads are issued
+      // before any is consumed (a per-round bounds branch around load + use
+      // would serialise them: one round of loads in flight per thread)
+      uint32_t p4[kPushR];
 #pragma unroll
-    for (int j = 0; j < (int)kPushR; ++j) {
-      const uint64_t i = (uint64_t)blockIdx.x * kPushSlice + (r0 + j) * round + threadIdx.x * kPushG;
-      if (aligned && i + kPushG <= n) {
-        const uint32_t p4 = __ldcs(reinterpret_cast<const uint32_t *>(pred + i));
+      for (int j = 0; j < (int)kPushR; ++j) {
+        const uint64_t i = i0 + j * round;
+        p4[j] = __ldcs(reinterpret_cast<const uint32_t *>(pred + i));
         if constexpr (ESZ * kPushG == 16) {
           const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ));
           memcpy(&v[j * kPushG], &q, 16);
@@ -811,9 +816,16 @@ __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char 
           memcpy(&v[j * kPushG], &q0, 16);
           memcpy(&v[j * kPushG + 2], &q1, 16);
         }
+      }
 #pragma unroll
-        for (int g = 0; g < (int)kPushG; ++g) mask |= ((p4 >> (8 * g)) & 0xffu ? 1u : 0u) << (j * kPushG + g);
-      } else {
+      for (int j = 0; j < (int)kPushR; ++j)
+#pragma unroll
+        for (int g = 0; g < (int)kPushG; ++g) mask |= ((p4[j] >> (8 * g)) & 0xffu ? 1u : 0u) << (j * kPushG + g);
+    } else {
+      // the last rounds of the input (or an unaligned input): element loads
+#pragma unroll
+      for (int j = 0; j < (int)kPushR; ++j) {
+        const uint64_t i = i0 + j * round;
 #pragma unroll
         for (int g = 0; g < (int)kPushG; ++g) {
           v[j * kPushG + g] = E(0);
@@ -1925,13 +1937,23 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   cudaStream_t st = S_(stream);
   if (n == 0) return GG_OK;
   const uint32_t B = 256;
-  // default grid: ~6 resident CTAs per SM (each CTA then loops over many
-  // rounds and each append call reserves up to R rounds at once), at least
-  // one CTA per shard
-  if (!grid)
+  // default grid: exactly the resident CTAs (one wave: each CTA then loops
+  // over many rounds and each append call reserves up to R rounds at once; a
+  // grid above residency leaves a half-empty second wave), at least one CTA
+  // per shard
+  if (!grid) {
+    int per_sm = 0;
+    switch (a->esz) {
+      case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<1, 256>, B, 0); break;
+      case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<2, 256>, B, 0); break;
+      case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<4, 256>, B, 0); break;
+      default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<8, 256>, B, 0); break;
+    }
+    if (per_sm <= 0) per_sm = 4;
     grid = (uint32_t)std::max<uint64_t>(
         a->S, std::min<uint64_t>((n + kPushSlice * 8 - 1) / (kPushSlice * 8),
-                                 (uint64_t)sm_count(a->dev) * 6));
+                                 (uint64_t)sm_count(a->dev) * per_sm));
+  }
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, st); if (frc_) return frc_; }
