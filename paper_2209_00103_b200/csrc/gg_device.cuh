@@ -181,6 +181,23 @@ __global__ void k_new_bucket(Tables t, uint32_t s, uint32_t b, int *won) {
   *won = alloc_bucket(t, s, b);
 }
 
+// view_finish's readback staging: size | cap | ops | pmask (u64 x S each) |
+// status (u32 x S, 8 B aligned) | misc (u64 x MISC_N)
+__host__ __device__ inline size_t view_pack_bytes(size_t S) { return S * 32 + ((S * 4 + 7) & ~size_t(7)) + MISC_N * 8; }
+__global__ void __launch_bounds__(256) k_view_pack(Tables t, char *dst) {
+  const size_t S = t.S;
+  uint64_t *hs = (uint64_t *)dst, *hc = hs + S, *ho = hc + S, *hp = ho + S;
+  uint32_t *hst = (uint32_t *)(hp + S);
+  unsigned long long *hm = (unsigned long long *)(dst + S * 32 + ((S * 4 + 7) & ~size_t(7)));
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < S) {
+    hs[i] = t.size[i]; hc[i] = t.cap[i]; ho[i] = t.ops[i]; hp[i] = t.pmask[i];
+    hst[i] = t.status[i];
+    t.status[i] = 0;
+  }
+  if (i < MISC_N) hm[i] = t.misc[i];
+}
+
 __global__ void k_fetch_add(Tables t, uint32_t s, uint64_t c) {
   atomicAdd((unsigned long long *)&t.size[s], (unsigned long long)c);
   t.ops[s] += 1;

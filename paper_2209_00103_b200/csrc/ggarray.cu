@@ -31,7 +31,7 @@ struct gg_array {
   std::vector<uint64_t> size, cap, ops, prefix, flags;  // flags: bitmask per shard
   std::vector<uint8_t> dirty;                            // shard saw a failed reservation
   uint64_t live = 0;                                     // bytes of live buckets
-  std::vector<uint32_t> headroom;                        // (s, b) backed for a device view
+  std::vector<uint32_t> headroom;                        // (b, s0, s1) runs backed for a device view
   bool cbase_dirty = false;                              // a class region appeared
   // metadata pass of the last planned append, not launched yet (eager issue
   // only): fused into the next grow, launched by any other device-touching call
@@ -72,10 +72,11 @@ struct gg_array {
   bool lanes_pend = false;
   cudaEvent_t lanes_ev = nullptr;
   uint64_t *h_lanes = nullptr;                           // pinned [S]
-  std::vector<uint32_t> lanes_head;                      // (s, b) backed for the upper bound
+  std::vector<uint32_t> lanes_head;                      // (b, s0, s1) runs backed for the upper bound
   uint64_t lanes_keep = 0;                               // mapped bytes before that backing
   uint64_t view_keep = 0;                                // mapped bytes before a device view's headroom
   char *h_view = nullptr;                                // pinned staging of view_finish
+  char *d_vpack = nullptr;                               // device staging of view_finish (in dmem)
   size_t h_view_cap = 0;
   // the last shrink asked to keep released chunks cached (release=False):
   // headroom returned by lanes inserts / device views stays cached too
@@ -674,9 +675,10 @@ int resolve_lanes(gg_array *a) {
     }
     need += a->size[s];
   }
-  for (size_t i = 0; i < a->lanes_head.size(); i += 2) {
-    const uint32_t s = a->lanes_head[i], b = a->lanes_head[i + 1];
-    if (!(a->flags[s] >> b & 1)) a->slab.unback(s, b);
+  for (size_t i = 0; i < a->lanes_head.size(); i += 3) {
+    const uint32_t b = a->lanes_head[i];
+    for (uint32_t s = a->lanes_head[i + 1]; s < a->lanes_head[i + 2]; ++s)
+      if (!(a->flags[s] >> b & 1)) a->slab.unback(s, b);
   }
   a->lanes_head.clear();
   const uint64_t keep = std::max<uint64_t>(2 * need * a->esz, a->lanes_keep);
@@ -904,7 +906,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
          o_ctl = take(S * 4), o_flag = take(T * 4), o_status = take(S * 4), o_ptr = take(T * 8),
          o_misc = take(MISC_N * 8), o_won = take(16), o_scr = take(64), o_am = take(S * 8),
          o_cb = take(max_buckets * 8), o_pm = take(S * 8), o_size2 = take(S * 8),
-         o_prefix2 = take((S + 1) * 8);
+         o_prefix2 = take((S + 1) * 8), o_vpack = take(view_pack_bytes(S));
   cudaError_t e = cudaMallocAsync(&a->dmem, bytes, 0);   // driver mempool: no device-wide sync
   if (e != cudaSuccess) { a->slab.destroy(); delete a; return fail(GG_ECUDA, cudaGetErrorString(e)); }
   cudaMemsetAsync(a->dmem, 0, bytes, 0);
@@ -922,6 +924,7 @@ int gg_create(int device, uint32_t shards, uint32_t fb, uint32_t dtype, uint32_t
   t.pmask = (unsigned long long *)(base + o_pm);
   t.S = shards; t.log2fb = a->log2fb; t.MB = max_buckets; t.esz = esz;
   a->d_won = (int *)(base + o_won);
+  a->d_vpack = base + o_vpack;
   a->d_scratch = base + o_scr;
   // creation work is queued on the legacy default stream (no device-wide
   // synchronize); the first call on another stream waits for it (order_stream)
@@ -1525,26 +1528,44 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   const uint32_t S = a->S;
   for (uint32_t s = 0; s < S; ++s)
     if (off[s + 1] > off[s] && a->dirty[s]) return GG_ENOTSUP;
-  // back the upper bound (all or nothing)
+  // back the upper bound (all or nothing), class by class in runs of
+  // consecutive shards that need the class (one batched refcount pass per
+  // run instead of one slab call per bucket: uniform lanes are one run)
   const uint64_t mapped0 = a->slab.mapped;
-  std::vector<uint32_t> head;
-  bool ok = true;
-  for (uint32_t s = 0; s < S && ok; ++s) {
+  std::vector<uint32_t> head;               // (b, s0, s1) runs backed
+  std::vector<uint32_t> nb0(S, 1), nb1(S, 0);
+  uint32_t bmin = a->MB, bmax = 0;
+  for (uint32_t s = 0; s < S; ++s) {
     const uint64_t U = (off[s + 1] - off[s]) * K;
     if (!U) continue;
-    uint32_t b0, b1; uint64_t o;
-    host_locate(a, a->size[s], b0, o);
-    host_locate(a, a->size[s] + U - 1, b1, o);
-    if (b1 >= a->MB) { ok = false; break; }
-    for (uint32_t b = b0; b <= b1; ++b) {
-      if (a->flags[s] >> b & 1) continue;
-      if (back_bucket(a, s, b) != GG_OK) { ok = false; break; }
-      head.push_back(s);
-      head.push_back(b);
+    uint64_t o;
+    host_locate(a, a->size[s], nb0[s], o);
+    host_locate(a, a->size[s] + U - 1, nb1[s], o);
+    if (nb1[s] >= a->MB) return GG_ENOTSUP;
+    bmin = std::min(bmin, nb0[s]);
+    bmax = std::max(bmax, nb1[s]);
+  }
+  bool ok = true;
+  for (uint32_t b = bmin; b <= bmax && b < a->MB && ok; ++b) {
+    bool have_region = false;
+    for (uint32_t s = 0; s < S && ok;) {
+      auto need = [&](uint32_t x) { return nb0[x] <= b && b <= nb1[x] && !(a->flags[x] >> b & 1); };
+      if (!need(s)) { ++s; continue; }
+      uint32_t e = s + 1;
+      while (e < S && need(e)) ++e;
+      if (!have_region) {
+        bool created = false;
+        if (a->slab.ensure_region(b, &created) != GG_OK) { ok = false; break; }
+        if (created) a->cbase_dirty = true;
+        have_region = true;
+      }
+      if (a->slab.back_range(b, s, e) != GG_OK) { ok = false; break; }
+      head.push_back(b); head.push_back(s); head.push_back(e);
+      s = e;
     }
   }
   if (!ok) {
-    for (size_t i = 0; i < head.size(); i += 2) a->slab.unback(head[i], head[i + 1]);
+    for (size_t i = 0; i < head.size(); i += 3) a->slab.unback_range(head[i], head[i + 1], head[i + 2]);
     return GG_ENOTSUP;
   }
   int rc = push_cbase(a, st);
@@ -1824,18 +1845,48 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
   uint64_t live = a->live;
   a->view_keep = a->slab.mapped;
   bool stop = false;
-  for (uint32_t s = 0; s < a->S; ++s) {
-    am[s] = a->flags[s];
-    if (!h_max_sizes || stop) continue;
-    const uint32_t k = std::min<uint32_t>(min_buckets_for(a, h_max_sizes[s]), a->MB);
-    for (uint32_t b = 0; b < k; ++b) {
-      if (a->flags[s] >> b & 1) continue;
-      const uint64_t nb = bucket_bytes(a, b);
-      if ((a->limit && live + nb > a->limit) || back_bucket(a, s, b) != GG_OK) { stop = true; break; }
-      live += nb;
-      am[s] |= 1ull << b;
-      a->headroom.push_back(s);
-      a->headroom.push_back(b);
+  for (uint32_t s = 0; s < a->S; ++s) am[s] = a->flags[s];
+  if (h_max_sizes && !a->limit) {
+    // no live-bytes cap: class by class in runs of consecutive shards (one
+    // batched refcount pass per run); best effort, stops at the first run
+    // that cannot be backed
+    std::vector<uint32_t> k(a->S);
+    uint32_t kmax = 0;
+    for (uint32_t s = 0; s < a->S; ++s) {
+      k[s] = std::min<uint32_t>(min_buckets_for(a, h_max_sizes[s]), a->MB);
+      kmax = std::max(kmax, k[s]);
+    }
+    for (uint32_t b = 0; b < kmax && !stop; ++b) {
+      bool have_region = false;
+      for (uint32_t s = 0; s < a->S && !stop;) {
+        auto need = [&](uint32_t x) { return b < k[x] && !(a->flags[x] >> b & 1); };
+        if (!need(s)) { ++s; continue; }
+        uint32_t e = s + 1;
+        while (e < a->S && need(e)) ++e;
+        if (!have_region) {
+          bool created = false;
+          if (a->slab.ensure_region(b, &created) != GG_OK) { stop = true; break; }
+          if (created) a->cbase_dirty = true;
+          have_region = true;
+        }
+        if (a->slab.back_range(b, s, e) != GG_OK) { stop = true; break; }
+        for (uint32_t x = s; x < e; ++x) am[x] |= 1ull << b;
+        a->headroom.push_back(b); a->headroom.push_back(s); a->headroom.push_back(e);
+        s = e;
+      }
+    }
+  } else if (h_max_sizes) {
+    // live-bytes cap: shard then bucket order, while the cap allows
+    for (uint32_t s = 0; s < a->S && !stop; ++s) {
+      const uint32_t k = std::min<uint32_t>(min_buckets_for(a, h_max_sizes[s]), a->MB);
+      for (uint32_t b = 0; b < k; ++b) {
+        if (a->flags[s] >> b & 1) continue;
+        const uint64_t nb = bucket_bytes(a, b);
+        if (live + nb > a->limit || back_bucket(a, s, b) != GG_OK) { stop = true; break; }
+        live += nb;
+        am[s] |= 1ull << b;
+        a->headroom.push_back(b); a->headroom.push_back(s); a->headroom.push_back(s + 1);
+      }
     }
   }
   int rc = push_cbase(a, st);
@@ -1857,7 +1908,7 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
 // counters into a pinned buffer and ONE stream synchronize
 int view_finish(gg_array *a, int32_t *h_status, cudaStream_t st) {
   const size_t S = a->S;
-  const size_t nb = S * 8 * 4 + ((S * 4 + 7) & ~size_t(7)) + MISC_N * 8;
+  const size_t nb = view_pack_bytes(S);
   if (!a->h_view || a->h_view_cap < nb) {
     if (a->h_view) CUDA_TRY(cudaFreeHost(a->h_view));
     a->h_view = nullptr;
@@ -1868,13 +1919,10 @@ int view_finish(gg_array *a, int32_t *h_status, cudaStream_t st) {
   uint64_t *hs = (uint64_t *)hb, *hc = hs + S, *ho = hc + S, *hp = ho + S;
   uint32_t *hst = (uint32_t *)(hp + S);
   unsigned long long *hm = (unsigned long long *)(hb + S * 32 + ((S * 4 + 7) & ~size_t(7)));
-  CUDA_TRY(cudaMemcpyAsync(hs, a->t.size, S * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(hc, a->t.cap, S * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(ho, a->t.ops, S * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(hp, a->t.pmask, S * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(hst, a->t.status, S * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(hm, a->t.misc, MISC_N * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemsetAsync(a->t.status, 0, S * 4, st));
+  // one packing kernel (which also clears the status words) + ONE copy
+  { k_view_pack<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(a->t, a->d_vpack); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(hb, a->d_vpack, nb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   a->view_out = false;
   bool any = false;
@@ -1890,10 +1938,12 @@ int view_finish(gg_array *a, int32_t *h_status, cudaStream_t st) {
   }
   a->alloc_calls = hm[MISC_ALLOCS];
   // headroom the kernel took becomes live; the rest is unbacked
-  for (size_t i = 0; i < a->headroom.size(); i += 2) {
-    const uint32_t s = a->headroom[i], b = a->headroom[i + 1];
-    if (a->flags[s] >> b & 1) a->live += bucket_bytes(a, b);
-    else a->slab.unback(s, b);
+  for (size_t i = 0; i < a->headroom.size(); i += 3) {
+    const uint32_t b = a->headroom[i];
+    for (uint32_t s = a->headroom[i + 1]; s < a->headroom[i + 2]; ++s) {
+      if (a->flags[s] >> b & 1) a->live += bucket_bytes(a, b);
+      else a->slab.unback(s, b);
+    }
   }
   a->headroom.clear();
   // headroom chunks no bucket took: released asynchronously down to
