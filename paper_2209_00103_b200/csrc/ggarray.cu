@@ -202,9 +202,26 @@ void plan_premap(gg_array *a, const Plan &p, const uint64_t *counts, const uint6
   }
 }
 
+// bookkeeping of bucket (s, b) taken by the plan (slot already backed)
+inline void plan_take(gg_array *a, Plan &p, uint32_t s, uint32_t b) {
+  p.live += bucket_bytes(a, b);
+  p.flags[s] |= uint64_t(1) << b;
+  p.cap[s] += bucket_elems(a, b);
+  p.alloc_calls += 1;
+  if (a->dirty[s]) { p.zero_pairs.push_back(s); p.zero_pairs.push_back(b); }
+}
+
 // Plan an append of counts[s] at starts (explicit) or at size[s] (reserve).
 void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *starts) {
   plan_premap(a, p, counts, starts);
+  // no allocator hook / arena limit: back the new buckets class by class in
+  // runs of consecutive shards (one batched refcount pass per run instead of
+  // one slab call per bucket); a run that cannot be backed falls back to
+  // per-shard backing, which fails exactly the shards concerned
+  const bool runs = !a->hook && !a->limit;
+  std::vector<uint64_t> need(runs ? a->S : 0, 0);
+  std::vector<uint32_t> fail_b(runs ? a->S : 0, ~0u);
+  uint64_t any = 0;
   for (uint32_t s = 0; s < a->S; ++s) {
     uint64_t c = counts[s];
     if (c == 0) continue;
@@ -219,6 +236,11 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
       p.any_fail = p.any_ctl = true;
       continue;
     }
+    if (runs) {
+      need[s] = ((b1 >= 63 ? ~0ull : ((2ull << b1) - 1)) & ~((1ull << b0) - 1)) & ~p.flags[s];
+      any |= need[s];
+      continue;
+    }
     for (uint32_t b = b0; b <= b1; ++b) {
       if (p.flags[s] >> b & 1) continue;
       if (!plan_alloc(a, p, s, b)) {         // bucket_vector.py:194-201
@@ -229,6 +251,34 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
       }
     }
   }
+  if (!runs) return;
+  for (uint64_t mm = any; mm; mm &= mm - 1) {   // ascending classes
+    const uint32_t b = (uint32_t)__builtin_ctzll(mm);
+    bool created = false;
+    const bool region = a->slab.ensure_region(b, &created) == GG_OK;
+    if (created) a->cbase_dirty = true;
+    auto wants = [&](uint32_t x) { return (need[x] >> b & 1) && fail_b[x] == ~0u; };
+    for (uint32_t s = 0; s < a->S;) {
+      if (!wants(s)) { ++s; continue; }
+      uint32_t e = s + 1;
+      while (e < a->S && wants(e)) ++e;
+      if (region && a->slab.back_range(b, s, e) == GG_OK) {
+        for (uint32_t x = s; x < e; ++x) plan_take(a, p, x, b);
+      } else {
+        for (uint32_t x = s; x < e; ++x) {
+          if (region && a->slab.back(x, b) == GG_OK) plan_take(a, p, x, b);
+          else fail_b[x] = b;
+        }
+      }
+      s = e;
+    }
+  }
+  for (uint32_t s = 0; s < a->S; ++s)
+    if (fail_b[s] != ~0u) {                  // bucket_vector.py:194-201
+      p.status[s] = GG_ENOMEM;
+      p.ctl[s] = fail_b[s] | kCtlZero;       // keep buckets < b; zero the reserved range
+      p.any_fail = p.any_ctl = true;
+    }
 }
 
 // class bases travel to the device when a new class region was reserved
