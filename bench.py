@@ -812,7 +812,7 @@ def insert_paths_leg(args, gg, torch, device, hbm):
         c.push_if(vals, pred, mode=mode, commit=False)
         ms = best(lambda: c.push_if(vals, pred, mode=mode, commit=False), lambda: c.shrink(0, release=False))
         rec(f"push_if_{mode}", ms, 5 * N + 4 * tot, tot,
-            {"candidates": N, "appended": tot, "kernel": f"k_push_if ({mode}_push_back_mask, 8 rounds per thread)"})
+            {"candidates": N, "appended": tot, "kernel": f"k_push_if ({mode}_push_back_staged, 8 rounds per thread)"})
         c.commit()
         out[f"push_if_{mode}"]["multiset_ok"] = bool(torch.equal(torch.sort(c.flatten_device())[0],
                                                                  vals[pred.bool()]))

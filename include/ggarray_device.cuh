@@ -12,6 +12,7 @@
  *   gg::warp_push_back(v, shard, pred, value);        // one atomicAdd per warp
  *   gg::warp_push_back_n<T, K>(v, shard, count, vals); // per-lane counts, one per warp
  *   gg::warp_push_back_mask<T, K>(v, shard, mask, vals);        // K candidates, bitmask
+ *   gg::warp_push_back_staged<T, K>(v, shard, mask, vals, stage); // 16 B stores
  *   gg::block_push_back_mask<BLOCK, T, K>(v, shard, mask, vals, scratch);
  *   gg::block_push_back_staged<BLOCK, T, K>(v, shard, mask, vals, scratch, stage); // 16 B stores
  *   gg::block_push_back<BLOCK>(v, shard, count, vals, scratch);  // one per block
@@ -336,6 +337,66 @@ __device__ inline uint64_t warp_push_back_mask(const gg_device_view &t, uint32_t
     }
   }
   return start + excl;
+}
+
+// Warp flavour of the staged variant: ONE atomicAdd per warp, the warp's run
+// staged in its own shared buffer (lane order, shifted congruent with the
+// destination mod 16 B) and written as aligned 16 B vector stores through the
+// bucket slots -- coalesced, unlike the per-lane element stores of
+// warp_push_back_mask.  stage: 32*K + 32/sizeof(T) elements of shared memory,
+// 16 B aligned, private to the warp.  Must be called by all 32 lanes; s
+// warp-uniform.  Returns the run's start index (or ~0ull).
+template <typename T, int K>
+__device__ inline uint64_t warp_push_back_staged(const gg_device_view &t, uint32_t s, uint32_t mask,
+                                                 const T (&vals)[K], T *stage) {
+  static_assert(16 % sizeof(T) == 0, "element size must divide 16 B");
+  constexpr uint32_t VE = 16 / sizeof(T);
+  const uint32_t lane = threadIdx.x & 31, count = __popc(mask);
+  uint32_t x = count;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, x, 31), excl = x - count;
+  if (!total) return ~0ull;
+  unsigned long long start = 0;
+  if (!warp_reserve_ensure(t, s, total, start)) return ~0ull;
+  const uint32_t esz_log = sizeof(T) == 1 ? 0 : sizeof(T) == 2 ? 1 : sizeof(T) == 4 ? 2 : 3;
+  const bool vec = t.log2fb + esz_log >= 4;               // every bucket is whole 16 B vectors
+  const uint32_t shift = vec ? (uint32_t)(start % VE) : 0u;
+  uint32_t r = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if ((mask >> j) & 1u) stage[shift + excl + r++] = vals[j];
+  __syncwarp();
+  if (vec) {
+    const uint32_t nv = (shift + total + VE - 1) / VE;
+    for (uint32_t v = lane; v < nv; v += 32) {
+      uint32_t b;
+      uint64_t o;
+      locate(start - shift + (uint64_t)v * VE, t.log2fb, b, o);
+      T *dp = reinterpret_cast<T *>(bucket_known(t, s, b)) + o;
+      const uint32_t k0 = v * VE;
+      if (k0 >= shift && k0 + VE <= shift + total) {
+        const uint4 q = reinterpret_cast<const uint4 *>(stage)[v];
+        asm volatile("st.global.cg.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(dp), "r"(q.x), "r"(q.y), "r"(q.z),
+                     "r"(q.w) : "memory");
+      } else {
+        for (uint32_t j = 0; j < VE; ++j)
+          if (k0 + j >= shift && k0 + j < shift + total) store_cg(dp + j, stage[k0 + j]);
+      }
+    }
+  } else {
+    for (uint32_t k = lane; k < total; k += 32) {
+      uint32_t b;
+      uint64_t o;
+      locate(start + k, t.log2fb, b, o);
+      store_cg(reinterpret_cast<T *>(bucket_known(t, s, b)) + o, stage[k]);
+    }
+  }
+  __syncwarp();                                           // the stage is reused by the next call
+  return start;
 }
 
 // Block flavour of the mask variant: a shared-memory scan of the lanes'

@@ -829,15 +829,16 @@ namespace gg {
 // leaves as 16 B vector stores); all indexing static (no local memory).
 constexpr uint32_t kPushG = 4, kPushSlice = 256 * kPushG;
 
-template <int ESZ, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char *vals,
-                                                   const uint8_t *pred, uint64_t n, int block_mode,
-                                                   int aligned) {
+template <int ESZ, int BLOCK, bool BLOCK_MODE>
+__global__ void __launch_bounds__(BLOCK, ESZ >= 4 ? 4 : 6) k_push_if(gg_device_view t, const char *vals,
+                                                   const uint8_t *pred, uint64_t n, int aligned) {
   typedef typename ElemT<ESZ>::T E;
   constexpr uint32_t kPushR = ESZ == 8 ? 4 : 8;         // rounds per append call
   constexpr int K = kPushG * kPushR;
   __shared__ unsigned long long scratch[34];
-  __shared__ __align__(16) E stage[BLOCK * K + 32 / ESZ];
+  // block mode: one run of up to BLOCK*K staged; warp mode: a private slice
+  // of 32*K + 32/ESZ elements per warp (16 B multiples)
+  __shared__ __align__(16) E stage[BLOCK * K + (BLOCK_MODE ? 1 : BLOCK / 32) * (32 / ESZ)];
   const uint32_t s = blockIdx.x % t.S;
   const uint64_t round = (uint64_t)gridDim.x * kPushSlice;
   for (uint64_t r0 = 0; (uint64_t)blockIdx.x * kPushSlice + r0 * round < n; r0 += kPushR) {
@@ -888,8 +889,8 @@ __global__ void __launch_bounds__(BLOCK) k_push_if(gg_device_view t, const char 
         }
       }
     }
-    if (block_mode) block_push_back_staged<BLOCK, E, K>(t, s, mask, v, scratch, stage);
-    else warp_push_back_mask<E, K>(t, s, mask, v);
+    if constexpr (BLOCK_MODE) block_push_back_staged<BLOCK, E, K>(t, s, mask, v, scratch, stage);
+    else warp_push_back_staged<E, K>(t, s, mask, v, stage + (threadIdx.x >> 5) * (32 * K + 32 / ESZ));
   }
 }
 
@@ -2043,12 +2044,16 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   // per shard
   if (!grid) {
     int per_sm = 0;
+#define GG_PUSH_OCC(ESZ_) \
+  (mode ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<ESZ_, 256, true>, B, 0) \
+        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<ESZ_, 256, false>, B, 0))
     switch (a->esz) {
-      case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<1, 256>, B, 0); break;
-      case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<2, 256>, B, 0); break;
-      case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<4, 256>, B, 0); break;
-      default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push_if<8, 256>, B, 0); break;
+      case 1: GG_PUSH_OCC(1); break;
+      case 2: GG_PUSH_OCC(2); break;
+      case 4: GG_PUSH_OCC(4); break;
+      default: GG_PUSH_OCC(8); break;
     }
+#undef GG_PUSH_OCC
     if (per_sm <= 0) per_sm = 4;
     grid = (uint32_t)std::max<uint64_t>(
         a->S, std::min<uint64_t>((n + kPushSlice * 8 - 1) / (kPushSlice * 8),
@@ -2071,10 +2076,14 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   if (rc) return rc;
   const int al = ((uintptr_t)d_vals % (kPushG * a->esz) == 0 && (uintptr_t)d_pred % kPushG == 0) ? 1 : 0;
   switch (a->esz) {
-    case 1: { k_push_if<1, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_push_if<2, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_push_if<4, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 8: { k_push_if<8, 256><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, mode, al); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
+#define GG_PUSH_CASE(ESZ_) \
+    case ESZ_: \
+      if (mode) k_push_if<ESZ_, 256, true><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, al); \
+      else k_push_if<ESZ_, 256, false><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, al); \
+      g_launches.fetch_add(1, std::memory_order_relaxed); \
+      break;
+    GG_PUSH_CASE(1) GG_PUSH_CASE(2) GG_PUSH_CASE(4) GG_PUSH_CASE(8)
+#undef GG_PUSH_CASE
   }
   CUDA_TRY(cudaGetLastError());
   return view_finish(a, h_status, st);

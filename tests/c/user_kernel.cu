@@ -2,8 +2,9 @@
 // public device header (include/ggarray_device.cuh) -- the paper's use case --
 // compiled separately from the library.  Thread i of block b emits i-th value
 // if it is odd; the warp appends its odd values to shard (b % S) with
-// gg::warp_push_back, the block variant with gg::block_push_back (modes 2-4:
-// the mask variants, 4 = block_push_back_staged, vector stores).
+// gg::warp_push_back, the block variant with gg::block_push_back (modes 2-5:
+// the mask variants, 4 = block_push_back_staged, 5 = warp_push_back_staged,
+// vector stores).
 // Built and driven by tests/test_gpu_user_kernel.py.
 #include <cstdint>
 #include <cstring>
@@ -15,7 +16,7 @@
 template <int BLOCK>
 __global__ void user_emit(gg::gg_device_view v, const int32_t *in, uint64_t n, int block_mode) {
   __shared__ unsigned long long scratch[34];
-  __shared__ __align__(16) int32_t stage[BLOCK * 4 + 8];
+  __shared__ __align__(16) int32_t stage[BLOCK * 4 + (BLOCK / 32) * 8];
   const uint32_t s = blockIdx.x % v.S;
   if (block_mode >= 2) {            // mask variants: 4 rounds of candidates per thread
     constexpr int K = 4;
@@ -29,7 +30,9 @@ __global__ void user_emit(gg::gg_device_view v, const int32_t *in, uint64_t n, i
         cand[j] = i < n ? in[i] : 0;
         mask |= (uint32_t)(i < n && (cand[j] & 1)) << j;
       }
-      if (block_mode == 4) gg::block_push_back_staged<BLOCK, int32_t, K>(v, s, mask, cand, scratch, stage);
+      if (block_mode == 5)
+        gg::warp_push_back_staged<int32_t, K>(v, s, mask, cand, stage + (threadIdx.x >> 5) * (32 * K + 8));
+      else if (block_mode == 4) gg::block_push_back_staged<BLOCK, int32_t, K>(v, s, mask, cand, scratch, stage);
       else if (block_mode == 3) gg::block_push_back_mask<BLOCK, int32_t, K>(v, s, mask, cand, scratch);
       else gg::warp_push_back_mask<int32_t, K>(v, s, mask, cand);
     }

@@ -30,7 +30,7 @@ def user_lib(tmp_path_factory):
     return lib
 
 
-@pytest.mark.parametrize("block_mode", [0, 1, 2, 3, 4])   # warp, block, warp_mask, block_mask, block_staged
+@pytest.mark.parametrize("block_mode", [0, 1, 2, 3, 4, 5])   # warp, block, warp_mask, block_mask, block_staged, warp_staged
 def test_user_kernel_appends(user_lib, block_mode):
     import torch
     import paper_2209_00103_b200 as gg
