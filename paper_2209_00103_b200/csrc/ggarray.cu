@@ -388,7 +388,9 @@ int walk_shard(const gg_array *a, const Tables &t, const char *src, char *dst, T
                uint64_t maxlen, cudaStream_t st) {
   constexpr uint64_t TL = (uint64_t)U * 256 * (16 / ESZ);
   const dim3 grid((unsigned)((maxlen + 16 + TL - 1) / TL), a->S);
-  cudaError_t e = launch_k(k_walk_shard<ESZ, W, T, U>, grid, kThreads, 0, st, t, src, dst, add, reps);
+  cudaError_t e;
+  if constexpr (W == W_DUP) e = launch_k(k_walk_shard_dup<ESZ, W, T, U>, grid, kThreads, 0, st, t, src, dst, add, reps);
+  else e = launch_k(k_walk_shard<ESZ, W, T, U>, grid, kThreads, 0, st, t, src, dst, add, reps);
   if (e != cudaSuccess) return fail(GG_ECUDA, std::string("walk launch: ") + cudaGetErrorString(e));
   return GG_OK;
 }
