@@ -171,22 +171,9 @@ bool plan_alloc(gg_array *a, Plan &p, uint32_t s, uint32_t b) {
 // Skipped with an allocator hook or an arena limit (exact per-shard failure
 // semantics first).  GG_PREMAP_CHUNKS caps an extent (default 8 grid chunks
 // = 1/2..1 class region; 0 = off).
-void plan_premap(gg_array *a, const Plan &p, const uint64_t *counts, const uint64_t *starts) {
+void plan_premap(gg_array *a, const std::vector<uint64_t> &need, uint64_t any) {
   static const size_t cap = [] { const char *e = getenv("GG_PREMAP_CHUNKS"); return e ? (size_t)atol(e) : (size_t)8; }();
   if (!cap || a->hook || a->limit) return;
-  std::vector<uint64_t> need(a->S, 0);          // bitmask of classes shard s will allocate
-  uint64_t any = 0;
-  for (uint32_t s = 0; s < a->S; ++s) {
-    if (!counts[s]) continue;
-    const uint64_t start = starts ? starts[s] : p.size[s];
-    uint32_t b0, b1; uint64_t o;
-    host_locate(a, start, b0, o);
-    host_locate(a, start + counts[s] - 1, b1, o);
-    if (b1 >= a->MB) continue;
-    const uint64_t m = ((b1 >= 63 ? ~0ull : ((2ull << b1) - 1)) & ~((1ull << b0) - 1)) & ~p.flags[s];
-    need[s] = m;
-    any |= m;
-  }
   for (uint64_t mm = any; mm; mm &= mm - 1) {
     const uint32_t b = (uint32_t)__builtin_ctzll(mm);
     bool created = false;
@@ -202,25 +189,15 @@ void plan_premap(gg_array *a, const Plan &p, const uint64_t *counts, const uint6
   }
 }
 
-// bookkeeping of bucket (s, b) taken by the plan (slot already backed)
-inline void plan_take(gg_array *a, Plan &p, uint32_t s, uint32_t b) {
-  p.live += bucket_bytes(a, b);
-  p.flags[s] |= uint64_t(1) << b;
-  p.cap[s] += bucket_elems(a, b);
-  p.alloc_calls += 1;
-  if (a->dirty[s]) { p.zero_pairs.push_back(s); p.zero_pairs.push_back(b); }
-}
-
 // Plan an append of counts[s] at starts (explicit) or at size[s] (reserve).
 void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *starts) {
-  plan_premap(a, p, counts, starts);
-  // no allocator hook / arena limit: back the new buckets class by class in
-  // runs of consecutive shards (one batched refcount pass per run instead of
-  // one slab call per bucket); a run that cannot be backed falls back to
-  // per-shard backing, which fails exactly the shards concerned
+  // no allocator hook / arena limit: the new buckets are backed class by
+  // class in runs of consecutive shards (one batched refcount pass per run
+  // instead of one slab call per bucket; a run that cannot be backed falls
+  // back to per-shard backing, which fails exactly the shards concerned),
+  // and each shard's plan is updated once from the mask of classes it took
   const bool runs = !a->hook && !a->limit;
   std::vector<uint64_t> need(runs ? a->S : 0, 0);
-  std::vector<uint32_t> fail_b(runs ? a->S : 0, ~0u);
   uint64_t any = 0;
   for (uint32_t s = 0; s < a->S; ++s) {
     uint64_t c = counts[s];
@@ -251,7 +228,9 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
       }
     }
   }
-  if (!runs) return;
+  if (!runs || !any) return;
+  plan_premap(a, need, any);
+  std::vector<uint32_t> fail_b(a->S, ~0u);
   for (uint64_t mm = any; mm; mm &= mm - 1) {   // ascending classes
     const uint32_t b = (uint32_t)__builtin_ctzll(mm);
     bool created = false;
@@ -262,23 +241,46 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
       if (!wants(s)) { ++s; continue; }
       uint32_t e = s + 1;
       while (e < a->S && wants(e)) ++e;
-      if (region && a->slab.back_range(b, s, e) == GG_OK) {
-        for (uint32_t x = s; x < e; ++x) plan_take(a, p, x, b);
-      } else {
-        for (uint32_t x = s; x < e; ++x) {
-          if (region && a->slab.back(x, b) == GG_OK) plan_take(a, p, x, b);
-          else fail_b[x] = b;
-        }
-      }
+      if (!region || a->slab.back_range(b, s, e) != GG_OK)
+        for (uint32_t x = s; x < e; ++x)
+          if (!region || a->slab.back(x, b) != GG_OK) fail_b[x] = b;
       s = e;
     }
   }
-  for (uint32_t s = 0; s < a->S; ++s)
+  // per-class element / byte prefix sums once, then one update per shard (a
+  // contiguous run of classes -- the usual case -- in closed form)
+  uint64_t pe[65], pb[65];
+  pe[0] = pb[0] = 0;
+  for (uint32_t b = 0; b < 64; ++b) {
+    pe[b + 1] = pe[b] + (b < a->MB ? bucket_elems(a, b) : 0);
+    pb[b + 1] = pb[b] + (b < a->MB ? bucket_bytes(a, b) : 0);
+  }
+  for (uint32_t s = 0; s < a->S; ++s) {
+    if (!need[s]) continue;
+    uint64_t took = need[s];
     if (fail_b[s] != ~0u) {                  // bucket_vector.py:194-201
+      took &= (uint64_t(1) << fail_b[s]) - 1;
       p.status[s] = GG_ENOMEM;
       p.ctl[s] = fail_b[s] | kCtlZero;       // keep buckets < b; zero the reserved range
       p.any_fail = p.any_ctl = true;
     }
+    if (!took) continue;
+    p.flags[s] |= took;
+    const uint32_t k = (uint32_t)__builtin_popcountll(took), lo = (uint32_t)__builtin_ctzll(took);
+    p.alloc_calls += k;
+    if ((took >> lo) == (k == 64 ? ~0ull : (1ull << k) - 1)) {     // classes lo .. lo + k - 1
+      p.cap[s] += pe[lo + k] - pe[lo];
+      p.live += pb[lo + k] - pb[lo];
+    } else {
+      for (uint64_t m = took; m; m &= m - 1) {
+        const uint32_t b = (uint32_t)__builtin_ctzll(m);
+        p.cap[s] += pe[b + 1] - pe[b];
+        p.live += pb[b + 1] - pb[b];
+      }
+    }
+    if (a->dirty[s])
+      for (uint64_t m = took; m; m &= m - 1) { p.zero_pairs.push_back(s); p.zero_pairs.push_back((uint32_t)__builtin_ctzll(m)); }
+  }
 }
 
 // class bases travel to the device when a new class region was reserved
