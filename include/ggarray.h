@@ -221,6 +221,12 @@ int gg_set_pdl(int32_t on);
  * queries (summary, host state, memory stats) see the up-to-date host
  * mirrors either way.  Process-wide; for A/B measurements. */
 int gg_set_defer(int32_t on);
+/* Batched backing of new bucket classes (default 1): append plans, lanes
+ * inserts and device views back each class in runs of consecutive shards
+ * (one refcount pass per run).  0 = one slab call per bucket; 2 = every run
+ * treated as unbackable, so the per-shard fallback (exact failure semantics)
+ * runs -- a test hook.  Process-wide. */
+int gg_set_batch_backing(int32_t mode);
 /* committed size, total (reserved) size, total capacity -- host mirrors */
 int gg_summary(gg_array *a, uint64_t *h_out3);
 

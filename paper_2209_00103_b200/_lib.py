@@ -83,6 +83,7 @@ _SIGS = {
     "gg_set_tuning": ([I32, I32, U32, U32], C.c_int),
     "gg_set_pdl": ([C.c_int32], C.c_int),
     "gg_set_defer": ([C.c_int32], C.c_int),
+    "gg_set_batch_backing": ([C.c_int32], C.c_int),
     "gg_capture_release": ([P], C.c_int),
     "gg_summary": ([P, PU64], C.c_int),
     "gg_host_state": ([P, PU64, PU64, PU64, PU64, PU64], C.c_int),

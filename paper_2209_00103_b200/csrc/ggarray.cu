@@ -189,6 +189,14 @@ void plan_premap(gg_array *a, const std::vector<uint64_t> &need, uint64_t any) {
   }
 }
 
+// Batched (run) backing of new bucket classes: 1 = on (default), 0 = one
+// slab call per bucket, 2 = runs path with every run treated as unbackable
+// (exercises the per-shard fallback; test hook).  gg_set_batch_backing.
+int g_batch_backing = 1;
+bool run_backed(gg_array *a, uint32_t b, uint32_t s0, uint32_t s1) {
+  return g_batch_backing != 2 && a->slab.back_range(b, s0, s1) == GG_OK;
+}
+
 // Plan an append of counts[s] at starts (explicit) or at size[s] (reserve).
 void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *starts) {
   // no allocator hook / arena limit: the new buckets are backed class by
@@ -196,7 +204,7 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
   // instead of one slab call per bucket; a run that cannot be backed falls
   // back to per-shard backing, which fails exactly the shards concerned),
   // and each shard's plan is updated once from the mask of classes it took
-  const bool runs = !a->hook && !a->limit;
+  const bool runs = g_batch_backing && !a->hook && !a->limit;
   std::vector<uint64_t> need(runs ? a->S : 0, 0);
   uint64_t any = 0;
   for (uint32_t s = 0; s < a->S; ++s) {
@@ -241,7 +249,7 @@ void plan_append(gg_array *a, Plan &p, const uint64_t *counts, const uint64_t *s
       if (!wants(s)) { ++s; continue; }
       uint32_t e = s + 1;
       while (e < a->S && wants(e)) ++e;
-      if (!region || a->slab.back_range(b, s, e) != GG_OK)
+      if (!region || !run_backed(a, b, s, e))
         for (uint32_t x = s; x < e; ++x)
           if (!region || a->slab.back(x, b) != GG_OK) fail_b[x] = b;
       s = e;
@@ -1614,7 +1622,14 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
         if (created) a->cbase_dirty = true;
         have_region = true;
       }
-      if (a->slab.back_range(b, s, e) != GG_OK) { ok = false; break; }
+      if (g_batch_backing == 1 ? a->slab.back_range(b, s, e) != GG_OK : g_batch_backing == 2) { ok = false; break; }
+      if (!g_batch_backing) {                    // one slab call per bucket (A/B)
+        uint32_t x = s;
+        for (; x < e && a->slab.back(x, b) == GG_OK; ++x) { head.push_back(b); head.push_back(x); head.push_back(x + 1); }
+        if (x < e) { ok = false; break; }
+        s = e;
+        continue;
+      }
       head.push_back(b); head.push_back(s); head.push_back(e);
       s = e;
     }
@@ -1901,10 +1916,10 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
   a->view_keep = a->slab.mapped;
   bool stop = false;
   for (uint32_t s = 0; s < a->S; ++s) am[s] = a->flags[s];
-  if (h_max_sizes && !a->limit) {
+  if (h_max_sizes && !a->limit && g_batch_backing) {
     // no live-bytes cap: class by class in runs of consecutive shards (one
-    // batched refcount pass per run); best effort, stops at the first run
-    // that cannot be backed
+    // batched refcount pass per run; a run that cannot be backed goes slot by
+    // slot); best effort, stops at the first slot that cannot be backed
     std::vector<uint32_t> k(a->S);
     uint32_t kmax = 0;
     for (uint32_t s = 0; s < a->S; ++s) {
@@ -1924,20 +1939,28 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
           if (created) a->cbase_dirty = true;
           have_region = true;
         }
-        if (a->slab.back_range(b, s, e) != GG_OK) { stop = true; break; }
-        for (uint32_t x = s; x < e; ++x) am[x] |= 1ull << b;
-        a->headroom.push_back(b); a->headroom.push_back(s); a->headroom.push_back(e);
+        if (run_backed(a, b, s, e)) {
+          for (uint32_t x = s; x < e; ++x) am[x] |= 1ull << b;
+          a->headroom.push_back(b); a->headroom.push_back(s); a->headroom.push_back(e);
+        } else {                                 // slot by slot, up to the first that fails
+          for (uint32_t x = s; x < e && !stop; ++x) {
+            if (a->slab.back(x, b) != GG_OK) { stop = true; break; }
+            am[x] |= 1ull << b;
+            a->headroom.push_back(b); a->headroom.push_back(x); a->headroom.push_back(x + 1);
+          }
+        }
         s = e;
       }
     }
   } else if (h_max_sizes) {
-    // live-bytes cap: shard then bucket order, while the cap allows
+    // live-bytes cap (or per-bucket backing): shard then bucket order, while
+    // the cap allows
     for (uint32_t s = 0; s < a->S && !stop; ++s) {
       const uint32_t k = std::min<uint32_t>(min_buckets_for(a, h_max_sizes[s]), a->MB);
       for (uint32_t b = 0; b < k; ++b) {
         if (a->flags[s] >> b & 1) continue;
         const uint64_t nb = bucket_bytes(a, b);
-        if (live + nb > a->limit || back_bucket(a, s, b) != GG_OK) { stop = true; break; }
+        if ((a->limit && live + nb > a->limit) || back_bucket(a, s, b) != GG_OK) { stop = true; break; }
         live += nb;
         am[s] |= 1ull << b;
         a->headroom.push_back(b); a->headroom.push_back(s); a->headroom.push_back(s + 1);
@@ -2103,6 +2126,12 @@ int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t thre
 
 int gg_set_pdl(int32_t on) {
   g_pdl = on != 0;
+  return GG_OK;
+}
+
+int gg_set_batch_backing(int32_t mode) {
+  if (mode < 0 || mode > 2) return fail(GG_EVALUE, "batch backing mode must be 0, 1 or 2");
+  g_batch_backing = mode;
   return GG_OK;
 }
 
