@@ -1620,10 +1620,13 @@ __device__ __forceinline__ void lanes_load(const char *vals, const uint32_t *cou
 }
 
 // scans + staging + stores of a loaded tile; returns the tile total
-template <int ESZ, int KB, bool VEC = true>
+struct NoSyncHook { __device__ void operator()() const {} };
+
+template <int ESZ, int KB, bool VEC = true, typename OnSync = NoSyncHook>
 __device__ __forceinline__ uint32_t lanes_store(const Tables &t, LaneSmem<ESZ, KB, VEC> &sm, uint32_t s,
                                                 const uint32_t (&c)[LaneShape<ESZ, KB, VEC>::R][LaneShape<ESZ, KB, VEC>::GL],
-                                                const uint32_t (&w)[16], uint64_t base, int par) {
+                                                const uint32_t (&w)[16], uint64_t base, int par,
+                                                OnSync on_sync = OnSync()) {
   typedef typename ElemT<ESZ>::T E;
   typedef LaneShape<ESZ, KB, VEC> L;
   constexpr uint32_t R = L::R, GL = L::GL, K = L::K, VE = L::VE;
@@ -1660,6 +1663,7 @@ __device__ __forceinline__ uint32_t lanes_store(const Tables &t, LaneSmem<ESZ, K
   }
   if (lane == 0) sm.wsum[par][wid] = carry;
   __syncthreads();
+  on_sync();                                    // (every thread holds its tile in registers)
   uint32_t woff = 0, total = 0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
@@ -1880,6 +1884,183 @@ __global__ void __launch_bounds__(256, KB == 4 ? 6 : 1) k_lanes_chunk(Tables t, 
     lanes_load<ESZ, KB, VEC>(vals, counts, t0, lo, lo + nl, c, w);
     base += lanes_store<ESZ, KB, VEC>(t, sm, s, c, w, base, par);
     par ^= 1;
+  }
+}
+
+// ---- the same one-pass insert with the value blocks streamed by TMA ------
+// k_lanes_bulk: as k_lanes_chunk, but each tile's [T x K] value block (16 KiB
+// = 256 threads x 64 B) arrives in a shared-memory ring of NS stages through
+// cp.async.bulk (the TMA's 1-D bulk copy, completion counted on an mbarrier):
+// thread 0 issues the chunk's first NS tiles before the counts are summed and
+// chained, and refills a stage as soon as the CTA has moved its tile into
+// registers, so the value loads of up to NS tiles are in flight while the
+// CTA scans / stages / stores -- without holding registers for them.  Counts
+// still come through the LSU (L2-resident after the count sum).  Tiles whose
+// copy would be misaligned or run past the value array take the register
+// path of k_lanes_chunk.  Used where it measured faster (lanes of 8, 32 or
+// 64 B, lanes_tiled).
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}"
+               ::"r"(bar), "r"(parity) : "memory");
+}
+
+// lanes_load with the values read from a tile staged in shared memory
+// (ring = the tile's first lane wlo; counts as in lanes_load)
+template <int ESZ, int KB>
+__device__ __forceinline__ void lanes_load_ring(const char *ring, const uint32_t *counts, uint64_t wlo, uint64_t vlo,
+                                                uint64_t vhi,
+                                                uint32_t (&c)[LaneShape<ESZ, KB, true>::R][LaneShape<ESZ, KB, true>::GL],
+                                                uint32_t (&w)[16]) {
+  typedef LaneShape<ESZ, KB, true> L;
+  const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr uint32_t GB = L::GL * KB;                 // bytes per group (16 or KB)
+#pragma unroll
+  for (uint32_t r = 0; r < L::R; ++r) {
+    const uint32_t gi = (wid * L::R + r) * 32 + lane;   // group index in the tile
+    const uint4 *sp = reinterpret_cast<const uint4 *>(ring + (size_t)gi * GB);
+#pragma unroll
+    for (uint32_t q = 0; q < GB / 16; ++q) {
+      const uint4 v = sp[q];
+      w[r * L::WPR + 4 * q] = v.x; w[r * L::WPR + 4 * q + 1] = v.y;
+      w[r * L::WPR + 4 * q + 2] = v.z; w[r * L::WPR + 4 * q + 3] = v.w;
+    }
+  }
+  const uint64_t ga = wlo + ((uint64_t)(wid * L::R) * 32 + lane) * L::GL;
+  const uint64_t gz = wlo + ((uint64_t)(wid * L::R + L::R - 1) * 32 + lane) * L::GL;
+  if (ga >= vlo && gz + L::GL <= vhi) {
+    uint32_t cr[L::R][L::GL];
+#pragma unroll
+    for (uint32_t r = 0; r < L::R; ++r) {
+      const uint64_t g0 = ga + (uint64_t)r * 32 * L::GL;
+      if constexpr (L::GL == 4) {
+        const uint4 x = __ldcs((const uint4 *)(counts + g0));
+        cr[r][0] = x.x; cr[r][1] = x.y; cr[r][2] = x.z; cr[r][3] = x.w;
+      } else if constexpr (L::GL == 2) {
+        const uint2 x = __ldcs((const uint2 *)(counts + g0));
+        cr[r][0] = x.x; cr[r][1] = x.y;
+      } else {
+        cr[r][0] = __ldcs(counts + g0);
+      }
+    }
+#pragma unroll
+    for (uint32_t r = 0; r < L::R; ++r)
+#pragma unroll
+      for (uint32_t g = 0; g < L::GL; ++g) c[r][g] = min(cr[r][g], L::K);
+  } else {
+#pragma unroll
+    for (uint32_t r = 0; r < L::R; ++r) {
+      const uint64_t g0 = wlo + ((uint64_t)(wid * L::R + r) * 32 + lane) * L::GL;
+#pragma unroll
+      for (uint32_t g = 0; g < L::GL; ++g)
+        c[r][g] = (g0 + g >= vlo && g0 + g < vhi) ? min(__ldcs(counts + g0 + g), L::K) : 0u;
+    }
+  }
+}
+
+template <int ESZ, int KB, int NS>
+__global__ void __launch_bounds__(256) k_lanes_bulk(Tables t, const char *vals, const uint32_t *counts,
+                                                    const uint32_t *cpre, unsigned long long *chain, uint32_t C) {
+  typedef LaneShape<ESZ, KB, true> L;
+  constexpr uint32_t K = L::K, T = L::T, TB = T * KB;
+  static_assert(TB == 16384, "a tile's value block is 256 threads x 64 B");
+  extern __shared__ __align__(128) char ring[];        // NS x TB
+  __shared__ LaneSmem<ESZ, KB, true> sm;
+  __shared__ uint32_t red[8];
+  __shared__ __align__(8) unsigned long long bar[NS];
+  pdl_begin();
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t chunk = blockIdx.x;
+  const uint32_t s = warp_find_u32(cpre, t.S, chunk);
+  const uint32_t first = cpre[s], last = cpre[s + 1] - 1;
+  const uint64_t lo = t.offsets[s] + (uint64_t)(chunk - first) * C;
+  const uint32_t nl = (uint32_t)min((uint64_t)C, t.offsets[s + 1] - lo);
+  const uint64_t hi = lo + nl, total = t.offsets[t.S];
+  const uint64_t wlo = lo - lo % L::GL;                 // tiles from a GL-aligned lane
+  const uint32_t ntiles = (uint32_t)((hi - wlo + T - 1) / T);
+  // bytes of tile i's bulk copy (0 = the tile takes the register path); the
+  // value array is 16 B aligned (lanes_tiled) and tiles start on 16 B
+  auto tile_bytes = [&](uint32_t i) -> uint32_t {
+    const uint64_t ts = wlo + (uint64_t)i * T, te = min(ts + T, hi);
+    if (te == total && ((te * KB) & 15)) return 0;     // the copy would run past the value array
+    return (uint32_t)(((te - ts) * KB + 15) & ~uint64_t(15));
+  };
+  auto issue = [&](uint32_t i) {
+    const uint32_t nb = tile_bytes(i);
+    if (!nb) return;
+    const uint32_t k = i % NS, b = smem_addr(&bar[k]);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(b), "r"(nb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(ring + (size_t)k * TB)), "l"(vals + (wlo + (uint64_t)i * T) * KB), "r"(nb), "r"(b)
+                 : "memory");
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(&bar[k])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t i = 0; i < (uint32_t)NS && i < ntiles; ++i) issue(i);
+  }
+  stage_cbase(t, sm.scb);
+  const uint32_t agg = chunk_count_sum(counts, lo, nl, K, red);   // (its barrier publishes the mbarrier init)
+  if (wid == 0) {
+    unsigned long long excl = 0;
+    if (chunk == first) {
+      if (lane == 0) {
+        excl = t.size[s];
+        st_chain(chain + chunk, kChainP | (excl + agg));
+      }
+      excl = __shfl_sync(0xffffffffu, excl, 0);
+    } else {
+      if (lane == 0) st_chain(chain + chunk, kChainA | agg);
+      int64_t j = (int64_t)chunk - 1;
+      for (;;) {
+        const int64_t idx = j - lane;
+        unsigned long long v;
+        do {
+          v = idx >= (int64_t)first ? ld_chain(chain + idx) : kChainP;
+        } while (__any_sync(0xffffffffu, (v >> 62) == 0));
+        const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const uint32_t stop = pm ? (uint32_t)(__ffs(pm) - 1) : 31u;
+        unsigned long long x = lane <= stop ? (v & kChainV) : 0ull;
+#pragma unroll
+        for (int d = 16; d; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+        excl += x;
+        if (pm) break;
+        j -= 32;
+      }
+      if (lane == 0) st_chain(chain + chunk, kChainP | (excl + agg));
+    }
+    if (lane == 0) {
+      sm.base = excl;
+      if (chunk == last) {
+        const unsigned long long start = t.size[s];
+        lanes_reserve_publish(t, s, start, excl + agg - start);
+      }
+    }
+  }
+  __syncthreads();
+  uint64_t base = sm.base;
+  uint32_t phase = 0;                                  // bit k: parity of stage k's next completion
+  for (uint32_t i = 0; i < ntiles; ++i) {
+    const uint64_t t0 = wlo + (uint64_t)i * T;
+    uint32_t c[L::R][L::GL], w[16];
+    if (tile_bytes(i)) {
+      const uint32_t k = i % NS;
+      mbar_wait(smem_addr(&bar[k]), (phase >> k) & 1u);
+      phase ^= 1u << k;
+      lanes_load_ring<ESZ, KB>(ring + (size_t)k * TB, counts, t0, lo, hi, c, w);
+    } else {
+      lanes_load<ESZ, KB, true>(vals, counts, t0, lo, hi, c, w);
+    }
+    // refill the stage right after lanes_store's barrier (every thread has
+    // moved its tile into registers by then)
+    base += lanes_store<ESZ, KB, true>(t, sm, s, c, w, base, (int)(i & 1), [&] {
+      if (tid == 0 && i + NS < ntiles) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before the async refill
+        issue(i + NS);
+      }
+    });
   }
 }
 

@@ -1586,7 +1586,7 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   const uint64_t KB = K * a->esz;
   // register-resident lanes: KB a power of two in [4, 64], 16 B-aligned values
   if (!on || a->hook || a->limit || KB < 4 || KB > 64 || (KB & (KB - 1)) ||
-      ((uintptr_t)d_values % std::min<uint64_t>(KB, 16)) || capturing_now(a, st))
+      ((uintptr_t)d_values % 16) || capturing_now(a, st))
     return GG_ENOTSUP;
   const uint32_t S = a->S;
   for (uint32_t s = 0; s < S; ++s)
@@ -1679,8 +1679,30 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
     cudaError_t e = cudaSuccess;
     const char *dv = (const char *)d_values;
     const uint32_t *tp = (const uint32_t *)d_tpre;
+    // TMA-streamed value blocks (k_lanes_bulk, a 2-stage ring) where they
+    // measured faster than the register path (tools/lanes_probe.py A/B, two
+    // runs: KB = 8 +5-7%, 32 +0-2%, 64 +4%; KB = 4 -12%, 16 -2..-8%: those
+    // keep k_lanes_chunk).  GG_LANES_BULK=0 / 1: never / always.
+    static const int bulk_env = [] {
+      const char *e = getenv("GG_LANES_BULK");
+      return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    const bool bulk = bulk_env == 1 || (bulk_env < 0 && (KB == 8 || KB == 32 || KB == 64));
 #define GG_CHAIN_CASE(ESZ_, KB_) \
-  case KB_: e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, kLanesChunk); break;
+  case KB_: \
+    if (bulk) { \
+      static std::atomic<uint64_t> attr{0}; \
+      const uint64_t bit = uint64_t(1) << (a->dev & 63); \
+      if (!(attr.load(std::memory_order_acquire) & bit)) { \
+        cudaFuncSetAttribute(k_lanes_bulk<ESZ_, KB_, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384); \
+        attr.fetch_or(bit, std::memory_order_acq_rel); \
+      } \
+      e = launch_k(k_lanes_bulk<ESZ_, KB_, 2>, (unsigned)nt, 256, (size_t)2 * 16384, st, t, dv, d_counts, tp, d_chain, \
+                   kLanesChunk); \
+    } else { \
+      e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, kLanesChunk); \
+    } \
+    break;
     switch (a->esz) {
       case 1: switch (KB) { GG_CHAIN_CASE(1, 4) GG_CHAIN_CASE(1, 8) GG_CHAIN_CASE(1, 16) GG_CHAIN_CASE(1, 32) GG_CHAIN_CASE(1, 64) } break;
       case 2: switch (KB) { GG_CHAIN_CASE(2, 4) GG_CHAIN_CASE(2, 8) GG_CHAIN_CASE(2, 16) GG_CHAIN_CASE(2, 32) GG_CHAIN_CASE(2, 64) } break;

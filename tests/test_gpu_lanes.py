@@ -50,7 +50,8 @@ def _check(a, o):
 @pytest.mark.parametrize("dtype,K,fb", [("int32", 8, 32), ("int32", 1, 32), ("int32", 3, 32),
                                         ("int8", 5, 16), ("int16", 8, 8), ("int64", 2, 32),
                                         ("float32", 33, 32), ("int32", 8, 1), ("float64", 7, 2),
-                                        ("int32", 1000, 32)])
+                                        ("int32", 1000, 32), ("int32", 2, 32), ("int8", 64, 16),
+                                        ("int64", 1, 32), ("int16", 16, 32)])
 def test_lanes_tiled_matches_oracle(gg, dtype, K, fb):
     import torch
     rng = np.random.default_rng(K * 7 + fb)
@@ -146,3 +147,23 @@ def test_lanes_footprint_settles(gg):
     a.insert_lanes(vals, cnt, lo, K)
     ms = a.memory_stats()
     assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"] + (2 << 20)
+
+
+@pytest.mark.parametrize("K,shift", [(1, 1), (4, 3), (8, 2)])
+def test_lanes_values_not_16B_aligned(gg, K, shift):
+    """Value blocks that do not start on a 16 B boundary cannot be streamed
+    by the bulk copy (k_lanes_bulk): every tile takes the register path (K = 1)
+    or the exact two-pass path (lanes wider than their alignment); the result
+    is the same compaction."""
+    import torch
+    rng = np.random.default_rng(K + shift)
+    S = 21
+    a = gg.GrowableArray(S, 32, dtype=np.int32)
+    o = O.OracleGGArray(S, 32, dtype=np.int32)
+    lo, counts = _lanes(rng, S, K, 9000, empty_every=4)
+    n = int(lo[-1]) * K
+    base = torch.arange(n + shift, dtype=torch.int32, device="cuda") * 3 - 7
+    vals = base[shift:]                                 # 4 B aligned, not 16 B
+    a.insert_lanes(vals, counts, lo, values_per_lane=K)
+    o.insert_parallel(_compact(vals.cpu().numpy(), counts, lo, K, S))
+    _check(a, o)
