@@ -35,6 +35,15 @@ for S, fb, dt in [(37, 4, np.int32), (5, 1, np.int8), (1100, 8, np.int64)]:
         pred = (torch.arange(m, device="cuda") % 3 == 0).to(torch.uint8)
         a.push_if(lv[:m], pred, mode=mode)
     a.close()
+# lanes inserts with many tiles per chunk: the TMA ring (k_lanes_bulk, 32 B
+# lanes) refills its stages, the register path (k_lanes_chunk, 4 B lanes)
+for K in (8, 1):
+    b = gg.GrowableArray(8, 32, dtype=np.int32)
+    Ln = 8 * 20011
+    cnt = torch.randint(0, K + 1, (Ln,), dtype=torch.int32, device="cuda")
+    b.insert_lanes(torch.arange(Ln * K, dtype=torch.int32, device="cuda"), cnt,
+                   np.arange(9, dtype=np.uint64) * 20011, K)
+    b.close()
 st = gg.StaticArray(1 << 16, dtype=np.int32)
 for algo in ("atomic", "warp", "block"):
     st._count = 0
