@@ -794,7 +794,10 @@ def insert_paths_leg(args, gg, torch, device, hbm):
         rec(f"lanes_K{K}", ms, layout, tot,
             {"lanes": L, "appended": tot, "algorithmic_bytes": layout, "useful_bytes": useful,
              "useful_frac": round(useful / (ms * 1e-3) / 1e9 / hbm, 4),
-             "kernels": "k_lanes_chunk (one pass: chunk count sums, decoupled look-back per LFVector, register-resident tile walk)"})
+             "kernels": ("k_lanes_bulk (one pass: chunk count sums, decoupled look-back per LFVector, value tiles "
+                         "streamed by TMA bulk copies into a 2-stage shared-memory ring)" if K == 8 else
+                         "k_lanes_chunk (one pass: chunk count sums, decoupled look-back per LFVector, "
+                         "register-resident tile walk)")})
         b.commit()
         mask = torch.arange(K, device=device)[None, :] < cnt[:, None]
         out[f"lanes_K{K}"]["contents_ok"] = bool(torch.equal(b.flatten_device(), vals.view(-1, K)[mask]))
