@@ -380,10 +380,15 @@ struct Slab {
   // unmap an extent without live buckets; its physical handle goes to the
   // process pool (released to the driver only when the pool is full)
   void unmap_extent(Region &r, size_t head) {
-    Chunk &hd = r.chunks[head];
     const uint64_t t0 = now_ns();
+    drv().unmap(r.base + head * r.chunk, r.chunks[head].len * r.chunk);
+    unmapped(r, head);
+    ns_unmap += now_ns() - t0;
+  }
+  // bookkeeping of an extent whose mapping is gone: handle to the pool
+  void unmapped(Region &r, size_t head) {
+    Chunk &hd = r.chunks[head];
     const size_t n = hd.len, bytes_ = n * r.chunk;
-    drv().unmap(r.base + head * r.chunk, bytes_);
     give_or_release(bytes_, hd.h);
     if (hd.doomed) doomed_bytes -= bytes_;
     for (size_t c = head; c < head + n; ++c) {
@@ -395,6 +400,33 @@ struct Slab {
     mapped -= bytes_;
     cached -= bytes_;
     n_unmap += 1;
+  }
+  // unmap a set of extents without live buckets, adjacent extents of a
+  // region with ONE cuMemUnmap (the driver charges per call -- ~1-10 ms on
+  // some boxes -- far more than per byte); an unmap the driver refuses over
+  // several mappings is retried extent by extent
+  void unmap_extents(std::vector<std::pair<Region *, size_t>> &v) {
+    if (v.empty()) return;
+    const uint64_t t0 = now_ns();
+    std::sort(v.begin(), v.end());
+    for (size_t i = 0; i < v.size();) {
+      Region &r = *v[i].first;
+      size_t end = v[i].second + r.chunks[v[i].second].len, j = i + 1;
+      while (j < v.size() && v[j].first == &r && v[j].second == end) {
+        end += r.chunks[v[j].second].len;
+        ++j;
+      }
+      const size_t c0 = v[i].second;
+      if (j - i > 1 && drv().unmap(r.base + c0 * r.chunk, (end - c0) * r.chunk) == CUDA_SUCCESS) {
+        for (size_t k = i; k < j; ++k) unmapped(r, v[k].second);
+      } else {
+        for (size_t k = i; k < j; ++k) {
+          drv().unmap(r.base + v[k].second * r.chunk, r.chunks[v[k].second].len * r.chunk);
+          unmapped(r, v[k].second);
+        }
+      }
+      i = j;
+    }
     ns_unmap += now_ns() - t0;
   }
   // Asynchronous trim: extents that lose their last live bucket in a shrink
@@ -436,11 +468,12 @@ struct Slab {
     if (doomed.empty()) return;
     if (wait) cudaEventSynchronize(doom_ev);
     else if (cudaEventQuery(doom_ev) != cudaSuccess) return;
+    std::vector<std::pair<Region *, size_t>> go;
     for (auto &d : doomed) {
       Chunk &hd = d.first->chunks[d.second];
-      if (hd.doomed && hd.mapped && hd.head == d.second && extent_free(*d.first, d.second))
-        unmap_extent(*d.first, d.second);
+      if (hd.doomed && hd.mapped && hd.head == d.second && extent_free(*d.first, d.second)) go.push_back(d);
     }
+    unmap_extents(go);
     doomed.clear();
     doomed_bytes = 0;
   }
@@ -539,14 +572,18 @@ struct Slab {
   void trim_to(uint64_t keep) {
     finalize_access();
     reap_doomed(true);
+    std::vector<std::pair<Region *, size_t>> sel;
+    uint64_t left = mapped;
     auto go = [&](Region &r, size_t head) {
-      if (mapped <= keep) return false;
-      unmap_extent(r, head);
+      if (left <= keep) return false;
+      sel.push_back({&r, head});
+      left -= r.chunks[head].len * r.chunk;
       return true;
     };
-    for (int b = (int)MB - 1; b >= 0 && mapped > keep && cached; --b)
+    for (int b = (int)MB - 1; b >= 0 && left > keep && cached; --b)
       if (small_off[b] == ~uint64_t(0)) for_free_extents(big[b], go);
-    if (mapped > keep) for_free_extents(small, go);
+    if (left > keep) for_free_extents(small, go);
+    unmap_extents(sel);
   }
   // unmap every extent without live buckets (caller synchronised)
   void trim() { trim_to(0); }
@@ -558,12 +595,19 @@ struct Slab {
     doomed_bytes = 0;
     if (doom_ev) cudaEventDestroy(doom_ev), doom_ev = nullptr;
     auto go = [&](Region &r) {
-      for (size_t c = 0; c < r.chunks.size(); ++c) {
-        Chunk &k = r.chunks[c];
-        if (k.mapped && k.head == c) {
-          drv().unmap(r.base + c * r.chunk, k.len * r.chunk);
-          give_or_release(k.len * r.chunk, k.h);
+      // runs of adjacent mapped extents: one cuMemUnmap each (per-extent
+      // calls if the driver refuses the run), handles to the pool
+      for (size_t c = 0; c < r.chunks.size();) {
+        if (!(r.chunks[c].mapped && r.chunks[c].head == c)) { ++c; continue; }
+        size_t e = c;
+        while (e < r.chunks.size() && r.chunks[e].mapped && r.chunks[e].head == e) e += r.chunks[e].len;
+        const bool one = e - c > r.chunks[c].len &&
+                         drv().unmap(r.base + c * r.chunk, (e - c) * r.chunk) == CUDA_SUCCESS;
+        for (size_t h = c; h < e; h += r.chunks[h].len) {
+          if (!one) drv().unmap(r.base + h * r.chunk, r.chunks[h].len * r.chunk);
+          give_or_release(r.chunks[h].len * r.chunk, r.chunks[h].h);
         }
+        c = e;
       }
       if (r.base) drv().addr_free(r.base, r.va);
       r = Region();
