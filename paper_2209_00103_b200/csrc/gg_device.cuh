@@ -1365,19 +1365,54 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
   }
 }
 
-template <int ESZ>
-__global__ void k_gather(Tables t, const int64_t *idx, uint64_t n, char *out, const char *vals,
-                         int scatter) {
+// get_many / set_many (sharded_array.py:152-158 batched): the directory
+// prefix[S+1] staged in shared memory (SMEM, S < 4096) so the bisect of each
+// index costs shared-memory loads, bucket addresses by slot arithmetic, and
+// U independent indices per thread so their random element accesses are in
+// flight together (the kernel is bound by random 32 B sectors, not by the
+// directory chain).
+constexpr int kGatherU = 4;                      // indices per thread (independent chains)
+template <int ESZ, bool SMEM, int U = kGatherU>
+__global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, uint64_t n, char *out,
+                                                const char *vals, int scatter) {
   typedef typename ElemT<ESZ>::T E;
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t g = (uint64_t)idx[j];
-    uint32_t s = upper_shard(t.prefix, t.S, g);
-    uint32_t b; uint64_t o;
-    locate(g - t.prefix[s], t.log2fb, b, o);
-    E *p = (E *)(t.ptr[(size_t)s * t.MB + b]) + o;
-    if (scatter) *p = ((const E *)vals)[j];
-    else ((E *)out)[j] = *p;
+  extern __shared__ uint64_t sdir[];
+  __shared__ char *scb[kMaxBuckets];
+  pdl_begin();
+  stage_cbase(t, scb);
+  if constexpr (SMEM)
+    for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) sdir[i] = t.prefix[i];
+  __syncthreads();
+  const uint64_t *dir = SMEM ? sdir : t.prefix;
+  const uint32_t lg0 = t.log2fb + (ESZ == 1 ? 0 : ESZ == 2 ? 1 : ESZ == 4 ? 2 : 3);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * U;
+  for (uint64_t j0 = (uint64_t)blockIdx.x * blockDim.x * U + threadIdx.x; j0 < n; j0 += stride) {
+    E *p[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t j = j0 + (uint64_t)u * blockDim.x;
+      const uint64_t g = j < n ? (uint64_t)__ldcs(idx + j) : 0;
+      const uint32_t s = upper_shard(dir, t.S, g);
+      uint32_t b; uint64_t o;
+      locate(g - dir[s], t.log2fb, b, o);
+      p[u] = (E *)slot_addr(scb, s, b, lg0) + o;
+    }
+    if (scatter) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t j = j0 + (uint64_t)u * blockDim.x;
+        if (j < n) *p[u] = ((const E *)vals)[j];
+      }
+    } else {
+      E v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = j0 + (uint64_t)u * blockDim.x < n ? *p[u] : E(0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t j = j0 + (uint64_t)u * blockDim.x;
+        if (j < n) ((E *)out)[j] = v[u];
+      }
+    }
   }
 }
 

@@ -1842,21 +1842,39 @@ int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *s
   return walk_copy<W_FLATTEN, false>(a, t, nullptr, base, hi, fz, S_(stream));
 }
 
+namespace {
+// one launch of k_gather for get_many (scatter = 0) / set_many (1)
+int launch_gather(gg_array *a, const int64_t *d_idx, uint64_t n, char *out, const char *vals, int scatter,
+                  cudaStream_t st) {
+  Tables t = tables_for_launch(a, false);
+  const bool smem = a->S < 4096;
+  const size_t sb = smem ? (size_t)(a->S + 1) * 8 : 0;
+  // one tile of 256 x kGatherU indices per CTA (no grid-stride cap): CTAs at different
+  // phases (index loads, bisects, random element accesses) overlap on an SM
+  const uint64_t per_cta = 256ull * kGatherU;
+  const int grid = (int)std::min<uint64_t>((n + per_cta - 1) / per_cta, 0x7fffffffull);
+  cudaError_t e = cudaSuccess;
+#define GG_GATHER(ESZ_) \
+  e = smem ? launch_k(k_gather<ESZ_, true>, grid, 256, sb, st, t, d_idx, n, out, vals, scatter) \
+           : launch_k(k_gather<ESZ_, false>, grid, 256, 0, st, t, d_idx, n, out, vals, scatter);
+  switch (a->esz) {
+    case 1: GG_GATHER(1) break;
+    case 2: GG_GATHER(2) break;
+    case 4: GG_GATHER(4) break;
+    default: GG_GATHER(8) break;
+  }
+#undef GG_GATHER
+  CUDA_TRY(e);
+  return GG_OK;
+}
+}  // namespace
+
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
   { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
-  Tables t = tables_for_launch(a, false);
-  int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
-  switch (a->esz) {
-    case 1: { k_gather<1><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_gather<2><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_gather<4><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 8: { k_gather<8><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, (char *)d_out, nullptr, 0); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-  }
-  CUDA_TRY(cudaGetLastError());
-  return GG_OK;
+  return launch_gather(a, d_idx, n, (char *)d_out, nullptr, 0, S_(stream));
 }
 
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
@@ -1864,16 +1882,7 @@ int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals
   use_dev(a->dev);
   { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
-  Tables t = tables_for_launch(a, false);
-  int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count(a->dev) * 8);
-  switch (a->esz) {
-    case 1: { k_gather<1><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 2: { k_gather<2><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 4: { k_gather<4><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-    case 8: { k_gather<8><<<grid, 256, 0, S_(stream)>>>(t, d_idx, n, nullptr, (const char *)d_vals, 1); g_launches.fetch_add(1, std::memory_order_relaxed); } break;
-  }
-  CUDA_TRY(cudaGetLastError());
-  return GG_OK;
+  return launch_gather(a, d_idx, n, nullptr, (const char *)d_vals, 1, S_(stream));
 }
 
 namespace {

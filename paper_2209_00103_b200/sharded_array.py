@@ -439,8 +439,10 @@ class GrowableArray:
         idx = torch.as_tensor(np.asarray(indices, np.int64) if not isinstance(indices, torch.Tensor)
                               else indices, dtype=torch.int64).to(self.device).contiguous()
         n = self.committed_size
-        if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= n):
-            raise IndexError(f"indices outside committed size {n}")
+        if idx.numel():
+            lo, hi = (int(x) for x in torch.aminmax(idx))    # one pass, one sync
+            if lo < 0 or hi >= n:
+                raise IndexError(f"indices outside committed size {n}")
         out = torch.empty(idx.numel(), dtype=self._torch_dtype, device=self.device)
         L.check(L.lib.gg_gather(self._h, C.c_void_p(idx.data_ptr()), idx.numel(),
                                 C.c_void_p(out.data_ptr()), self._stream()), "gather")
@@ -451,8 +453,10 @@ class GrowableArray:
         idx = torch.as_tensor(np.asarray(indices, np.int64) if not isinstance(indices, torch.Tensor)
                               else indices, dtype=torch.int64).to(self.device).contiguous()
         n = self.committed_size
-        if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= n):
-            raise IndexError(f"indices outside committed size {n}")
+        if idx.numel():
+            lo, hi = (int(x) for x in torch.aminmax(idx))    # one pass, one sync
+            if lo < 0 or hi >= n:
+                raise IndexError(f"indices outside committed size {n}")
         vals = self._device_values(values)
         if vals.numel() != idx.numel():
             raise ValueError("indices and values differ in length")
