@@ -70,6 +70,7 @@ struct gg_array {
   // behind an event and are applied by resolve_lanes (at the next call that
   // reads the host mirrors), which also unbacks the headroom no bucket took.
   bool lanes_pend = false;
+  bool view_pend = false;                                // push_if mirrors pending behind lanes_ev
   cudaEvent_t lanes_ev = nullptr;
   uint64_t *h_lanes = nullptr;                           // pinned [S]
   std::vector<uint32_t> lanes_head;                      // (b, s0, s1) runs backed for the upper bound
@@ -714,7 +715,71 @@ int finish_status(gg_array *a, const Plan &p, int32_t *h_status) {
 // unbacked, and chunks the backing newly mapped beyond max(2 x needed, the
 // mapped bytes before it) are released asynchronously (doomed behind an
 // event, taken back in place if an operation needs them first).
+// issue the readback: one packing kernel (which also clears the status
+// words) + ONE copy into the pinned staging
+int view_finish_issue(gg_array *a, cudaStream_t st) {
+  const size_t S = a->S;
+  const size_t nb = view_pack_bytes(S);
+  if (!a->h_view || a->h_view_cap < nb) {
+    if (a->h_view) CUDA_TRY(cudaFreeHost(a->h_view));
+    a->h_view = nullptr;
+    CUDA_TRY(cudaMallocHost(&a->h_view, nb));
+    a->h_view_cap = nb;
+  }
+  { k_view_pack<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(a->t, a->d_vpack); g_launches.fetch_add(1, std::memory_order_relaxed); }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(a->h_view, a->d_vpack, nb, cudaMemcpyDeviceToHost, st));
+  return GG_OK;
+}
+
+// the host half, once the copy landed: mirrors from the device tables,
+// headroom the kernel took becomes live, the rest is unbacked
+int view_finish_host(gg_array *a, int32_t *h_status, cudaStream_t st) {
+  const size_t S = a->S;
+  char *hb = a->h_view;
+  uint64_t *hs = (uint64_t *)hb, *hc = hs + S, *ho = hc + S, *hp = ho + S;
+  uint32_t *hst = (uint32_t *)(hp + S);
+  unsigned long long *hm = (unsigned long long *)(hb + S * 32 + ((S * 4 + 7) & ~size_t(7)));
+  bool any = false;
+  for (size_t s = 0; s < S; ++s) {
+    a->size[s] = hs[s];
+    a->cap[s] = hc[s];
+    a->ops[s] = ho[s];
+    // pmask bits are set after the once-flag is published (and never for a
+    // rolled-back allocation): at kernel completion they are the published set
+    a->flags[s] = hp[s];
+    if (h_status) h_status[s] = (int32_t)hst[s];
+    if (hst[s]) { any = true; a->dirty[s] = 1; }
+  }
+  a->alloc_calls = hm[MISC_ALLOCS];
+  for (size_t i = 0; i < a->headroom.size(); i += 3) {
+    const uint32_t b = a->headroom[i];
+    for (uint32_t s = a->headroom[i + 1]; s < a->headroom[i + 2]; ++s) {
+      if (a->flags[s] >> b & 1) a->live += bucket_bytes(a, b);
+      else a->slab.unback(s, b);
+    }
+  }
+  a->headroom.clear();
+  // headroom chunks no bucket took: released asynchronously down to
+  // max(2 x needed, the mapped bytes before the view), unless the array
+  // keeps its cache (release=False)
+  uint64_t need = 0;
+  for (size_t s = 0; s < S; ++s) need += a->size[s];
+  const uint64_t keep = std::max<uint64_t>(2 * need * a->esz, a->view_keep);
+  if (!a->keep_cached && a->slab.cached && a->slab.mapped - a->slab.doomed_bytes > keep) {
+    int drc = a->slab.doom_to(keep, st);
+    if (drc) return drc;
+  }
+  return any ? fail(GG_EPARTIAL, "device-side appends failed on some shards") : GG_OK;
+}
+
 int resolve_lanes(gg_array *a) {
+  if (a->view_pend) {                 // a push_if whose appends could not fail (see gg_push_if)
+    CUDA_TRY(cudaEventSynchronize(a->lanes_ev));
+    a->view_pend = false;
+    const int rc = view_finish_host(a, nullptr, a->have_last ? a->last_st : nullptr);
+    if (rc && rc != GG_EPARTIAL) return rc;
+  }
   if (!a->lanes_pend) return GG_OK;
   CUDA_TRY(cudaEventSynchronize(a->lanes_ev));
   a->lanes_pend = false;
@@ -1940,7 +2005,8 @@ namespace {
 // live-bytes cap allows) and publish the backed-slot masks on stream st.
 // sync: wait for the device (the public entry point, whose user kernel may
 // run on any stream); the library's own push_if stays stream-ordered.
-int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool sync, gg_device_view *out) {
+int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool sync, gg_device_view *out,
+                 bool *complete = nullptr) {
   if (a->view_out) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
   std::vector<unsigned long long> am(a->S);
   uint64_t live = a->live;
@@ -1998,6 +2064,7 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
       }
     }
   }
+  if (complete) *complete = !stop;
   int rc = push_cbase(a, st);
   if (rc) return rc;
   void *dst[1] = {a->t.amask};
@@ -2016,56 +2083,11 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
 // asynchronous copy of sizes / capacities / ops / published masks / status /
 // counters into a pinned buffer and ONE stream synchronize
 int view_finish(gg_array *a, int32_t *h_status, cudaStream_t st) {
-  const size_t S = a->S;
-  const size_t nb = view_pack_bytes(S);
-  if (!a->h_view || a->h_view_cap < nb) {
-    if (a->h_view) CUDA_TRY(cudaFreeHost(a->h_view));
-    a->h_view = nullptr;
-    CUDA_TRY(cudaMallocHost(&a->h_view, nb));
-    a->h_view_cap = nb;
-  }
-  char *hb = a->h_view;
-  uint64_t *hs = (uint64_t *)hb, *hc = hs + S, *ho = hc + S, *hp = ho + S;
-  uint32_t *hst = (uint32_t *)(hp + S);
-  unsigned long long *hm = (unsigned long long *)(hb + S * 32 + ((S * 4 + 7) & ~size_t(7)));
-  // one packing kernel (which also clears the status words) + ONE copy
-  { k_view_pack<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(a->t, a->d_vpack); g_launches.fetch_add(1, std::memory_order_relaxed); }
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaMemcpyAsync(hb, a->d_vpack, nb, cudaMemcpyDeviceToHost, st));
+  int rc = view_finish_issue(a, st);
+  if (rc) return rc;
   CUDA_TRY(cudaStreamSynchronize(st));
   a->view_out = false;
-  bool any = false;
-  for (size_t s = 0; s < S; ++s) {
-    a->size[s] = hs[s];
-    a->cap[s] = hc[s];
-    a->ops[s] = ho[s];
-    // pmask bits are set after the once-flag is published (and never for a
-    // rolled-back allocation): at kernel completion they are the published set
-    a->flags[s] = hp[s];
-    if (h_status) h_status[s] = (int32_t)hst[s];
-    if (hst[s]) { any = true; a->dirty[s] = 1; }
-  }
-  a->alloc_calls = hm[MISC_ALLOCS];
-  // headroom the kernel took becomes live; the rest is unbacked
-  for (size_t i = 0; i < a->headroom.size(); i += 3) {
-    const uint32_t b = a->headroom[i];
-    for (uint32_t s = a->headroom[i + 1]; s < a->headroom[i + 2]; ++s) {
-      if (a->flags[s] >> b & 1) a->live += bucket_bytes(a, b);
-      else a->slab.unback(s, b);
-    }
-  }
-  a->headroom.clear();
-  // headroom chunks no bucket took: released asynchronously down to
-  // max(2 x needed, the mapped bytes before the view), unless the array
-  // keeps its cache (release=False)
-  uint64_t need = 0;
-  for (size_t s = 0; s < S; ++s) need += a->size[s];
-  const uint64_t keep = std::max<uint64_t>(2 * need * a->esz, a->view_keep);
-  if (!a->keep_cached && a->slab.cached && a->slab.mapped - a->slab.doomed_bytes > keep) {
-    int drc = a->slab.doom_to(keep, st);
-    if (drc) return drc;
-  }
-  return any ? fail(GG_EPARTIAL, "device-side appends failed on some shards") : GG_OK;
+  return view_finish_host(a, h_status, st);
 }
 }  // namespace
 
@@ -2130,8 +2152,15 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   }
   for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += a->size[s];
   gg_device_view v;
-  int rc = view_prepare(a, maxsz.data(), st, false, &v);
+  bool backed = false;
+  int rc = view_prepare(a, maxsz.data(), st, false, &v, &backed);
   if (rc) return rc;
+  // every slot the launch can reach is backed and within max_buckets: no
+  // append can fail, so the host mirrors are refreshed lazily (the readback
+  // is queued behind an event and resolved by the next call that needs the
+  // mirrors, like the lanes insert) instead of waiting for the kernel here
+  bool can_fail = !backed;
+  for (uint32_t s = 0; s < a->S && !can_fail; ++s) can_fail = min_buckets_for(a, maxsz[s]) > a->MB;
   const int al = ((uintptr_t)d_vals % (kPushG * a->esz) == 0 && (uintptr_t)d_pred % kPushG == 0) ? 1 : 0;
   switch (a->esz) {
 #define GG_PUSH_CASE(ESZ_) \
@@ -2144,7 +2173,14 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
 #undef GG_PUSH_CASE
   }
   CUDA_TRY(cudaGetLastError());
-  return view_finish(a, h_status, st);
+  if (can_fail || capturing_now(a, st)) return view_finish(a, h_status, st);
+  if ((rc = view_finish_issue(a, st))) return rc;
+  if (!a->lanes_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->lanes_ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(a->lanes_ev, st));
+  a->view_pend = true;
+  a->view_out = false;
+  if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
+  return GG_OK;
 }
 
 int gg_set_tuning(int32_t ls, int32_t unroll, uint32_t tile_bytes, uint32_t threads) {
