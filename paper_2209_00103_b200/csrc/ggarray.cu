@@ -1710,7 +1710,14 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   // (GG_LANES_CHAIN=0): tiles of T lanes for k_lanes_sum / k_lanes_scatter
   static const bool chain = [] { const char *e = getenv("GG_LANES_CHAIN"); return !e || e[0] != '0'; }();
   const uint32_t T = (uint32_t)(256 * (64 / KB));
-  const uint32_t unit = chain ? kLanesChunk : T;
+  // lanes per chunk (GG_LANES_C: A/B, a multiple of the tile)
+  static const uint32_t chunk_lanes = [] {
+    const char *e = getenv("GG_LANES_C");
+    const long v = e ? atol(e) : 0;
+    return v >= 4096 && v <= (1 << 20) && (v & (v - 1)) == 0 ? (uint32_t)v : kLanesChunk;
+  }();
+  const uint32_t C = std::max<uint32_t>(chunk_lanes, T);
+  const uint32_t unit = chain ? C : T;
   std::vector<uint32_t> tpre(S + 1);
   uint64_t nt = 0;
   for (uint32_t s = 0; s < S; ++s) {
@@ -1763,9 +1770,9 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
         attr.fetch_or(bit, std::memory_order_acq_rel); \
       } \
       e = launch_k(k_lanes_bulk<ESZ_, KB_, 2>, (unsigned)nt, 256, (size_t)2 * 16384, st, t, dv, d_counts, tp, d_chain, \
-                   kLanesChunk); \
+                   C); \
     } else { \
-      e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, kLanesChunk); \
+      e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, C); \
     } \
     break;
     switch (a->esz) {
