@@ -47,6 +47,16 @@ for name, title in (("lanes_host_probe", "insert_lanes host time per call (µs)"
     d = data.get(name)
     if d:
         L += [f"## {title}", "", "```", json.dumps(d, indent=1), "```", ""]
+gp = data.get("gather_probe")
+if gp and "get_many" in gp:
+    L += ["## get_many / set_many, 2^24 random global indices on a 2^30-element GGArray (512 LFVectors)", "",
+          "Next to torch's index_select / index_put_ on the flat array with the same index stream (the "
+          "random-access reference: each access costs a DRAM burst whatever the layout).", "",
+          "| op | GGArray ms | Gelem/s | torch flat ms | Gelem/s | contents ok |", "|---|---|---|---|---|---|",
+          f"| gather | {gp['get_many']['ms']} | {gp['get_many']['gelem_s']} | {gp['torch_flat_gather']['ms']} | "
+          f"{gp['torch_flat_gather']['gelem_s']} | {gp['get_ok']} |",
+          f"| scatter | {gp['set_many']['ms']} | {gp['set_many']['gelem_s']} | {gp['torch_flat_scatter']['ms']} | "
+          f"{gp['torch_flat_scatter']['gelem_s']} | {gp['set_ok']} |", ""]
 vm = data.get("vmm_fresh_probe")
 if vm:
     L += ["## CUDA VMM cost in a fresh process (8 GiB, create + map + access, then unmap + release; "
