@@ -138,11 +138,11 @@ __device__ inline bool ensure_buckets(const gg_device_view &t, uint32_t s, uint6
   locate(start, t.log2fb, b0, o);
   locate(start + n - 1, t.log2fb, b1, o);
   bool ok = b1 < t.MB;
-  // the once-flag (acquire) is the authority, not pmask: a bucket another warp
-  // is still allocating (flag 1) must be waited for, or this warp's lanes
-  // would find it unpublished and drop their stores
   // fast path: one acquire load of the shard's published-bucket mask (a pmask
-  // bit is set only after its flag was released as published)
+  // bit is set only after its flag was released as published).  A missing
+  // bit proves nothing -- the bucket may be mid-publication -- so the
+  // once-flag is the authority below: a bucket another warp is still
+  // allocating (flag 1) is waited for, a rolled-back one (no backing) fails
   if (ok) {
     const unsigned long long want = (b1 >= 63 ? ~0ull : ((2ull << b1) - 1ull)) & ~((1ull << b0) - 1ull);
     if ((ld_acquire64(reinterpret_cast<const uint64_t *>(t.pmask + s)) & want) == want) return true;
@@ -227,6 +227,9 @@ __device__ inline bool warp_reserve_ensure(const gg_device_view &t, uint32_t s, 
 // Bucket base of (s, b) read with acquire order: the flag load synchronises
 // with the allocator's release, so the pointer read after it is current even
 // if another SM allocated the bucket (plain loads could hit a stale L1 line).
+// For user kernels that read buckets they did not reserve themselves; the
+// append paths above use bucket_known (their reservation already proved the
+// bucket published).
 __device__ __forceinline__ char *bucket_acquire(const gg_device_view &t, uint32_t s, uint32_t b) {
   if (b >= t.MB || ld_acquire(t.flag + (size_t)s * t.MB + b) != kFlagPublished) return nullptr;
   char *p;
