@@ -899,69 +899,90 @@ namespace gg {
 // candidates i of its slices with pred[i] != 0 to shard b % S, warp- or
 // block-aggregated.  Slice = kPushSlice consecutive candidates: block b
 // takes slice b of every round of grid x kPushSlice candidates.  Each thread
-// loads G = 4 consecutive candidates per round (one 16 B / 8 B / 4 B vector
-// of values + 4 predicate bytes) for R rounds into registers with a
-// (G x R)-bit keep mask and appends them with ONE warp- or block-aggregated
-// reservation per call (block mode: the run is staged in shared memory and
-// leaves as 16 B vector stores); all indexing static (no local memory).
-constexpr uint32_t kPushG = 4, kPushSlice = 256 * kPushG;
+// loads G consecutive candidates at a time -- one 16 B vector of values
+// (32 B for 8 B elements) and G predicate bytes (a 4 / 8 / 16 B vector) --
+// K per append call, into registers with a K-bit keep mask, and appends them
+// with ONE warp- or block-aggregated reservation per call (block mode: the
+// run is staged in shared memory and leaves as 16 B vector stores); all
+// indexing static (no local memory).  For 1 / 2 B elements G = 16 / 8, so a
+// slice is covered by 64 / 128 threads and one load sweep of the block
+// covers 4 / 2 rounds (the same 8 rounds per call as 4 B elements).
+constexpr uint32_t kPushSlice = 1024;
+
+template <int ESZ, int BLOCK>
+struct PushShape {
+  static constexpr uint32_t G = ESZ >= 4 ? 4 : 16 / ESZ;   // candidates per load
+  static constexpr uint32_t K = ESZ == 8 ? 16 : 32;         // candidates per thread per append call
+  static constexpr uint32_t J = K / G;                      // loads per thread per call
+  static constexpr uint32_t TPS = kPushSlice / G;           // threads per slice
+  static constexpr uint32_t RPL = BLOCK / TPS;              // rounds per load sweep
+  static constexpr uint32_t RPC = J * RPL;                  // rounds per call
+  static_assert(BLOCK % TPS == 0, "a block covers whole slices");
+};
 
 template <int ESZ, int BLOCK, bool BLOCK_MODE>
 __global__ void __launch_bounds__(BLOCK, ESZ >= 4 ? 4 : 6) k_push_if(gg_device_view t, const char *vals,
                                                    const uint8_t *pred, uint64_t n, int aligned) {
   typedef typename ElemT<ESZ>::T E;
-  constexpr uint32_t kPushR = ESZ == 8 ? 4 : 8;         // rounds per append call
-  constexpr int K = kPushG * kPushR;
+  typedef PushShape<ESZ, BLOCK> P;
+  constexpr uint32_t G = P::G, J = P::J, RPL = P::RPL;
+  constexpr int K = (int)P::K;
   __shared__ unsigned long long scratch[34];
   // block mode: one run of up to BLOCK*K staged; warp mode: a private slice
   // of 32*K + 32/ESZ elements per warp (16 B multiples)
   __shared__ __align__(16) E stage[BLOCK * K + (BLOCK_MODE ? 1 : BLOCK / 32) * (32 / ESZ)];
   const uint32_t s = blockIdx.x % t.S;
   const uint64_t round = (uint64_t)gridDim.x * kPushSlice;
-  for (uint64_t r0 = 0; (uint64_t)blockIdx.x * kPushSlice + r0 * round < n; r0 += kPushR) {
+  // this thread's candidates: load j of a call starting at round r0 covers
+  // round r0 + j * RPL + sub, positions [pos, pos + G) of the block's slice
+  const uint64_t sub = threadIdx.x / P::TPS, pos = (threadIdx.x % P::TPS) * G;
+  for (uint64_t r0 = 0; (uint64_t)blockIdx.x * kPushSlice + r0 * round < n; r0 += P::RPC) {
     E v[K];
     uint32_t mask = 0;
-    const uint64_t i0 = (uint64_t)blockIdx.x * kPushSlice + r0 * round + threadIdx.x * kPushG;
-    if (aligned && i0 + (kPushR - 1) * round + kPushG <= n) {
-      // interior: every round in bounds -- all R rounds' loads are issued
-      // before any is consumed (a per-round bounds branch around load + use
-      // would serialise them: one round of loads in flight per thread)
-      uint32_t p4[kPushR];
+    const uint64_t i0 = (uint64_t)blockIdx.x * kPushSlice + (r0 + sub) * round + pos;
+    if (aligned && i0 + (uint64_t)(J - 1) * RPL * round + G <= n) {
+      // interior: every load in bounds -- all J loads are issued before any
+      // is consumed (a per-load bounds branch around load + use would
+      // serialise them: one load in flight per thread)
+      uint32_t pw[J][G / 4];
 #pragma unroll
-      for (int j = 0; j < (int)kPushR; ++j) {
-        const uint64_t i = i0 + j * round;
-        p4[j] = __ldcs(reinterpret_cast<const uint32_t *>(pred + i));
-        if constexpr (ESZ * kPushG == 16) {
+      for (int j = 0; j < (int)J; ++j) {
+        const uint64_t i = i0 + (uint64_t)j * RPL * round;
+        if constexpr (G == 16) {
+          const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(pred + i));
+          pw[j][0] = q.x; pw[j][1] = q.y; pw[j][2] = q.z; pw[j][3] = q.w;
+        } else if constexpr (G == 8) {
+          const uint2 q = __ldcs(reinterpret_cast<const uint2 *>(pred + i));
+          pw[j][0] = q.x; pw[j][1] = q.y;
+        } else {
+          pw[j][0] = __ldcs(reinterpret_cast<const uint32_t *>(pred + i));
+        }
+        if constexpr (ESZ * G == 16) {
           const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ));
-          memcpy(&v[j * kPushG], &q, 16);
-        } else if constexpr (ESZ * kPushG == 8) {
-          const uint2 q = __ldcs(reinterpret_cast<const uint2 *>(vals + i * ESZ));
-          memcpy(&v[j * kPushG], &q, 8);
-        } else if constexpr (ESZ * kPushG == 4) {
-          const uint32_t q = __ldcs(reinterpret_cast<const uint32_t *>(vals + i * ESZ));
-          memcpy(&v[j * kPushG], &q, 4);
+          memcpy(&v[j * G], &q, 16);
         } else {
           const uint4 q0 = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ));
           const uint4 q1 = __ldcs(reinterpret_cast<const uint4 *>(vals + i * ESZ) + 1);
-          memcpy(&v[j * kPushG], &q0, 16);
-          memcpy(&v[j * kPushG + 2], &q1, 16);
+          memcpy(&v[j * G], &q0, 16);
+          memcpy(&v[j * G + 2], &q1, 16);
         }
       }
 #pragma unroll
-      for (int j = 0; j < (int)kPushR; ++j)
+      for (int j = 0; j < (int)J; ++j)
 #pragma unroll
-        for (int g = 0; g < (int)kPushG; ++g) mask |= ((p4[j] >> (8 * g)) & 0xffu ? 1u : 0u) << (j * kPushG + g);
+        for (int g = 0; g < (int)G; ++g)
+          mask |= ((pw[j][g >> 2] >> (8 * (g & 3))) & 0xffu ? 1u : 0u) << (j * G + g);
     } else {
       // the last rounds of the input (or an unaligned input): element loads
 #pragma unroll
-      for (int j = 0; j < (int)kPushR; ++j) {
-        const uint64_t i = i0 + j * round;
+      for (int j = 0; j < (int)J; ++j) {
+        const uint64_t i = i0 + (uint64_t)j * RPL * round;
 #pragma unroll
-        for (int g = 0; g < (int)kPushG; ++g) {
-          v[j * kPushG + g] = E(0);
+        for (int g = 0; g < (int)G; ++g) {
+          v[j * G + g] = E(0);
           if (i + g < n) {
-            v[j * kPushG + g] = __ldcs(reinterpret_cast<const E *>(vals) + i + g);
-            mask |= (__ldcs(pred + i + g) ? 1u : 0u) << (j * kPushG + g);
+            v[j * G + g] = __ldcs(reinterpret_cast<const E *>(vals) + i + g);
+            mask |= (__ldcs(pred + i + g) ? 1u : 0u) << (j * G + g);
           }
         }
       }
@@ -2168,7 +2189,9 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   // mirrors, like the lanes insert) instead of waiting for the kernel here
   bool can_fail = !backed;
   for (uint32_t s = 0; s < a->S && !can_fail; ++s) can_fail = min_buckets_for(a, maxsz[s]) > a->MB;
-  const int al = ((uintptr_t)d_vals % (kPushG * a->esz) == 0 && (uintptr_t)d_pred % kPushG == 0) ? 1 : 0;
+  // vector loads: 16 B of values (8 B elements: 32 B) and G predicate bytes
+  const uint32_t pg = a->esz >= 4 ? 4 : 16 / a->esz;
+  const int al = ((uintptr_t)d_vals % (pg * a->esz) == 0 && (uintptr_t)d_pred % pg == 0) ? 1 : 0;
   switch (a->esz) {
 #define GG_PUSH_CASE(ESZ_) \
     case ESZ_: \
