@@ -375,11 +375,26 @@ __device__ inline uint64_t warp_push_back_staged(const gg_device_view &t, uint32
   __syncwarp();
   if (vec) {
     const uint32_t nv = (shift + total + VE - 1) / VE;
+    // the run (warp-uniform) usually lies in ONE bucket: one address
+    // computation, each vector an offset from it
+    // (4 / 8 B elements; for 1 / 2 B the extra live registers cost more)
+    uint32_t bf = 0, bl = 1;
+    uint64_t of = 0, ol;
+    if (sizeof(T) >= 4) {
+      locate(start - shift, t.log2fb, bf, of);
+      locate(start + total - 1, t.log2fb, bl, ol);
+    }
+    T *const rbase = bf == bl ? reinterpret_cast<T *>(bucket_known(t, s, bf)) + of : nullptr;
     for (uint32_t v = lane; v < nv; v += 32) {
-      uint32_t b;
-      uint64_t o;
-      locate(start - shift + (uint64_t)v * VE, t.log2fb, b, o);
-      T *dp = reinterpret_cast<T *>(bucket_known(t, s, b)) + o;
+      T *dp;
+      if (bf == bl) {
+        dp = rbase + v * VE;
+      } else {
+        uint32_t b;
+        uint64_t o;
+        locate(start - shift + (uint64_t)v * VE, t.log2fb, b, o);
+        dp = reinterpret_cast<T *>(bucket_known(t, s, b)) + o;
+      }
       const uint32_t k0 = v * VE;
       if (k0 >= shift && k0 + VE <= shift + total) {
         const uint4 q = reinterpret_cast<const uint4 *>(stage)[v];
@@ -529,13 +544,29 @@ __device__ inline uint64_t block_push_back_staged(const gg_device_view &t, uint3
   if (ok && total) {
     if (vec) {
       const uint32_t nv = (uint32_t)((shift + total + VE - 1) / VE);
+      // the run usually lies in ONE bucket: one address computation, each
+      // vector an offset from it
+      // (4 / 8 B elements; for 1 / 2 B the extra live registers cost more)
+      uint32_t bf = 0, bl = 1;
+      uint64_t of = 0, ol;
+      if (sizeof(T) >= 4) {
+        locate(start - shift, t.log2fb, bf, of);
+        locate(start + total - 1, t.log2fb, bl, ol);
+      }
+      T *const rbase = bf == bl && bptr_s[bf] ? reinterpret_cast<T *>(bptr_s[bf]) + of : nullptr;
       for (uint32_t v = tid; v < nv; v += BLOCK) {
-        uint32_t b;
-        uint64_t o;
-        locate(start - shift + (uint64_t)v * VE, t.log2fb, b, o);
-        char *base = bptr_s[b];
-        if (!base) continue;
-        T *dp = reinterpret_cast<T *>(base) + o;
+        T *dp;
+        if (bf == bl) {
+          if (!rbase) break;
+          dp = rbase + v * VE;
+        } else {
+          uint32_t b;
+          uint64_t o;
+          locate(start - shift + (uint64_t)v * VE, t.log2fb, b, o);
+          char *base = bptr_s[b];
+          if (!base) continue;
+          dp = reinterpret_cast<T *>(base) + o;
+        }
         const uint32_t k0 = v * VE;
         if (k0 >= shift && k0 + VE <= shift + total) {
           const uint4 q = reinterpret_cast<const uint4 *>(stage)[v];
