@@ -24,6 +24,9 @@
 
 using namespace gg;
 
+// pending tiled lanes inserts that may chain before their sizes are read back
+constexpr uint32_t kLanesChain = 8;
+
 struct gg_array {
   int dev;
   uint32_t S, fb, log2fb, dtype, esz, MB;
@@ -69,10 +72,16 @@ struct gg_array {
   // values_per_lane; the sizes it reached come back through a pinned buffer
   // behind an event and are applied by resolve_lanes (at the next call that
   // reads the host mirrors), which also unbacks the headroom no bucket took.
+  // Consecutive tiled lanes inserts chain without that round trip: the next
+  // one plans on the pending upper bounds (lanes_ub, buckets already backed
+  // for them in lanes_hb) and queues its own readback (up to kLanesChain
+  // pending calls; resolve_lanes applies them in order).
   bool lanes_pend = false;
+  uint32_t lanes_n = 0;                                  // pending tiled lanes calls
+  std::vector<uint64_t> lanes_ub, lanes_hb;              // [S] pending upper bounds / backed-bucket masks
   bool view_pend = false;                                // push_if mirrors pending behind lanes_ev
   cudaEvent_t lanes_ev = nullptr;
-  uint64_t *h_lanes = nullptr;                           // pinned [S]
+  uint64_t *h_lanes = nullptr;                           // pinned [kLanesChain x S]
   std::vector<uint32_t> lanes_head;                      // (b, s0, s1) runs backed for the upper bound
   uint64_t lanes_keep = 0;                               // mapped bytes before that backing
   uint64_t view_keep = 0;                                // mapped bytes before a device view's headroom
@@ -783,11 +792,19 @@ int resolve_lanes(gg_array *a) {
   if (!a->lanes_pend) return GG_OK;
   CUDA_TRY(cudaEventSynchronize(a->lanes_ev));
   a->lanes_pend = false;
+  const uint32_t n = a->lanes_n;
+  a->lanes_n = 0;
+  std::fill(a->lanes_hb.begin(), a->lanes_hb.end(), 0);
   uint64_t need = 0;
   for (uint32_t s = 0; s < a->S; ++s) {
-    const uint64_t ns = a->h_lanes[s], os = a->size[s];
+    const uint64_t os = a->size[s];
+    uint64_t ns = os;
+    for (uint32_t k = 0; k < n; ++k)            // the pending calls in order: one op each that appended
+      if (a->h_lanes[(size_t)k * a->S + s] > ns) {
+        ns = a->h_lanes[(size_t)k * a->S + s];
+        a->ops[s] += 1;
+      }
     if (ns > os) {
-      a->ops[s] += 1;
       uint32_t b0, b1; uint64_t o;
       host_locate(a, os, b0, o);
       host_locate(a, ns - 1, b1, o);
@@ -1684,12 +1701,17 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   std::vector<uint32_t> head;               // (b, s0, s1) runs backed
   std::vector<uint32_t> nb0(S, 1), nb1(S, 0);
   uint32_t bmin = a->MB, bmax = 0;
+  // the sizes this call starts from: exact, or the upper bounds of the
+  // pending (chained) calls
+  if (a->lanes_ub.size() != S) { a->lanes_ub.assign(S, 0); a->lanes_hb.assign(S, 0); }
+  const uint64_t *base = a->lanes_pend ? a->lanes_ub.data() : a->size.data();
+  const uint64_t *hb = a->lanes_hb.data();  // buckets the pending calls backed (zero when none)
   for (uint32_t s = 0; s < S; ++s) {
     const uint64_t U = (off[s + 1] - off[s]) * K;
     if (!U) continue;
     uint64_t o;
-    host_locate(a, a->size[s], nb0[s], o);
-    host_locate(a, a->size[s] + U - 1, nb1[s], o);
+    host_locate(a, base[s], nb0[s], o);
+    host_locate(a, base[s] + U - 1, nb1[s], o);
     if (nb1[s] >= a->MB) return GG_ENOTSUP;
     bmin = std::min(bmin, nb0[s]);
     bmax = std::max(bmax, nb1[s]);
@@ -1698,7 +1720,7 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   for (uint32_t b = bmin; b <= bmax && b < a->MB && ok; ++b) {
     bool have_region = false;
     for (uint32_t s = 0; s < S && ok;) {
-      auto need = [&](uint32_t x) { return nb0[x] <= b && b <= nb1[x] && !(a->flags[x] >> b & 1); };
+      auto need = [&](uint32_t x) { return nb0[x] <= b && b <= nb1[x] && !((a->flags[x] | hb[x]) >> b & 1); };
       if (!need(s)) { ++s; continue; }
       uint32_t e = s + 1;
       while (e < S && need(e)) ++e;
@@ -1763,7 +1785,7 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
   const void *src[2] = {off, tpre.data()};
   size_t bytes[2] = {(size_t)(S + 1) * 8, (size_t)(S + 1) * 4};
   if ((rc = a->up.upload(st, 2, dst, src, bytes))) return rc;
-  if (!a->h_lanes) CUDA_TRY(cudaMallocHost(&a->h_lanes, S * 8));
+  if (!a->h_lanes) CUDA_TRY(cudaMallocHost(&a->h_lanes, (size_t)kLanesChain * S * 8));
   if (!a->lanes_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->lanes_ev, cudaEventDisableTiming));
   Tables t = tables_for_launch(a, false);
   if (chain) {
@@ -1822,11 +1844,20 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
 #undef GG_LANES_CASE
   CUDA_TRY(e);
   }
-  CUDA_TRY(cudaMemcpyAsync(a->h_lanes, a->t.size, S * 8, cudaMemcpyDeviceToHost, st));
+  const uint32_t k = a->lanes_pend ? a->lanes_n : 0;
+  CUDA_TRY(cudaMemcpyAsync(a->h_lanes + (size_t)k * S, a->t.size, S * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaEventRecord(a->lanes_ev, st));
+  if (!a->lanes_pend) {
+    a->lanes_head.swap(head);
+    a->lanes_keep = mapped0;
+  } else {
+    a->lanes_head.insert(a->lanes_head.end(), head.begin(), head.end());
+  }
+  for (size_t i = 0; i < head.size(); i += 3)
+    for (uint32_t s = head[i + 1]; s < head[i + 2]; ++s) a->lanes_hb[s] |= uint64_t(1) << head[i];
+  for (uint32_t s = 0; s < S; ++s) a->lanes_ub[s] = base[s] + (off[s + 1] - off[s]) * K;
   a->lanes_pend = true;
-  a->lanes_head.swap(head);
-  a->lanes_keep = mapped0;
+  a->lanes_n = k + 1;
   return GG_OK;
 }
 }  // namespace
@@ -1836,8 +1867,18 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
                     int32_t *h_status, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   cudaStream_t st = S_(stream);
+  // a tiled lanes insert pending (and nothing else): chain behind it without
+  // waiting for its sizes (lanes_tiled plans on its upper bounds); any other
+  // path resolves it first
+  const bool chain = a->lanes_pend && !a->view_pend && a->lanes_n < kLanesChain;
+  {
+    int frc_ = check_no_view(a);
+    if (!frc_) frc_ = chain ? order_stream(a, st) : enter(a, st);
+    if (!frc_ && chain) frc_ = flush_meta(a, st, true);
+    if (!frc_ && chain) frc_ = flush_grow(a, st, true);
+    if (frc_) return frc_;
+  }
   if (h_lane_offsets[0] != 0) return fail(GG_EVALUE, "lane offsets must start at 0");
   for (uint32_t s = 0; s < a->S; ++s)
     if (h_lane_offsets[s + 1] < h_lane_offsets[s]) return fail(GG_EVALUE, "lane offsets must be non-decreasing");
@@ -1852,6 +1893,8 @@ int gg_insert_lanes(gg_array *a, const void *d_values, const uint32_t *d_counts,
       if (!frc && h_status) memset(h_status, 0, a->S * sizeof(int32_t));
       return frc;
     }
+    // the exact path plans on exact sizes: finish what the chain skipped
+    if (chain && (frc = enter(a, st))) return frc;
   }
   // exact two-pass path (allocator hook, live-bytes limit, shards with a
   // failed reservation, capacity exhaustion possible within the upper bound,

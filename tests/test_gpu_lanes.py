@@ -167,3 +167,38 @@ def test_lanes_values_not_16B_aligned(gg, K, shift):
     a.insert_lanes(vals, counts, lo, values_per_lane=K)
     o.insert_parallel(_compact(vals.cpu().numpy(), counts, lo, K, S))
     _check(a, o)
+
+
+def test_lanes_chained_calls(gg):
+    """Consecutive tiled lanes inserts chain without a host round trip (each
+    plans on the previous calls' upper bounds, kLanesChain = 8 pending at
+    most): 20 calls with mixed widths, element-sized ragged shards, a call
+    that must take the exact path mid-chain (unaligned values) and calls on a
+    second stream; sizes, capacities, bucket flags, ops and contents equal
+    the oracle fed the same compactions in order, and the upper-bound
+    backing is returned once the chain resolves."""
+    import torch
+    rng = np.random.default_rng(2024)
+    S, fb = 29, 8
+    a = gg.GrowableArray(S, fb, dtype=np.int32)
+    o = O.OracleGGArray(S, fb, dtype=np.int32)
+    side = torch.cuda.Stream()
+    for rnd in range(20):
+        K = [1, 2, 4, 8, 16, 3][rnd % 6]
+        lo, counts = _lanes(rng, S, K, [5, 300, 4000][rnd % 3], empty_every=3 + rnd % 4)
+        n = int(lo[-1]) * K
+        shift = 1 if rnd == 11 else 0                  # 4 B aligned only: exact path mid-chain
+        base = torch.from_numpy(rng.integers(-2**31, 2**31 - 1, n + shift).astype(np.int32)).cuda()
+        vals = base[shift:]
+        if rnd in (6, 7, 15):
+            torch.cuda.current_stream().synchronize()
+            with torch.cuda.stream(side):
+                a.insert_lanes(vals, counts, lo, values_per_lane=K, commit=False)
+        else:
+            a.insert_lanes(vals, counts, lo, values_per_lane=K, commit=False)
+        o.insert_parallel(_compact(vals.cpu().numpy(), counts, lo, K, S))
+    a.commit()
+    o.commit()
+    _check(a, o)
+    ms = a.memory_stats()
+    assert ms["mapped_bytes"] <= 2 * ms["needed_bytes"] + (4 << 20)

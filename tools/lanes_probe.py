@@ -3,7 +3,9 @@ K and element sizes at ~2^28 appended elements over 512 LFVectors; A/B of the
 one-pass chained kernel against the 3-pass path with GG_LANES_CHAIN=0.
 Algorithmic bytes = counts (4 B / lane) + the [lanes x K] value block + the
 compacted output.  Also a repetition check of the look-back (contents of
-every run compared) with PROBE_REPS."""
+every run compared) with PROBE_REPS.  `chained`: CHAIN back-to-back calls
+between two events (each planned on the previous calls' upper bounds, no
+wait for their sizes), per call."""
 import json
 import os
 import sys
@@ -24,7 +26,10 @@ TD = {1: torch.int8, 2: torch.int16, 4: torch.int32, 8: torch.int64}
 ND = {1: np.int8, 2: np.int16, 4: np.int32, 8: np.int64}
 
 
-def run(K, esz, target=1 << 28, reps=5, ragged=False):
+CHAIN = 4
+
+
+def run(K, esz, target=1 << 28, reps=5, ragged=False, chained=True):
     L = max(S, (2 * target // K) // S * S) if K > 1 else target
     g = torch.Generator(device=dev).manual_seed(K * 10 + esz)
     cnt = torch.randint(0, K + 1, (L,), dtype=torch.int32, device=dev, generator=g)
@@ -51,12 +56,37 @@ def run(K, esz, target=1 << 28, reps=5, ragged=False):
         best = min(best, e0.elapsed_time(e1))
     a.commit()
     mask = torch.arange(K, device=dev)[None, :] < cnt[:, None]
-    ok = bool(torch.equal(a.flatten_device(), vals.view(-1, K)[mask]))
+    comp = vals.view(-1, K)[mask]
+    ok = bool(torch.equal(a.flatten_device(), comp))
     nbytes = 4 * L + esz * L * K + esz * tot
+    # CHAIN back-to-back calls between two events: each plans on the previous
+    # calls' upper bounds (no wait for their sizes), so host planning overlaps
+    # the device work of the call before
+    best_c = 1e9
+    for _ in range(3 if chained else 0):
+        a.shrink(0, release=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        for _ in range(CHAIN):
+            a.insert_lanes(vals, cnt, lo, K, commit=False)
+        e1.record()
+        torch.cuda.synchronize()
+        best_c = min(best_c, e0.elapsed_time(e1) / CHAIN)
+    res = {"lanes": L, "appended": tot, "ms": round(best, 4),
+           "gbs": round(nbytes / (best * 1e-3) / 1e9, 1),
+           "frac": round(nbytes / (best * 1e-3) / 1e9 / PEAK, 4), "contents_ok": ok}
+    if chained:
+        a.commit()
+        ends = torch.cumsum(torch.clamp(cnt.to(torch.int64), max=K), 0)
+        b = [0] + [int(ends[int(x) - 1]) if int(x) else 0 for x in lo[1:]]
+        exp = torch.cat([comp[b[s]:b[s + 1]].repeat(CHAIN) for s in range(S)])
+        res["chained"] = {"calls": CHAIN, "ms_per_call": round(best_c, 4),
+                          "gbs": round(nbytes / (best_c * 1e-3) / 1e9, 1),
+                          "frac": round(nbytes / (best_c * 1e-3) / 1e9 / PEAK, 4),
+                          "contents_ok": bool(torch.equal(a.flatten_device(), exp))}
     a.close()
-    return {"lanes": L, "appended": tot, "ms": round(best, 4),
-            "gbs": round(nbytes / (best * 1e-3) / 1e9, 1),
-            "frac": round(nbytes / (best * 1e-3) / 1e9 / PEAK, 4), "contents_ok": ok}
+    return res
 
 
 for K, esz in ((1, 4), (2, 4), (4, 4), (8, 4), (16, 4), (4, 8), (16, 1), (1, 8)):
@@ -68,7 +98,7 @@ reps = int(os.environ.get("PROBE_REPS", "0"))
 if reps:
     bad = 0
     for i in range(reps):
-        r = run(1 + (i % 8), 4, target=1 << 22, reps=1, ragged=bool(i & 1))
+        r = run(1 + (i % 8), 4, target=1 << 22, reps=1, ragged=bool(i & 1), chained=False)
         bad += not r["contents_ok"]
     out["stress"] = {"runs": reps, "bad": bad}
 print(json.dumps(out))
