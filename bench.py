@@ -709,7 +709,8 @@ def insert_paths_leg(args, gg, torch, device, hbm):
         counts uniform in [0, K]; algorithmic bytes = counts (4 B / lane) +
         the [lanes x K] value block the counts select from + the compacted
         output (the layout the API takes), the useful bytes (counts + kept
-        values read + written) beside it;
+        values read + written) beside it; `chained`: 4 back-to-back calls per
+        event pair (each planned on the previous calls' upper bounds);
       * push_if (the device push_back API from a kernel): 2^28 candidates,
         predicate density 1/2; bytes = values + predicates read + kept written.
     Eager timings are CUDA events around the public call (host planning and
@@ -800,7 +801,21 @@ def insert_paths_leg(args, gg, torch, device, hbm):
                          "register-resident tile walk)")})
         b.commit()
         mask = torch.arange(K, device=device)[None, :] < cnt[:, None]
-        out[f"lanes_K{K}"]["contents_ok"] = bool(torch.equal(b.flatten_device(), vals.view(-1, K)[mask]))
+        comp = vals.view(-1, K)[mask]
+        out[f"lanes_K{K}"]["contents_ok"] = bool(torch.equal(b.flatten_device(), comp))
+        # 4 back-to-back calls between two events: each plans on the previous
+        # calls' upper bounds instead of waiting for their sizes (chained)
+        ms4 = best(lambda: [b.insert_lanes(vals, cnt, lo, K, commit=False) for _ in range(4)],
+                   lambda: b.shrink(0, release=False), reps=3) / 4
+        b.commit()
+        ends = torch.cumsum(cnt.to(torch.int64), 0)
+        bnd = [0] + [int(ends[int(x) - 1]) for x in lo[1:]]
+        exp = torch.cat([comp[bnd[s]:bnd[s + 1]].repeat(4) for s in range(S)])
+        out[f"lanes_K{K}"]["chained"] = {
+            "calls": 4, "ms_per_call": round(ms4, 4), "frac": round(layout / (ms4 * 1e-3) / 1e9 / hbm, 4),
+            "gelem_s": round(tot / (ms4 * 1e-3) / 1e9, 2),
+            "contents_ok": bool(torch.equal(b.flatten_device(), exp))}
+        del comp, exp
         b.close()
         del b, vals, cnt, mask
         torch.cuda.empty_cache()
@@ -817,8 +832,17 @@ def insert_paths_leg(args, gg, torch, device, hbm):
         rec(f"push_if_{mode}", ms, 5 * N + 4 * tot, tot,
             {"candidates": N, "appended": tot, "kernel": f"k_push_if ({mode}_push_back_staged, 8 rounds per thread)"})
         c.commit()
-        out[f"push_if_{mode}"]["multiset_ok"] = bool(torch.equal(torch.sort(c.flatten_device())[0],
-                                                                 vals[pred.bool()]))
+        kept = vals[pred.bool()]
+        out[f"push_if_{mode}"]["multiset_ok"] = bool(torch.equal(torch.sort(c.flatten_device())[0], kept))
+        # 4 back-to-back calls between two events (chained: each plans on the
+        # previous calls' upper bounds instead of waiting for their readback)
+        ms4 = best(lambda: [c.push_if(vals, pred, mode=mode, commit=False) for _ in range(4)],
+                   lambda: c.shrink(0, release=False), reps=3) / 4
+        c.commit()
+        out[f"push_if_{mode}"]["chained"] = {
+            "calls": 4, "ms_per_call": round(ms4, 4),
+            "frac": round((5 * N + 4 * tot) / (ms4 * 1e-3) / 1e9 / hbm, 4),
+            "multiset_ok": bool(torch.equal(torch.sort(c.flatten_device())[0], torch.sort(kept.repeat(4))[0]))}
         c.close()
         del c
     del vals, pred

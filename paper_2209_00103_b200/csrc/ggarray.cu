@@ -80,6 +80,8 @@ struct gg_array {
   uint32_t lanes_n = 0;                                  // pending tiled lanes calls
   std::vector<uint64_t> lanes_ub, lanes_hb;              // [S] pending upper bounds / backed-bucket masks
   bool view_pend = false;                                // push_if mirrors pending behind lanes_ev
+  uint32_t view_n = 0;                                   // pending push_if calls (they chain like lanes)
+  std::vector<uint64_t> view_ub, view_hb;                // [S] pending upper bounds / headroom-bucket masks
   cudaEvent_t lanes_ev = nullptr;
   uint64_t *h_lanes = nullptr;                           // pinned [kLanesChain x S]
   std::vector<uint32_t> lanes_head;                      // (b, s0, s1) runs backed for the upper bound
@@ -786,6 +788,8 @@ int resolve_lanes(gg_array *a) {
   if (a->view_pend) {                 // a push_if whose appends could not fail (see gg_push_if)
     CUDA_TRY(cudaEventSynchronize(a->lanes_ev));
     a->view_pend = false;
+    a->view_n = 0;
+    std::fill(a->view_hb.begin(), a->view_hb.end(), 0);
     const int rc = view_finish_host(a, nullptr, a->have_last ? a->last_st : nullptr);
     if (rc && rc != GG_EPARTIAL) return rc;
   }
@@ -2076,14 +2080,16 @@ namespace {
 // live-bytes cap allows) and publish the backed-slot masks on stream st.
 // sync: wait for the device (the public entry point, whose user kernel may
 // run on any stream); the library's own push_if stays stream-ordered.
+// pend_hb: buckets pending (chained) push_if calls already backed as headroom
+// -- allowed in the mask, not backed again
 int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool sync, gg_device_view *out,
-                 bool *complete = nullptr) {
+                 bool *complete = nullptr, const uint64_t *pend_hb = nullptr) {
   if (a->view_out) return fail(GG_EVALUE, "a device view is outstanding (call gg_device_view_sync)");
   std::vector<unsigned long long> am(a->S);
   uint64_t live = a->live;
-  a->view_keep = a->slab.mapped;
+  if (!pend_hb) a->view_keep = a->slab.mapped;
   bool stop = false;
-  for (uint32_t s = 0; s < a->S; ++s) am[s] = a->flags[s];
+  for (uint32_t s = 0; s < a->S; ++s) am[s] = a->flags[s] | (pend_hb ? pend_hb[s] : 0);
   if (h_max_sizes && !a->limit && g_batch_backing) {
     // no live-bytes cap: class by class in runs of consecutive shards (one
     // batched refcount pass per run; a run that cannot be backed goes slot by
@@ -2097,7 +2103,7 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
     for (uint32_t b = 0; b < kmax && !stop; ++b) {
       bool have_region = false;
       for (uint32_t s = 0; s < a->S && !stop;) {
-        auto need = [&](uint32_t x) { return b < k[x] && !(a->flags[x] >> b & 1); };
+        auto need = [&](uint32_t x) { return b < k[x] && !(am[x] >> b & 1); };
         if (!need(s)) { ++s; continue; }
         uint32_t e = s + 1;
         while (e < a->S && need(e)) ++e;
@@ -2126,7 +2132,7 @@ int view_prepare(gg_array *a, const uint64_t *h_max_sizes, cudaStream_t st, bool
     for (uint32_t s = 0; s < a->S && !stop; ++s) {
       const uint32_t k = std::min<uint32_t>(min_buckets_for(a, h_max_sizes[s]), a->MB);
       for (uint32_t b = 0; b < k; ++b) {
-        if (a->flags[s] >> b & 1) continue;
+        if (am[s] >> b & 1) continue;
         const uint64_t nb = bucket_bytes(a, b);
         if ((a->limit && live + nb > a->limit) || back_bucket(a, s, b) != GG_OK) { stop = true; break; }
         live += nb;
@@ -2212,7 +2218,18 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   }
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);
-  { int frc_ = check_no_view(a); if (!frc_) frc_ = enter(a, st); if (frc_) return frc_; }
+  // a deferred push_if pending (and nothing else): chain behind it, planning
+  // on its upper bounds, without waiting for its readback
+  const bool chain = a->view_pend && !a->lanes_pend && !a->limit && g_batch_backing &&
+                     a->view_n < kLanesChain && !capturing_now(a, st);
+  {
+    int frc_ = check_no_view(a);
+    if (!frc_) frc_ = chain ? order_stream(a, st) : enter(a, st);
+    if (!frc_ && chain) frc_ = flush_meta(a, st, true);
+    if (!frc_ && chain) frc_ = flush_grow(a, st, true);
+    if (frc_) return frc_;
+  }
+  if (a->view_ub.size() != a->S) { a->view_ub.assign(a->S, 0); a->view_hb.assign(a->S, 0); }
   // worst case: every candidate of shard s appended (block blk takes slice
   // blk of every round of grid * kPushSlice candidates)
   std::vector<uint64_t> maxsz(a->S, 0);
@@ -2221,10 +2238,12 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
     const uint64_t lo = (uint64_t)blk * kPushSlice;
     maxsz[blk % a->S] += full * kPushSlice + (rem > lo ? std::min<uint64_t>(kPushSlice, rem - lo) : 0);
   }
-  for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += a->size[s];
+  const uint64_t *base = chain ? a->view_ub.data() : a->size.data();
+  for (uint32_t s = 0; s < a->S; ++s) maxsz[s] += base[s];
   gg_device_view v;
   bool backed = false;
-  int rc = view_prepare(a, maxsz.data(), st, false, &v, &backed);
+  const size_t h0 = a->headroom.size();
+  int rc = view_prepare(a, maxsz.data(), st, false, &v, &backed, chain ? a->view_hb.data() : nullptr);
   if (rc) return rc;
   // every slot the launch can reach is backed and within max_buckets: no
   // append can fail, so the host mirrors are refreshed lazily (the readback
@@ -2246,11 +2265,22 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
 #undef GG_PUSH_CASE
   }
   CUDA_TRY(cudaGetLastError());
-  if (can_fail || capturing_now(a, st)) return view_finish(a, h_status, st);
+  if (can_fail || capturing_now(a, st)) {
+    // synchronous readback: the device tables it copies are exact, so it
+    // also settles any chained calls before this one (all their headroom)
+    a->view_pend = false;
+    a->view_n = 0;
+    std::fill(a->view_hb.begin(), a->view_hb.end(), 0);
+    return view_finish(a, h_status, st);
+  }
   if ((rc = view_finish_issue(a, st))) return rc;
   if (!a->lanes_ev) CUDA_TRY(cudaEventCreateWithFlags(&a->lanes_ev, cudaEventDisableTiming));
   CUDA_TRY(cudaEventRecord(a->lanes_ev, st));
+  for (size_t i = h0; i < a->headroom.size(); i += 3)
+    for (uint32_t s = a->headroom[i + 1]; s < a->headroom[i + 2]; ++s) a->view_hb[s] |= uint64_t(1) << a->headroom[i];
+  for (uint32_t s = 0; s < a->S; ++s) a->view_ub[s] = maxsz[s];
   a->view_pend = true;
+  a->view_n += 1;
   a->view_out = false;
   if (h_status) memset(h_status, 0, a->S * sizeof(int32_t));
   return GG_OK;

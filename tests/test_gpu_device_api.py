@@ -96,3 +96,47 @@ def test_push_if_repeated_contention(gg):
                     fails.append((it, mode, s))
             a.close()
     assert not fails, fails[:5]
+
+
+def test_push_if_chained_calls(gg):
+    """Consecutive push_if calls whose appends cannot fail chain: each plans on
+    the previous calls' upper bounds and headroom without waiting for their
+    readback.  12 calls per array (block / warp, several grids and
+    densities); with max_buckets = 12 some calls' upper bounds exceed the
+    bucket table, so they take the synchronous path mid-chain, which settles
+    the calls before them.  Every shard holds the multiset of its appends,
+    sizes / capacities / flags are the minimal bucket prefix, and the
+    headroom is returned once the chain settles."""
+    import torch
+    rng = np.random.default_rng(77)
+    S, fb = 11, 8
+    for mb in (64, 12):
+        a = gg.GrowableArray(S, fb, dtype=np.int32, max_buckets=mb)   # 12: 32760 elements per shard
+        exp = [[] for _ in range(S)]
+        for it in range(12):
+            if mb == 12 and it % 4 in (0, 3):
+                # one block -> shard 0 only: its upper bound grows by 20000 a
+                # call (the third such call in a chain exceeds the table), its
+                # appends by ~1000
+                n, grid, dens = 20_000, 1, 0.05
+            else:
+                n = int(rng.integers(1, 60_000 if mb == 64 else 20_000))
+                grid, dens = [64, 11, 200, 33][it % 4], [0.5, 0.05, 0.95][it % 3]
+            vals = rng.integers(-2**31, 2**31 - 1, n, dtype=np.int64).astype(np.int32)
+            pred = rng.random(n) < dens
+            a.push_if(torch.from_numpy(vals).cuda(), torch.from_numpy(pred).cuda(),
+                      mode="block" if it % 2 else "warp", grid=grid, commit=False)
+            for s, e in enumerate(_expected(vals, pred, S, grid)):
+                exp[s].append(e)
+        a.commit()
+        st = a._parity_state()
+        for s in range(S):
+            got = a.shards[s].to_numpy()
+            assert np.array_equal(np.sort(got), np.sort(np.concatenate(exp[s]))), (mb, s)
+            k = O.min_buckets_for(len(got), fb)
+            assert st["sizes"][s] == len(got)
+            assert st["caps"][s] == O.capacity_of(k, fb)
+            assert st["flags"][s] == (1 << k) - 1
+        ms = a.memory_stats()
+        assert ms["mapped_bytes"] - ms["bucket_bytes"] < 64 << 20
+        a.close()
