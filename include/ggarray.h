@@ -181,6 +181,11 @@ int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *s
 /* get_global / set_global for index arrays (sharded_array.py:139-158) */
 int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream);
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream);
+/* gg_gather with the bounds check of get_global (sharded_array.py:152-155:
+ * IndexError outside the committed size) fused into the gather: returns
+ * GG_EINDEX if any index is outside [0, committed size) (d_out then holds
+ * no meaningful values); synchronizes the stream to read the check back */
+int gg_gather_checked(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream);
 /* single-element ShardVector.get / set (bucket_vector.py:259-277) */
 int gg_get(gg_array *a, uint32_t shard, uint64_t i, void *h_out, void *stream);
 int gg_set(gg_array *a, uint32_t shard, uint64_t i, const void *h_val, void *stream);

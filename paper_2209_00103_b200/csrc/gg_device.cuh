@@ -1372,9 +1372,38 @@ __global__ void __launch_bounds__(kThreads) k_rw_global(Tables t, uint64_t total
 // flight together (the kernel is bound by random 32 B sectors, not by the
 // directory chain).
 constexpr int kGatherU = 4;                      // indices per thread (independent chains)
+
+// the random element read of the gather, by cache policy (ldm, uniform):
+// 0 = default (L1-allocating: ncu showed 4 L2 sectors = a 128 B line
+// requested per random 4 B element), 1 = .cg (L2 only), 2 =
+// .L1::no_allocate, 3 = .nc.L1::no_allocate, 4 = .cs
+#define GG_LDR(Q, T, R)                                                                            \
+  if (ldm == 1) asm volatile("ld.global.cg." T " %0, [%1];" : "=" R(v) : "l"(p));                   \
+  else if (ldm == 2) asm volatile("ld.global.L1::no_allocate." T " %0, [%1];" : "=" R(v) : "l"(p)); \
+  else if (ldm == 3) asm volatile("ld.global.nc.L1::no_allocate." T " %0, [%1];" : "=" R(v) : "l"(p)); \
+  else if (ldm == 4) asm volatile("ld.global.cs." T " %0, [%1];" : "=" R(v) : "l"(p));              \
+  else v = (Q)*p;
+template <int ESZ>
+__device__ __forceinline__ typename ElemT<ESZ>::T ld_rand(const typename ElemT<ESZ>::T *p, int ldm) {
+  typedef typename ElemT<ESZ>::T E;
+  if constexpr (ESZ == 8) {
+    unsigned long long v;
+    GG_LDR(unsigned long long, "u64", "l")
+    return (E)v;
+  } else {
+    uint32_t v;
+    if constexpr (ESZ == 4) { GG_LDR(uint32_t, "u32", "r") }
+    else if constexpr (ESZ == 2) { GG_LDR(uint16_t, "u16", "r") }
+    else { GG_LDR(uint8_t, "u8", "r") }
+    return (E)v;
+  }
+}
+#undef GG_LDR
+
 template <int ESZ, bool SMEM, int U = kGatherU>
 __global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, uint64_t n, char *out,
-                                                const char *vals, int scatter) {
+                                                const char *vals, int scatter, int ldm, uint64_t lim,
+                                                unsigned int *bad) {
   typedef typename ElemT<ESZ>::T E;
   extern __shared__ uint64_t sdir[];
   __shared__ char *scb[kMaxBuckets];
@@ -1391,7 +1420,11 @@ __global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, ui
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t j = j0 + (uint64_t)u * blockDim.x;
-      const uint64_t g = j < n ? (uint64_t)__ldcs(idx + j) : 0;
+      uint64_t g = j < n ? (uint64_t)__ldcs(idx + j) : 0;
+      if (bad && g >= lim) {                      // checked gather: flag it, read element 0
+        *bad = 1u;                                // (lim > 0; the call fails with GG_EINDEX)
+        g = 0;
+      }
       const uint32_t s = upper_shard(dir, t.S, g);
       uint32_t b; uint64_t o;
       locate(g - dir[s], t.log2fb, b, o);
@@ -1406,7 +1439,7 @@ __global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, ui
     } else {
       E v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = j0 + (uint64_t)u * blockDim.x < n ? *p[u] : E(0);
+      for (int u = 0; u < U; ++u) v[u] = j0 + (uint64_t)u * blockDim.x < n ? ld_rand<ESZ>(p[u], ldm) : E(0);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint64_t j = j0 + (uint64_t)u * blockDim.x;

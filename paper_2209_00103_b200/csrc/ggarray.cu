@@ -1985,7 +1985,7 @@ int gg_flatten_range(gg_array *a, uint64_t lo, uint64_t hi, void *d_out, void *s
 namespace {
 // one launch of k_gather for get_many (scatter = 0) / set_many (1)
 int launch_gather(gg_array *a, const int64_t *d_idx, uint64_t n, char *out, const char *vals, int scatter,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint64_t lim = 0, unsigned int *bad = nullptr) {
   Tables t = tables_for_launch(a, false);
   const bool smem = a->S < 4096;
   const size_t sb = smem ? (size_t)(a->S + 1) * 8 : 0;
@@ -1993,10 +1993,14 @@ int launch_gather(gg_array *a, const int64_t *d_idx, uint64_t n, char *out, cons
   // phases (index loads, bisects, random element accesses) overlap on an SM
   const uint64_t per_cta = 256ull * kGatherU;
   const int grid = (int)std::min<uint64_t>((n + per_cta - 1) / per_cta, 0x7fffffffull);
+  // cache policy of the random element reads (A/B: GG_GATHER_LD, see ld_rand)
+  // (.L1::no_allocate by default: a random element is read once; 2% faster under ncu than the
+  // L1-allocating load, profiles/r02_gather_ld_ab.json)
+  static const int ldm = [] { const char *e = getenv("GG_GATHER_LD"); return e ? atoi(e) : 2; }();
   cudaError_t e = cudaSuccess;
 #define GG_GATHER(ESZ_) \
-  e = smem ? launch_k(k_gather<ESZ_, true>, grid, 256, sb, st, t, d_idx, n, out, vals, scatter) \
-           : launch_k(k_gather<ESZ_, false>, grid, 256, 0, st, t, d_idx, n, out, vals, scatter);
+  e = smem ? launch_k(k_gather<ESZ_, true>, grid, 256, sb, st, t, d_idx, n, out, vals, scatter, ldm, lim, bad) \
+           : launch_k(k_gather<ESZ_, false>, grid, 256, 0, st, t, d_idx, n, out, vals, scatter, ldm, lim, bad);
   switch (a->esz) {
     case 1: GG_GATHER(1) break;
     case 2: GG_GATHER(2) break;
@@ -2015,6 +2019,29 @@ int gg_gather(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *
   { int frc_ = enter(a, S_(stream)); if (frc_) return frc_; }
   if (n == 0) return GG_OK;
   return launch_gather(a, d_idx, n, (char *)d_out, nullptr, 0, S_(stream));
+}
+
+int gg_gather_checked(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  cudaStream_t st = S_(stream);
+  { int frc_ = enter(a, st); if (frc_) return frc_; }
+  if (n == 0) return GG_OK;
+  const uint64_t lim = a->prefix[a->S];
+  if (lim == 0) return fail(GG_EINDEX, "index outside the committed size");
+  // the bounds check rides in the gather (no separate pass over the
+  // indices): a flag word in the device scratch, cleared first, read back
+  unsigned int *d_bad = (unsigned int *)(a->d_scratch + 48);
+  CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(unsigned int), st));
+  int rc = launch_gather(a, d_idx, n, (char *)d_out, nullptr, 0, st, lim, d_bad);
+  if (rc) return rc;
+  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
+  CUDA_TRY(cudaMemcpyAsync(a->h_scratch + 48, d_bad, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  unsigned int badv;
+  memcpy(&badv, a->h_scratch + 48, sizeof badv);
+  if (badv) return fail(GG_EINDEX, "index outside the committed size");
+  return GG_OK;
 }
 
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {

@@ -438,14 +438,13 @@ class GrowableArray:
         import torch
         idx = torch.as_tensor(np.asarray(indices, np.int64) if not isinstance(indices, torch.Tensor)
                               else indices, dtype=torch.int64).to(self.device).contiguous()
-        n = self.committed_size
-        if idx.numel():
-            lo, hi = (int(x) for x in torch.aminmax(idx))    # one pass, one sync
-            if lo < 0 or hi >= n:
-                raise IndexError(f"indices outside committed size {n}")
         out = torch.empty(idx.numel(), dtype=self._torch_dtype, device=self.device)
-        L.check(L.lib.gg_gather(self._h, C.c_void_p(idx.data_ptr()), idx.numel(),
-                                C.c_void_p(out.data_ptr()), self._stream()), "gather")
+        # bounds check fused into the gather kernel (one flag word read back)
+        rc = L.lib.gg_gather_checked(self._h, C.c_void_p(idx.data_ptr()), idx.numel(),
+                                     C.c_void_p(out.data_ptr()), self._stream())
+        if rc == L.GG_EINDEX:
+            raise IndexError(f"indices outside committed size {self.committed_size}")
+        L.check(rc, "gather")
         return out
 
     def set_many(self, indices, values) -> None:

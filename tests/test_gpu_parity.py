@@ -76,6 +76,41 @@ def test_get_many_set_many(gg):
         a.get_many([100000])
 
 
+@pytest.mark.parametrize("dtype", [np.int8, np.int16, np.float32, np.int64])
+def test_get_many_checked_in_kernel(gg, dtype):
+    """get_many's bounds check rides in the gather kernel (gg_gather_checked):
+    one bad index anywhere in a large batch, negative indices, an empty
+    array -> IndexError (get_global, sharded_array.py:152-155); the array and
+    later gathers are unaffected."""
+    import ctypes as C
+    import torch
+    from paper_2209_00103_b200 import _lib as L
+    n = 300007
+    vals = (np.arange(n) % 120).astype(dtype)
+    a = gg.GrowableArray.from_flat(vals, shards=37, first_bucket_size=16)
+    rng = np.random.default_rng(3)
+    idx = rng.integers(0, n, 1 << 18)
+    assert np.array_equal(a.get_many(idx).cpu().numpy(), vals[idx])
+    for bad in (n, n + 12345, -1, -(1 << 40)):
+        j = idx.copy()
+        j[rng.integers(0, j.size)] = bad
+        with pytest.raises(IndexError):
+            a.get_many(j)
+    assert np.array_equal(a.get_many(idx[:1000]).cpu().numpy(), vals[idx[:1000]])
+    assert a.get_many(np.zeros(0, np.int64)).numel() == 0
+    # the C-ABI entry directly: GG_EINDEX, and GG_OK on in-range indices
+    d = torch.as_tensor(np.array([0, n - 1, n], np.int64), device="cuda")
+    out = torch.empty(3, dtype=torch.from_numpy(vals[:1]).dtype, device="cuda")
+    assert L.lib.gg_gather_checked(a._h, C.c_void_p(d.data_ptr()), 3, C.c_void_p(out.data_ptr()),
+                                   a._stream()) == L.GG_EINDEX
+    assert L.lib.gg_gather_checked(a._h, C.c_void_p(d.data_ptr()), 2, C.c_void_p(out.data_ptr()),
+                                   a._stream()) == L.GG_OK
+    assert out[:2].cpu().numpy().tolist() == [vals[0], vals[n - 1]]
+    e = gg.GrowableArray(4, 8, dtype=dtype)
+    with pytest.raises(IndexError):
+        e.get_many([0])
+
+
 def test_lanes_insert_matches_compaction(gg):
     import torch
     rng = np.random.default_rng(11)
