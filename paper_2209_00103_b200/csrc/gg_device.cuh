@@ -1869,6 +1869,13 @@ __global__ void __launch_bounds__(256) k_lanes_scatter(Tables t, const char *val
 // lanes per chunk: 64 KiB of counts (L2-resident between steps 1 and 3); 4 B lanes run
 // 6 CTAs per SM (more tiles in flight: 0.57 -> 0.64 of HBM at K = 1 int32)
 constexpr uint32_t kLanesChunk = 16384;
+
+// TMA bulk prefetch of [p, p + bytes) into L2 (a hint: no completion, no
+// destination); p 16 B aligned, bytes a multiple of 16 (rounded down here)
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+  bytes &= ~15u;
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 constexpr unsigned long long kChainA = 1ull << 62, kChainP = 2ull << 62, kChainV = (1ull << 62) - 1;
 
 __device__ __forceinline__ unsigned long long ld_chain(const unsigned long long *p) {
@@ -1907,7 +1914,7 @@ __device__ __forceinline__ uint32_t chunk_count_sum(const uint32_t *counts, uint
 template <int ESZ, int KB, bool VEC = true>
 __global__ void __launch_bounds__(256, KB == 4 ? 6 : 1) k_lanes_chunk(Tables t, const char *vals, const uint32_t *counts,
                                                      const uint32_t *cpre, unsigned long long *chain,
-                                                     uint32_t C) {
+                                                     uint32_t C, uint32_t pf) {
   typedef LaneShape<ESZ, KB, VEC> L;
   constexpr uint32_t K = L::K, T = L::T;
   __shared__ LaneSmem<ESZ, KB, VEC> sm;
@@ -1920,6 +1927,13 @@ __global__ void __launch_bounds__(256, KB == 4 ? 6 : 1) k_lanes_chunk(Tables t, 
   const uint64_t lo = t.offsets[s] + (uint64_t)(chunk - first) * C;
   const uint32_t nl = (uint32_t)min((uint64_t)C, t.offsets[s + 1] - lo);
   stage_cbase(t, sm.scb);
+  // pf tiles ahead of the walk, the value block is prefetched into L2 by TMA
+  // (the first pf tiles while the counts are summed and chained)
+  const uint64_t wlo = lo - lo % L::GL;
+  auto pf_tile = [&](uint64_t p0) {
+    if (p0 < lo + nl) prefetch_l2(vals + p0 * KB, (uint32_t)(min((uint64_t)T, lo + nl - p0) * KB));
+  };
+  if (tid < pf) pf_tile(wlo + (uint64_t)tid * T);
   const uint32_t agg = chunk_count_sum(counts, lo, nl, K, red);
   if (wid == 0) {
     unsigned long long excl = 0;
@@ -1961,9 +1975,9 @@ __global__ void __launch_bounds__(256, KB == 4 ? 6 : 1) k_lanes_chunk(Tables t, 
   uint64_t base = sm.base;
   int par = 0;
   // tiles from a GL-aligned lane: whole groups take the vector loads
-  const uint64_t wlo = lo - lo % L::GL;
   for (uint64_t t0 = wlo; t0 < lo + nl; t0 += T) {
     uint32_t c[L::R][L::GL], w[16];
+    if (pf && tid == 0) pf_tile(t0 + (uint64_t)pf * T);
     lanes_load<ESZ, KB, VEC>(vals, counts, t0, lo, lo + nl, c, w);
     base += lanes_store<ESZ, KB, VEC>(t, sm, s, c, w, base, par);
     par ^= 1;

@@ -943,7 +943,7 @@ struct PushShape {
 
 template <int ESZ, int BLOCK, bool BLOCK_MODE>
 __global__ void __launch_bounds__(BLOCK, ESZ >= 4 ? 4 : 6) k_push_if(gg_device_view t, const char *vals,
-                                                   const uint8_t *pred, uint64_t n, int aligned) {
+                                                   const uint8_t *pred, uint64_t n, int aligned, uint32_t pf) {
   typedef typename ElemT<ESZ>::T E;
   typedef PushShape<ESZ, BLOCK> P;
   constexpr uint32_t G = P::G, J = P::J, RPL = P::RPL;
@@ -957,7 +957,21 @@ __global__ void __launch_bounds__(BLOCK, ESZ >= 4 ? 4 : 6) k_push_if(gg_device_v
   // this thread's candidates: load j of a call starting at round r0 covers
   // round r0 + j * RPL + sub, positions [pos, pos + G) of the block's slice
   const uint64_t sub = threadIdx.x / P::TPS, pos = (threadIdx.x % P::TPS) * G;
+  // the next call's slices (values and predicates of RPC rounds) are
+  // prefetched into L2 by TMA while this call loads and appends (pf = 1)
+  auto pf_call = [&](uint64_t rc) {
+    const uint32_t j = threadIdx.x >> 1;
+    if (j < P::RPC) {
+      const uint64_t i = (uint64_t)blockIdx.x * kPushSlice + (rc + j) * round;
+      if (i + kPushSlice <= n) {
+        if (threadIdx.x & 1) prefetch_l2(pred + i, kPushSlice);
+        else prefetch_l2(vals + i * ESZ, kPushSlice * ESZ);
+      }
+    }
+  };
+  if (pf && aligned) pf_call(0);
   for (uint64_t r0 = 0; (uint64_t)blockIdx.x * kPushSlice + r0 * round < n; r0 += P::RPC) {
+    if (pf && aligned) pf_call(r0 + P::RPC);
     E v[K];
     uint32_t mask = 0;
     const uint64_t i0 = (uint64_t)blockIdx.x * kPushSlice + (r0 + sub) * round + pos;
@@ -1802,6 +1816,11 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
     // measured faster than the register path (tools/lanes_probe.py A/B, two
     // runs: KB = 8 +5-7%, 32 +0-2%, 64 +4%; KB = 4 -12%, 16 -2..-8%: those
     // keep k_lanes_chunk).  GG_LANES_BULK=0 / 1: never / always.
+    // L2 bulk prefetch distance (tiles) of the register-path lanes walk: one
+    // tile ahead for 4 / 8 B elements (K1 int32 0.75 -> 0.79, K4 0.82 -> 0.86
+    // of HBM), off for 1 / 2 B elements (instruction-bound: 0.46 -> 0.44);
+    // profiles/r02_prefetch_ab.json.  A/B: GG_LANES_PF = distance
+    static const int lanes_pf_env = [] { const char *e = getenv("GG_LANES_PF"); return e ? atoi(e) : -1; }();
     static const int bulk_env = [] {
       const char *e = getenv("GG_LANES_BULK");
       return e ? (e[0] == '0' ? 0 : 1) : -1;
@@ -1819,7 +1838,8 @@ int lanes_tiled(gg_array *a, const void *d_values, const uint32_t *d_counts, con
       e = launch_k(k_lanes_bulk<ESZ_, KB_, 2>, (unsigned)nt, 256, (size_t)2 * 16384, st, t, dv, d_counts, tp, d_chain, \
                    C); \
     } else { \
-      e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, C); \
+      e = launch_k(k_lanes_chunk<ESZ_, KB_>, (unsigned)nt, 256, 0, st, t, dv, d_counts, tp, d_chain, C, \
+                   lanes_pf_env >= 0 ? (uint32_t)lanes_pf_env : (ESZ_ >= 4 ? 1u : 0u)); \
     } \
     break;
     switch (a->esz) {
@@ -1991,6 +2011,7 @@ int launch_gather(gg_array *a, const int64_t *d_idx, uint64_t n, char *out, cons
   const size_t sb = smem ? (size_t)(a->S + 1) * 8 : 0;
   // one tile of 256 x kGatherU indices per CTA (no grid-stride cap): CTAs at different
   // phases (index loads, bisects, random element accesses) overlap on an SM
+  // (8 indices per thread measured slower: 0.467 -> 0.493 ms, profiles/r02_prefetch_ab.json)
   const uint64_t per_cta = 256ull * kGatherU;
   const int grid = (int)std::min<uint64_t>((n + per_cta - 1) / per_cta, 0x7fffffffull);
   // cache policy of the random element reads (A/B: GG_GATHER_LD, see ld_rand)
@@ -2281,11 +2302,17 @@ int gg_push_if(gg_array *a, const void *d_vals, const uint8_t *d_pred, uint64_t 
   // vector loads: 16 B of values (8 B elements: 32 B) and G predicate bytes
   const uint32_t pg = a->esz >= 4 ? 4 : 16 / a->esz;
   const int al = ((uintptr_t)d_vals % (pg * a->esz) == 0 && (uintptr_t)d_pred % pg == 0) ? 1 : 0;
+  // L2 bulk prefetch of the next append call's slices: on in block mode for
+  // 4 / 8 B elements (block int32 0.73 -> 0.76, int64 0.79 -> 0.87 of HBM),
+  // off in warp mode (int32 0.79 -> 0.72 with it) and for 1 / 2 B elements;
+  // profiles/r02_prefetch_ab.json.  A/B: GG_PUSH_PF = 0 | 1
+  static const int push_pf_env = [] { const char *e = getenv("GG_PUSH_PF"); return e ? atoi(e) : -1; }();
+  const uint32_t push_pf = push_pf_env >= 0 ? (uint32_t)push_pf_env : (mode && a->esz >= 4 ? 1u : 0u);
   switch (a->esz) {
 #define GG_PUSH_CASE(ESZ_) \
     case ESZ_: \
-      if (mode) k_push_if<ESZ_, 256, true><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, al); \
-      else k_push_if<ESZ_, 256, false><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, al); \
+      if (mode) k_push_if<ESZ_, 256, true><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, al, push_pf); \
+      else k_push_if<ESZ_, 256, false><<<grid, B, 0, st>>>(v, (const char *)d_vals, d_pred, n, al, push_pf); \
       g_launches.fetch_add(1, std::memory_order_relaxed); \
       break;
     GG_PUSH_CASE(1) GG_PUSH_CASE(2) GG_PUSH_CASE(4) GG_PUSH_CASE(8)

@@ -453,7 +453,7 @@ class GrowableArray:
                               else indices, dtype=torch.int64).to(self.device).contiguous()
         n = self.committed_size
         if idx.numel():
-            lo, hi = (int(x) for x in torch.aminmax(idx))    # one pass, one sync
+            lo, hi = torch.stack(torch.aminmax(idx)).tolist()   # one pass, one sync
             if lo < 0 or hi >= n:
                 raise IndexError(f"indices outside committed size {n}")
         vals = self._device_values(values)
