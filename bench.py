@@ -750,6 +750,18 @@ def insert_paths_leg(args, gg, torch, device, hbm):
     reset = lambda: a.shrink(0, release=False)
     rec("ragged_insert_csr", best(lambda: (a.insert_csr(src, off), a.flush()), reset), 8 * N, N)
 
+    def chained_csr(calls=4):
+        # back-to-back public calls between two events: each call's host
+        # planning overlaps the previous call's kernel (no readback between)
+        for _ in range(calls):
+            a.insert_csr(src, off)
+        a.flush()
+    ms4 = best(chained_csr, reset)
+    out["ragged_insert_csr"]["chained"] = {
+        "calls": 4, "ms_per_call": round(ms4 / 4, 4),
+        "frac": round(8 * N / (ms4 / 4 * 1e-3) / 1e9 / hbm, 4),
+        "gelem_s": round(N / (ms4 / 4 * 1e-3) / 1e9, 2)}
+
     def graph_ms(fn, reps=10):
         g = a.capture(fn)
         for _ in range(3):
@@ -1046,7 +1058,12 @@ def config5_leg(args, gg, torch, device, hbm):
     in 180 GB (SURVEY 8e caveat), a streamed one does.  Contents checked in
     full against the closed form of the schedule.  Falls back to 2^33 if the
     GPU cannot hold 2^34 next to the rest of the bench."""
-    out = {}
+    out = {"device_free_gib_at_entry": round(torch.cuda.mem_get_info(device)[0] / 2**30, 1)}
+    # the process slab cache may still hold earlier legs' slabs: hand them
+    # back to the driver first (2^34 needs 128 GiB next to the rest)
+    gg.pool_trim(device.index)
+    torch.cuda.empty_cache()
+    out["device_free_gib_after_trim"] = round(torch.cuda.mem_get_info(device)[0] / 2**30, 1)
     for rounds in (14, 13):
         a = None
         try:
