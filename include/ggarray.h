@@ -186,6 +186,11 @@ int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals
  * GG_EINDEX if any index is outside [0, committed size) (d_out then holds
  * no meaningful values); synchronizes the stream to read the check back */
 int gg_gather_checked(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out, void *stream);
+/* gg_scatter with set_global's bounds check (sharded_array.py:156-158): a
+ * bounds pass over the indices, then the scatter, which writes nothing if
+ * any index is outside [0, committed size) (GG_EINDEX, no partial update);
+ * synchronizes the stream to read the check back */
+int gg_scatter_checked(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream);
 /* single-element ShardVector.get / set (bucket_vector.py:259-277) */
 int gg_get(gg_array *a, uint32_t shard, uint64_t i, void *h_out, void *stream);
 int gg_set(gg_array *a, uint32_t shard, uint64_t i, const void *h_val, void *stream);

@@ -73,6 +73,7 @@ _SIGS = {
     "gg_flatten_range": ([P, U64, U64, P, P], C.c_int),
     "gg_gather": ([P, P, U64, P, P], C.c_int),
     "gg_gather_checked": ([P, P, U64, P, P], C.c_int),
+    "gg_scatter_checked": ([P, P, U64, P, P], C.c_int),
     "gg_scatter": ([P, P, U64, P, P], C.c_int),
     "gg_get": ([P, U32, U64, P, P], C.c_int),
     "gg_set": ([P, U32, U64, P, P], C.c_int),

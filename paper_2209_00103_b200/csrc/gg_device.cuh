@@ -1408,6 +1408,8 @@ __global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, ui
   extern __shared__ uint64_t sdir[];
   __shared__ char *scb[kMaxBuckets];
   pdl_begin();
+  // checked scatter: k_check_idx (the predecessor) flagged a bad index -> no writes at all
+  if (scatter && bad && *(volatile unsigned int *)bad) return;
   stage_cbase(t, scb);
   if constexpr (SMEM)
     for (uint32_t i = threadIdx.x; i <= t.S; i += blockDim.x) sdir[i] = t.prefix[i];
@@ -1421,7 +1423,7 @@ __global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, ui
     for (int u = 0; u < U; ++u) {
       const uint64_t j = j0 + (uint64_t)u * blockDim.x;
       uint64_t g = j < n ? (uint64_t)__ldcs(idx + j) : 0;
-      if (bad && g >= lim) {                      // checked gather: flag it, read element 0
+      if (!scatter && bad && g >= lim) {                      // checked gather: flag it, read element 0
         *bad = 1u;                                // (lim > 0; the call fails with GG_EINDEX)
         g = 0;
       }
@@ -1447,6 +1449,20 @@ __global__ void __launch_bounds__(256) k_gather(Tables t, const int64_t *idx, ui
       }
     }
   }
+}
+
+// bounds pass of the checked scatter: flag any index outside [0, lim)
+// (negative int64 indices are huge as uint64); the scatter behind it skips
+// every write when the flag is set
+__global__ void __launch_bounds__(256) k_check_idx(const int64_t *idx, uint64_t n, uint64_t lim,
+                                                   unsigned int *bad) {
+  pdl_begin();
+  bool oob = false;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+#pragma unroll 4
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride)
+    oob |= (uint64_t)__ldcs(idx + j) >= lim;
+  if (__any_sync(0xffffffffu, oob) && (threadIdx.x & 31) == 0) *bad = 1u;
 }
 
 // zero whole buckets listed as (shard, bucket) pairs (dirty shards only)

@@ -2065,6 +2065,31 @@ int gg_gather_checked(gg_array *a, const int64_t *d_idx, uint64_t n, void *d_out
   return GG_OK;
 }
 
+int gg_scatter_checked(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
+  std::lock_guard<std::mutex> g(a->mu);
+  use_dev(a->dev);
+  cudaStream_t st = S_(stream);
+  { int frc_ = enter(a, st); if (frc_) return frc_; }
+  if (n == 0) return GG_OK;
+  const uint64_t lim = a->prefix[a->S];
+  if (lim == 0) return fail(GG_EINDEX, "index outside the committed size");
+  // bounds pass -> flag; the scatter behind it writes nothing if the flag is
+  // set (no partial update on error); the flag is read back at the end
+  unsigned int *d_bad = (unsigned int *)(a->d_scratch + 48);
+  CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(unsigned int), st));
+  const int grid = (int)std::min<uint64_t>((n + 1023) / 1024, (uint64_t)sm_count(a->dev) * 8);
+  CUDA_TRY(launch_k(k_check_idx, std::max(grid, 1), 256, 0, st, d_idx, n, lim, d_bad));
+  int rc = launch_gather(a, d_idx, n, nullptr, (const char *)d_vals, 1, st, lim, d_bad);
+  if (rc) return rc;
+  if (!a->h_scratch) CUDA_TRY(cudaMallocHost(&a->h_scratch, 64));   // pinned, on first use
+  CUDA_TRY(cudaMemcpyAsync(a->h_scratch + 48, d_bad, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  unsigned int badv;
+  memcpy(&badv, a->h_scratch + 48, sizeof badv);
+  if (badv) return fail(GG_EINDEX, "index outside the committed size");
+  return GG_OK;
+}
+
 int gg_scatter(gg_array *a, const int64_t *d_idx, uint64_t n, const void *d_vals, void *stream) {
   std::lock_guard<std::mutex> g(a->mu);
   use_dev(a->dev);

@@ -451,16 +451,15 @@ class GrowableArray:
         import torch
         idx = torch.as_tensor(np.asarray(indices, np.int64) if not isinstance(indices, torch.Tensor)
                               else indices, dtype=torch.int64).to(self.device).contiguous()
-        n = self.committed_size
-        if idx.numel():
-            lo, hi = torch.stack(torch.aminmax(idx)).tolist()   # one pass, one sync
-            if lo < 0 or hi >= n:
-                raise IndexError(f"indices outside committed size {n}")
         vals = self._device_values(values)
         if vals.numel() != idx.numel():
             raise ValueError("indices and values differ in length")
-        L.check(L.lib.gg_scatter(self._h, C.c_void_p(idx.data_ptr()), idx.numel(),
-                                 C.c_void_p(vals.data_ptr()), self._stream()), "scatter")
+        # bounds pass + scatter that writes nothing on a bad index (one flag read back)
+        rc = L.lib.gg_scatter_checked(self._h, C.c_void_p(idx.data_ptr()), idx.numel(),
+                                      C.c_void_p(vals.data_ptr()), self._stream())
+        if rc == L.GG_EINDEX:
+            raise IndexError(f"indices outside committed size {self.committed_size}")
+        L.check(rc, "scatter")
 
     # ------------------------------------------------------------ traversal
     def for_each_shard(self, op: Callable, workers: int | None = 1) -> None:

@@ -109,6 +109,37 @@ def test_get_many_checked_in_kernel(gg, dtype):
     e = gg.GrowableArray(4, 8, dtype=dtype)
     with pytest.raises(IndexError):
         e.get_many([0])
+    with pytest.raises(IndexError):
+        e.set_many([0], np.zeros(1, dtype))
+
+
+@pytest.mark.parametrize("dtype", [np.int8, np.float32, np.int64])
+def test_set_many_checked_no_partial_update(gg, dtype):
+    """set_many (gg_scatter_checked): a bounds pass flags any index outside
+    the committed size and the scatter behind it writes NOTHING (set_global,
+    sharded_array.py:156-158, raises before touching the array); a clean
+    batch lands exactly (distinct targets), odd lengths and unaligned index
+    slices included."""
+    n = 200003
+    vals = (np.arange(n) % 100).astype(dtype)
+    a = gg.GrowableArray.from_flat(vals, shards=29, first_bucket_size=8)
+    rng = np.random.default_rng(9)
+    idx = rng.permutation(n)[:(1 << 16) + 1]
+    new = (rng.integers(0, 100, idx.size)).astype(dtype)
+    for bad in (n, -1, 1 << 50):
+        j = idx.copy()
+        j[rng.integers(0, j.size)] = bad
+        with pytest.raises(IndexError):
+            a.set_many(j, new)
+        assert np.array_equal(a.flatten(), vals)          # untouched
+    import torch
+    dj = torch.as_tensor(np.concatenate([[0], idx]), device="cuda")[1:]   # 8 B-aligned, not 16 B
+    a.set_many(dj, new)
+    want = vals.copy()
+    want[idx] = new
+    assert np.array_equal(a.flatten(), want)
+    a.set_many(np.zeros(0, np.int64), np.zeros(0, dtype))
+    assert np.array_equal(a.flatten(), want)
 
 
 def test_lanes_insert_matches_compaction(gg):
